@@ -1,0 +1,306 @@
+#!/usr/bin/env python
+"""bench.py -- batched regularized-LQR solves on B200 (BASELINE.json metric, configs[1] = C2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-cpu-baseline]
+
+One step = one rr_factor_solve over the whole per-GPU batch (all hot-path rows of the fused
+solve: stage data in HBM, backward matrix + vector sweep, forward sweep, dual recovery).
+C2: 65,536 random stable LQR instances, n_x=12, n_u=4, N=100, δ=1e-4, FP64, per GPU (weak
+scaling: rank r solves global instances [r·B, (r+1)·B)).  Inputs (18.7 GB/GPU) exceed the
+126 MB L2, so no flush is needed between steps.  Timing: CUDA events on the launching stream,
+barrier + synchronize around the timed region, max over ranks.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "regularized-LQR solves/sec & stage-updates/s vs roofline at 1/2/4/8 B200"
+NX, NU, HORIZON, BATCH, SEED, DELTA = 12, 4, 100, 65536, 2509, 1e-4
+# Algorithmic model per (instance, stage), SURVEY.md §8(d) / DESIGN.md §7 (C2 row):
+ALG_BYTES_PER_STAGE = 6976     # fused two-sweep: inputs once + policy write/read + A,B,c re-read + x,u,y
+ALG_FLOPS_PER_STAGE = 15769    # 13,077 factor + 864 vector backward + 1,828 forward
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=BATCH, help=argparse.SUPPRESS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample wall time")
+    return ap.parse_args()
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl")
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, ws):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def cpu_baseline(target_s, cores=None):
+    """The oracle (plain C T2 recursion, as it stands) on the host cores, on a bounded sample of
+    the same C2 workload (same generator, global ids 0..S-1)."""
+    import synth
+    import oracle
+    cores = cores or os.cpu_count() or 1
+    cal = synth.random_stable_lqr(NX, NU, HORIZON, 16, SEED, DELTA)
+    t0 = time.perf_counter()
+    oracle.rr_solve_t2(cal, nthreads=1)
+    per_inst = (time.perf_counter() - t0) / 16
+    S = max(cores, int(target_s * cores / max(per_inst, 1e-6)))
+    S = min(S, 65536)
+    prob = synth.random_stable_lqr(NX, NU, HORIZON, S, SEED, DELTA)
+    t0 = time.perf_counter()
+    out = oracle.rr_solve_t2(prob, nthreads=cores)
+    dt = time.perf_counter() - t0
+    assert int((out["status"] != 0).sum()) == 0
+    return {"value": S / dt, "unit": "solves/s", "cores": cores, "kind": "oracle",
+            "stage_updates_per_s": S * HORIZON / dt,
+            "sample": "%d of the %d C2 instances (global ids 0..%d), T2 plain-C oracle, %d threads, %.1f s"
+                      % (S, BATCH, S - 1, cores, dt)}
+
+
+def run_reference(a, ws, rank):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import synth
+    import oracle
+    cores = os.cpu_count() or 1
+    cal = synth.random_stable_lqr(NX, NU, HORIZON, 16, SEED, DELTA)
+    t0 = time.perf_counter()
+    oracle.rr_solve_t2(cal, nthreads=1)
+    per_inst = (time.perf_counter() - t0) / 16
+    # each step: a bounded sample sized so warmup+steps finish in ~2-3 minutes
+    budget = 150.0 / max(1, a.steps + a.warmup)
+    S = max(cores, min(BATCH, int(budget * cores / max(per_inst, 1e-6))))
+    prob = synth.random_stable_lqr(NX, NU, HORIZON, S, SEED, DELTA)
+    for _ in range(a.warmup):
+        oracle.rr_solve_t2(prob, nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        oracle.rr_solve_t2(prob, nthreads=cores)
+    dt = (time.perf_counter() - t0) / a.steps
+    val = S / dt
+    line = {"metric": METRIC, "value": val, "unit": "solves/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "C2: random stable regularized LQR n_x=12 n_u=4 N=100 delta=1e-4 (oracle sample)",
+                       "global_batch": S, "seq_len": HORIZON, "parallelism": "host threads"},
+            "stage_updates_per_s": val * HORIZON,
+            "cpu_baseline": {"value": val, "unit": "solves/s", "cores": cores, "kind": "oracle",
+                             "sample": "%d of %d C2 instances per step, T2 plain-C oracle" % (S, BATCH)},
+            "e2e": {"value": val, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    ws, rank, local = dist_init()
+    if a.impl == "reference":
+        run_reference(a, ws, rank)
+        barrier(ws)
+        return
+    import torch
+    import synth
+    import paper_2509_16370_b200 as rr
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    B = a.batch
+    first = rank * B
+    # ---- inputs resident in HBM (generation excluded from timing) ----
+    prob = synth.empty_problem(NX, NU, HORIZON, B, device=dev)
+    for s in range(0, B, 4096):
+        e = min(B, s + 4096)
+        p = synth.random_stable_lqr(NX, NU, HORIZON, e - s, SEED, DELTA, first=first + s, device=dev)
+        for f in synth.RRProblem.FIELDS:
+            getattr(prob, f)[s:e].copy_(getattr(p, f))
+        del p
+    sol = rr.alloc_solution(prob)
+    call = rr.Marshalled(prob, sol)   # fac = NULL: outputs x, u, y (policy stays in the workspace)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(3, a.warmup)):
+        call.launch(stream)
+    torch.cuda.synchronize()
+    assert int((sol["status"] != 0).sum()) == 0, "instance failures in the bench batch"
+
+    clocks = ClockSampler(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per_launch = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(a.steps)]
+    clocks.start()
+    time.sleep(0.3)
+    barrier(ws)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for k in range(a.steps):
+        per_launch[k][0].record(stream)
+        call.launch(stream)
+        per_launch[k][1].record(stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = clocks.stop()
+    t_ms = ev0.elapsed_time(ev1)
+    t_ms = max_over_ranks(t_ms, ws)
+    ms_step = t_ms / a.steps
+    kern_ms = statistics.mean(s.elapsed_time(e) for s, e in per_launch)
+    solves = B * ws / (ms_step / 1e3)
+
+    # ---- end to end: pinned host inputs -> H2D -> kernel -> D2H of x, u, y, status ----
+    e2e = None
+    if not a.no_e2e:
+        hp = synth.empty_problem(NX, NU, HORIZON, B, device="cpu", pin_memory=True)
+        for f in synth.RRProblem.FIELDS:
+            getattr(hp, f).copy_(getattr(prob, f))
+        hs = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in sol.items()}
+        stage_p = synth.empty_problem(NX, NU, HORIZON, B, device=dev)
+        stage_s = rr.alloc_solution(stage_p)
+        hcall = rr.HostMarshalled(hp, hs, stage_p, stage_s, ws=call.ws)
+        hcall.launch(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_steps = max(1, min(a.steps, 5))
+        e0.record(stream)
+        for _ in range(e_steps):
+            hcall.launch(stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+        e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
+        assert int((hs["status"] != 0).sum()) == 0
+        e2e = {"value": B * ws / (e_ms / 1e3), "unit": "solves/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": hcall.h2d_bytes, "d2h_bytes_per_step": hcall.d2h_bytes,
+               "path": "rr_factor_solve_host (C-ABI, pinned host buffers)"}
+        del hp, hs, stage_p, stage_s, hcall
+
+    if rank != 0:
+        barrier(ws)
+        return
+    peak, peak_src = measured_peaks()
+    alg_bytes = ALG_BYTES_PER_STAGE * B * HORIZON
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": solves, "unit": "solves/s", "n_gpus": ws, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2: %d random stable regularized LQR per GPU, n_x=%d n_u=%d N=%d delta=%g, FP64"
+                               % (B, NX, NU, HORIZON, DELTA),
+                   "global_batch": B * ws, "seq_len": HORIZON, "parallelism": "batch-shard x%d" % ws,
+                   "l2": "inputs 18.7 GB/GPU > 126 MB L2 (no flush needed)"},
+        "stage_updates_per_s": solves * HORIZON,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "rr_fused_kernel<12,4,16>", "kernel_ms": kern_ms,
+                     "alg_bytes_per_stage": ALG_BYTES_PER_STAGE, "peak_source": peak_src,
+                     "fp64_alg_tflops": ALG_FLOPS_PER_STAGE * B * HORIZON / (kern_ms / 1e3) / 1e12},
+        "clocks": clk,
+        "e2e": e2e,
+        "gpu_launches": a.steps,
+    }
+    if not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(a.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    barrier(ws)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,134 @@
+/*
+ * rr.h -- C-ABI of the B200 (sm_100a) batched regularized-Riccati / regularized-IPM library
+ *         (paper_2509_16370_b200/librr_b200.so).
+ *
+ * Method: arXiv 2509.16370.  P:n = line n of the paper text.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Precision: IEEE FP64 throughout.
+ *  - Memory: every pointer in the problem / factor / solution / workspace structs is a DEVICE
+ *    pointer on the current CUDA device, allocated and owned by the caller.  The library never
+ *    allocates on a call path and keeps no global mutable state; size-query functions
+ *    give the workspace sizes.  Calls are asynchronous on the caller's stream and do not
+ *    synchronise the host.  Calls on distinct streams/devices are independent.
+ *  - Layout: one array per operand, instance-major [batch][stage][element] (terminal data
+ *    [batch][element]); matrices COLUMN-MAJOR; symmetric matrices (Q, R, Q_N, V) PACKED LOWER
+ *    in LAPACK 'L' packed order: element (r, c), r >= c, at c*(2n-c-1)/2 + r.
+ *    Every per-instance block must be 8-byte aligned (16-byte alignment enables vector copies).
+ *  - Call-level errors (return value): RR_OK, RR_E_INVALID (bad dims, null required pointer,
+ *    workspace too small), RR_E_UNSUPPORTED (shape outside the compiled kernels), RR_E_CUDA
+ *    (launch error).  rr_last_error() returns a thread-local message.
+ *  - Per-instance errors: int32 status[batch] (device), 0 = OK, else (code | stage << 8) with
+ *    code RR_ST_*.  A failed instance's x, u, y are NaN-filled; other instances are unaffected.
+ */
+#ifndef RR_B200_H
+#define RR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t rr_err;
+#define RR_OK 0
+#define RR_E_INVALID (-1)
+#define RR_E_UNSUPPORTED (-2)
+#define RR_E_CUDA (-3)
+
+/* per-instance status codes (low byte); stage index in bits 8.. */
+#define RR_ST_OK 0
+#define RR_ST_G_NOT_PD 1     /* Cholesky/elimination pivot of G_i = BᵀWB + R not > 0 */
+#define RR_ST_S_NOT_PD 2     /* pivot of S = I + δV_{i+1} not > 0; stage i       */
+#define RR_ST_NONFINITE 3    /* non-finite output without a pivot failure                 */
+#define RR_ST_NONPOS_SLACK 4 /* ipm_step: s <= 0 or z <= 0 on entry (P:53-59 needs log s)  */
+#define RR_ST_LS_FAILED 5    /* ipm_step: no Armijo point within max_backtracks           */
+
+typedef struct {
+  int32_t nx;    /* state dimension n   (1 <= nx)            */
+  int32_t nu;    /* control dimension m (1 <= nu)            */
+  int32_t N;     /* horizon (number of stages, N >= 0)       */
+  int32_t flags; /* reserved, must be 0                      */
+  int64_t batch; /* number of independent instances (>= 0)  */
+} rr_dims;
+
+/*
+ * Regularized LQR problem (§1.4): the linear system
+ *     [P  Cᵀ; C  -δI] [x; y] = -[s; c]
+ * with P = blkdiag(P_0..P_{N-1}, Q_N), P_i = [[Q_i, M_i], [M_iᵀ, R_i]] (P_i PSD, R_i PD),
+ * C the banded dynamics Jacobian with block rows -x_0 and A_i x_i + B_i u_i - x_{i+1},
+ * s = (q_0, r_0, ..., q_N), c = (c_0, ..., c_N) (N+1 blocks, reading R1), δ >= 0.
+ */
+typedef struct {
+  const double* A;     /* [batch][N][n*n]      A_i, column-major                    */
+  const double* B;     /* [batch][N][n*m]      B_i, column-major                    */
+  const double* Q;     /* [batch][N][n(n+1)/2] Q_i, packed lower                    */
+  const double* M;     /* [batch][N][n*m]      M_i, column-major                    */
+  const double* R;     /* [batch][N][m(m+1)/2] R_i, packed lower                    */
+  const double* q;     /* [batch][N][n]        q_i                                  */
+  const double* r;     /* [batch][N][m]        r_i                                  */
+  const double* c;     /* [batch][N][n]        c[i] = c_{i+1}, residual of the row producing x_{i+1} */
+  const double* QN;    /* [batch][n(n+1)/2]    Q_N, packed lower                    */
+  const double* qN;    /* [batch][n]           q_N                                  */
+  const double* c0;    /* [batch][n]           c_0 (initial-state row, Jacobian -I) */
+  const double* delta; /* [batch]              δ >= 0 (δ = 0: classic LQR)   */
+} rr_problem;
+
+/* Policy of Eq.(RR).  Any pointer may be NULL (not written). */
+typedef struct {
+  double* V; /* [batch][N+1][n(n+1)/2] V_i packed lower, V_N = Q_N */
+  double* v; /* [batch][N+1][n]        v_i, v_N = q_N               */
+  double* K; /* [batch][N][m*n]        K_i column-major (m×n)       */
+  double* k; /* [batch][N][m]          k_i                          */
+} rr_factor_buf;
+
+/* Solution: x = (x_0..x_N), u = (u_0..u_{N-1}), y = (y_0..y_N). */
+typedef struct {
+  double* x; /* [batch][N+1][n] */
+  double* u; /* [batch][N][m]   */
+  double* y; /* [batch][N+1][n] */
+} rr_solution;
+
+/* Bytes of device workspace rr_factor_solve needs for `dims` (>= 0), or -1 if unsupported. */
+int64_t rr_workspace_bytes(const rr_dims* dims);
+
+/*
+ * rr_factor_solve: the fused hot path, rows a2-a5 of DESIGN.md §1:
+ *   backward sweep i = N-1..0 of Eq.(RR):
+ *     W_i = (I+δV_{i+1})⁻¹V_{i+1}; G_i = BᵀWB + R; g_i = v_{i+1} + W(c_{i+1} - δv_{i+1});
+ *     H_i = BᵀWA + Mᵀ; h_i = r + Bᵀg; K_i = -G⁻¹H; k_i = -G⁻¹h;
+ *     V_i = AᵀWA + Q + KᵀH; v_i = q + Aᵀg + Kᵀh           (V_N = Q_N, v_N = q_N)
+ *   forward sweep: x_0 = (I+δV_0)⁻¹(c_0 - δv_0); u_i = K_i x_i + k_i;
+ *     x_{i+1} = (I+δV_{i+1})⁻¹(A_i x_i + B_i u_i + c_{i+1} - δv_{i+1});
+ *   dual recovery: y_i = V_i x_i + v_i.
+ * prob, sol, status: required.  fac: optional (NULL or any NULL member = not written).
+ * workspace: device buffer of >= rr_workspace_bytes(dims) bytes, 256-byte aligned; contents
+ * are scratch.  Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
+ */
+rr_err rr_factor_solve(const rr_dims* dims, const rr_problem* prob, const rr_factor_buf* fac,
+                       const rr_solution* sol, void* workspace, int64_t workspace_bytes,
+                       int32_t* status, void* stream);
+
+/*
+ * rr_factor_solve_host: the same computation with HOST buffers (the end-to-end path).
+ * prob_host / sol_host / status_host: host pointers (pinned memory makes the copies
+ * asynchronous); prob_dev / sol_dev / status_dev: caller-owned device staging buffers of the
+ * same shapes (rr_problem's members are written through a cast: they must be writable device
+ * memory).  Enqueues on `stream`: H2D copy of every problem operand, rr_factor_solve, D2H copy
+ * of x, u, y and status.  The caller synchronises `stream` before reading sol_host.
+ */
+rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* prob_host, const rr_solution* sol_host,
+                            int32_t* status_host, const rr_problem* prob_dev, const rr_solution* sol_dev,
+                            int32_t* status_dev, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Human-readable message of the last call-level error on this host thread. */
+const char* rr_last_error(void);
+
+/* Library version string and build target (e.g. "rr_b200 0.1 sm_100a"). */
+const char* rr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RR_B200_H */

@@ -1,0 +1,8 @@
+"""B200-native (sm_100a) batched regularized Riccati recursion and regularized-IPM step of
+arXiv 2509.16370.  All compute runs in the in-tree CUDA library librr_b200.so (include/rr.h);
+this package only marshals torch CUDA tensors into the C-ABI.  There is no CPU fallback."""
+from ._lib import RRError, LIB_PATH  # noqa: F401
+from .rr import (rr_factor_solve, alloc_solution, alloc_factor, alloc_workspace,  # noqa: F401
+                 workspace_bytes, Marshalled, HostMarshalled, version)
+
+__version__ = "0.1"

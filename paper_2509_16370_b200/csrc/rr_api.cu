@@ -1,0 +1,110 @@
+// rr_api.cu -- the C-ABI entry points declared in include/rr.h (host side: validation + launch).
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "rr.h"
+#include "rr_fused.cuh"
+
+namespace {
+thread_local char g_err[512] = "";
+
+rr_err set_err(rr_err code, const char* fmt, const char* what = "") {
+  snprintf(g_err, sizeof(g_err), fmt, what);
+  return code;
+}
+
+bool dims_ok(const rr_dims* d) {
+  return d != nullptr && d->nx >= 1 && d->nu >= 1 && d->N >= 0 && d->batch >= 0 && d->flags == 0;
+}
+}  // namespace
+
+extern "C" {
+
+const char* rr_last_error(void) { return g_err; }
+
+const char* rr_version(void) { return "rr_b200 0.1 sm_100a"; }
+
+int64_t rr_workspace_bytes(const rr_dims* dims) {
+  if (!dims_ok(dims)) return -1;
+  return rrk::fused_workspace_bytes(dims->nx, dims->nu, dims->N, dims->batch);
+}
+
+rr_err rr_factor_solve(const rr_dims* dims, const rr_problem* prob, const rr_factor_buf* fac,
+                       const rr_solution* sol, void* workspace, int64_t workspace_bytes,
+                       int32_t* status, void* stream) {
+  if (!dims_ok(dims)) return set_err(RR_E_INVALID, "rr_factor_solve: invalid dims%s");
+  if (prob == nullptr || sol == nullptr || status == nullptr)
+    return set_err(RR_E_INVALID, "rr_factor_solve: null %s", "prob/sol/status");
+  if (dims->batch == 0) return RR_OK;
+  const double* req[] = {prob->QN, prob->qN, prob->c0, prob->delta};
+  for (const double* p : req)
+    if (p == nullptr) return set_err(RR_E_INVALID, "rr_factor_solve: null %s", "terminal/initial operand");
+  if (dims->N > 0) {
+    const double* req2[] = {prob->A, prob->B, prob->Q, prob->M, prob->R, prob->q, prob->r, prob->c};
+    for (const double* p : req2)
+      if (p == nullptr) return set_err(RR_E_INVALID, "rr_factor_solve: null %s", "stage operand");
+  }
+  if (sol->x == nullptr || sol->y == nullptr || (dims->N > 0 && sol->u == nullptr))
+    return set_err(RR_E_INVALID, "rr_factor_solve: null %s", "solution pointer");
+  const int64_t need = rr_workspace_bytes(dims);
+  if (need < 0)
+    return set_err(RR_E_UNSUPPORTED, "rr_factor_solve: no kernel compiled for this (nx, nu)%s");
+  if (dims->N > 0 && (workspace == nullptr || workspace_bytes < need))
+    return set_err(RR_E_INVALID, "rr_factor_solve: workspace missing or smaller than %s",
+                   "rr_workspace_bytes()");
+  rrk::FusedArgs a;
+  a.nx = dims->nx;
+  a.nu = dims->nu;
+  a.N = dims->N;
+  a.batch = dims->batch;
+  a.p = *prob;
+  rr_factor_buf none = {nullptr, nullptr, nullptr, nullptr};
+  a.f = fac ? *fac : none;
+  a.s = *sol;
+  a.ws = static_cast<double*>(workspace);
+  a.status = status;
+  bool supported = false;
+  cudaError_t e = rrk::fused_launch(a, static_cast<cudaStream_t>(stream), &supported);
+  if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_factor_solve: unsupported shape%s");
+  if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_factor_solve: CUDA error %s", cudaGetErrorString(e));
+  return RR_OK;
+}
+
+rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* ph, const rr_solution* sh,
+                            int32_t* status_host, const rr_problem* pd, const rr_solution* sd,
+                            int32_t* status_dev, void* workspace, int64_t workspace_bytes, void* stream) {
+  if (!dims_ok(dims)) return set_err(RR_E_INVALID, "rr_factor_solve_host: invalid dims%s");
+  if (!ph || !sh || !pd || !sd || !status_host || !status_dev)
+    return set_err(RR_E_INVALID, "rr_factor_solve_host: null %s", "argument");
+  if (dims->batch == 0) return RR_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t b = dims->batch, N = dims->N, n = dims->nx, m = dims->nu;
+  const int64_t sn = n * (n + 1) / 2, sm = m * (m + 1) / 2;
+  struct Op { const double* h; const double* d; int64_t cnt; } ops[] = {
+      {ph->A, pd->A, b * N * n * n}, {ph->B, pd->B, b * N * n * m}, {ph->Q, pd->Q, b * N * sn},
+      {ph->M, pd->M, b * N * n * m}, {ph->R, pd->R, b * N * sm},    {ph->q, pd->q, b * N * n},
+      {ph->r, pd->r, b * N * m},     {ph->c, pd->c, b * N * n},     {ph->QN, pd->QN, b * sn},
+      {ph->qN, pd->qN, b * n},       {ph->c0, pd->c0, b * n},       {ph->delta, pd->delta, b}};
+  for (const Op& o : ops) {
+    if (o.cnt == 0) continue;
+    if (!o.h || !o.d) return set_err(RR_E_INVALID, "rr_factor_solve_host: null %s", "operand");
+    cudaError_t e = cudaMemcpyAsync(const_cast<double*>(o.d), o.h, sizeof(double) * o.cnt,
+                                    cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_factor_solve_host: H2D %s", cudaGetErrorString(e));
+  }
+  rr_err rc = rr_factor_solve(dims, pd, nullptr, sd, workspace, workspace_bytes, status_dev, stream);
+  if (rc != RR_OK) return rc;
+  struct Out { double* h; const double* d; int64_t cnt; } outs[] = {
+      {sh->x, sd->x, b * (N + 1) * n}, {sh->u, sd->u, b * N * m}, {sh->y, sd->y, b * (N + 1) * n}};
+  for (const Out& o : outs) {
+    if (o.cnt == 0 || o.h == nullptr) continue;
+    cudaError_t e = cudaMemcpyAsync(o.h, o.d, sizeof(double) * o.cnt, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_factor_solve_host: D2H %s", cudaGetErrorString(e));
+  }
+  cudaError_t e = cudaMemcpyAsync(status_host, status_dev, sizeof(int32_t) * b, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_factor_solve_host: D2H %s", cudaGetErrorString(e));
+  return RR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,52 @@
+// rr_common.cuh -- small device helpers shared by the B200 kernels of this library.
+// (Product code only; the CPU oracle under oracle/ shares nothing with this file.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rr.h"
+
+#define RR_FULL_MASK 0xffffffffu
+
+namespace rrk {
+
+// LAPACK 'L' packed index of (r, c) with r >= c in an n×n symmetric matrix.
+__host__ __device__ __forceinline__ int pidx(int n, int r, int c) { return c * (2 * n - c - 1) / 2 + r; }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Ampere-style asynchronous global->shared copies (SASS LDGSTS), L1-bypassing for 16 B.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Copy `cnt` doubles global->shared with the `width` lanes of a lane group (lane index j).
+__device__ __forceinline__ void copy_async(double* dst, const double* src, int cnt, int j, int width) {
+  const bool vec = (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u) == 0) &&
+                   ((cnt & 1) == 0);
+  if (vec) {
+    for (int e = 2 * j; e < cnt; e += 2 * width) cp_async16(dst + e, src + e);
+  } else {
+    for (int e = j; e < cnt; e += width) cp_async8(dst + e, src + e);
+  }
+}
+
+__device__ __forceinline__ int32_t mk_status(int code, int stage) { return code | (stage << 8); }
+
+// Status combine key: the failure met first in the backward sweep (highest stage) wins; at
+// equal stage the larger code wins (S_NOT_PD is detected before G_NOT_PD, as in the oracle).
+__device__ __forceinline__ int64_t status_key(int32_t st) {
+  return st == 0 ? -1 : ((int64_t)(st >> 8) << 8) | (st & 0xff);
+}
+
+}  // namespace rrk

@@ -1,0 +1,25 @@
+// rr_fused.cuh -- internal launch interface of the fused Riccati kernel (rr_fused.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rr.h"
+
+namespace rrk {
+
+struct FusedArgs {
+  int nx, nu, N;
+  int64_t batch;
+  rr_problem p;
+  rr_factor_buf f;
+  rr_solution s;
+  double* ws;
+  int32_t* status;
+};
+
+// Bytes of workspace for this shape (-1 if no kernel is compiled for it).
+int64_t fused_workspace_bytes(int nx, int nu, int N, int64_t batch);
+// Launch on stream s; *supported = false if no kernel covers (nx, nu).
+cudaError_t fused_launch(const FusedArgs& a, cudaStream_t s, bool* supported);
+
+}  // namespace rrk

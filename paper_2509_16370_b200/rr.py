@@ -1,0 +1,129 @@
+"""Thin Python binding of the C-ABI (include/rr.h): argument marshalling only.
+
+Tensors are torch CUDA float64 tensors in the C-ABI layout (synth.RRProblem documents it);
+every step of the method runs in librr_b200.so.  torch supplies device memory and streams."""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import torch
+
+from ._lib import RRError, check, lib, rr_dims, rr_factor_buf, rr_problem, rr_solution
+
+PROBLEM_FIELDS = ("A", "B", "Q", "M", "R", "q", "r", "c", "QN", "qN", "c0", "delta")
+
+
+def _p(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda or t.dtype != torch.float64 and t.dtype != torch.int32:
+        raise RRError("expected a CUDA float64/int32 tensor, got %s on %s" % (t.dtype, t.device))
+    if not t.is_contiguous():
+        raise RRError("tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def dims_of(prob) -> rr_dims:
+    return rr_dims(prob.nx, prob.nu, prob.N, 0, prob.batch)
+
+
+def workspace_bytes(nx: int, nu: int, N: int, batch: int) -> int:
+    d = rr_dims(nx, nu, N, 0, batch)
+    nb = lib().rr_workspace_bytes(ctypes.byref(d))
+    if nb < 0:
+        raise RRError("no kernel compiled for nx=%d nu=%d" % (nx, nu))
+    return int(nb)
+
+
+def alloc_solution(prob, device=None):
+    device = device or prob.delta.device
+    b, N, n, m = prob.batch, prob.N, prob.nx, prob.nu
+    kw = dict(dtype=torch.float64, device=device)
+    return dict(x=torch.empty(b, N + 1, n, **kw), u=torch.empty(b, N, m, **kw),
+                y=torch.empty(b, N + 1, n, **kw), status=torch.empty(b, dtype=torch.int32, device=device))
+
+
+def alloc_factor(prob, device=None):
+    device = device or prob.delta.device
+    b, N, n, m = prob.batch, prob.N, prob.nx, prob.nu
+    kw = dict(dtype=torch.float64, device=device)
+    return dict(V=torch.empty(b, N + 1, n * (n + 1) // 2, **kw), v=torch.empty(b, N + 1, n, **kw),
+                K=torch.empty(b, N, m * n, **kw), k=torch.empty(b, N, m, **kw))
+
+
+def alloc_workspace(prob, device=None) -> torch.Tensor:
+    device = device or prob.delta.device
+    nb = workspace_bytes(prob.nx, prob.nu, prob.N, prob.batch)
+    return torch.empty((nb + 7) // 8, dtype=torch.float64, device=device)
+
+
+class Marshalled:
+    """Pre-built ctypes argument structs for repeated launches on fixed buffers (bench loop)."""
+
+    def __init__(self, prob, sol, fac=None, ws=None):
+        self.prob, self.sol, self.fac = prob, sol, fac
+        self.ws = ws if ws is not None else alloc_workspace(prob)
+        self.d = dims_of(prob)
+        self.p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
+        self.f = rr_factor_buf(*[_p(fac[k]) if fac is not None else None for k in ("V", "v", "K", "k")])
+        self.s = rr_solution(_p(sol["x"]), _p(sol["u"]), _p(sol["y"]))
+        self.st = _p(sol["status"])
+        self.wsp = _p(self.ws)
+        self.wsb = self.ws.numel() * 8
+
+    def launch(self, stream: Optional[torch.cuda.Stream] = None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.prob.delta.device)
+        rc = lib().rr_factor_solve(ctypes.byref(self.d), ctypes.byref(self.p), ctypes.byref(self.f),
+                                   ctypes.byref(self.s), self.wsp, self.wsb, self.st,
+                                   ctypes.c_void_p(s.cuda_stream))
+        check(rc, "rr_factor_solve")
+
+
+def rr_factor_solve(prob, want_factor: bool = False, out=None, fac=None, workspace=None, stream=None):
+    """Fused factor + solve of every instance (rows a2-a5).  Returns dict x, u, y, status
+    (+ V, v, K, k when want_factor).  Asynchronous on `stream` (default: current stream)."""
+    if not prob.delta.is_cuda:
+        raise RRError("rr_factor_solve needs CUDA tensors (no CPU fallback)")
+    sol = out if out is not None else alloc_solution(prob)
+    if want_factor and fac is None:
+        fac = alloc_factor(prob)
+    Marshalled(prob, sol, fac, workspace).launch(stream)
+    res = dict(sol)
+    if fac is not None:
+        res.update(fac)
+    return res
+
+
+def version() -> str:
+    return lib().rr_version().decode()
+
+
+class HostMarshalled:
+    """End-to-end path through rr_factor_solve_host: problem in (pinned) host tensors, result
+    copied back to host tensors; device staging buffers are allocated once by the caller."""
+
+    def __init__(self, prob_host, sol_host, prob_dev, sol_dev, ws=None):
+        for t in (prob_host.delta, sol_host["x"]):
+            if t.is_cuda:
+                raise RRError("host buffers expected")
+        self.keep = (prob_host, sol_host, prob_dev, sol_dev)
+        self.d = dims_of(prob_host)
+        hp = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
+        self.ph = rr_problem(*[hp(getattr(prob_host, f)) for f in PROBLEM_FIELDS])
+        self.sh = rr_solution(hp(sol_host["x"]), hp(sol_host["u"]), hp(sol_host["y"]))
+        self.sth = hp(sol_host["status"])
+        self.pd = rr_problem(*[_p(getattr(prob_dev, f)) for f in PROBLEM_FIELDS])
+        self.sd = rr_solution(_p(sol_dev["x"]), _p(sol_dev["u"]), _p(sol_dev["y"]))
+        self.std = _p(sol_dev["status"])
+        self.ws = ws if ws is not None else alloc_workspace(prob_dev)
+        self.wsp, self.wsb = _p(self.ws), self.ws.numel() * 8
+        self.h2d_bytes = sum(getattr(prob_host, f).numel() * 8 for f in PROBLEM_FIELDS)
+        self.d2h_bytes = sum(sol_host[k].numel() * 8 for k in ("x", "u", "y")) + sol_host["status"].numel() * 4
+
+    def launch(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = lib().rr_factor_solve_host(ctypes.byref(self.d), ctypes.byref(self.ph), ctypes.byref(self.sh),
+                                        self.sth, ctypes.byref(self.pd), ctypes.byref(self.sd), self.std,
+                                        self.wsp, self.wsb, ctypes.c_void_p(s.cuda_stream))
+        check(rc, "rr_factor_solve_host")

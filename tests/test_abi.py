@@ -1,0 +1,47 @@
+"""CPU checks of the boundary: the C-ABI library builds, loads without a GPU, and exports every
+function include/*.h declares; the binding fails loudly without CUDA tensors (no CPU fallback)."""
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        txt = open(h).read()
+        txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+        for mm in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\*?\s*([a-z_][a-z0-9_]*)\s*\(", txt, re.M):
+            names.add(mm.group(1))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2509_16370_b200 import build
+    path = build.build()
+    lib = ctypes.CDLL(path)
+    names = declared_functions()
+    assert {"rr_factor_solve", "rr_workspace_bytes", "rr_last_error", "rr_version"} <= names
+    for nm in names:
+        assert hasattr(lib, nm), nm
+
+
+def test_workspace_query_and_version():
+    import paper_2509_16370_b200 as m
+    assert "sm_100a" in m.version()
+    assert m.workspace_bytes(12, 4, 100, 65536) > 0
+    with pytest.raises(m.RRError):
+        m.workspace_bytes(40, 30, 10, 4)   # no compiled kernel
+
+
+def test_binding_rejects_cpu_tensors():
+    import paper_2509_16370_b200 as m
+    import synth
+    p = synth.random_stable_lqr(4, 1, 3, 2, seed=0)
+    with pytest.raises(m.RRError):
+        m.rr_factor_solve(p)
