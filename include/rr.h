@@ -122,6 +122,93 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* prob_host, co
                             int32_t* status_host, const rr_problem* prob_dev, const rr_solution* sol_dev,
                             int32_t* status_dev, void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ================================ regularized IPM step (rows a1-a8) ================================
+ * One iteration of the regularized interior point method of §1.2 on the stagewise OCP of
+ * §1.1, per instance, with the Newton system solved stagewise (§1.3):
+ *   a1 condense: Σ = (S Z⁻¹ + I/η)⁻¹ (W = Z⁻¹S), r_z = g + μ Z⁻¹e,
+ *      P̃_i = P_i + G_iᵀΣG_i + η C_eᵀC_e,  s̃_i = ∇ₓℒ + G_iᵀΣ r_z + η C_eᵀ c_e,
+ *      c_0 = s_0 − x̄_0, c_{i+1} = d_i(x̄_i, ū_i) − x̄_{i+1}, δ = 1/η;
+ *   a2-a5 regularized Riccati solve of the condensed problem (Δx, Δu, Δy = LQR y; reading R8);
+ *   a6 expand: Δz = Σ(GΔ + r_z), Δλ = η(C_eΔ + c_e), Δs = −Z⁻¹SΔz + μZ⁻¹e − s;
+ *   a7 merit 𝒜 and D = ∇ₓ𝒜·Δx + ∇ₛ𝒜·Δs (Theorem);
+ *   a8 α_max = min(1, min τs/(−Δs)); largest α = α_max βᵏ (k ≤ max_backtracks) with
+ *      𝒜(x̄+αΔx, s+αΔs) ≤ 𝒜(x̄, s) + c₁ α D (reading R12); α_d = min(1, min τz/(−Δz));
+ *      update x, u, s, y, λ with α, z with α_d (in place).
+ * Trial merit values use the built-in model `model` (reading R19): IPM_MODEL_LQ (dynamics,
+ * constraints linear: trial values exact from the linearisation) or IPM_MODEL_CARTPOLE (dynamics
+ * x⁺ = cartpole(x, u; model_params = [dt, m_c, m_p, l, g]) evaluated at trial points).  Costs are
+ * quadratic with Hessian P for both, so f(x̄ + αΔ) = f̄ + α∇fᵀΔ + ½α²ΔᵀPΔ exactly.
+ */
+#define IPM_MODEL_LQ 0
+#define IPM_MODEL_CARTPOLE 1
+
+typedef struct {
+  int32_t nx, nu, N;
+  int32_t ng;    /* inequalities per stage i < N        */
+  int32_t ngN;   /* terminal inequalities (on x_N)      */
+  int32_t nc;    /* stage equalities per stage i < N    */
+  int32_t ncN;   /* terminal equalities                 */
+  int32_t model; /* IPM_MODEL_*                         */
+  int64_t batch;
+} ipm_dims;
+
+/* Problem data evaluated at the current iterate.  Device pointers. Matrices column-major,
+ * symmetric packed lower; "w" = n+m (stage i < N) — Jacobian rows are over (x_i, u_i). */
+typedef struct {
+  const double* s0;           /* [b][n]         fixed initial state                       */
+  const double* fval;         /* [b]            f(x̄) (for the merit)                             */
+  const double* gradf;        /* [b][N][w]      ∇_{x_i,u_i} f                                    */
+  const double* gradfN;       /* [b][n]         ∇_{x_N} f                                        */
+  const double *Q, *M, *R;    /* [b][N][sym n], [b][N][n*m], [b][N][sym m]: P_i (PD approx) */
+  const double* QN;           /* [b][sym n]                                                       */
+  const double *A, *B;        /* [b][N][n*n], [b][N][n*m]: ∂d_i/∂x, ∂d_i/∂u at the iterate      */
+  const double* dres;         /* [b][N][n]      d_i(x̄_i, ū_i) − x̄_{i+1}                          */
+  const double *ce, *Ce;      /* [b][N][nc], [b][N][nc*w]   stage equalities c_i = 0 and Jacobian */
+  const double *ceN, *CeN;    /* [b][ncN], [b][ncN*n]                                             */
+  const double *gv, *Gj;      /* [b][N][ng], [b][N][ng*w]   stage inequalities g_i ≤ 0, Jacobian  */
+  const double *gvN, *GjN;    /* [b][ngN], [b][ngN*n]                                             */
+  const double* model_params; /* [8] shared by the batch (cart-pole: dt, m_c, m_p, l, g)         */
+} ipm_stage_data;
+
+/* Iterate (updated in place on success). */
+typedef struct {
+  double *x, *u;        /* [b][N+1][n], [b][N][m]                           */
+  double *s, *z;        /* [b][N][ng] slacks / inequality duals (> 0)       */
+  double *sN, *zN;      /* [b][ngN]                                         */
+  double* y;            /* [b][N+1][n] initial-state + dynamics multipliers */
+  double *lam, *lamN;   /* [b][N][nc], [b][ncN] stage-equality multipliers  */
+  const double *mu, *eta; /* [b] barrier and penalty parameters (δ = 1/η)   */
+} ipm_iterate;
+
+typedef struct {
+  double tau;      /* fraction to boundary, e.g. 0.995 */
+  double armijo_c; /* c₁, e.g. 1e-4                    */
+  double beta;     /* backtracking factor, e.g. 0.5    */
+  int32_t max_backtracks; /* e.g. 50                   */
+  int32_t pad;
+} ipm_params;
+
+/* Outputs (device).  Direction arrays have the iterate's shapes. */
+typedef struct {
+  double *dx, *du, *ds, *dsN, *dy, *dlam, *dlamN, *dz, *dzN;
+  double* alpha_p;       /* [b] accepted primal step (0 on failure)   */
+  double* alpha_d;       /* [b] dual step for z                        */
+  double* D;             /* [b] directional derivative ∇𝒜·(Δx, Δs)    */
+  double* merit0;        /* [b] 𝒜 at the iterate                       */
+  double* merit_acc;     /* [b] 𝒜 at the accepted point               */
+  int32_t* n_backtracks; /* [b] k of the accepted α = α_max βᵏ         */
+} ipm_result;
+
+/* Bytes of device workspace ipm_step needs (-1 if no kernel covers the dims). */
+int64_t ipm_workspace_bytes(const ipm_dims* dims);
+
+/* One batched regularized-IPM step (rows a1-a8).  status: [b] (RR_ST_NONPOS_SLACK: s or z not > 0
+ * on entry -> iterate untouched, direction NaN; RR_ST_LS_FAILED: no Armijo point -> iterate
+ * untouched, alpha_p = 0; pivot failures as in rr_factor_solve). */
+rr_err ipm_step(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it,
+                const ipm_params* params, const ipm_result* res, void* workspace, int64_t workspace_bytes,
+                int32_t* status, void* stream);
+
 /* Human-readable message of the last call-level error on this host thread. */
 const char* rr_last_error(void);
 

@@ -286,7 +286,24 @@ static int32_t ipm_step_one(const orc_ipm_args* a, int64_t b) {
   for (int i = 0; i <= N; ++i) {
     stg_t S = stage(&I, i);
     for (int e = 0; e < S.ng; ++e)
-      if (!(S.s[e] > 0.0) || !(S.z[e] > 0.0)) return OIPM_NONPOS_SLACK | (i << 8);
+      if (!(S.s[e] > 0.0) || !(S.z[e] > 0.0)) {
+        /* iterate untouched; direction NaN; steps 0; merit and D NaN */
+        for (int64_t k = 0; k < (int64_t)(N + 1) * n; ++k) { I.dx[k] = NAN; I.dy[k] = NAN; }
+        for (int64_t k = 0; k < (int64_t)N * m; ++k) I.du[k] = NAN;
+        for (int q = 0; q <= N; ++q) {
+          stg_t T = stage(&I, q);
+          for (int f = 0; f < T.ng; ++f) { T.ds[f] = NAN; T.dz[f] = NAN; }
+          for (int f = 0; f < T.nc; ++f) T.dlam[f] = NAN;
+        }
+        if (a->alpha_p) a->alpha_p[b] = 0.0;
+        if (a->alpha_d) a->alpha_d[b] = 0.0;
+        if (a->D) a->D[b] = NAN;
+        if (a->D_closed) a->D_closed[b] = NAN;
+        if (a->merit0) a->merit0[b] = NAN;
+        if (a->merit_acc) a->merit_acc[b] = NAN;
+        if (a->n_backtracks) a->n_backtracks[b] = 0;
+        return OIPM_NONPOS_SLACK | (i << 8);
+      }
   }
   /* ---- condense into a regularized LQR problem ---- */
   const int64_t sn = symn(n), sm = symn(m);

@@ -5,4 +5,6 @@ from ._lib import RRError, LIB_PATH  # noqa: F401
 from .rr import (rr_factor_solve, alloc_solution, alloc_factor, alloc_workspace,  # noqa: F401
                  workspace_bytes, Marshalled, HostMarshalled, version)
 
+from .ipm import ipm_step, IpmCall  # noqa: F401,E402
+
 __version__ = "0.1"

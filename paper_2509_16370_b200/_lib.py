@@ -33,6 +33,35 @@ class rr_solution(ctypes.Structure):
     _fields_ = [(f, ctypes.c_void_p) for f in ("x", "u", "y")]
 
 
+class ipm_dims(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int32) for f in ("nx", "nu", "N", "ng", "ngN", "nc", "ncN", "model")] + \
+               [("batch", ctypes.c_int64)]
+
+
+IPM_DATA_FIELDS = ("s0", "fval", "gradf", "gradfN", "Q", "M", "R", "QN", "A", "B", "dres",
+                   "ce", "Ce", "ceN", "CeN", "gv", "Gj", "gvN", "GjN", "model_params")
+IPM_ITER_FIELDS = ("x", "u", "s", "z", "sN", "zN", "y", "lam", "lamN", "mu", "eta")
+IPM_RES_FIELDS = ("dx", "du", "ds", "dsN", "dy", "dlam", "dlamN", "dz", "dzN",
+                  "alpha_p", "alpha_d", "D", "merit0", "merit_acc", "n_backtracks")
+
+
+class ipm_stage_data(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in IPM_DATA_FIELDS]
+
+
+class ipm_iterate(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in IPM_ITER_FIELDS]
+
+
+class ipm_params(ctypes.Structure):
+    _fields_ = [("tau", ctypes.c_double), ("armijo_c", ctypes.c_double), ("beta", ctypes.c_double),
+                ("max_backtracks", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class ipm_result(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in IPM_RES_FIELDS]
+
+
 def lib():
     """The loaded library (raises RRError if librr_b200.so is absent)."""
     global _lib
@@ -55,6 +84,13 @@ def lib():
                                                ctypes.POINTER(rr_solution), ctypes.c_void_p,
                                                ctypes.POINTER(rr_problem), ctypes.POINTER(rr_solution),
                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+            L.ipm_workspace_bytes.restype = ctypes.c_int64
+            L.ipm_workspace_bytes.argtypes = [ctypes.POINTER(ipm_dims)]
+            L.ipm_step.restype = ctypes.c_int32
+            L.ipm_step.argtypes = [ctypes.POINTER(ipm_dims), ctypes.POINTER(ipm_stage_data),
+                                   ctypes.POINTER(ipm_iterate), ctypes.POINTER(ipm_params),
+                                   ctypes.POINTER(ipm_result), ctypes.c_void_p, ctypes.c_int64,
+                                   ctypes.c_void_p, ctypes.c_void_p]
             _lib = L
     return _lib
 

@@ -1,0 +1,622 @@
+// ipm.cu -- fused batched regularized-IPM step (rows a1-a8), one lane group per instance (sm_100a).
+//
+// Method (arXiv 2509.16370, P:n = PAPER.md line n), per instance (see include/rr.h, ipm_step):
+//   pass 1 (backward): per stage, condense the inequality duals (Σ = (S/Z + I/η)⁻¹,
+//     r_z = g + μ/z) and stage-equality duals (η C_eᵀC_e) into the stage's LQR blocks, then one
+//     backward step of Eq.(RR) with δ = 1/η (rr_stage.cuh);
+//   pass 2 (forward): Δx_{i+1} = Φ Δx_i + φ, Δu, Δy, expand Δz, Δλ, Δs
+//     (P:224-227), accumulate D = ∇𝒜·(Δx, Δs), the merit at the
+//     iterate and the coefficients of its polynomial part in α, α_max, α_d;
+//   pass 3: Armijo backtracking on 𝒜 (reading R12); trial points of the built-in model;
+//   pass 4: in-place iterate update.
+// Lane roles: lane j < NZ owns column j of the stage matrices (as in rr_stage.cuh); lane e < NG
+// owns inequality e, lane e < NC owns stage equality e for the expansion; the line-search pass
+// distributes stages over lanes.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ipm.cuh"
+#include "rr_common.cuh"
+#include "rr_stage.cuh"
+
+namespace rrk {
+
+template <int NX, int NU, int NG, int NC>
+struct IpmBuf {  // padded per-stage IPM data in shared memory (doubles, even offsets)
+  static constexpr int NZ = NX + NU;
+  static constexpr int E2 = 2;
+  static constexpr int F = 0;                         // [A B] col-major NX × NZ
+  static constexpr int P = F + NX * NZ;               // P full NZ × NZ col-major
+  static constexpr int gf = P + NZ * NZ;              // ∇f (NZ)
+  static constexpr int cv = gf + ((NZ + 1) & ~1);     // dres (NX)
+  static constexpr int G = cv + NX;                   // G col-major NG × NZ
+  static constexpr int gv = G + ((NG * NZ + 1) & ~1); // g (NG)
+  static constexpr int s = gv + ((NG + 1) & ~1);
+  static constexpr int z = s + ((NG + 1) & ~1);
+  static constexpr int sig = z + ((NG + 1) & ~1);     // Σ_e
+  static constexpr int rz = sig + ((NG + 1) & ~1);    // r_z,e
+  static constexpr int Ce = rz + ((NG + 1) & ~1);     // C_e col-major NC × NZ
+  static constexpr int ce = Ce + ((NC * NZ + 1) & ~1);
+  static constexpr int lam = ce + ((NC + 1) & ~1);
+  static constexpr int yi = lam + ((NC + 1) & ~1);    // y_i
+  static constexpr int yn = yi + NX;                  // y_{i+1}
+  static constexpr int xb = yn + NX;                  // x̄_i
+  static constexpr int ub = xb + NX;                  // ū_i
+  static constexpr int du = ub + ((NU + 1) & ~1);     // Δu_i exchange
+  static constexpr int SIZE = du + ((NU + 1) & ~1);
+  static constexpr int PAD = (SIZE + 1) & ~1;
+};
+
+// cart-pole, explicit Euler (C4); θ from the hanging position, φ = θ − π.
+__device__ __forceinline__ void cartpole_step(const double* prm, const double* x, double u, double* xn) {
+  const double dt = prm[0], mc = prm[1], mp = prm[2], l = prm[3], g = prm[4];
+  const double phi = x[1] - 3.14159265358979323846;
+  double sp, cp;
+  sincos(phi, &sp, &cp);
+  const double thd = x[3];
+  const double mt = mc + mp;
+  const double tmp = (u + mp * l * thd * thd * sp) / mt;
+  const double thdd = (g * sp - cp * tmp) / (l * (4.0 / 3.0 - mp * cp * cp / mt));
+  const double pdd = tmp - mp * l * thdd * cp / mt;
+  xn[0] = x[0] + dt * x[2];
+  xn[1] = x[1] + dt * x[3];
+  xn[2] = x[2] + dt * pdd;
+  xn[3] = x[3] + dt * thdd;
+}
+
+template <int NX, int NU, int NG, int NC, int LG, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
+  using ST = Stage<NX, NU, LG>;
+  using WK = Work<NX, NU>;
+  using RC = Rec<NX, NU>;
+  using IB = IpmBuf<NX, NU, NG, NC>;
+  constexpr int NZ = NX + NU;
+  constexpr int IPW = 32 / LG;
+  constexpr int SLOT = ((IB::PAD + WK::PAD + 2 * RC::PAD + NX + 1) & ~1);
+  static_assert(NG <= LG && NC <= LG, "constraint count per stage exceeds the lane group");
+
+  const int n = a.d.nx, m = a.d.nu, N = a.d.N, w = n + m;
+  const int sn = n * (n + 1) / 2, sm = m * (m + 1) / 2;
+
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / LG, j = lane % LG, gbase = grp * LG;
+  double* slot = smem + (warp * IPW + grp) * SLOT;
+  double* sb = slot;              // IPM stage data (padded)
+  double* wk = slot + IB::PAD;    // Riccati work area
+  double* rbuf = wk + WK::PAD;    // one forward record
+  double* xs = rbuf + 2 * RC::PAD;
+
+  int64_t inst = ((int64_t)blockIdx.x * WARPS + warp) * IPW + grp;
+  const bool valid = inst < a.d.batch;
+  if (!valid) inst = a.d.batch - 1;
+  const int64_t sN = N;
+  const double mu = a.it.mu[inst], eta = a.it.eta[inst];
+  const double delta = 1.0 / eta;  // P:387-394 (reading R15)
+  double* rec0 = a.ws + inst * sN * RC::PAD;
+  int32_t st = 0;
+  int nonpos_stage = 0x7fffffff;
+
+  // ---- load stage i (i == N: terminal) of the IPM data into the padded shared layout ----
+  auto load_stage = [&](int i) {
+    const bool term = (i == N);
+    const int ww = term ? n : w;
+    const int ng = term ? a.d.ngN : a.d.ng;
+    const int nc = term ? a.d.ncN : a.d.nc;
+    const int64_t si = inst * sN + i;
+    for (int e = j; e < NX * NZ; e += LG) {  // F
+      const int k = e % NX, c = e / NX;
+      double v = 0.0;
+      if (!term && k < n) {
+        if (c < NX) v = (c < n) ? a.d_.A[si * n * n + k + c * n] : 0.0;
+        else if (c - NX < m) v = a.d_.B[si * n * m + k + (c - NX) * n];
+      }
+      sb[IB::F + e] = v;
+    }
+    for (int e = j; e < NZ * NZ; e += LG) {  // P (padded u-diagonal = 1)
+      const int r = e % NZ, c = e / NZ;
+      double v = 0.0;
+      const bool rx = r < NX, cx = c < NX;
+      const int rr = rx ? r : r - NX, cc = cx ? c : c - NX;
+      if (term) {
+        if (rx && cx && r < n && c < n) v = a.d_.QN[inst * sn + (r >= c ? pidx(n, r, c) : pidx(n, c, r))];
+        else if (!rx && !cx && rr == cc) v = 1.0;
+      } else {
+        if (rx && cx) {
+          if (r < n && c < n) v = a.d_.Q[si * sn + (r >= c ? pidx(n, r, c) : pidx(n, c, r))];
+        } else if (rx && !cx) {
+          if (r < n && cc < m) v = a.d_.M[si * n * m + r + cc * n];
+        } else if (!rx && cx) {
+          if (c < n && rr < m) v = a.d_.M[si * n * m + c + rr * n];
+        } else {
+          if (rr < m && cc < m) v = a.d_.R[si * sm + (rr >= cc ? pidx(m, rr, cc) : pidx(m, cc, rr))];
+          else if (rr == cc) v = 1.0;
+        }
+      }
+      sb[IB::P + e] = v;
+    }
+    for (int e = j; e < NZ; e += LG) {  // ∇f in the padded (x | u) layout
+      double v = 0.0;
+      if (e < NX) {
+        if (e < n) v = term ? a.d_.gradfN[inst * n + e] : a.d_.gradf[si * w + e];
+      } else if (!term && e - NX < m) {
+        v = a.d_.gradf[si * w + n + (e - NX)];
+      }
+      sb[IB::gf + e] = v;
+    }
+    for (int e = j; e < NX; e += LG) {
+      sb[IB::cv + e] = (!term && e < n) ? a.d_.dres[si * n + e] : 0.0;
+      sb[IB::yi + e] = (e < n) ? a.it.y[(inst * (sN + 1) + i) * n + e] : 0.0;
+      sb[IB::yn + e] = (!term && e < n) ? a.it.y[(inst * (sN + 1) + i + 1) * n + e] : 0.0;
+      sb[IB::xb + e] = (e < n) ? a.it.x[(inst * (sN + 1) + i) * n + e] : 0.0;
+    }
+    for (int e = j; e < NU; e += LG) sb[IB::ub + e] = (!term && e < m) ? a.it.u[si * m + e] : 0.0;
+    // inequalities: G rows over the padded (x | u) columns
+    const double* Gsrc = term ? a.d_.GjN + inst * (int64_t)ng * n : a.d_.Gj + si * (int64_t)ng * ww;
+    for (int e = j; e < NG * NZ; e += LG) {
+      const int q = e % NG, c = e / NG;
+      double v = 0.0;
+      if (q < ng) {
+        if (c < NX) { if (c < n) v = Gsrc[q + (int64_t)c * ng]; }
+        else if (!term && c - NX < m) v = Gsrc[q + (int64_t)(n + c - NX) * ng];
+      }
+      sb[IB::G + e] = v;
+    }
+    for (int e = j; e < NG; e += LG) {
+      double gvv = 0.0, sv = 1.0, zv = 1.0;
+      if (e < ng) {
+        gvv = term ? a.d_.gvN[inst * ng + e] : a.d_.gv[si * ng + e];
+        sv = term ? a.it.sN[inst * ng + e] : a.it.s[si * ng + e];
+        zv = term ? a.it.zN[inst * ng + e] : a.it.z[si * ng + e];
+        if (!(sv > 0.0) || !(zv > 0.0)) nonpos_stage = min(nonpos_stage, i);
+      }
+      sb[IB::gv + e] = gvv;
+      sb[IB::s + e] = sv;
+      sb[IB::z + e] = zv;
+      // Σ = (s/z + 1/η)⁻¹ and r_z = g + μ/z; padded rows: G row is zero
+      sb[IB::sig + e] = (e < ng) ? 1.0 / (sv / zv + 1.0 / eta) : 0.0;
+      sb[IB::rz + e] = (e < ng) ? gvv + mu / zv : 0.0;
+    }
+    const double* Csrc = term ? a.d_.CeN + inst * (int64_t)nc * n : a.d_.Ce + si * (int64_t)nc * ww;
+    for (int e = j; e < NC * NZ; e += LG) {
+      const int q = e % NC, c = e / NC;
+      double v = 0.0;
+      if (q < nc) {
+        if (c < NX) { if (c < n) v = Csrc[q + (int64_t)c * nc]; }
+        else if (!term && c - NX < m) v = Csrc[q + (int64_t)(n + c - NX) * nc];
+      }
+      sb[IB::Ce + e] = v;
+    }
+    for (int e = j; e < NC; e += LG) {
+      double cev = 0.0, lv = 0.0;
+      if (e < nc) {
+        cev = term ? a.d_.ceN[inst * nc + e] : a.d_.ce[si * nc + e];
+        lv = term ? a.it.lamN[inst * nc + e] : a.it.lam[si * nc + e];
+      }
+      sb[IB::ce + e] = cev;
+      sb[IB::lam + e] = lv;
+    }
+    __syncwarp();
+  };
+
+  // condensed P̃ column j: P + GᵀΣG + η C_eᵀC_e
+  auto Pt = [&](int s) -> double {
+    if (j >= NZ) return 0.0;
+    double v = sb[IB::P + j * NZ + s];
+#pragma unroll
+    for (int e = 0; e < NG; ++e) v = fma(sb[IB::G + e + s * NG] * sb[IB::sig + e], sb[IB::G + e + j * NG], v);
+#pragma unroll
+    for (int e = 0; e < NC; ++e) v = fma(eta * sb[IB::Ce + e + s * NC], sb[IB::Ce + e + j * NC], v);
+    return v;
+  };
+  // condensed gradient s̃_j = ∇ₓℒ + GᵀΣ r_z + η C_eᵀ c_e, ∇ₓℒ = ∇f + Cᵀy + Gᵀz + C_eᵀλ
+  auto qt = [&]() -> double {
+    if (j >= NZ) return 0.0;
+    double v = sb[IB::gf + j];
+    if (j < NX) v -= sb[IB::yi + j];
+#pragma unroll
+    for (int r = 0; r < NX; ++r) v = fma(sb[IB::F + r + j * NX], sb[IB::yn + r], v);
+#pragma unroll
+    for (int e = 0; e < NG; ++e)
+      v = fma(sb[IB::G + e + j * NG], sb[IB::z + e] + sb[IB::sig + e] * sb[IB::rz + e], v);
+#pragma unroll
+    for (int e = 0; e < NC; ++e) v = fma(sb[IB::Ce + e + j * NC], sb[IB::lam + e] + eta * sb[IB::ce + e], v);
+    return v;
+  };
+
+  // ================= pass 1: backward (condense + Eq.(RR)) =================
+  double Vc[NX];
+  load_stage(N);
+  {
+    // terminal: V_N = Q̃_N (condensed), v_N = q̃_N
+#pragma unroll
+    for (int r = 0; r < NX; ++r) Vc[r] = (j < NX) ? Pt(r) : 0.0;
+    const double qj = qt();
+    __syncwarp();
+    if (j < NX) wk[WK::vs + j] = qj;
+    __syncwarp();
+  }
+  for (int i = N - 1; i >= 0; --i) {
+    load_stage(i);
+    auto Pcol = [&](int s) -> double { return Pt(s); };
+    const double qj = qt();
+    double U[NZ], b[NZ];
+    ST::backward(sb + IB::F, sb + IB::cv, Pcol, qj, delta, j, wk, Vc, U, b, rec0 + (int64_t)i * RC::PAD, i, st);
+  }
+
+  // ================= pass 2: forward + expand + merit/D accumulation =================
+  // Δx_0 = (I + δV_0)⁻¹(c_0 − δ v_0), c_0 = s_0 − x̄_0
+  ST::invS(Vc, delta, j, wk, 0, st);
+  double xr[NX];
+  double c0v[NX];
+#pragma unroll
+  for (int r = 0; r < NX; ++r) {
+    c0v[r] = (r < n) ? (a.d_.s0[inst * n + r] - a.it.x[inst * (sN + 1) * n + r]) : 0.0;
+    xr[r] = c0v[r] - delta * wk[WK::vs + r];
+  }
+  ST::mulSinv(xr, wk);
+  __syncwarp();
+  // per-lane partial sums
+  double sD = 0.0, sK0 = 0.0, sK1 = 0.0, sK2 = 0.0, sLog = 0.0;
+  double amax = 1.0, admax = 1.0;
+  const double tau = a.prm.tau;
+  const int model = a.d.model;
+  bool bad = false;
+  // row 0 (initial state): c_0(α) = c_0 − αΔx_0 (linear for every model)
+  if (j < n) {
+    double x0 = 0.0, c0 = 0.0;
+#pragma unroll
+    for (int r = 0; r < NX; ++r) {
+      x0 = (r == j) ? xr[r] : x0;
+      c0 = (r == j) ? c0v[r] : c0;
+    }
+    const double y0 = a.it.y[inst * (sN + 1) * n + j];
+    const double cd = -x0;
+    sD += (y0 + eta * c0) * cd;
+    sK0 += y0 * c0 + 0.5 * eta * c0 * c0;
+    sK1 += y0 * cd + eta * c0 * cd;
+    sK2 += 0.5 * eta * cd * cd;
+    if (valid) a.r.dx[inst * (sN + 1) * n + j] = x0;
+  }
+  const int ui = j - NX;
+  auto expand_stage = [&](int i, const double (&dz_full)[NZ]) {
+    // inequality e on lane e; equality e on lane e
+    const bool term = (i == N);
+    const int ng = term ? a.d.ngN : a.d.ng;
+    const int nc = term ? a.d.ncN : a.d.nc;
+    const int64_t si = inst * sN + i;
+    if (j < ng) {
+      double gd = 0.0;
+#pragma unroll
+      for (int c = 0; c < NZ; ++c) gd = fma(sb[IB::G + j + c * NG], dz_full[c], gd);
+      const double s = sb[IB::s + j], z = sb[IB::z + j], g = sb[IB::gv + j];
+      const double dzv = sb[IB::sig + j] * (gd + sb[IB::rz + j]);
+      const double dsv = -(s / z) * dzv + mu / z - s;
+      if (dsv < 0.0) amax = fmin(amax, tau * s / (-dsv));
+      if (dzv < 0.0) admax = fmin(admax, tau * z / (-dzv));
+      const double gs = g + s, bq = gd + dsv;
+      sD += (z + eta * gs) * bq + (-mu / s) * dsv;
+      sK0 += z * gs + 0.5 * eta * gs * gs;
+      sK1 += z * bq + eta * gs * bq;
+      sK2 += 0.5 * eta * bq * bq;
+      sLog += log(s);
+      if (valid) {
+        if (term) {
+          a.r.dsN[inst * ng + j] = dsv;
+          a.r.dzN[inst * ng + j] = dzv;
+        } else {
+          a.r.ds[si * ng + j] = dsv;
+          a.r.dz[si * ng + j] = dzv;
+        }
+      }
+      bad |= !isfinite(dsv) || !isfinite(dzv);
+    }
+    if (j < nc) {
+      double cd = 0.0;
+#pragma unroll
+      for (int c = 0; c < NZ; ++c) cd = fma(sb[IB::Ce + j + c * NC], dz_full[c], cd);
+      const double ce = sb[IB::ce + j], lam = sb[IB::lam + j];
+      const double dl = eta * (cd + ce);
+      sD += (lam + eta * ce) * cd;
+      sK0 += lam * ce + 0.5 * eta * ce * ce;
+      sK1 += lam * cd + eta * ce * cd;
+      sK2 += 0.5 * eta * cd * cd;
+      if (valid) {
+        if (term) a.r.dlamN[inst * nc + j] = dl;
+        else a.r.dlam[si * nc + j] = dl;
+      }
+      bad |= !isfinite(dl);
+    }
+    // cost: ∇fᵀΔ and ½ΔᵀPΔ (lane j < NZ owns entry j)
+    if (j < NZ) {
+      double pd = 0.0;
+#pragma unroll
+      for (int c = 0; c < NZ; ++c) pd = fma(sb[IB::P + j * NZ + c], dz_full[c], pd);
+      double dj = 0.0;
+#pragma unroll
+      for (int c = 0; c < NZ; ++c) dj = (c == j) ? dz_full[c] : dj;
+      const double gd = sb[IB::gf + j] * dj;
+      sD += gd;
+      sK1 += gd;
+      sK2 += 0.5 * dj * pd;
+    }
+  };
+
+  for (int i = 0; i < N; ++i) {
+    load_stage(i);
+    // record i -> shared
+    {
+      const double* rg = rec0 + (int64_t)i * RC::PAD;
+      for (int e = j; e < RC::SIZE; e += LG) rbuf[e] = rg[e];
+      __syncwarp();
+    }
+    const double* rc = rbuf;
+    double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
+    if (j < NX) {
+      a0 = rc[RC::phi + j];
+      c0 = rc[RC::v + j];
+#pragma unroll
+      for (int k = 0; k < NX; ++k) {
+        a0 = fma(rc[RC::PHI + k * NX + j], xr[k], a0);
+        const int ik = k >= j ? pidx(NX, k, j) : pidx(NX, j, k);
+        c1 = fma(rc[RC::V + ik], xr[k], c1);
+      }
+    } else if (ui < NU) {
+      a0 = rc[RC::k + ui];
+#pragma unroll
+      for (int k = 0; k < NX; ++k) a1 = fma(rc[RC::K + k * NU + ui], xr[k], a1);
+    }
+    const double acc1 = a0 + a1, acc2 = c0 + c1;  // x_{i+1}[j] | u_i[ui];  y_i[j]
+    if (j < NX) xs[j] = acc1;
+    if (ui >= 0 && ui < NU) sb[IB::du + ui] = acc1;
+    __syncwarp();
+    double dz_full[NZ];
+#pragma unroll
+    for (int c = 0; c < NX; ++c) dz_full[c] = xr[c];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) dz_full[NX + u] = sb[IB::du + u];
+    double xn[NX];
+    ST::bcast(xs, xn);
+    if (valid) {
+      if (j < n) {
+        a.r.dy[(inst * (sN + 1) + i) * n + j] = acc2;
+        a.r.dx[(inst * (sN + 1) + i + 1) * n + j] = acc1;
+      }
+      if (ui >= 0 && ui < m) a.r.du[(inst * sN + i) * m + ui] = acc1;
+    }
+    bad |= ((j < n) && !(isfinite(acc1) && isfinite(acc2))) || ((ui >= 0 && ui < m) && !isfinite(acc1));
+    expand_stage(i, dz_full);
+    // dynamics row i+1: (CΔ)_r = (FΔ)_r − Δx_{i+1,r};  c_{i+1} at the iterate
+    if (j < n) {
+      double fd = 0.0;
+#pragma unroll
+      for (int c = 0; c < NZ; ++c) fd = fma(sb[IB::F + j + c * NX], dz_full[c], fd);
+      double xnj = 0.0;
+#pragma unroll
+      for (int r = 0; r < NX; ++r) xnj = (r == j) ? xn[r] : xnj;
+      const double cd = fd - xnj;
+      const double yn = sb[IB::yn + j];
+      const double dres = sb[IB::cv + j];
+      sD += (yn + eta * dres) * cd;
+      if (model == IPM_MODEL_LQ) {
+        sK0 += yn * dres + 0.5 * eta * dres * dres;
+        sK1 += yn * cd + eta * dres * cd;
+        sK2 += 0.5 * eta * cd * cd;
+      }
+    }
+    if (model == IPM_MODEL_CARTPOLE && j == 0) {
+      // dynamics terms at α = 0 through the model (as the oracle's merit does)
+      double xnm[4];
+      const double* prm = a.d_.model_params;
+      cartpole_step(prm, sb + IB::xb, sb[IB::ub], xnm);
+      const double* xb1 = a.it.x + (inst * (sN + 1) + i + 1) * n;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double cr = xnm[r] - xb1[r];
+        sK0 += sb[IB::yn + r] * cr + 0.5 * eta * cr * cr;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NX; ++r) xr[r] = xn[r];
+    __syncwarp();
+  }
+  // terminal stage: y_N = Ṽ_N x_N + ṽ_N with the condensed terminal blocks; expansions on x_N
+  load_stage(N);
+  {
+    double dz_full[NZ];
+#pragma unroll
+    for (int c = 0; c < NZ; ++c) dz_full[c] = (c < NX) ? xr[c] : 0.0;
+    // ṽ_N, Ṽ_N recomputed from the condensed terminal data
+    const double qj = qt();
+    double yj = qj;
+#pragma unroll
+    for (int r = 0; r < NX; ++r) yj = fma(Pt(r), xr[r], yj);  // Ṽ_N symmetric: row j = column j
+    if (valid && j < n) a.r.dy[(inst * (sN + 1) + N) * n + j] = yj;
+    bad |= (j < n) && !isfinite(yj);
+    expand_stage(N, dz_full);
+  }
+  // ---- reduce the partial sums over the lane group ----
+  auto gsum = [&](double v) {
+#pragma unroll
+    for (int off = LG / 2; off > 0; off >>= 1) v += __shfl_xor_sync(RR_FULL_MASK, v, off);
+    return v;
+  };
+  auto gmin = [&](double v) {
+#pragma unroll
+    for (int off = LG / 2; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(RR_FULL_MASK, v, off));
+    return v;
+  };
+  const double D = gsum(sD);
+  const double K0 = gsum(sK0) + a.d_.fval[inst];
+  const double K1 = gsum(sK1), K2 = gsum(sK2);
+  const double A0 = K0 - mu * gsum(sLog);
+  amax = gmin(amax);
+  admax = gmin(admax);
+  int32_t status = st;
+  int np = nonpos_stage;
+#pragma unroll
+  for (int off = LG / 2; off > 0; off >>= 1) {
+    status = max(status, __shfl_xor_sync(RR_FULL_MASK, status, off));
+    np = min(np, __shfl_xor_sync(RR_FULL_MASK, np, off));
+  }
+  const unsigned gmask = (LG == 32) ? 0xffffffffu : (((1u << LG) - 1u) << gbase);
+  if (status == 0 && (__ballot_sync(RR_FULL_MASK, bad) & gmask)) status = RR_ST_NONFINITE;
+  if (np != 0x7fffffff) status = mk_status(RR_ST_NONPOS_SLACK, np);
+
+  // ================= pass 3: Armijo backtracking over (x, s) with 𝒜 =================
+  double alpha = amax, Aacc = __longlong_as_double(0x7ff8000000000000LL);
+  int nb = 0;
+  bool accepted = false;
+  if (status == 0) {
+    for (nb = 0; nb <= a.prm.max_backtracks; ++nb) {
+      double sl = 0.0, sdyn = 0.0;
+      bool pos = true;
+      for (int i = j; i <= N; i += LG) {  // stages distributed over the lanes
+        const bool term = (i == N);
+        const int ng = term ? a.d.ngN : a.d.ng;
+        const double* sp = term ? a.it.sN + inst * ng : a.it.s + (inst * sN + i) * ng;
+        const double* dsp = term ? a.r.dsN + inst * ng : a.r.ds + (inst * sN + i) * ng;
+        for (int e = 0; e < ng; ++e) {
+          const double sa = sp[e] + alpha * dsp[e];
+          pos &= sa > 0.0;
+          sl += log(sa);
+        }
+        if (model == IPM_MODEL_CARTPOLE && !term) {
+          double xa[4], xnm[4];
+          const double* xb = a.it.x + (inst * (sN + 1) + i) * n;
+          const double* dxb = a.r.dx + (inst * (sN + 1) + i) * n;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) xa[r] = xb[r] + alpha * dxb[r];
+          const double ua = a.it.u[inst * sN + i] + alpha * a.r.du[inst * sN + i];
+          cartpole_step(a.d_.model_params, xa, ua, xnm);
+          const double* yb = a.it.y + (inst * (sN + 1) + i + 1) * n;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const double cr = xnm[r] - (xb[n + r] + alpha * dxb[n + r]);
+            sdyn += yb[r] * cr + 0.5 * eta * cr * cr;
+          }
+        }
+      }
+      sl = gsum(sl);
+      sdyn = gsum(sdyn);
+      const bool allpos = __all_sync(RR_FULL_MASK, pos);
+      const double At = K0 + alpha * (K1 + alpha * K2) - mu * sl + sdyn;
+      if (allpos && At <= A0 + a.prm.armijo_c * alpha * D) {
+        Aacc = At;
+        accepted = true;
+        break;
+      }
+      alpha *= a.prm.beta;
+    }
+    if (!accepted) {
+      status = RR_ST_LS_FAILED;
+      alpha = 0.0;
+      nb = a.prm.max_backtracks + 1;
+    }
+  }
+
+  // ================= pass 4: update the iterate in place =================
+  if (valid && accepted) {
+    const int64_t nx1 = (sN + 1) * n;
+    for (int64_t e = j; e < nx1; e += LG) {
+      a.it.x[inst * nx1 + e] += alpha * a.r.dx[inst * nx1 + e];
+      a.it.y[inst * nx1 + e] += alpha * a.r.dy[inst * nx1 + e];
+    }
+    for (int64_t e = j; e < sN * m; e += LG) a.it.u[inst * sN * m + e] += alpha * a.r.du[inst * sN * m + e];
+    const int64_t ngt = sN * a.d.ng, nct = sN * a.d.nc;
+    for (int64_t e = j; e < ngt; e += LG) {
+      a.it.s[inst * ngt + e] += alpha * a.r.ds[inst * ngt + e];
+      a.it.z[inst * ngt + e] += admax * a.r.dz[inst * ngt + e];
+    }
+    for (int e = j; e < a.d.ngN; e += LG) {
+      a.it.sN[inst * a.d.ngN + e] += alpha * a.r.dsN[inst * a.d.ngN + e];
+      a.it.zN[inst * a.d.ngN + e] += admax * a.r.dzN[inst * a.d.ngN + e];
+    }
+    for (int64_t e = j; e < nct; e += LG) a.it.lam[inst * nct + e] += alpha * a.r.dlam[inst * nct + e];
+    for (int e = j; e < a.d.ncN; e += LG) a.it.lamN[inst * a.d.ncN + e] += alpha * a.r.dlamN[inst * a.d.ncN + e];
+  }
+  if (valid && j == 0) {
+    a.status[inst] = status;
+    const bool ok = (status == 0);
+    const bool searched = ok || status == RR_ST_LS_FAILED;  // direction, D and 𝒜(0) are defined
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    if (a.r.alpha_p) a.r.alpha_p[inst] = ok ? alpha : 0.0;
+    if (a.r.alpha_d) a.r.alpha_d[inst] = ok ? admax : 0.0;
+    if (a.r.D) a.r.D[inst] = searched ? D : nan;
+    if (a.r.merit0) a.r.merit0[inst] = searched ? A0 : nan;
+    if (a.r.merit_acc) a.r.merit_acc[inst] = ok ? Aacc : nan;
+    if (a.r.n_backtracks) a.r.n_backtracks[inst] = searched ? nb : 0;
+  }
+  if (valid && (status & 0xff) == RR_ST_NONPOS_SLACK) {  // direction undefined: NaN-fill
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    const int64_t nx1 = (sN + 1) * n;
+    for (int64_t e = j; e < nx1; e += LG) {
+      a.r.dx[inst * nx1 + e] = nan;
+      a.r.dy[inst * nx1 + e] = nan;
+    }
+    for (int64_t e = j; e < sN * m; e += LG) a.r.du[inst * sN * m + e] = nan;
+    const int64_t ngt = sN * a.d.ng, nct = sN * a.d.nc;
+    for (int64_t e = j; e < ngt; e += LG) {
+      a.r.ds[inst * ngt + e] = nan;
+      a.r.dz[inst * ngt + e] = nan;
+    }
+    for (int e = j; e < a.d.ngN; e += LG) {
+      a.r.dsN[inst * a.d.ngN + e] = nan;
+      a.r.dzN[inst * a.d.ngN + e] = nan;
+    }
+    for (int64_t e = j; e < nct; e += LG) a.r.dlam[inst * nct + e] = nan;
+    for (int e = j; e < a.d.ncN; e += LG) a.r.dlamN[inst * a.d.ncN + e] = nan;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+template <int NX, int NU, int NG, int NC, int LG>
+struct IpmCfg {
+  static constexpr int WARPS = 4;
+  static constexpr int IPB = WARPS * (32 / LG);
+  static constexpr int SLOT = ((IpmBuf<NX, NU, NG, NC>::PAD + Work<NX, NU>::PAD + 2 * Rec<NX, NU>::PAD + NX + 1) & ~1);
+  static size_t smem_bytes() { return sizeof(double) * (size_t)IPB * SLOT; }
+  static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * Rec<NX, NU>::PAD; }
+  static cudaError_t launch(const IpmArgs& a, cudaStream_t s) {
+    auto k = ipm_step_kernel<NX, NU, NG, NC, LG, WARPS>;
+    const size_t sm = smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    const int64_t blocks = (a.d.batch + IPB - 1) / IPB;
+    k<<<(unsigned)blocks, WARPS * 32, sm, s>>>(a);
+    return cudaGetLastError();
+  }
+};
+
+template <typename F>
+static bool dispatch_ipm(const ipm_dims& d, F&& f) {
+  const int ngm = d.ng > d.ngN ? d.ng : d.ngN;
+  const int ncm = d.nc > d.ncN ? d.nc : d.ncN;
+  if (d.model == IPM_MODEL_CARTPOLE && (d.nx != 4 || d.nu != 1)) return false;
+  if (d.nx <= 4 && d.nu <= 1 && ngm <= 4 && ncm == 0) return f(IpmCfg<4, 1, 4, 0, 8>{});
+  if (d.nx <= 4 && d.nu <= 4 && ngm <= 8 && ncm <= 4) return f(IpmCfg<4, 4, 8, 4, 8>{});
+  if (d.nx <= 8 && d.nu <= 8 && ngm <= 16 && ncm <= 8) return f(IpmCfg<8, 8, 16, 8, 16>{});
+  if (d.nx <= 12 && d.nu <= 4 && ngm <= 16 && ncm <= 8) return f(IpmCfg<12, 4, 16, 8, 16>{});
+  return false;
+}
+
+int64_t ipm_ws_bytes(const ipm_dims& d) {
+  int64_t out = -1;
+  dispatch_ipm(d, [&](auto cfg) {
+    out = 8 * decltype(cfg)::ws_doubles(d.batch, d.N) + 256;
+    return true;
+  });
+  return out;
+}
+
+cudaError_t ipm_launch(const IpmArgs& a, cudaStream_t s, bool* supported) {
+  cudaError_t err = cudaSuccess;
+  *supported = dispatch_ipm(a.d, [&](auto cfg) {
+    err = decltype(cfg)::launch(a, s);
+    return true;
+  });
+  return err;
+}
+
+}  // namespace rrk

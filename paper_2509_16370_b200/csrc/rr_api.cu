@@ -4,6 +4,7 @@
 #include <string.h>
 
 #include "rr.h"
+#include "ipm.cuh"
 #include "rr_fused.cuh"
 
 namespace {
@@ -104,6 +105,49 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* ph, const rr_
   }
   cudaError_t e = cudaMemcpyAsync(status_host, status_dev, sizeof(int32_t) * b, cudaMemcpyDeviceToHost, s);
   if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_factor_solve_host: D2H %s", cudaGetErrorString(e));
+  return RR_OK;
+}
+
+
+static bool ipm_dims_ok(const ipm_dims* d) {
+  return d != nullptr && d->nx >= 1 && d->nu >= 1 && d->N >= 0 && d->batch >= 0 && d->ng >= 0 && d->ngN >= 0 &&
+         d->nc >= 0 && d->ncN >= 0 && (d->model == IPM_MODEL_LQ || d->model == IPM_MODEL_CARTPOLE);
+}
+
+int64_t ipm_workspace_bytes(const ipm_dims* dims) {
+  if (!ipm_dims_ok(dims)) return -1;
+  return rrk::ipm_ws_bytes(*dims);
+}
+
+rr_err ipm_step(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it, const ipm_params* params,
+                const ipm_result* res, void* workspace, int64_t workspace_bytes, int32_t* status, void* stream) {
+  if (!ipm_dims_ok(dims)) return set_err(RR_E_INVALID, "ipm_step: invalid dims%s");
+  if (!data || !it || !params || !res || !status) return set_err(RR_E_INVALID, "ipm_step: null %s", "argument");
+  if (dims->batch == 0) return RR_OK;
+  if (!(params->tau > 0.0 && params->tau < 1.0) || !(params->armijo_c > 0.0 && params->armijo_c < 0.5) ||
+      !(params->beta > 0.0 && params->beta < 1.0) || params->max_backtracks < 0)
+    return set_err(RR_E_INVALID, "ipm_step: invalid %s", "line-search parameters");
+  const int64_t need = ipm_workspace_bytes(dims);
+  if (need < 0) return set_err(RR_E_UNSUPPORTED, "ipm_step: no kernel compiled for these dims/model%s");
+  if (dims->N > 0 && (workspace == nullptr || workspace_bytes < need))
+    return set_err(RR_E_INVALID, "ipm_step: workspace missing or smaller than %s", "ipm_workspace_bytes()");
+  if (!data->s0 || !data->fval || !data->gradfN || !data->QN || !it->x || !it->y || !it->mu || !it->eta ||
+      !res->dx || !res->dy)
+    return set_err(RR_E_INVALID, "ipm_step: null %s", "required pointer");
+  if (dims->model == IPM_MODEL_CARTPOLE && data->model_params == nullptr)
+    return set_err(RR_E_INVALID, "ipm_step: cart-pole model needs %s", "model_params");
+  rrk::IpmArgs a;
+  a.d = *dims;
+  a.d_ = *data;
+  a.it = *it;
+  a.prm = *params;
+  a.r = *res;
+  a.ws = static_cast<double*>(workspace);
+  a.status = status;
+  bool supported = false;
+  cudaError_t e = rrk::ipm_launch(a, static_cast<cudaStream_t>(stream), &supported);
+  if (!supported) return set_err(RR_E_UNSUPPORTED, "ipm_step: unsupported dims%s");
+  if (e != cudaSuccess) return set_err(RR_E_CUDA, "ipm_step: CUDA error %s", cudaGetErrorString(e));
   return RR_OK;
 }
 

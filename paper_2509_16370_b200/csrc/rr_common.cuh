@@ -41,6 +41,18 @@ __device__ __forceinline__ void copy_async(double* dst, const double* src, int c
   }
 }
 
+// Reciprocal for pivots: hardware approximation (rcp.approx.ftz.f64, ~2^-20 relative) refined by
+// two Newton steps (error ~2^-80 before rounding, i.e. within 1 ulp of 1/d).  No IEEE slow path:
+// d = 0 gives inf/NaN, which the pivot checks (d > 0) report anyway.
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ int32_t mk_status(int code, int stage) { return code | (stage << 8); }
 
 // Status combine key: the failure met first in the backward sweep (highest stage) wins; at

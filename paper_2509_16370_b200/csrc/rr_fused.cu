@@ -5,57 +5,56 @@
 //   dual recovery y_i = V_i x_i + v_i.
 //
 // B200 design (kernel K1):
-//   * One lane group of LG lanes (LG = 4, 8, 16 or 32; 32/LG instances per warp) owns one instance.
-//     Lane j owns COLUMN j of the stage's (n+m)-wide matrices: F = [A B], T = W F, U = Fᵀ W F + P,
-//     so the dense contractions are register-resident FMA loops fed by broadcast shared-memory reads.
+//   * One lane group of LG lanes (32/LG instances per warp) owns one instance; lane j owns
+//     COLUMN j of the stage's (n+m)-wide matrices (rr_stage.cuh), so the dense contractions are
+//     register-resident FMA chains fed by broadcast shared-memory reads.
 //   * The stage inputs (A, B, Q, M, R, q, r, c) of stage i-1 stream into a double-buffered
 //     per-instance shared-memory slot with cp.async while stage i computes.
-//   * S = I + δV_{i+1} is factored by a right-looking Cholesky (pivot column broadcast through
-//     shared memory); W = S⁻¹V, and later the closed-loop Φ_i = S⁻¹(A + B K_i) and
-//     φ_i = S⁻¹(B k_i + c_{i+1} - δ v_{i+1}), are column-parallel triangular solves.
-//   * G⁻¹H, G⁻¹h and the Schur complement AᵀWA + Q - HᵀG⁻¹H = V_i are ONE Gauss-Jordan
-//     elimination of the u-block of U (pivot columns via warp shuffles), applied to the
-//     right-hand side b = [q + Aᵀg; r + Bᵀg] as well, which yields v_i and -k_i (P:606-611,
-//     the HᵀK = KᵀH identities make this the paper's V_i, v_i).  G is SPD (R PD), so Gauss-Jordan
-//     without pivoting is the Cholesky-equivalent elimination (reading R9).
-//   * The forward sweep is then x_{i+1} = Φ_i x_i + φ_i, u_i = K_i x_i + k_i, y_i = V_i x_i + v_i,
-//     reading one per-stage record written by the backward sweep (no re-read of A, B, c and no
-//     second Cholesky), so its serial chain per stage is one matrix-vector product.
+//   * S = I + δV_{i+1} is factored by a shuffle-broadcast Cholesky; W = S⁻¹V, Φ_i = S⁻¹(A + B K_i)
+//     and φ_i = S⁻¹(B k_i + c_{i+1} - δ v_{i+1}) are column-parallel triangular solves.
+//   * G⁻¹H, G⁻¹h and V_i = AᵀWA + Q - HᵀG⁻¹H, v_i come out of ONE Gauss-Jordan elimination of the
+//     u-block (P:606-611 identities; G SPD so no pivoting is needed, reading R9).
+//   * The forward sweep is x_{i+1} = Φ_i x_i + φ_i, u_i = K_i x_i + k_i, y_i = V_i x_i + v_i from
+//     one per-stage record (no re-read of A, B, c, no second Cholesky).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "rr_common.cuh"
 #include "rr_fused.cuh"
+#include "rr_stage.cuh"
 
 namespace rrk {
 
-template <int NX, int NU>
+template <int NX, int NU, bool EXACT>
 struct FusedLayout {
   static constexpr int NZ = NX + NU;
   static constexpr int STG = NX * NX + 2 * NX * NU + NX * (NX + 1) / 2 + NU * (NU + 1) / 2 + 2 * NX + NU;
   static constexpr int STG_PAD = (STG + 1) & ~1;
-  // per-instance shared slot (doubles): 2 stage buffers | Lc | Wb | invd | vb | gb | vs | pad
-  static constexpr int SLOT = 2 * STG_PAD + 2 * NX * NX + NX + NZ + 2 * NX;
+  static constexpr int PADF = EXACT ? 0 : (NX * NZ + NX);  // padded F and c for the generic kernels
+  // per-instance shared slot (doubles): 2 stage buffers | work area | padded F, c  (backward);
+  // reused as 2 record buffers in the forward sweep
+  static constexpr int SLOT_B = 2 * STG_PAD + Work<NX, NU>::PAD + PADF;
+  static constexpr int SLOT_F = 2 * Rec<NX, NU>::PAD + NX;
+  static constexpr int SLOT = SLOT_B > SLOT_F ? SLOT_B : SLOT_F;
   static constexpr int SLOT_PAD = (SLOT + 1) & ~1;
-  // per-stage workspace record (doubles): Phi NX*NX | phi NX | K NU*NX | k NU | V NX*NX | v NX
-  static constexpr int REC = 2 * NX * NX + NU * NX + NU + 2 * NX;
-  static constexpr int REC_PAD = (REC + 1) & ~1;
 };
 
-template <int NX, int NU, int LG, int WARPS, bool EXACT>
-__global__ void __launch_bounds__(WARPS * 32) rr_fused_kernel(const FusedArgs a) {
-  using LY = FusedLayout<NX, NU>;
+template <int NX, int NU, int LG, int WARPS, int MINB, bool EXACT>
+__global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_kernel(const FusedArgs a) {
+  using LY = FusedLayout<NX, NU, EXACT>;
+  using ST = Stage<NX, NU, LG>;
+  using WK = Work<NX, NU>;
+  using RC = Rec<NX, NU>;
   constexpr int NZ = LY::NZ;
   constexpr int IPW = 32 / LG;
-  static_assert(NZ <= LG, "lane group narrower than n+m");
   static_assert(32 % LG == 0, "lane group must divide the warp");
 
   const int n = EXACT ? NX : a.nx;
   const int m = EXACT ? NU : a.nu;
   const int N = a.N;
   const int sn = n * (n + 1) / 2, sm = m * (m + 1) / 2;
-  // stage-record offsets inside a stage buffer (same element order as the global operands)
   const int oA = 0, oB = oA + n * n, oQ = oB + n * m, oM = oQ + sn, oR = oM + n * m, oq = oR + sm,
             orr = oq + n, oc = orr + m;
 
@@ -65,24 +64,17 @@ __global__ void __launch_bounds__(WARPS * 32) rr_fused_kernel(const FusedArgs a)
   double* slot = smem + (warp * IPW + grp) * LY::SLOT_PAD;
   double* stg0 = slot;
   double* stg1 = slot + LY::STG_PAD;
-  double* Lc = slot + 2 * LY::STG_PAD;  // Cholesky factor of S, column-major NX×NX (lower)
-  double* Wb = Lc + NX * NX;            // W_i column-major NX×NX
-  double* invd = Wb + NX * NX;          // 1 / L_kk
-  double* vb = invd + NX;               // b vector (NZ)
-  double* gb = vb + NZ;                 // g_i (NX)
-  double* vs = gb + NX;                 // v_{i+1} (NX), then x (forward)
+  double* wk = slot + 2 * LY::STG_PAD;
+  double* Fp = wk + WK::PAD;  // generic kernels only: padded F (NX × NZ) and c (NX)
+  double* cp = Fp + NX * NZ;
 
   int64_t inst = ((int64_t)blockIdx.x * WARPS + warp) * IPW + grp;
   const bool valid = inst < a.batch;
   if (!valid) inst = a.batch - 1;
   const double delta = a.p.delta[inst];
   const int64_t sN = (int64_t)N;
-  double* rec0 = a.ws + inst * sN * LY::REC_PAD;
-
-  int32_t st = 0;  // first failure seen by this lane (backward order)
-  auto fail = [&](int code, int stage) {
-    if (st == 0) st = mk_status(code, stage);
-  };
+  double* rec0 = a.ws + inst * sN * RC::PAD;
+  int32_t st = 0;
 
   auto issue_stage = [&](int i, double* dst) {
     const int64_t s = inst * sN + i;
@@ -96,19 +88,13 @@ __global__ void __launch_bounds__(WARPS * 32) rr_fused_kernel(const FusedArgs a)
     copy_async(dst + oc, a.p.c + s * n, n, j, LG);
   };
 
-  // ---- padded accessors (column s < NX: x-part, s >= NX: u-part a = s - NX) ----
-  auto Fat = [&](const double* sb, int k, int s) -> double {  // F = [A B], NX rows, NZ cols
-    if (k >= n) return 0.0;
-    if (s < NX) return s < n ? sb[oA + k + s * n] : 0.0;
-    const int u = s - NX;
-    return u < m ? sb[oB + k + u * n] : 0.0;
-  };
-  auto Pat = [&](const double* sb, int s, int t) -> double {  // P = [[Q M]; [Mᵀ R]] padded
+  // P = [[Q M]; [Mᵀ R]] column j, padded (padded u-diagonal = 1 keeps G_pad = I)
+  auto Pat = [&](const double* sb, int s, int t) -> double {
     if (s < NX && t < NX) {
       if (s >= n || t >= n) return 0.0;
       return s >= t ? sb[oQ + pidx(n, s, t)] : sb[oQ + pidx(n, t, s)];
     }
-    if (s < NX) {  // t in u
+    if (s < NX) {
       const int u = t - NX;
       return (s < n && u < m) ? sb[oM + s + u * n] : 0.0;
     }
@@ -121,47 +107,7 @@ __global__ void __launch_bounds__(WARPS * 32) rr_fused_kernel(const FusedArgs a)
     return u == w ? 1.0 : 0.0;
   };
 
-  // ---- Cholesky of S = I + δV (lane j holds column j of V in Vc) into Lc / invd ----
-  auto cholS = [&](const double (&Vc)[NX], int stage) {
-    double Sc[NX];
-#pragma unroll
-    for (int r = 0; r < NX; ++r) Sc[r] = delta * Vc[r] + (r == j ? 1.0 : 0.0);
-#pragma unroll
-    for (int p = 0; p < NX; ++p) {
-      if (j == p) {
-        const double d = Sc[p];
-        if (!(d > 0.0)) fail(RR_ST_S_NOT_PD, stage);
-        const double ip = rsqrt(d);
-        invd[p] = ip;
-        Lc[p * NX + p] = d * ip;
-#pragma unroll
-        for (int r = p + 1; r < NX; ++r) Lc[p * NX + r] = Sc[r] * ip;
-      }
-      __syncwarp();
-      if (j > p && j < NX) {
-        const double ljp = Lc[p * NX + j];
-#pragma unroll
-        for (int r = p + 1; r < NX; ++r) Sc[r] = fma(-Lc[p * NX + r], ljp, Sc[r]);
-      }
-    }
-  };
-  // in-place solve (L Lᵀ) X = X with the factor in Lc / invd
-  auto cholSolve = [&](double (&X)[NX]) {
-#pragma unroll
-    for (int k = 0; k < NX; ++k) {
-      X[k] *= invd[k];
-#pragma unroll
-      for (int r = k + 1; r < NX; ++r) X[r] = fma(-Lc[k * NX + r], X[k], X[r]);
-    }
-#pragma unroll
-    for (int k = NX - 1; k >= 0; --k) {
-      X[k] *= invd[k];
-#pragma unroll
-      for (int r = 0; r < k; ++r) X[r] = fma(-Lc[r * NX + k], X[k], X[r]);
-    }
-  };
-
-  // ---- carried state: Vc = column j of V_{i+1}; vs[] = v_{i+1} ----
+  // ---- carried state: Vc = column j of V_N = Q_N; v_N = q_N ----
   double Vc[NX];
   {
     const double* QN = a.p.QN + inst * sn;
@@ -171,8 +117,7 @@ __global__ void __launch_bounds__(WARPS * 32) rr_fused_kernel(const FusedArgs a)
       if (j < n && r < n) val = r >= j ? QN[pidx(n, r, j)] : QN[pidx(n, j, r)];
       Vc[r] = val;
     }
-    if (j < n) vs[j] = a.p.qN[inst * n + j];
-    else if (j < NX) vs[j] = 0.0;
+    if (j < NX) wk[WK::vs + j] = (j < n) ? a.p.qN[inst * n + j] : 0.0;
     if (valid && a.f.V != nullptr && j < n) {
       double* Vo = a.f.V + (inst * (sN + 1) + N) * sn;
       for (int r = j; r < n; ++r) Vo[pidx(n, r, j)] = QN[pidx(n, r, j)];
@@ -180,10 +125,8 @@ __global__ void __launch_bounds__(WARPS * 32) rr_fused_kernel(const FusedArgs a)
     if (valid && a.f.v != nullptr && j < n) a.f.v[(inst * (sN + 1) + N) * n + j] = a.p.qN[inst * n + j];
   }
 
-  if (N > 0) {
-    issue_stage(N - 1, stg0);
-    cp_async_commit();
-  }
+  if (N > 0) issue_stage(N - 1, stg0);
+  cp_async_commit();
   __syncwarp();
 
   for (int i = N - 1; i >= 0; --i) {
@@ -193,123 +136,30 @@ __global__ void __launch_bounds__(WARPS * 32) rr_fused_kernel(const FusedArgs a)
     cp_async_commit();
     cp_async_wait<1>();
     __syncwarp();
+    const double* F = sb + oA;
+    const double* cv = sb + oc;
+    if (!EXACT) {  // scatter into the padded NX × NZ layout
+      for (int e = j; e < NX * NZ; e += LG) {
+        const int k = e % NX, s = e / NX;
+        double val = 0.0;
+        if (k < n) {
+          if (s < NX) val = (s < n) ? sb[oA + k + s * n] : 0.0;
+          else val = (s - NX < m) ? sb[oB + k + (s - NX) * n] : 0.0;
+        }
+        Fp[e] = val;
+      }
+      for (int e = j; e < NX; e += LG) cp[e] = (e < n) ? sb[oc + e] : 0.0;
+      __syncwarp();
+      F = Fp;
+      cv = cp;
+    }
+    auto Pcol = [&](int s) -> double { return (j < NZ) ? Pat(sb, s, j) : 0.0; };
+    const double qj = (j < NX) ? ((j < n) ? sb[oq + j] : 0.0) : ((j < NZ && j - NX < m) ? sb[orr + j - NX] : 0.0);
 
-    // (1) S = I + δ V_{i+1} = L Lᵀ
-    cholS(Vc, i);
-    // (2) W_i = S⁻¹ V_{i+1}, column j
-    double X[NX];
-#pragma unroll
-    for (int r = 0; r < NX; ++r) X[r] = Vc[r];
-    cholSolve(X);
-    // (3) W to shared; g_i = v_{i+1} + W (c_{i+1} - δ v_{i+1}); W symmetric: row j = X
-    if (j < NX) {
-#pragma unroll
-      for (int r = 0; r < NX; ++r) Wb[j * NX + r] = X[r];
-      double gj = (j < n) ? vs[j] : 0.0;
-#pragma unroll
-      for (int k = 0; k < NX; ++k) {
-        const double e = (k < n) ? (sb[oc + k] - delta * vs[k]) : 0.0;
-        gj = fma(X[k], e, gj);
-      }
-      gb[j] = gj;
-    }
-    __syncwarp();
-    // (4) T = W F, column j (lane j's column of F in registers)
-    double Fc[NX];
-#pragma unroll
-    for (int k = 0; k < NX; ++k) Fc[k] = (j < NZ) ? Fat(sb, k, j) : 0.0;
-    double T[NX];
-#pragma unroll
-    for (int r = 0; r < NX; ++r) T[r] = 0.0;
-#pragma unroll
-    for (int k = 0; k < NX; ++k)
-#pragma unroll
-      for (int r = 0; r < NX; ++r) T[r] = fma(Wb[k * NX + r], Fc[k], T[r]);
-    // (5) U = Fᵀ W F + P, column j  (blocks AᵀWA+Q, H = BᵀWA+Mᵀ, G = BᵀWB+R: P:617)
-    double U[NZ];
-#pragma unroll
-    for (int s = 0; s < NZ; ++s) {
-      double acc = (j < NZ) ? Pat(sb, s, j) : 0.0;
-#pragma unroll
-      for (int k = 0; k < NX; ++k) acc = fma(Fat(sb, k, s), T[k], acc);
-      U[s] = acc;
-    }
-    // b_j = [q + Aᵀ g ; r + Bᵀ g]_j
-    if (j < NZ) {
-      double bj = (j < NX) ? ((j < n) ? sb[oq + j] : 0.0) : ((j - NX < m) ? sb[orr + j - NX] : 0.0);
-#pragma unroll
-      for (int k = 0; k < NX; ++k) bj = fma(Fc[k], gb[k], bj);
-      vb[j] = bj;
-    }
-    __syncwarp();
-    double b[NZ];
-#pragma unroll
-    for (int s = 0; s < NZ; ++s) b[s] = vb[s];
-    // (6) Gauss-Jordan on the u-block: G⁻¹H, G⁻¹h, V_i = AᵀWA+Q-HᵀG⁻¹H, v_i
-#pragma unroll
-    for (int p = NX; p < NZ; ++p) {
-      double colp[NZ];
-#pragma unroll
-      for (int s = 0; s < NZ; ++s) colp[s] = __shfl_sync(RR_FULL_MASK, U[s], gbase + p);
-      const double piv = colp[p];
-      if (!(piv > 0.0)) fail(RR_ST_G_NOT_PD, i);
-      const double ip = 1.0 / piv;
-      const double rp = U[p] * ip;
-      const double bp = b[p] * ip;
-#pragma unroll
-      for (int s = 0; s < NZ; ++s) {
-        if (s == p) continue;
-        U[s] = fma(-colp[s], rp, U[s]);
-        b[s] = fma(-colp[s], bp, b[s]);
-      }
-      U[p] = rp;
-      b[p] = bp;
-    }
-    // now: lane j < n: U[0..NX) = V_i[:, j], U[NX..) = -K_i[:, j];  b = [v_i ; -k_i]
-    // (7) closed loop for the forward sweep: Φ_i = S⁻¹(A + B K_i) (lanes j < NX),
-    //     φ_i = S⁻¹(B k_i + c_{i+1} - δ v_{i+1}) (lane NX); S = I + δV_{i+1} still in Lc/invd.
-    double t[NX];
-#pragma unroll
-    for (int r = 0; r < NX; ++r) {
-      double base = 0.0;
-      if (j < NX) base = Fc[r];
-      else if (j == NX) base = (r < n) ? (sb[oc + r] - delta * vs[r]) : 0.0;
-      t[r] = base;
-    }
-#pragma unroll
-    for (int u = 0; u < NU; ++u) {
-      const double coef = (j < NX) ? -U[NX + u] : ((j == NX) ? -b[NX + u] : 0.0);
-#pragma unroll
-      for (int r = 0; r < NX; ++r) t[r] = fma(Fat(sb, r, NX + u), coef, t[r]);
-    }
-    cholSolve(t);
-    // (8) stores: workspace record i, optional factor outputs
-    double* rec = rec0 + (int64_t)i * LY::REC_PAD;
-    double* rPhi = rec;
-    double* rphi = rPhi + NX * NX;
-    double* rK = rphi + NX;
-    double* rk = rK + NU * NX;
-    double* rV = rk + NU;
-    double* rv = rV + NX * NX;
-    if (j < NX) {
-#pragma unroll
-      for (int r = 0; r < NX; ++r) {
-        rPhi[j * NX + r] = t[r];
-        rV[j * NX + r] = U[r];
-      }
-#pragma unroll
-      for (int u = 0; u < NU; ++u) rK[j * NU + u] = -U[NX + u];
-    } else if (j == NX) {
-#pragma unroll
-      for (int r = 0; r < NX; ++r) rphi[r] = t[r];
-    }
-    if (j == 0) {
-#pragma unroll
-      for (int r = 0; r < NX; ++r) rv[r] = b[r];
-#pragma unroll
-      for (int u = 0; u < NU; ++u) rk[u] = -b[NX + u];
-    }
-    if (valid) {
+    double U[NZ], b[NZ];
+    ST::backward(F, cv, Pcol, qj, delta, j, wk, Vc, U, b, rec0 + (int64_t)i * RC::PAD, i, st);
+
+    if (valid) {  // optional factor outputs (policy of Eq.(RR))
       if (a.f.V != nullptr && j < n) {
         double* Vo = a.f.V + (inst * (sN + 1) + i) * sn;
 #pragma unroll
@@ -322,79 +172,49 @@ __global__ void __launch_bounds__(WARPS * 32) rr_fused_kernel(const FusedArgs a)
         for (int u = 0; u < NU; ++u)
           if (u < m) Ko[j * m + u] = -U[NX + u];
       }
-      if (j == 0) {
-        if (a.f.v != nullptr) {
-          double* vo = a.f.v + (inst * (sN + 1) + i) * n;
+      if (j == 0 && a.f.v != nullptr) {
+        double* vo = a.f.v + (inst * (sN + 1) + i) * n;
 #pragma unroll
-          for (int r = 0; r < NX; ++r)
-            if (r < n) vo[r] = b[r];
-        }
-        if (a.f.k != nullptr) {
-          double* ko = a.f.k + (inst * sN + i) * m;
+        for (int r = 0; r < NX; ++r)
+          if (r < n) vo[r] = b[r];
+      }
+      if (j == 0 && a.f.k != nullptr) {
+        double* ko = a.f.k + (inst * sN + i) * m;
 #pragma unroll
-          for (int u = 0; u < NU; ++u)
-            if (u < m) ko[u] = -b[NX + u];
-        }
+        for (int u = 0; u < NU; ++u)
+          if (u < m) ko[u] = -b[NX + u];
       }
     }
-    // (9) carry V_i, v_i
-#pragma unroll
-    for (int r = 0; r < NX; ++r) Vc[r] = (j < NX) ? U[r] : 0.0;
-    __syncwarp();  // everyone done reading vs (v_{i+1}) and the stage buffer
-    if (j == 0) {
-#pragma unroll
-      for (int r = 0; r < NX; ++r) vs[r] = b[r];
-    }
-    __syncwarp();
   }
 
   // ---- x_0 = (I + δV_0)⁻¹ (c_0 - δ v_0) ----
-  cholS(Vc, 0);
+  ST::invS(Vc, delta, j, wk, 0, st);
   double xr[NX];  // x_i replicated in every lane of the group
-  {
-    double t0[NX];
 #pragma unroll
-    for (int r = 0; r < NX; ++r) t0[r] = (r < n) ? (a.p.c0[inst * n + r] - delta * vs[r]) : 0.0;
-    cholSolve(t0);
-#pragma unroll
-    for (int r = 0; r < NX; ++r) xr[r] = t0[r];
-  }
+  for (int r = 0; r < NX; ++r) xr[r] = (r < n) ? (a.p.c0[inst * n + r] - delta * wk[WK::vs + r]) : 0.0;
+  ST::mulSinv(xr, wk);
 
-  // ---- status of the backward sweep, combined over the group ----
-  int64_t key = status_key(st);
+  // ---- status of the backward sweep, combined over the group (first failure in sweep order) ----
+  int32_t status = st;
 #pragma unroll
   for (int off = LG / 2; off > 0; off >>= 1) {
-    const int64_t o = __shfl_xor_sync(RR_FULL_MASK, key, off);
-    key = o > key ? o : key;
+    const int32_t o = __shfl_xor_sync(RR_FULL_MASK, status, off);
+    status = o > status ? o : status;
   }
-  int32_t status = key < 0 ? 0 : (int32_t)(((key >> 8) << 8) | (key & 0xff));
 
   // ---- forward sweep: y_i = V_i x_i + v_i, u_i = K_i x_i + k_i, x_{i+1} = Φ_i x_i + φ_i ----
   bool bad = false;
   double* xo = a.s.x + inst * (sN + 1) * n;
   double* uo = a.s.u + inst * sN * m;
   double* yo = a.s.y + inst * (sN + 1) * n;
-  const int ui = j - NX;  // control row owned by this lane (if 0 <= ui < m)
-  // register prefetch of record i: row j of Φ, V (lanes < NX) or row ui of K (lanes NX..)
-  double pr_Phi[NX], pr_V[NX], pr_phi = 0.0, pr_v = 0.0;
-  auto load_rec = [&](int i) {
-    const double* rec = rec0 + (int64_t)i * LY::REC_PAD;
-    if (j < NX) {
-#pragma unroll
-      for (int k = 0; k < NX; ++k) {
-        pr_Phi[k] = rec[k * NX + j];
-        pr_V[k] = rec[NX * NX + NX + NU * NX + NU + k * NX + j];
-      }
-      pr_phi = rec[NX * NX + j];
-      pr_v = rec[2 * NX * NX + NX + NU * NX + NU + j];
-    } else if (ui >= 0 && ui < NU) {
-#pragma unroll
-      for (int k = 0; k < NX; ++k) pr_Phi[k] = rec[NX * NX + NX + k * NU + ui];
-      pr_phi = rec[NX * NX + NX + NU * NX + ui];
-    }
-  };
-  if (N > 0) load_rec(0);
-  // store x_0 (lane j writes element j; xr is replicated so use a shuffle-free select)
+  const int ui = j - NX;  // control row owned by this lane (if 0 <= ui < NU)
+  __syncwarp();            // the work area (x_0 solve) is free from here on: slot -> record buffers
+  double* rbuf0 = slot;
+  double* rbuf1 = slot + RC::PAD;
+  double* xs = slot + 2 * RC::PAD;  // x_{i+1} exchange
+  auto issue_rec = [&](int i, double* dst) { copy_async(dst, rec0 + (int64_t)i * RC::PAD, RC::SIZE, j, LG); };
+  if (N > 0) issue_rec(0, rbuf0);
+  cp_async_commit();
   {
     double xj = 0.0;
 #pragma unroll
@@ -403,29 +223,46 @@ __global__ void __launch_bounds__(WARPS * 32) rr_fused_kernel(const FusedArgs a)
     bad |= (j < n) && !isfinite(xj);
   }
   for (int i = 0; i < N; ++i) {
-    double cPhi[NX], cV[NX];
+    const double* rc = (i & 1) ? rbuf1 : rbuf0;
+    if (i + 1 < N) issue_rec(i + 1, (i & 1) ? rbuf0 : rbuf1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
+    if (j < NX) {
+      a0 = rc[RC::phi + j];
+      c0 = rc[RC::v + j];
 #pragma unroll
-    for (int k = 0; k < NX; ++k) {
-      cPhi[k] = pr_Phi[k];
-      cV[k] = pr_V[k];
-    }
-    const double cphi = pr_phi, cv = pr_v;
-    if (i + 1 < N) load_rec(i + 1);
-    double acc1 = cphi, acc2 = cv;
+      for (int k = 0; k < NX; k += 2) {
+        a0 = fma(rc[RC::PHI + k * NX + j], xr[k], a0);
+        a1 = fma(rc[RC::PHI + (k + 1) * NX + j], xr[k + 1], a1);
+        const int i0 = k >= j ? pidx(NX, k, j) : pidx(NX, j, k);
+        const int i1 = k + 1 >= j ? pidx(NX, k + 1, j) : pidx(NX, j, k + 1);
+        c0 = fma(rc[RC::V + i0], xr[k], c0);
+        c1 = fma(rc[RC::V + i1], xr[k + 1], c1);
+      }
+    } else if (ui < NU) {
+      a0 = rc[RC::k + ui];
 #pragma unroll
-    for (int k = 0; k < NX; ++k) {
-      acc1 = fma(cPhi[k], xr[k], acc1);
-      acc2 = fma(cV[k], xr[k], acc2);
+      for (int k = 0; k < NX; k += 2) {
+        a0 = fma(rc[RC::K + k * NU + ui], xr[k], a0);
+        a1 = fma(rc[RC::K + (k + 1) * NU + ui], xr[k + 1], a1);
+      }
     }
+    const double acc1 = a0 + a1, acc2 = c0 + c1;
     // lanes < NX: acc1 = x_{i+1}[j], acc2 = y_i[j];  lanes NX..: acc1 = u_i[ui]
     if (valid) {
-      if (j < n) yo[(int64_t)i * n + j] = acc2;
+      if (j < n) {
+        yo[(int64_t)i * n + j] = acc2;
+        xo[(int64_t)(i + 1) * n + j] = acc1;
+      }
       if (ui >= 0 && ui < m) uo[(int64_t)i * m + ui] = acc1;
-      if (j < n) xo[(int64_t)(i + 1) * n + j] = acc1;
     }
     bad |= ((j < n) && !(isfinite(acc1) && isfinite(acc2))) || ((ui >= 0 && ui < m) && !isfinite(acc1));
-#pragma unroll
-    for (int r = 0; r < NX; ++r) xr[r] = __shfl_sync(RR_FULL_MASK, acc1, gbase + r);
+    if (j < NX) xs[j] = acc1;
+    __syncwarp();
+    ST::bcast(xs, xr);
+    __syncwarp();  // buffer rc is refilled next iteration
   }
   // y_N = Q_N x_N + q_N
   {
@@ -454,14 +291,13 @@ __global__ void __launch_bounds__(WARPS * 32) rr_fused_kernel(const FusedArgs a)
 }
 
 // ------------------------------------------------------------------------------------------
-template <int NX, int NU, int LG, bool EXACT>
+template <int NX, int NU, int LG, int WARPS, int MINB, bool EXACT>
 struct FusedCfg {
-  static constexpr int WARPS = 4;
   static constexpr int IPB = WARPS * (32 / LG);  // instances per block
-  static size_t smem_bytes() { return sizeof(double) * (size_t)IPB * FusedLayout<NX, NU>::SLOT_PAD; }
-  static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * FusedLayout<NX, NU>::REC_PAD; }
+  static size_t smem_bytes() { return sizeof(double) * (size_t)IPB * FusedLayout<NX, NU, EXACT>::SLOT_PAD; }
+  static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * Rec<NX, NU>::PAD; }
   static cudaError_t launch(const FusedArgs& a, cudaStream_t s) {
-    auto k = rr_fused_kernel<NX, NU, LG, WARPS, EXACT>;
+    auto k = rr_fused_kernel<NX, NU, LG, WARPS, MINB, EXACT>;
     const size_t sm = smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
@@ -472,15 +308,27 @@ struct FusedCfg {
 };
 
 // Shape dispatch: exact specialisations for the BASELINE configs, padded fallbacks otherwise.
+// RR_B200_VARIANT (environment, read per call; tuning knob for the 12x4 kernel): 0 = default
+// (3 CTAs/SM register budget), 1 = 2 CTAs/SM (no spills), 2 = 2 warps per CTA.
+static int variant() {
+  const char* v = getenv("RR_B200_VARIANT");
+  return v ? atoi(v) : 0;
+}
+
 template <typename F>
 static bool dispatch_fused(int nx, int nu, F&& f) {
-  if (nx == 12 && nu == 4) return f(FusedCfg<12, 4, 16, true>{});
-  if (nx == 4 && nu == 1) return f(FusedCfg<4, 1, 8, true>{});
-  if (nx == 2 && nu == 1) return f(FusedCfg<2, 1, 4, true>{});
-  if (nx <= 2 && nu <= 2) return f(FusedCfg<2, 2, 4, false>{});
-  if (nx <= 4 && nu <= 4) return f(FusedCfg<4, 4, 8, false>{});
-  if (nx <= 8 && nu <= 8) return f(FusedCfg<8, 8, 16, false>{});
-  if (nx <= 16 && nu <= 16) return f(FusedCfg<16, 16, 32, false>{});
+  if (nx == 12 && nu == 4) {
+    const int v = variant();
+    if (v == 1) return f(FusedCfg<12, 4, 16, 4, 2, true>{});
+    if (v == 2) return f(FusedCfg<12, 4, 16, 2, 6, true>{});
+    return f(FusedCfg<12, 4, 16, 4, 3, true>{});
+  }
+  if (nx == 4 && nu == 1) return f(FusedCfg<4, 1, 8, 4, 4, true>{});
+  if (nx == 2 && nu == 1) return f(FusedCfg<2, 1, 4, 4, 4, true>{});
+  if (nx <= 2 && nu <= 2) return f(FusedCfg<2, 2, 4, 4, 1, false>{});
+  if (nx <= 4 && nu <= 4) return f(FusedCfg<4, 4, 8, 4, 1, false>{});
+  if (nx <= 8 && nu <= 8) return f(FusedCfg<8, 8, 16, 4, 1, false>{});
+  if (nx <= 16 && nu <= 16) return f(FusedCfg<16, 16, 32, 4, 1, false>{});
   return false;
 }
 

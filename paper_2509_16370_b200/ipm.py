@@ -1,0 +1,74 @@
+"""Binding of ipm_step (include/rr.h): one batched regularized-IPM step, rows a1-a8.
+Argument marshalling only; all arithmetic runs in librr_b200.so."""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from ._lib import (IPM_DATA_FIELDS, IPM_ITER_FIELDS, IPM_RES_FIELDS, RRError, check, ipm_dims, ipm_iterate,
+                   ipm_params, ipm_result, ipm_stage_data, lib)
+
+RES_SHAPE_OF = dict(dx="x", du="u", ds="s", dsN="sN", dy="y", dlam="lam", dlamN="lamN", dz="z", dzN="zN")
+
+
+def _p(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise RRError("ipm_step needs CUDA tensors (no CPU fallback)")
+    if not t.is_contiguous():
+        raise RRError("tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr()) if t.numel() > 0 else None
+
+
+def dims_of(b) -> ipm_dims:
+    return ipm_dims(b.nx, b.nu, b.N, b.ng, b.ngN, b.nc, b.ncN, b.model, b.batch)
+
+
+def workspace_bytes(b) -> int:
+    nb = lib().ipm_workspace_bytes(ctypes.byref(dims_of(b)))
+    if nb < 0:
+        raise RRError("no ipm_step kernel compiled for these dims/model")
+    return int(nb)
+
+
+def alloc_result(b):
+    dev = b.it["mu"].device
+    res = {k: torch.empty_like(b.it[v]) for k, v in RES_SHAPE_OF.items()}
+    for k in ("alpha_p", "alpha_d", "D", "merit0", "merit_acc"):
+        res[k] = torch.empty(b.batch, dtype=torch.float64, device=dev)
+    res["n_backtracks"] = torch.empty(b.batch, dtype=torch.int32, device=dev)
+    res["status"] = torch.empty(b.batch, dtype=torch.int32, device=dev)
+    return res
+
+
+class IpmCall:
+    """Pre-marshalled ipm_step launch on fixed buffers (iterate updated in place)."""
+
+    def __init__(self, b, res=None, ws=None, tau=0.995, armijo_c=1e-4, beta=0.5, max_backtracks=50):
+        self.b = b
+        self.res = res if res is not None else alloc_result(b)
+        nb = workspace_bytes(b)
+        self.ws = ws if ws is not None else torch.empty((nb + 7) // 8, dtype=torch.float64, device=b.it["mu"].device)
+        self.d = dims_of(b)
+        self.data = ipm_stage_data(*[_p(b.data[f]) for f in IPM_DATA_FIELDS])
+        self.it = ipm_iterate(*[_p(b.it[f]) for f in IPM_ITER_FIELDS])
+        self.prm = ipm_params(tau, armijo_c, beta, max_backtracks, 0)
+        self.r = ipm_result(*[_p(self.res[f]) for f in IPM_RES_FIELDS])
+        self.st = _p(self.res["status"])
+        self.wsp, self.wsb = _p(self.ws), self.ws.numel() * 8
+
+    def launch(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.b.it["mu"].device)
+        rc = lib().ipm_step(ctypes.byref(self.d), ctypes.byref(self.data), ctypes.byref(self.it),
+                            ctypes.byref(self.prm), ctypes.byref(self.r), self.wsp, self.wsb, self.st,
+                            ctypes.c_void_p(s.cuda_stream))
+        check(rc, "ipm_step")
+        return self.res
+
+
+def ipm_step(b, tau=0.995, armijo_c=1e-4, beta=0.5, max_backtracks=50, stream=None):
+    """One regularized-IPM step for every instance of the IPMBatch `b` (CUDA tensors); the iterate
+    b.it is updated in place.  Returns the result dict (direction, α_p, α_d, D, 𝒜(0), 𝒜(α), k, status)."""
+    return IpmCall(b, tau=tau, armijo_c=armijo_c, beta=beta, max_backtracks=max_backtracks).launch(stream)

@@ -1,0 +1,101 @@
+"""GPU parity of ipm_step (rows a1-a8, librr_b200.so through the C-ABI) against the CPU oracle
+(condense -> T2 -> expand -> merit/D -> Armijo line search -> update), on the same input bits.
+Bar: per instance and block, normwise relative error ≤ 1e-9 (FP64); status and the accepted
+backtracking index k bit-exact (no Armijo ties: margins ≥ 5e-6 relative)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.ipm import ipm_step_oracle
+from synth.ipm_workloads import cartpole_c4, random_lq_ocp
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def rel_blocks(g, o):
+    g = np.asarray(g).reshape(g.shape[0], -1)
+    o = np.asarray(o).reshape(o.shape[0], -1)
+    if g.shape[1] == 0:
+        return 0.0
+    return float(np.max(np.max(np.abs(g - o), axis=1) / np.maximum(np.max(np.abs(o), axis=1), 1e-300)))
+
+
+def run(p, **kw):
+    import paper_2509_16370_b200 as rr
+    dev = p.to("cuda")
+    res = rr.ipm_step(dev, **kw)
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in res.items()}
+    git = {k: v.cpu().numpy() for k, v in dev.it.items()}
+    o, oit = ipm_step_oracle(p, nthreads=8, **kw)
+    return g, git, o, oit
+
+
+def assert_ipm_parity(g, git, o, oit):
+    assert np.array_equal(g["status"], o["status"]), (g["status"], o["status"])
+    ok = o["status"] == 0
+    assert np.array_equal(g["n_backtracks"][ok], o["n_backtracks"][ok])
+    for k in ("dx", "du", "dy", "ds", "dsN", "dz", "dzN", "dlam", "dlamN"):
+        assert rel_blocks(g[k][ok], o[k][ok]) <= TOL, k
+    for k in ("alpha_p", "alpha_d"):
+        assert np.max(np.abs(g[k] - o[k]) / np.maximum(np.abs(o[k]), 1e-300)) <= 1e-12, k
+    for k in ("D", "merit0", "merit_acc"):
+        a, b = g[k][ok], o[k][ok]
+        assert np.all(np.abs(a - b) <= TOL * np.maximum(np.abs(b), 1.0)), (k, np.max(np.abs(a - b)))
+    for k in ("x", "u", "y", "s", "z", "sN", "zN", "lam", "lamN"):
+        assert rel_blocks(git[k][ok], oit[k][ok]) <= TOL, k
+
+
+@pytest.mark.parametrize("n,m,N,ng,ngN,nc,ncN,eta", [
+    (3, 2, 6, 2, 1, 1, 1, 1e3),
+    (4, 1, 10, 4, 2, 0, 0, 1e4),
+    (2, 2, 5, 3, 2, 2, 1, 1e2),
+    (6, 3, 7, 5, 3, 2, 2, 1e4),
+    (12, 4, 8, 8, 4, 3, 2, 1e4),
+    (4, 4, 3, 8, 8, 4, 4, 1e6),
+])
+def test_ipm_parity_random_lq(n, m, N, ng, ngN, nc, ncN, eta):
+    p = random_lq_ocp(n, m, N, 37, seed=n * 31 + N, ng=ng, ngN=ngN, nc=nc, ncN=ncN, eta=eta)
+    assert_ipm_parity(*run(p))
+
+
+def test_ipm_parity_c4_cartpole():
+    p = cartpole_c4(300, seed=2511, N=100)
+    g, git, o, oit = run(p)
+    assert np.all(o["status"] == 0)
+    assert_ipm_parity(g, git, o, oit)
+
+
+def test_ipm_parity_c4_ls_backtracking():
+    p = cartpole_c4(200, seed=7, N=30, variant="C4-LS")
+    g, git, o, oit = run(p)
+    assert np.max(o["n_backtracks"]) >= 2
+    assert_ipm_parity(g, git, o, oit)
+
+
+def test_ipm_nonpositive_slack_status():
+    p = random_lq_ocp(3, 2, 5, 6, seed=3, ng=2, ngN=1, nc=1, ncN=1)
+    p.it["s"][2, 3, 1] = -1e-3
+    g, git, o, oit = run(p)
+    assert o["status"][2] == (4 | (3 << 8)) and g["status"][2] == o["status"][2]
+    assert np.all(np.isnan(g["dx"][2]))
+    np.testing.assert_array_equal(git["x"][2], p.it["x"][2].numpy())  # untouched
+    assert_ipm_parity(g, git, o, oit)
+
+
+def test_ipm_c4_full_batch_sampled():
+    """BASELINE configs[3] at full size: 16,384 cart-pole instances, N = 100; 128 sampled
+    instances recomputed by the oracle."""
+    import paper_2509_16370_b200 as rr
+    p = cartpole_c4(16384, seed=2511, N=100, device="cuda")
+    host = p.to("cpu")
+    res = rr.ipm_step(p)
+    torch.cuda.synchronize()
+    assert int((res["status"] != 0).sum()) == 0
+    idx = np.sort(np.random.default_rng(1).choice(16384, 128, replace=False))
+    sub = host.select(torch.from_numpy(idx))
+    o, oit = ipm_step_oracle(sub, nthreads=8)
+    g = {k: v[torch.from_numpy(idx).cuda()].cpu().numpy() for k, v in res.items()}
+    git = {k: v[torch.from_numpy(idx).cuda()].cpu().numpy() for k, v in p.it.items()}
+    assert_ipm_parity(g, git, o, oit)
