@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   __syncwarp();
   // per-lane partial sums
   double sD = 0.0, sK0 = 0.0, sK1 = 0.0, sK2 = 0.0, sLog = 0.0;
+  double sDyn0 = 0.0;  // nonlinear-model dynamics terms of 𝒜 at α = 0 (trial points recompute them)
   double amax = 1.0, admax = 1.0;
   const double tau = a.prm.tau;
   const int model = a.d.model;
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const double cr = xnm[r] - xb1[r];
-        sK0 += sb[IB::yn + r] * cr + 0.5 * eta * cr * cr;
+        sDyn0 += sb[IB::yn + r] * cr + 0.5 * eta * cr * cr;
       }
     }
 #pragma unroll
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   const double D = gsum(sD);
   const double K0 = gsum(sK0) + a.d_.fval[inst];
   const double K1 = gsum(sK1), K2 = gsum(sK2);
-  const double A0 = K0 - mu * gsum(sLog);
+  const double A0 = K0 + gsum(sDyn0) - mu * gsum(sLog);
   amax = gmin(amax);
   admax = gmin(admax);
   int32_t status = st;

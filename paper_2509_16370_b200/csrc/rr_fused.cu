@@ -24,6 +24,7 @@
 #include "rr_common.cuh"
 #include "rr_fused.cuh"
 #include "rr_stage.cuh"
+#include "rr_stage_mma.cuh"
 
 namespace rrk {
 
@@ -307,9 +308,254 @@ struct FusedCfg {
   }
 };
 
+
+// ------------------------------------------------------------------------------------------
+// K1-MMA: same method, stage contractions on DMMA (rr_stage_mma.cuh); exact shapes with
+// NX % 4 == 0, NX + NU <= 16; two instances per warp (lane groups of 16).
+template <int NX, int NU>
+struct MmaLayout {
+  static constexpr int STG = NX * NX + 2 * NX * NU + NX * (NX + 1) / 2 + NU * (NU + 1) / 2 + 2 * NX + NU;
+  static constexpr int STG_PAD = (STG + 1) & ~1;
+  static constexpr int SLOT_B = 2 * STG_PAD + WorkM<NX, NU>::PAD;
+  static constexpr int SLOT_F = 2 * RecM<NX, NU>::PAD + NX;
+  static constexpr int SLOT = SLOT_B > SLOT_F ? SLOT_B : SLOT_F;
+  static constexpr int SLOT_PAD = (SLOT + 1) & ~1;
+};
+
+template <int NX, int NU, int WARPS, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const FusedArgs a) {
+  using LY = MmaLayout<NX, NU>;
+  using SM = StageMMA<NX, NU>;
+  using ST = Stage<NX, NU, 16>;
+  using WK = Work<NX, NU>;
+  using RC = RecM<NX, NU>;
+  constexpr int NZ = NX + NU;
+  constexpr int n = NX, m = NU;
+  constexpr int sn = n * (n + 1) / 2, sm = m * (m + 1) / 2;
+  constexpr int oA = 0, oB = oA + n * n, oQ = oB + n * m, oM = oQ + sn, oR = oM + n * m, oq = oR + sm,
+                orr = oq + n, oc = orr + m;
+  const int N = a.N;
+
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane >> 4, j = lane & 15, gbase = grp * 16;
+  double* slotq[2] = {smem + (warp * 2 + 0) * LY::SLOT_PAD, smem + (warp * 2 + 1) * LY::SLOT_PAD};
+  double* slot = grp ? slotq[1] : slotq[0];
+  double* wkq[2] = {slotq[0] + 2 * LY::STG_PAD, slotq[1] + 2 * LY::STG_PAD};
+  double* wk = grp ? wkq[1] : wkq[0];
+
+  const int64_t inst0 = ((int64_t)blockIdx.x * WARPS + warp) * 2;
+  int64_t instq[2] = {inst0, inst0 + 1};
+  bool validq[2] = {instq[0] < a.batch, instq[1] < a.batch};
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    if (!validq[q]) instq[q] = a.batch - 1;
+  const int64_t inst = grp ? instq[1] : instq[0];
+  const bool valid = grp ? validq[1] : validq[0];
+  const double delta = a.p.delta[inst];
+  const int64_t sN = (int64_t)N;
+  double* rec0 = a.ws + inst * sN * RC::PAD;
+  double* rec0q[2] = {validq[0] ? a.ws + instq[0] * sN * RC::PAD : nullptr,
+                      validq[1] ? a.ws + instq[1] * sN * RC::PAD : nullptr};
+  int32_t st = 0;
+
+  auto issue_stage = [&](int i, double* dst) {
+    const int64_t s = inst * sN + i;
+    copy_async(dst + oA, a.p.A + s * n * n, n * n, j, 16);
+    copy_async(dst + oB, a.p.B + s * n * m, n * m, j, 16);
+    copy_async(dst + oQ, a.p.Q + s * sn, sn, j, 16);
+    copy_async(dst + oM, a.p.M + s * n * m, n * m, j, 16);
+    copy_async(dst + oR, a.p.R + s * sm, sm, j, 16);
+    copy_async(dst + oq, a.p.q + s * n, n, j, 16);
+    copy_async(dst + orr, a.p.r + s * m, m, j, 16);
+    copy_async(dst + oc, a.p.c + s * n, n, j, 16);
+  };
+  // P = [[Q M]; [Mᵀ R]] of the stage buffer sb (exact shape: no padding inside NZ)
+  auto Pat = [&](const double* sb, int s, int t) -> double {
+    if (s < NX && t < NX) return s >= t ? sb[oQ + pidx(n, s, t)] : sb[oQ + pidx(n, t, s)];
+    if (s < NX) return sb[oM + s + (t - NX) * n];
+    if (t < NX) return sb[oM + t + (s - NX) * n];
+    const int u = s - NX, w = t - NX;
+    return u >= w ? sb[oR + pidx(m, u, w)] : sb[oR + pidx(m, w, u)];
+  };
+
+  double Vc[NX];
+  {
+    const double* QN = a.p.QN + inst * sn;
+#pragma unroll
+    for (int r = 0; r < NX; ++r) Vc[r] = (j < n) ? (r >= j ? QN[pidx(n, r, j)] : QN[pidx(n, j, r)]) : 0.0;
+    if (j < NX) wk[WK::vs + j] = a.p.qN[inst * n + j];
+    if (valid && a.f.V != nullptr && j < n) {
+      double* Vo = a.f.V + (inst * (sN + 1) + N) * sn;
+      for (int r = j; r < n; ++r) Vo[pidx(n, r, j)] = QN[pidx(n, r, j)];
+    }
+    if (valid && a.f.v != nullptr && j < n) a.f.v[(inst * (sN + 1) + N) * n + j] = a.p.qN[inst * n + j];
+  }
+  if (N > 0) issue_stage(N - 1, slot);
+  cp_async_commit();
+  __syncwarp();
+
+  for (int i = N - 1; i >= 0; --i) {
+    const int cur = (N - 1 - i) & 1;
+    const double* sbq[2] = {slotq[0] + cur * LY::STG_PAD, slotq[1] + cur * LY::STG_PAD};
+    if (i > 0) issue_stage(i - 1, slot + (cur ^ 1) * LY::STG_PAD);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const double* Fq[2] = {sbq[0] + oA, sbq[1] + oA};
+    const double* cvq[2] = {sbq[0] + oc, sbq[1] + oc};
+    const double* sb = grp ? sbq[1] : sbq[0];
+    const double qj = (j < NX) ? sb[oq + j] : sb[orr + j - NX];
+    auto P2 = [&](int q, int s, int t) -> double { return Pat(sbq[q], s, t); };
+    double* recq[2] = {rec0q[0] ? rec0q[0] + (int64_t)i * RC::PAD : nullptr,
+                       rec0q[1] ? rec0q[1] + (int64_t)i * RC::PAD : nullptr};
+    double U[NZ], b[NZ];
+    SM::backward(wkq, Fq, cvq, P2, qj, delta, grp, j, lane, Vc, U, b, recq, i, st);
+    if (valid) {
+      if (a.f.V != nullptr && j < n) {
+        double* Vo = a.f.V + (inst * (sN + 1) + i) * sn;
+#pragma unroll
+        for (int r = 0; r < NX; ++r)
+          if (r >= j) Vo[pidx(n, r, j)] = U[r];
+      }
+      if (a.f.K != nullptr && j < n) {
+        double* Ko = a.f.K + (inst * sN + i) * m * n;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) Ko[j * m + u] = -U[NX + u];
+      }
+      if (j == 0 && a.f.v != nullptr) {
+        double* vo = a.f.v + (inst * (sN + 1) + i) * n;
+#pragma unroll
+        for (int r = 0; r < NX; ++r) vo[r] = b[r];
+      }
+      if (j == 0 && a.f.k != nullptr) {
+        double* ko = a.f.k + (inst * sN + i) * m;
+#pragma unroll
+        for (int u = 0; u < NU; ++u) ko[u] = -b[NX + u];
+      }
+    }
+  }
+
+  // x_0 = (I + δV_0)⁻¹ (c_0 − δ v_0)
+  ST::invS(Vc, delta, j, wk, 0, st);
+  double xr[NX];
+#pragma unroll
+  for (int r = 0; r < NX; ++r) xr[r] = a.p.c0[inst * n + r] - delta * wk[WK::vs + r];
+  ST::mulSinv(xr, wk);
+  int32_t status = st;
+#pragma unroll
+  for (int off = 8; off > 0; off >>= 1) {
+    const int32_t o = __shfl_xor_sync(RR_FULL_MASK, status, off);
+    status = o > status ? o : status;
+  }
+
+  // forward sweep from the records (row-major [Φ | φ], packed V)
+  bool bad = false;
+  double* xo = a.s.x + inst * (sN + 1) * n;
+  double* uo = a.s.u + inst * sN * m;
+  double* yo = a.s.y + inst * (sN + 1) * n;
+  const int ui = j - NX;
+  __syncwarp();
+  double* rbuf0 = slot;
+  double* rbuf1 = slot + RC::PAD;
+  double* xs = slot + 2 * RC::PAD;
+  auto issue_rec = [&](int i, double* dst) { copy_async(dst, rec0 + (int64_t)i * RC::PAD, RC::SIZE, j, 16); };
+  if (N > 0) issue_rec(0, rbuf0);
+  cp_async_commit();
+  {
+    double xj = 0.0;
+#pragma unroll
+    for (int r = 0; r < NX; ++r) xj = (r == j) ? xr[r] : xj;
+    if (valid && j < n) xo[j] = xj;
+    bad |= (j < n) && !isfinite(xj);
+  }
+  for (int i = 0; i < N; ++i) {
+    const double* rc = (i & 1) ? rbuf1 : rbuf0;
+    if (i + 1 < N) issue_rec(i + 1, (i & 1) ? rbuf0 : rbuf1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
+    if (j < NX) {
+      const double* row = rc + RC::PHI + j * RC::LD;
+      a0 = row[NX];
+      c0 = rc[RC::v + j];
+#pragma unroll
+      for (int k = 0; k < NX; k += 2) {
+        const double2 p2 = *reinterpret_cast<const double2*>(row + k);
+        a0 = fma(p2.x, xr[k], a0);
+        a1 = fma(p2.y, xr[k + 1], a1);
+        const int i0 = k >= j ? pidx(NX, k, j) : pidx(NX, j, k);
+        const int i1 = k + 1 >= j ? pidx(NX, k + 1, j) : pidx(NX, j, k + 1);
+        c0 = fma(rc[RC::V + i0], xr[k], c0);
+        c1 = fma(rc[RC::V + i1], xr[k + 1], c1);
+      }
+    } else if (ui < NU) {
+      a0 = rc[RC::k + ui];
+#pragma unroll
+      for (int k = 0; k < NX; k += 2) {
+        a0 = fma(rc[RC::K + k * NU + ui], xr[k], a0);
+        a1 = fma(rc[RC::K + (k + 1) * NU + ui], xr[k + 1], a1);
+      }
+    }
+    const double acc1 = a0 + a1, acc2 = c0 + c1;
+    if (valid) {
+      if (j < n) {
+        yo[(int64_t)i * n + j] = acc2;
+        xo[(int64_t)(i + 1) * n + j] = acc1;
+      }
+      if (ui >= 0 && ui < m) uo[(int64_t)i * m + ui] = acc1;
+    }
+    bad |= ((j < n) && !(isfinite(acc1) && isfinite(acc2))) || ((ui >= 0 && ui < m) && !isfinite(acc1));
+    if (j < NX) xs[j] = acc1;
+    __syncwarp();
+    ST::bcast(xs, xr);
+    __syncwarp();
+  }
+  {
+    const double* QN = a.p.QN + inst * sn;
+    if (j < n) {
+      double acc = a.p.qN[inst * n + j];
+#pragma unroll
+      for (int k = 0; k < NX; ++k) acc = fma(k >= j ? QN[pidx(n, k, j)] : QN[pidx(n, j, k)], xr[k], acc);
+      if (valid) yo[sN * n + j] = acc;
+      bad |= !isfinite(acc);
+    }
+  }
+  const unsigned anybad = __ballot_sync(RR_FULL_MASK, bad);
+  const unsigned gmask = 0xffffu << gbase;
+  if (status == 0 && (anybad & gmask)) status = RR_ST_NONFINITE;
+  if (valid && status != 0) {
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    for (int64_t e = j; e < (sN + 1) * n; e += 16) {
+      xo[e] = nan;
+      yo[e] = nan;
+    }
+    for (int64_t e = j; e < sN * m; e += 16) uo[e] = nan;
+  }
+  if (valid && j == 0) a.status[inst] = status;
+}
+
+template <int NX, int NU, int WARPS, int MINB>
+struct MmaCfg {
+  static constexpr int IPB = WARPS * 2;
+  static size_t smem_bytes() { return sizeof(double) * (size_t)IPB * MmaLayout<NX, NU>::SLOT_PAD; }
+  static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * RecM<NX, NU>::PAD; }
+  static cudaError_t launch(const FusedArgs& a, cudaStream_t s) {
+    auto k = rr_fused_mma_kernel<NX, NU, WARPS, MINB>;
+    const size_t sm = smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    const int64_t blocks = (a.batch + IPB - 1) / IPB;
+    k<<<(unsigned)blocks, WARPS * 32, sm, s>>>(a);
+    return cudaGetLastError();
+  }
+};
+
 // Shape dispatch: exact specialisations for the BASELINE configs, padded fallbacks otherwise.
 // RR_B200_VARIANT (environment, read per call; tuning knob for the 12x4 kernel): 0 = default
-// (3 CTAs/SM register budget), 1 = 2 CTAs/SM (no spills), 2 = 2 warps per CTA.
+// (SIMT stage kernel, 3 CTAs/SM), 1/2 = SIMT with 2 CTAs/SM / 2-warp CTAs, 3/4 = DMMA stage
+// kernel (rr_stage_mma.cuh) with 3 / 2 CTAs/SM (measured slower: occupancy, profiles/).
 static int variant() {
   const char* v = getenv("RR_B200_VARIANT");
   return v ? atoi(v) : 0;
@@ -321,6 +567,8 @@ static bool dispatch_fused(int nx, int nu, F&& f) {
     const int v = variant();
     if (v == 1) return f(FusedCfg<12, 4, 16, 4, 2, true>{});
     if (v == 2) return f(FusedCfg<12, 4, 16, 2, 6, true>{});
+    if (v == 3) return f(MmaCfg<12, 4, 4, 3>{});
+    if (v == 4) return f(MmaCfg<12, 4, 4, 2>{});
     return f(FusedCfg<12, 4, 16, 4, 3, true>{});
   }
   if (nx == 4 && nu == 1) return f(FusedCfg<4, 1, 8, 4, 4, true>{});

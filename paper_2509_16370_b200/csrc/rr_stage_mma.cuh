@@ -1,0 +1,339 @@
+// rr_stage_mma.cuh -- backward step of Eq.(RR) with the dense stage contractions on the FP64
+// tensor-core path (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4), two instances per warp.
+//
+// Method: arXiv 2509.16370, Eq.(RR) and the forward-sweep quantities of P:496-509.
+// Why: with one lane per column the SIMT products need one 128-bit shared-memory broadcast per
+// two FMAs, which caps them at ~50% of the FP64 pipe (profiles/r01_*).  DMMA consumes register
+// fragments with 8×8 reuse inside the unit (256 FMA per instruction), so the products run on
+// the FP64 pipe with half the shared-memory traffic.  tcgen05 has no FP64 kind; DMMA runs on the
+// same FP64 units (measured 37.1 TF/s vs 34.1 TF/s DFMA, profiles/r01_k0_fp64_probe.txt).
+//
+// Matrices are padded to 16×16 tiles (two 8-row × two 8-column DMMA tiles); valid extents:
+// NX (states), NZ = NX + NU (stage columns), NX % 4 == 0 (K blocks of 4), NZ <= 16.
+// Fragment layouts of m8n8k4.row.col.f64 (g = lane>>2, t = lane&3):
+//   A (8×4): a = A[g][t];  B (4×8): b = B[t][g];  C (8×8): c0 = C[g][2t], c1 = C[g][2t+1].
+// Per stage, lane group q (16 lanes, instance q of the warp) runs the SIMT parts; the whole warp
+// runs the DMMA parts for instance 0 then instance 1:
+//   (1) SIMT  S⁻¹ (symmetric sweep, rr_stage.cuh); Vs = [V_{i+1} | V_{i+1} e], e = c_{i+1} − δ v_{i+1}
+//   (2) DMMA  [W | W e] = S⁻¹ Vs                       (W = (I+δV)⁻¹V; g = v + W e)
+//   (3) SIMT  g, b = [q + Aᵀg; r + Bᵀg]
+//   (4) DMMA  T = W F                                   (F = [A B])
+//   (5) DMMA  U = Fᵀ T + P                              (AᵀWA+Q, H = BᵀWA+Mᵀ, G = BᵀWB+R)
+//   (6) SIMT  Gauss-Jordan on the u-block of U and b    (−K_i, V_i, −k_i, v_i)
+//   (7) SIMT  M = [A + B K_i | B k_i + c_{i+1} − δ v_{i+1}]
+//   (8) DMMA  [Φ_i | φ_i] = S⁻¹ M -> workspace record (row-major, ld NX+2)
+#pragma once
+#include "rr_stage.cuh"
+
+namespace rrk {
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Workspace record of the MMA kernel: PhiT row-major NX × (NX+2) (column NX = φ) | K | k | V packed | v
+template <int NX, int NU>
+struct RecM {
+  static constexpr int LD = NX + 2;
+  static constexpr int PHI = 0;
+  static constexpr int K = NX * LD;
+  static constexpr int k = K + NU * NX;
+  static constexpr int V = k + NU;
+  static constexpr int v = V + NX * (NX + 1) / 2;
+  static constexpr int SIZE = v + NX;
+  static constexpr int PAD = (SIZE + 1) & ~1;
+};
+
+// Per-instance work area of the MMA stage (doubles, even offsets).
+template <int NX, int NU>
+struct WorkM {
+  static constexpr int NZ = NX + NU;
+  static constexpr int base = Work<NX, NU>::PAD;  // Si, Wb(unused), pub, pq, vb, gb, vs of Work
+  static constexpr int X1 = base;                 // NX × 16 (ld NX): Vs, then T, then M
+  static constexpr int X2 = X1 + NX * 16;         // 16 × 16 (ld 16 for U; ld NX for W)
+  static constexpr int SIZE = X2 + 16 * 16;
+  static constexpr int PAD = (SIZE + 1) & ~1;
+};
+
+template <int NX, int NU>
+struct StageMMA {
+  static constexpr int NZ = NX + NU;
+  static constexpr int LG = 16;
+  static constexpr int KT = NX / 4;          // K blocks over the state dimension
+  static constexpr int MT = (NX + 7) / 8;    // row tiles over states
+  static constexpr int ZT = (NZ + 7) / 8;    // tiles over stage columns
+  static constexpr int CT = (NX + 1 + 7) / 8;  // tiles over NX+1 columns ([W | We], [Φ | φ])
+  static_assert(NX % 4 == 0 && NZ <= 16 && NX + 1 <= 16, "MMA stage needs NX % 4 == 0 and NX + NU <= 16");
+  using ST = Stage<NX, NU, 16>;
+  using WK = Work<NX, NU>;
+  using WM = WorkM<NX, NU>;
+  using RC = RecM<NX, NU>;
+
+  // one backward step for the two instances of the warp.
+  //   wkq[q]: work area of instance q; F_q, cv_q: stage F / c_{i+1} of instance q (in the stage buffers)
+  //   grp/j: this lane's instance and column; Pcol(q, s, t): P_i[s][t] of instance q (padded)
+  template <typename PFun>
+  __device__ static __forceinline__ void backward(double* const (&wkq)[2], const double* const (&Fq)[2],
+                                                  const double* const (&cvq)[2], PFun&& Pat, double qj,
+                                                  double delta, int grp, int j, int lane, double (&Vc)[NX],
+                                                  double (&U)[NZ], double (&b)[NZ], double* const (&recq)[2],
+                                                  int stage, int32_t& st) {
+    double* wk = grp ? wkq[1] : wkq[0];
+    const double* F = grp ? Fq[1] : Fq[0];
+    const double* cv = grp ? cvq[1] : cvq[0];
+    const int g = lane >> 2, t = lane & 3;
+    // (1) S⁻¹, and Vs = [V | V e] (V symmetric: (V e)_j = column j · e)
+    ST::invS(Vc, delta, j, wk, stage, st);
+    if (j < NX) {
+      ST::store_col(wk + WM::X1 + j * NX, Vc);
+      double ve0 = 0.0, ve1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < NX; k += 2) {
+        ve0 = fma(Vc[k], cv[k] - delta * wk[WK::vs + k], ve0);
+        ve1 = fma(Vc[k + 1], cv[k + 1] - delta * wk[WK::vs + k + 1], ve1);
+      }
+      wk[WM::X1 + NX * NX + j] = ve0 + ve1;  // column NX of Vs
+    }
+    __syncwarp();
+    // (2) [W | W e] = S⁻¹ Vs   (rows < NX, cols <= NX);  keep the S⁻¹ A-fragments for (8)
+    double aS[2][MT][KT];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double* Si = wkq[q] + WK::Si;
+      const double* Vs = wkq[q] + WM::X1;
+      double c[MT][CT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < CT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r = 8 * mt + g;
+          aS[q][mt][kt] = (r < NX) ? Si[(4 * kt + t) * NX + r] : 0.0;
+        }
+#pragma unroll
+        for (int nt = 0; nt < CT; ++nt) {
+          const int col = 8 * nt + g;
+          const double bv = (col <= NX) ? Vs[col * NX + 4 * kt + t] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aS[q][mt][kt], bv);
+        }
+      }
+      double* Wb = wkq[q] + WM::X2;  // W col-major ld NX, column NX = W e
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < CT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * mt + g, col = 8 * nt + 2 * t + e;
+            if (r < NX && col <= NX) Wb[col * NX + r] = c[mt][nt][e];
+          }
+    }
+    __syncwarp();
+    // (3) g = v + W e;  b_j = [q + Aᵀg; r + Bᵀg]_j
+    if (j < NX) wk[WK::gb + j] = wk[WK::vs + j] + wk[WM::X2 + NX * NX + j];
+    __syncwarp();
+    const int jc = (j < NZ) ? j : 0;
+    {
+      double gk[NX];
+      ST::bcast(wk + WK::gb, gk);
+      double b0 = qj, b1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < NX; k += 2) {
+        const double2 f2 = *reinterpret_cast<const double2*>(F + jc * NX + k);
+        b0 = fma(f2.x, gk[k], b0);
+        b1 = fma(f2.y, gk[k + 1], b1);
+      }
+      if (j < NZ) wk[WK::vb + j] = b0 + b1;
+    }
+    // (4) T = W F (NX × NZ) -> X1 (ld NX);  keep F fragments (B of T, A of Fᵀ)
+    double fF[2][ZT][KT];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double* Wb = wkq[q] + WM::X2;
+      const double* Fx = Fq[q];
+      double c[MT][ZT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < ZT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        double aW[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r = 8 * mt + g;
+          aW[mt] = (r < NX) ? Wb[(4 * kt + t) * NX + r] : 0.0;
+        }
+#pragma unroll
+        for (int nt = 0; nt < ZT; ++nt) {
+          const int col = 8 * nt + g;
+          fF[q][nt][kt] = (col < NZ) ? Fx[col * NX + 4 * kt + t] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aW[mt], fF[q][nt][kt]);
+        }
+      }
+      __syncwarp();  // all lanes done reading Vs (X1) of instance q before T overwrites it
+      double* Tb = wkq[q] + WM::X1;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < ZT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * mt + g, col = 8 * nt + 2 * t + e;
+            if (r < NX && col < NZ) Tb[col * NX + r] = c[mt][nt][e];
+          }
+    }
+    __syncwarp();
+    // (5) U = Fᵀ T + P (NZ × NZ) -> X2 (ld 16)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double* Tb = wkq[q] + WM::X1;
+      double c[ZT][ZT][2];
+#pragma unroll
+      for (int mt = 0; mt < ZT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < ZT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * mt + g, col = 8 * nt + 2 * t + e;
+            c[mt][nt][e] = (r < NZ && col < NZ) ? Pat(q, r, col) : 0.0;
+          }
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+        for (int nt = 0; nt < ZT; ++nt) {
+          const int col = 8 * nt + g;
+          const double bT = (col < NZ) ? Tb[col * NX + 4 * kt + t] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < ZT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], fF[q][mt][kt], bT);
+        }
+      double* Ub = wkq[q] + WM::X2;
+#pragma unroll
+      for (int mt = 0; mt < ZT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < ZT; ++nt) {
+          const int r = 8 * mt + g, col = 8 * nt + 2 * t;
+          Ub[col * 16 + r] = c[mt][nt][0];
+          Ub[(col + 1) * 16 + r] = c[mt][nt][1];
+        }
+    }
+    __syncwarp();
+    // (6) Gauss-Jordan on the u-block (SIMT, lane j owns column j)
+#pragma unroll
+    for (int s = 0; s < NZ; ++s) U[s] = (j < NZ) ? wk[WM::X2 + jc * 16 + s] : 0.0;
+#pragma unroll
+    for (int s = 0; s < NZ; ++s) b[s] = wk[WK::vb + s];
+#pragma unroll
+    for (int p = NX; p < NZ; ++p) {
+      double* pb = wk + WK::pub + (p & 1) * WK::NZP;
+      if (j < NZ) pb[j] = U[p];
+      if (j == p) {
+#pragma unroll
+        for (int qq = NX; qq < p; ++qq) wk[WK::pq + (qq - NX)] = U[qq];
+      }
+      __syncwarp();
+      double col[NZ];
+#pragma unroll
+      for (int s = 0; s < NZ; ++s) col[s] = (s >= NX && s < p) ? wk[WK::pq + (s - NX)] : pb[s];
+      const double piv = col[p];
+      if (!(piv > 0.0) && st == 0) st = mk_status(RR_ST_G_NOT_PD, stage);
+      const double ip = rcp_nr(piv);
+      const double rp = U[p] * ip;
+      const double bp = b[p] * ip;
+#pragma unroll
+      for (int s = 0; s < NZ; ++s) {
+        if (s == p) continue;
+        U[s] = fma(-col[s], rp, U[s]);
+        b[s] = fma(-col[s], bp, b[s]);
+      }
+      U[p] = rp;
+      b[p] = bp;
+      __syncwarp();
+    }
+    // (7) M = [A + B K | B k + c − δ v] -> X1 (ld NX, NX+1 columns)
+    if (j <= NX) {
+      double tcol[NX];
+#pragma unroll
+      for (int r = 0; r < NX; r += 2) {
+        const double2 f2 = *reinterpret_cast<const double2*>(F + jc * NX + r);
+        tcol[r] = (j < NX) ? f2.x : cv[r] - delta * wk[WK::vs + r];
+        tcol[r + 1] = (j < NX) ? f2.y : cv[r + 1] - delta * wk[WK::vs + r + 1];
+      }
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        const double coef = (j < NX) ? -U[NX + u] : -b[NX + u];
+        const double* Fu = F + (NX + u) * NX;
+#pragma unroll
+        for (int r = 0; r < NX; r += 2) {
+          const double2 f2 = *reinterpret_cast<const double2*>(Fu + r);
+          tcol[r] = fma(f2.x, coef, tcol[r]);
+          tcol[r + 1] = fma(f2.y, coef, tcol[r + 1]);
+        }
+      }
+      ST::store_col(wk + WM::X1 + j * NX, tcol);
+    }
+    __syncwarp();
+    // (8) [Φ | φ] = S⁻¹ M -> record (row-major, ld NX+2), straight from the C fragments
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double* Mb = wkq[q] + WM::X1;
+      double c[MT][CT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < CT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+        for (int nt = 0; nt < CT; ++nt) {
+          const int col = 8 * nt + g;
+          const double bM = (col <= NX) ? Mb[col * NX + 4 * kt + t] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aS[q][mt][kt], bM);
+        }
+      double* rec = recq[q];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < CT; ++nt) {
+          const int r = 8 * mt + g, col = 8 * nt + 2 * t;
+          if (rec != nullptr && r < NX && col <= NX)
+            *reinterpret_cast<double2*>(rec + RC::PHI + r * RC::LD + col) = make_double2(c[mt][nt][0], c[mt][nt][1]);
+        }
+    }
+    // (9) record K, k, V (packed), v; carry V_i, v_i
+    if ((grp ? recq[1] : recq[0]) != nullptr) {
+      double* rec = grp ? recq[1] : recq[0];
+      if (j < NX) {
+#pragma unroll
+        for (int u = 0; u < NU; ++u) rec[RC::K + j * NU + u] = -U[NX + u];
+        double* Vp = rec + RC::V + j * (2 * NX - j - 1) / 2;
+#pragma unroll
+        for (int r = 0; r < NX; ++r)
+          if (r >= j) Vp[r] = U[r];
+      } else if (j == NX) {
+#pragma unroll
+        for (int r = 0; r < NX; ++r) rec[RC::v + r] = b[r];
+#pragma unroll
+        for (int u = 0; u < NU; ++u) rec[RC::k + u] = -b[NX + u];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NX; ++r) Vc[r] = (j < NX) ? U[r] : 0.0;
+    __syncwarp();
+    if (j == 0) {
+#pragma unroll
+      for (int r = 0; r < NX; ++r) wk[WK::vs + r] = b[r];
+    }
+    __syncwarp();
+  }
+};
+
+}  // namespace rrk

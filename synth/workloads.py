@@ -249,3 +249,68 @@ def small_random(nx, nu, N, batch, seed, delta, psd_q=False, first=0) -> RRProbl
         p.Q = pack_lower(Qs).contiguous()
         p.M = torch.zeros_like(p.M)
     return p
+
+
+# ----------------------------------------------------------------------------- C5 quadrotor
+OP_XT, OP_UT, OP_XREF = 9, 10, 11
+
+
+def quadrotor_f(x, u, mass=0.5, J=(2.32e-3, 2.32e-3, 4e-3), g=9.81):
+    """Continuous quadrotor dynamics (workload definition): x = (p, ZYX Euler angles (φ, θ, ψ),
+    world velocity, body rates ω), u = (thrust T, torques τ)."""
+    phi, th, psi = x[..., 3], x[..., 4], x[..., 5]
+    v = x[..., 6:9]
+    w = x[..., 9:12]
+    sph, cph, sth, cth, sps, cps = (torch.sin(phi), torch.cos(phi), torch.sin(th), torch.cos(th),
+                                    torch.sin(psi), torch.cos(psi))
+    # Euler-angle rates = W(φ, θ) ω
+    dphi = w[..., 0] + sph * sth / cth * w[..., 1] + cph * sth / cth * w[..., 2]
+    dth = cph * w[..., 1] - sph * w[..., 2]
+    dpsi = sph / cth * w[..., 1] + cph / cth * w[..., 2]
+    # world acceleration = R(φ, θ, ψ) [0, 0, T/m] − [0, 0, g]   (ZYX: R = Rz(ψ) Ry(θ) Rx(φ))
+    T = u[..., 0]
+    ax = (cps * sth * cph + sps * sph) * T / mass
+    ay = (sps * sth * cph - cps * sph) * T / mass
+    az = cth * cph * T / mass - g
+    Jx, Jy, Jz = J
+    tx, ty, tz = u[..., 1], u[..., 2], u[..., 3]
+    dwx = (tx - (Jz - Jy) * w[..., 1] * w[..., 2]) / Jx
+    dwy = (ty - (Jx - Jz) * w[..., 2] * w[..., 0]) / Jy
+    dwz = (tz - (Jy - Jx) * w[..., 0] * w[..., 1]) / Jz
+    return torch.stack([v[..., 0], v[..., 1], v[..., 2], dphi, dth, dpsi, ax, ay, az, dwx, dwy, dwz], dim=-1)
+
+
+def quadrotor_c5(batch, seed=2512, N=200, first=0, device="cpu", dt=0.02, delta=1e-4) -> RRProblem:
+    """C5 (BASELINE configs[4]): quadrotor LQR instances, n = 12, m = 4, N = 200.
+    A_i = I + dt ∂f/∂x, B_i = dt ∂f/∂u (autograd) at random x̃ (p ~ U, angles ~ 0.3U, v ~ U,
+    ω ~ 0.5U) and ũ = (m g (1 + 0.1U), 0.01U); Q = diag(10,10,10,1,1,1,1,1,1,.1,.1,.1),
+    R = diag(0.1, 1, 1, 1), M = 0, Q_N = 10 Q, q = −Q x_ref (x_ref ~ U), r = 0, c ~ 0.01U,
+    c_0 ~ U, δ = 1e-4."""
+    dev = torch.device(device)
+    n, m = 12, 4
+    inst = torch.arange(first, first + batch, dtype=torch.int64, device=dev)
+    st = torch.arange(N, dtype=torch.int64, device=dev)
+    xs = uniform(seed, inst, st, OP_XT, n) * torch.tensor([1, 1, 1, .3, .3, .3, 1, 1, 1, .5, .5, .5],
+                                                          dtype=torch.float64, device=dev)
+    uu = uniform(seed, inst, st, OP_UT, m)
+    us = torch.stack([0.5 * 9.81 * (1 + 0.1 * uu[..., 0]), 0.01 * uu[..., 1], 0.01 * uu[..., 2],
+                      0.01 * uu[..., 3]], dim=-1)
+    jac = torch.func.vmap(torch.func.jacrev(quadrotor_f, argnums=(0, 1)))
+    Jx, Ju = jac(xs.reshape(-1, n), us.reshape(-1, m))
+    eye = torch.eye(n, dtype=torch.float64, device=dev)
+    A = colmajor(eye + dt * Jx).reshape(batch, N, n * n)
+    B = colmajor(dt * Ju).reshape(batch, N, n * m)
+    qd = torch.tensor([10, 10, 10, 1, 1, 1, 1, 1, 1, .1, .1, .1], dtype=torch.float64, device=dev)
+    rd = torch.tensor([0.1, 1, 1, 1], dtype=torch.float64, device=dev)
+    Q = pack_lower(torch.diag(qd)).expand(batch, N, sym_size(n)).contiguous()
+    R = pack_lower(torch.diag(rd)).expand(batch, N, sym_size(m)).contiguous()
+    xref = uniform(seed, inst, st, OP_XREF, n)
+    q = -qd * xref
+    xrefN = uniform(seed, inst, N, OP_XREF, n)
+    return RRProblem(n, m, N, A=A.contiguous(), B=B.contiguous(), Q=Q,
+                     M=torch.zeros(batch, N, n * m, dtype=torch.float64, device=dev), R=R, q=q.contiguous(),
+                     r=torch.zeros(batch, N, m, dtype=torch.float64, device=dev),
+                     c=(0.01 * uniform(seed, inst, st, OP_C, n)).contiguous(),
+                     QN=pack_lower(torch.diag(10 * qd)).expand(batch, sym_size(n)).contiguous(),
+                     qN=(-10 * qd * xrefN).contiguous(), c0=uniform(seed, inst, 0, OP_C0, n).contiguous(),
+                     delta=torch.full((batch,), float(delta), dtype=torch.float64, device=dev))
