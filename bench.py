@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample wall time")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
+                    help="c2 (default, BASELINE configs[1]); c4 = ipm_step on 16,384 cart-pole instances")
     return ap.parse_args()
 
 
@@ -62,13 +64,9 @@ def barrier(ws):
 
 
 def max_over_ranks(v, ws):
-    if ws == 1:
-        return v
+    from paper_2509_16370_b200.shard import max_over_ranks as _m
     import torch
-    import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return _m(v, device=torch.device("cuda", torch.cuda.current_device())) if ws > 1 else v
 
 
 class ClockSampler:
@@ -121,6 +119,17 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ncu_traffic(kernel_key):
+    """DRAM bytes per launch of the kernel from the committed ncu --set full capture summary
+    (profiles/traffic.json, written by tools/record_traffic.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d.get(kernel_key)
+    except (OSError, ValueError):
+        return None
 
 
 def measured_peaks():
@@ -203,8 +212,10 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if a.workload == "c4":
+        return run_c4(a, ws, rank, local)
     B = a.batch
-    first = rank * B
+    first = rank * B  # weak scaling: every rank owns B instances (global ids [rB, (r+1)B))
     # ---- inputs resident in HBM (generation excluded from timing) ----
     prob = synth.empty_problem(NX, NU, HORIZON, B, device=dev)
     for s in range(0, B, 4096):
@@ -288,7 +299,7 @@ def main():
                    "l2": "inputs 18.7 GB/GPU > 126 MB L2 (no flush needed)"},
         "stage_updates_per_s": solves * HORIZON,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": ncu_traffic("rr_fused_c2"),
                      "kernel": "rr_fused_kernel<12,4,16>", "kernel_ms": kern_ms,
                      "alg_bytes_per_stage": ALG_BYTES_PER_STAGE, "peak_source": peak_src,
                      "fp64_alg_tflops": ALG_FLOPS_PER_STAGE * B * HORIZON / (kern_ms / 1e3) / 1e12},
@@ -300,6 +311,48 @@ def main():
         line["cpu_baseline"] = cpu_baseline(a.cpu_seconds)
     print(json.dumps(line), flush=True)
     barrier(ws)
+
+
+def run_c4(a, ws, rank, local):
+    """Extra line (not the driver's default): one batched regularized-IPM step (rows a1-a8) on the
+    C4 cart-pole workload, 16,384 instances per GPU, N = 100.  The iterate is updated in place, so
+    consecutive timed steps are consecutive IPM iterations at fixed (μ, η)."""
+    import torch
+    import paper_2509_16370_b200 as rr
+    from synth.ipm_workloads import cartpole_c4
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    B, Nh = 16384, 100
+    b = cartpole_c4(B, seed=2511, N=Nh, first=rank * B, device=dev)
+    call = rr.IpmCall(b)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(3, a.warmup)):
+        call.launch(stream)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    barrier(ws)
+    torch.cuda.synchronize()
+    for k in range(a.steps):
+        ev[k][0].record(stream)
+        call.launch(stream)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    ms = max_over_ranks(sum(s_.elapsed_time(e_) for s_, e_ in ev) / a.steps, ws)
+    st = call.res["status"]
+    if rank == 0:
+        alg = 1900 * B * Nh  # SURVEY §8(d) C4 row: ~1.9 KB per (instance, stage)
+        peak, src = measured_peaks()
+        print(json.dumps({
+            "metric": "regularized-IPM steps/s (C4 cart-pole, rows a1-a8)", "value": B * ws / (ms / 1e3),
+            "unit": "instance-steps/s", "n_gpus": ws, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C4: %d cart-pole IPM iterates per GPU, N=%d, n_g=4" % (B, Nh)},
+            "status_nonzero": int((st != 0).sum()),
+            "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": ncu_traffic("ipm_c4"),
+                         "alg_bytes_per_stage": 1900, "peak_source": src},
+            "gpu_launches": a.steps}), flush=True)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,416 @@
+// rr_cta.cu -- fused regularized-Riccati factor + solve for LARGE stages (C3: n_x = 64, n_u = 32):
+// one CTA per instance, all stage matrices resident in shared memory, every dense contraction on
+// the FP64 tensor-core path (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4), pivots on the SIMT path.
+//
+// Method (arXiv 2509.16370, P:n = PAPER.md line n), per stage i = N-1..0 (Eq.(RR)):
+//   S⁻¹ = (I + δV_{i+1})⁻¹                      symmetric sweep (SPD, eigenvalues >= 1)
+//   [W | W e] = S⁻¹ [V | V e], e = c_{i+1} − δ v_{i+1}          (W_i; g_i = v + W e)
+//   [T | g] = [W F | g],  F = [A B]
+//   [U | b] = Fᵀ [T | g] + [P | (q; r)]          U = [[AᵀWA+Q, Hᵀ]; [H, G]], b = [q+Aᵀg; r+Bᵀg]
+//   G⁻¹ by a symmetric sweep; K̃ = G⁻¹ [H | h]                    (−K_i, −k_i)
+//   [V_i | v_i] = [AᵀWA+Q | q+Aᵀg] − Hᵀ K̃                        (P:623-624 with P:606-611)
+//   [Φ_i | φ_i] = S⁻¹ ([A | c_{i+1} − δ v_{i+1}] − B K̃)  -> record for the forward sweep
+// forward: x_{i+1} = Φ_i x_i + φ_i, u_i = K_i x_i + k_i, y_i = V_i x_i + v_i.
+// Shared-memory plan (doubles) for one instance: stage input (cp.async) | S⁻¹ | V/W/U | T/K̃/M |
+// vectors -- about 230 KB, one CTA per SM; the next stage's input streams in during the last
+// contraction of the current stage.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "rr_common.cuh"
+#include "rr_cta.cuh"
+#include "rr_stage_mma.cuh"
+
+namespace rrk {
+
+template <int NX, int NU>
+struct CtaLayout {
+  static constexpr int NZ = NX + NU;
+  static constexpr int SN = NX * (NX + 1) / 2, SMU = NU * (NU + 1) / 2;
+  // stage input in the global operand order: A | B (= F, col-major ld NX) | Q | M | R | q | r | c
+  static constexpr int oA = 0, oB = NX * NX, oQ = oB + NX * NU, oM = oQ + SN, oR = oM + NX * NU, oq = oR + SMU,
+                       orr = oq + NX, oc = orr + NU;
+  static constexpr int IN = ((oc + NX + 1) & ~1);
+  static constexpr int SI = IN;                                   // S⁻¹, NX × NX (ld NX)
+  static constexpr int VW = SI + NX * NX;                         // [V | Ve] / [W | We] (ld NX, NX+1 cols)
+  // U parts (after W is consumed): Uxx | bx (ld NX, NX+1 cols), Uux | bu (ld NU, NX+1 cols), Uuu (ld NU)
+  static constexpr int Uxx = VW;
+  static constexpr int Uux = Uxx + NX * (NX + 1);
+  static constexpr int Uuu = Uux + NU * (NX + 1);
+  static constexpr int VWU_END = Uuu + NU * NU;
+  static constexpr int TT = ((VWU_END + 1) & ~1);                 // [T | g] (ld NX, NZ+1 cols); later K̃, M
+  static constexpr int Kt = TT;                                   // K̃ = G⁻¹[Uux | bu] (ld NU, NX+1 cols)
+  static constexpr int MM = Kt + ((NU * (NX + 1) + 1) & ~1);      // M (ld NX, NX+1 cols)
+  static constexpr int T_END = TT + (NX * (NZ + 1) > (MM - TT) + NX * (NX + 1) ? NX * (NZ + 1) : (MM - TT) + NX * (NX + 1));
+  static constexpr int VEC = ((T_END + 1) & ~1);
+  static constexpr int vs = VEC;         // v_{i+1} (NX)
+  static constexpr int pr = vs + NX;     // pivot column buffer / g / x_{i+1} (2 × NX)
+  static constexpr int xs = pr + 2 * NX;  // x (NX)
+  static constexpr int TOTAL = xs + NX;
+  static constexpr int red = TT;          // forward-pass partial sums (4 × (2NX+NU)), TT is dead then
+  static_assert(4 * (2 * NX + NU) <= T_END - TT, "partial-sum buffer does not fit the T region");
+  // forward record (global, per stage): Φ̃ (ld NX, NX+1 cols) | K (ld NU, NX cols) | k | V (ld NX) | v
+  static constexpr int rPHI = 0, rK = NX * (NX + 1), rk = rK + NU * NX, rV = rk + NU, rv = rV + NX * NX;
+  static constexpr int REC = ((rv + NX + 1) & ~1);
+};
+
+// C (rows < Mlim, cols < Nlim) = sign * op(A) · B + Cinit, all column-major in shared memory.
+// op(A) = A (M×K, ld lda) or Aᵀ (A stored K×M, ld lda).  M, N multiples of 8 (padded tiles are
+// computed and masked on store); K multiple of 4.  Warps take 16×16 super-tiles round-robin.
+// Cinit(r, c) is a functor (returns 0 for a plain product).  Store(r, c, v) writes the result.
+template <int M, int N, int K, bool TRANS_A, typename LoadA, typename LoadB, typename Init, typename Store>
+__device__ __forceinline__ void cta_gemm(LoadA&& la, LoadB&& lb, Init&& init, Store&& store, int warp, int nwarps,
+                                         int lane) {
+  constexpr int MT = (M + 15) / 16, NT = (N + 15) / 16, KT = K / 4;
+  static_assert(K % 4 == 0, "K must be a multiple of 4");
+  const int g = lane >> 2, t = lane & 3;
+  for (int tile = warp; tile < MT * NT; tile += nwarps) {
+    const int m0 = (tile % MT) * 16, n0 = (tile / MT) * 16;
+    double c[2][2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = m0 + 8 * a + g, col = n0 + 8 * b + 2 * t + e;
+          c[a][b][e] = (r < M && col < N) ? init(r, col) : 0.0;
+        }
+#pragma unroll 4
+    for (int kt = 0; kt < KT; ++kt) {
+      double av[2], bv[2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int r = m0 + 8 * a + g;
+        av[a] = (r < M) ? la(r, 4 * kt + t) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int col = n0 + 8 * b + g;
+        bv[b] = (col < N) ? lb(4 * kt + t, col) : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma884(c[a][b][0], c[a][b][1], av[a], bv[b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = m0 + 8 * a + g, col = n0 + 8 * b + 2 * t + e;
+          if (r < M && col < N) store(r, col, c[a][b][e]);
+        }
+  }
+}
+
+// In-place symmetric sweep of the n×n SPD matrix A (ld lda) in shared memory: A <- −A⁻¹.
+// Pivot p: Ã_pp = −1/A_pp, Ã_rp = A_rp/A_pp, Ã_pc = A_pc/A_pp, Ã_rc = A_rc − A_rp A_pc/A_pp.
+// Returns (in *fail) whether a pivot was not > 0 (block-uniform).
+template <int n>
+__device__ __forceinline__ void cta_sweep(double* A, int lda, double* colbuf, int tid, int nthreads, bool* fail) {
+  bool bad = false;
+  for (int p = 0; p < n; ++p) {
+    for (int r = tid; r < n; r += nthreads) colbuf[r] = A[r + p * lda];  // column p (= row p)
+    __syncthreads();
+    const double d = colbuf[p];
+    bad |= !(d > 0.0);
+    const double id = rcp_nr(d);
+    for (int e = tid; e < n * n; e += nthreads) {
+      const int r = e % n, c = e / n;
+      const double arc = A[r + c * lda];
+      double v;
+      if (r == p && c == p) v = -id;
+      else if (r == p) v = colbuf[c] * id;           // row p = column p (symmetric)
+      else if (c == p) v = colbuf[r] * id;
+      else v = fma(-colbuf[r] * id, colbuf[c], arc);
+      A[r + c * lda] = v;
+    }
+    __syncthreads();
+  }
+  *fail = bad;
+}
+
+template <int NX, int NU, int NTHREADS>
+__global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) {
+  using L = CtaLayout<NX, NU>;
+  constexpr int NZ = NX + NU;
+  constexpr int n = NX, m = NU;
+  constexpr int NW = NTHREADS / 32;
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t inst = blockIdx.x;
+  const int N = a.N;
+  const int64_t sN = N;
+  const double delta = a.p.delta[inst];
+  double* rec0 = a.ws + inst * sN * L::REC;
+  int32_t st = 0;
+
+  auto issue_stage = [&](int i) {
+    const int64_t s = inst * sN + i;
+    copy_async(sm + L::oA, a.p.A + s * n * n, n * n, tid, NTHREADS);
+    copy_async(sm + L::oB, a.p.B + s * n * m, n * m, tid, NTHREADS);
+    copy_async(sm + L::oQ, a.p.Q + s * L::SN, L::SN, tid, NTHREADS);
+    copy_async(sm + L::oM, a.p.M + s * n * m, n * m, tid, NTHREADS);
+    copy_async(sm + L::oR, a.p.R + s * L::SMU, L::SMU, tid, NTHREADS);
+    copy_async(sm + L::oq, a.p.q + s * n, n, tid, NTHREADS);
+    copy_async(sm + L::orr, a.p.r + s * m, m, tid, NTHREADS);
+    copy_async(sm + L::oc, a.p.c + s * n, n, tid, NTHREADS);
+    cp_async_commit();
+  };
+  // V_N = Q_N -> [V | ·] region (ld NX), v_N = q_N
+  {
+    const double* QN = a.p.QN + inst * L::SN;
+    for (int e = tid; e < n * n; e += NTHREADS) {
+      const int r = e % n, c = e / n;
+      sm[L::VW + e] = r >= c ? QN[pidx(n, r, c)] : QN[pidx(n, c, r)];
+    }
+    for (int r = tid; r < n; r += NTHREADS) sm[L::vs + r] = a.p.qN[inst * n + r];
+    if (a.f.V != nullptr)
+      for (int e = tid; e < L::SN; e += NTHREADS) a.f.V[(inst * (sN + 1) + N) * L::SN + e] = QN[e];
+    if (a.f.v != nullptr)
+      for (int r = tid; r < n; r += NTHREADS) a.f.v[(inst * (sN + 1) + N) * n + r] = a.p.qN[inst * n + r];
+  }
+  if (N > 0) issue_stage(N - 1);
+  __syncthreads();
+
+  auto Pat = [&](int s, int t) -> double {  // P = [[Q M]; [Mᵀ R]] from the stage input
+    if (s < NX && t < NX) return s >= t ? sm[L::oQ + pidx(n, s, t)] : sm[L::oQ + pidx(n, t, s)];
+    if (s < NX) return sm[L::oM + s + (t - NX) * n];
+    if (t < NX) return sm[L::oM + t + (s - NX) * n];
+    const int u = s - NX, w = t - NX;
+    return u >= w ? sm[L::oR + pidx(m, u, w)] : sm[L::oR + pidx(m, w, u)];
+  };
+
+  for (int i = N - 1; i >= 0; --i) {
+    cp_async_wait<0>();
+    __syncthreads();
+    double* rec = rec0 + (int64_t)i * L::REC;
+    // S = I + δV -> SI; column NX of [V | ·] = V e with e = c_{i+1} − δ v_{i+1}
+    for (int e = tid; e < n * n; e += NTHREADS) {
+      const int r = e % n, c = e / n;
+      sm[L::SI + e] = delta * sm[L::VW + e] + (r == c ? 1.0 : 0.0);
+    }
+    for (int r = tid; r < n; r += NTHREADS) {
+      double acc = 0.0;
+      for (int k = 0; k < n; ++k) acc = fma(sm[L::VW + r + k * n], sm[L::oc + k] - delta * sm[L::vs + k], acc);
+      sm[L::VW + n * n + r] = acc;
+    }
+    __syncthreads();
+    bool fail = false;
+    cta_sweep<NX>(sm + L::SI, n, sm + L::pr, tid, NTHREADS, &fail);  // SI = −S⁻¹
+    if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, i);
+    // [W | We] = S⁻¹ [V | Ve]  -> TT region temporarily (ld NX), then g = v + We
+    cta_gemm<NX, NX + 1, NX, false>(
+        [&](int r, int k) { return -sm[L::SI + r + k * n]; }, [&](int k, int c) { return sm[L::VW + k + c * n]; },
+        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::TT + r + c * n] = v; }, warp, NW, lane);
+    __syncthreads();
+    // W -> VW region; g = v + We -> column NZ of [T | g] comes later (keep in pr)
+    for (int e = tid; e < n * n; e += NTHREADS) sm[L::VW + e] = sm[L::TT + e];
+    for (int r = tid; r < n; r += NTHREADS) sm[L::pr + r] = sm[L::vs + r] + sm[L::TT + n * n + r];
+    __syncthreads();
+    // [T | g] = [W F | g]   (F = [A B] = stage input columns, ld NX)
+    cta_gemm<NX, NZ, NX, false>(
+        [&](int r, int k) { return sm[L::VW + r + k * n]; }, [&](int k, int c) { return sm[L::oA + k + c * n]; },
+        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::TT + r + c * n] = v; }, warp, NW, lane);
+    for (int r = tid; r < n; r += NTHREADS) sm[L::TT + NZ * n + r] = sm[L::pr + r];
+    __syncthreads();
+    // [U | b] = Fᵀ [T | g] + [P | (q; r)]: rows x -> Uxx|bx (ld NX), rows u -> Uux|bu, Uuu (ld NU)
+    cta_gemm<NZ, NZ + 1, NX, true>(
+        [&](int r, int k) { return sm[L::oA + k + r * n]; }, [&](int k, int c) { return sm[L::TT + k + c * n]; },
+        [&](int r, int c) { return c < NZ ? Pat(r, c) : (r < NX ? sm[L::oq + r] : sm[L::orr + r - NX]); },
+        [&](int r, int c, double v) {
+          if (r < NX) {
+            if (c < NX) sm[L::Uxx + r + c * n] = v;
+            else if (c == NZ) sm[L::Uxx + r + NX * n] = v;  // b_x
+          } else {
+            const int u = r - NX;
+            if (c < NX) sm[L::Uux + u + c * m] = v;
+            else if (c == NZ) sm[L::Uux + u + NX * m] = v;  // b_u
+            else sm[L::Uuu + u + (c - NX) * m] = v;          // G
+          }
+        },
+        warp, NW, lane);
+    __syncthreads();
+    // G⁻¹ (sweep in place: Uuu = −G⁻¹), K̃ = G⁻¹ [H | h]
+    cta_sweep<NU>(sm + L::Uuu, m, sm + L::pr, tid, NTHREADS, &fail);
+    if (fail && st == 0) st = mk_status(RR_ST_G_NOT_PD, i);
+    cta_gemm<NU, NX + 1, NU, false>(
+        [&](int r, int k) { return -sm[L::Uuu + r + k * m]; }, [&](int k, int c) { return sm[L::Uux + k + c * m]; },
+        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::Kt + r + c * m] = v; }, warp, NW, lane);
+    __syncthreads();
+    // [V_i | v_i] = [Uxx | bx] − Hᵀ K̃  (in place: each tile reads its own init)
+    cta_gemm<NX, NX + 1, NU, true>(
+        [&](int r, int k) { return -sm[L::Uux + k + r * m]; }, [&](int k, int c) { return sm[L::Kt + k + c * m]; },
+        [&](int r, int c) { return sm[L::Uxx + r + c * n]; }, [&](int r, int c, double v) { sm[L::Uxx + r + c * n] = v; },
+        warp, NW, lane);
+    // M = [A | c − δ v_{i+1}] − B K̃  (K̃ column NX = G⁻¹h = −k)
+    cta_gemm<NX, NX + 1, NU, false>(
+        [&](int r, int k) { return -sm[L::oB + r + k * n]; }, [&](int k, int c) { return sm[L::Kt + k + c * m]; },
+        [&](int r, int c) { return c < NX ? sm[L::oA + r + c * n] : sm[L::oc + r] - delta * sm[L::vs + r]; },
+        [&](int r, int c, double v) { sm[L::MM + r + c * n] = v; }, warp, NW, lane);
+    __syncthreads();
+    // record K = −K̃[:, :NX] (ld NU), k = −K̃[:, NX], V_i (ld NX), v_i; optional factor outputs
+    for (int e = tid; e < m * n; e += NTHREADS) rec[L::rK + e] = -sm[L::Kt + e];
+    for (int u = tid; u < m; u += NTHREADS) rec[L::rk + u] = -sm[L::Kt + u + NX * m];
+    for (int e = tid; e < n * n; e += NTHREADS) rec[L::rV + e] = sm[L::Uxx + e];
+    for (int r = tid; r < n; r += NTHREADS) rec[L::rv + r] = sm[L::Uxx + NX * n + r];
+    if (a.f.K != nullptr)
+      for (int e = tid; e < m * n; e += NTHREADS) a.f.K[(inst * sN + i) * m * n + e] = -sm[L::Kt + e];
+    if (a.f.k != nullptr)
+      for (int u = tid; u < m; u += NTHREADS) a.f.k[(inst * sN + i) * m + u] = -sm[L::Kt + u + NX * m];
+    if (a.f.V != nullptr)
+      for (int e = tid; e < L::SN; e += NTHREADS) {
+        int c = 0, off = e;
+        while (off >= n - c) { off -= n - c; ++c; }
+        a.f.V[(inst * (sN + 1) + i) * L::SN + e] = sm[L::Uxx + (c + off) + c * n];
+      }
+    if (a.f.v != nullptr)
+      for (int r = tid; r < n; r += NTHREADS) a.f.v[(inst * (sN + 1) + i) * n + r] = sm[L::Uxx + NX * n + r];
+    __syncthreads();
+    // stage input is dead: stream the next stage in while [Φ | φ] = S⁻¹ M is formed
+    if (i > 0) issue_stage(i - 1);
+    cta_gemm<NX, NX + 1, NX, false>(
+        [&](int r, int k) { return -sm[L::SI + r + k * n]; }, [&](int k, int c) { return sm[L::MM + k + c * n]; },
+        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { rec[L::rPHI + r + c * n] = v; }, warp, NW, lane);
+    // carry: V_i -> VW region (already in place: Uxx == VW with ld NX), v_i -> vs
+    for (int r = tid; r < n; r += NTHREADS) sm[L::vs + r] = sm[L::Uxx + NX * n + r];
+    __syncthreads();
+  }
+
+  // x_0 = (I + δV_0)⁻¹ (c_0 − δ v_0)
+  for (int e = tid; e < n * n; e += NTHREADS) {
+    const int r = e % n, c = e / n;
+    sm[L::SI + e] = delta * sm[L::VW + e] + (r == c ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  {
+    bool fail = false;
+    cta_sweep<NX>(sm + L::SI, n, sm + L::pr, tid, NTHREADS, &fail);
+    if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, 0);
+  }
+  for (int r = tid; r < n; r += NTHREADS) {
+    double acc = 0.0;
+    for (int k = 0; k < n; ++k) acc = fma(-sm[L::SI + r + k * n], a.p.c0[inst * n + k] - delta * sm[L::vs + k], acc);
+    sm[L::xs + r] = acc;
+  }
+  __syncthreads();
+  // block-wide status: any thread's failure (same value on all threads of a block in practice)
+  __shared__ int sst;
+  if (tid == 0) sst = 0;
+  __syncthreads();
+  if (st != 0) atomicMax(&sst, st);
+  __syncthreads();
+  int32_t status = sst;
+
+  double* xo = a.s.x + inst * (sN + 1) * n;
+  double* uo = a.s.u + inst * sN * m;
+  double* yo = a.s.y + inst * (sN + 1) * n;
+  for (int r = tid; r < n; r += NTHREADS) xo[r] = sm[L::xs + r];
+  bool bad = false;
+  // forward: thread (row, part): row = tid % NZ-ish split; 4 partial sums per output row
+  constexpr int PARTS = NTHREADS / 64 > 4 ? 4 : NTHREADS / 64;
+  for (int i = 0; i < N; ++i) {
+    const double* rec = rec0 + (int64_t)i * L::REC;
+    for (int task = tid; task < PARTS * (2 * NX + NU); task += NTHREADS) {
+      const int part = task / (2 * NX + NU), row = task % (2 * NX + NU);
+      const int k0 = part * (NX / PARTS), k1 = k0 + NX / PARTS;
+      double acc = 0.0;
+      if (row < NX) {  // x_{i+1} row
+        for (int k = k0; k < k1; ++k) acc = fma(rec[L::rPHI + row + k * n], sm[L::xs + k], acc);
+      } else if (row < 2 * NX) {  // y_i row
+        const int rr = row - NX;
+        for (int k = k0; k < k1; ++k) acc = fma(rec[L::rV + rr + k * n], sm[L::xs + k], acc);
+      } else {  // u_i row
+        const int u = row - 2 * NX;
+        for (int k = k0; k < k1; ++k) acc = fma(rec[L::rK + u + k * m], sm[L::xs + k], acc);
+      }
+      sm[L::red + part * (2 * NX + NU) + row] = acc;
+    }
+    __syncthreads();
+    for (int row = tid; row < 2 * NX + NU; row += NTHREADS) {
+      double acc = 0.0;
+      for (int p = 0; p < PARTS; ++p) acc += sm[L::red + p * (2 * NX + NU) + row];
+      if (row < NX) {
+        acc += rec[L::rPHI + row + NX * n];
+        xo[(int64_t)(i + 1) * n + row] = acc;
+        sm[L::pr + row] = acc;
+      } else if (row < 2 * NX) {
+        acc += rec[L::rv + row - NX];
+        yo[(int64_t)i * n + row - NX] = acc;
+      } else {
+        acc += rec[L::rk + row - 2 * NX];
+        uo[(int64_t)i * m + row - 2 * NX] = acc;
+      }
+      bad |= !isfinite(acc);
+    }
+    __syncthreads();
+    for (int r = tid; r < n; r += NTHREADS) sm[L::xs + r] = sm[L::pr + r];
+    __syncthreads();
+  }
+  {  // y_N = Q_N x_N + q_N
+    const double* QN = a.p.QN + inst * L::SN;
+    for (int r = tid; r < n; r += NTHREADS) {
+      double acc = a.p.qN[inst * n + r];
+      for (int k = 0; k < n; ++k) acc = fma(k >= r ? QN[pidx(n, k, r)] : QN[pidx(n, r, k)], sm[L::xs + k], acc);
+      yo[sN * n + r] = acc;
+      bad |= !isfinite(acc);
+    }
+  }
+  if (__syncthreads_or(bad) && status == 0) status = RR_ST_NONFINITE;
+  if (status != 0) {
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    for (int64_t e = tid; e < (sN + 1) * n; e += NTHREADS) {
+      xo[e] = nan;
+      yo[e] = nan;
+    }
+    for (int64_t e = tid; e < sN * m; e += NTHREADS) uo[e] = nan;
+  }
+  if (tid == 0) a.status[inst] = status;
+}
+
+template <int NX, int NU>
+struct CtaCfg {
+  static constexpr int NTHREADS = 256;
+  static size_t smem_bytes() { return sizeof(double) * (size_t)CtaLayout<NX, NU>::TOTAL; }
+  static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * CtaLayout<NX, NU>::REC; }
+  static cudaError_t launch(const FusedArgs& a, cudaStream_t s) {
+    auto k = rr_cta_kernel<NX, NU, NTHREADS>;
+    const size_t smb = smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
+    if (e != cudaSuccess) return e;
+    k<<<(unsigned)a.batch, NTHREADS, smb, s>>>(a);
+    return cudaGetLastError();
+  }
+};
+
+template <typename F>
+static bool dispatch_cta(int nx, int nu, F&& f) {
+  if (nx == 64 && nu == 32) return f(CtaCfg<64, 32>{});
+  if (nx == 32 && nu == 16) return f(CtaCfg<32, 16>{});
+  if (nx == 24 && nu == 8) return f(CtaCfg<24, 8>{});
+  return false;
+}
+
+int64_t cta_workspace_bytes(int nx, int nu, int N, int64_t batch) {
+  int64_t out = -1;
+  dispatch_cta(nx, nu, [&](auto cfg) {
+    out = 8 * decltype(cfg)::ws_doubles(batch, N) + 256;
+    return true;
+  });
+  return out;
+}
+
+cudaError_t cta_launch(const FusedArgs& a, cudaStream_t s, bool* supported) {
+  cudaError_t err = cudaSuccess;
+  *supported = dispatch_cta(a.nx, a.nu, [&](auto cfg) {
+    err = decltype(cfg)::launch(a, s);
+    return true;
+  });
+  return err;
+}
+
+}  // namespace rrk

@@ -25,6 +25,7 @@
 #include "rr_fused.cuh"
 #include "rr_stage.cuh"
 #include "rr_stage_mma.cuh"
+#include "rr_cta.cuh"
 
 namespace rrk {
 
@@ -582,10 +583,11 @@ static bool dispatch_fused(int nx, int nu, F&& f) {
 
 int64_t fused_workspace_bytes(int nx, int nu, int N, int64_t batch) {
   int64_t out = -1;
-  dispatch_fused(nx, nu, [&](auto cfg) {
+  const bool small = dispatch_fused(nx, nu, [&](auto cfg) {
     out = 8 * decltype(cfg)::ws_doubles(batch, N) + 256;
     return true;
   });
+  if (!small) out = cta_workspace_bytes(nx, nu, N, batch);  // large stages: CTA per instance
   return out;
 }
 
@@ -595,6 +597,7 @@ cudaError_t fused_launch(const FusedArgs& a, cudaStream_t s, bool* supported) {
     err = decltype(cfg)::launch(a, s);
     return true;
   });
+  if (!*supported) err = cta_launch(a, s, supported);
   return err;
 }
 
