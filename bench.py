@@ -29,6 +29,7 @@ NX, NU, HORIZON, BATCH, SEED, DELTA = 12, 4, 100, 65536, 2509, 1e-4
 # Algorithmic model per (instance, stage), SURVEY.md §8(d) / DESIGN.md §7 (C2 row):
 ALG_BYTES_PER_STAGE = 6976     # fused two-sweep: inputs once + policy write/read + A,B,c re-read + x,u,y
 ALG_FLOPS_PER_STAGE = 15769    # 13,077 factor + 864 vector backward + 1,828 forward
+FP64_DMMA_TFLOPS = 37.1        # measured on this pool by tools/k0_probe.cu (profiles/r01_k0_fp64_probe.txt)
 
 
 def parse():
@@ -41,8 +42,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample wall time")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
-                    help="c2 (default, BASELINE configs[1]); c4 = ipm_step on 16,384 cart-pole instances")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
+                    help="c2 (default, BASELINE configs[1]); c3 = 4,096 dense n64 m32 N50 (configs[2]); "
+                         "c4 = ipm_step on 16,384 cart-pole instances (configs[3])")
     return ap.parse_args()
 
 
@@ -214,12 +216,20 @@ def main():
     dev = torch.device("cuda", local)
     if a.workload == "c4":
         return run_c4(a, ws, rank, local)
+    global NX, NU, HORIZON, BATCH, SEED, ALG_BYTES_PER_STAGE, ALG_FLOPS_PER_STAGE
+    if a.workload == "c3":
+        # 206,208 B and 2.42M flop per stage (algorithmic)
+        NX, NU, HORIZON, BATCH, SEED = 64, 32, 50, 4096, 2510
+        ALG_BYTES_PER_STAGE, ALG_FLOPS_PER_STAGE = 206208, 2420000
+        if a.batch == 65536:
+            a.batch = BATCH
     B = a.batch
     first = rank * B  # weak scaling: every rank owns B instances (global ids [rB, (r+1)B))
     # ---- inputs resident in HBM (generation excluded from timing) ----
     prob = synth.empty_problem(NX, NU, HORIZON, B, device=dev)
-    for s in range(0, B, 4096):
-        e = min(B, s + 4096)
+    gchunk = 4096 if NX <= 16 else 256
+    for s in range(0, B, gchunk):
+        e = min(B, s + gchunk)
         p = synth.random_stable_lqr(NX, NU, HORIZON, e - s, SEED, DELTA, first=first + s, device=dev)
         for f in synth.RRProblem.FIELDS:
             getattr(prob, f)[s:e].copy_(getattr(p, f))
@@ -289,25 +299,36 @@ def main():
     peak, peak_src = measured_peaks()
     alg_bytes = ALG_BYTES_PER_STAGE * B * HORIZON
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    fp64_tflops = ALG_FLOPS_PER_STAGE * B * HORIZON / (kern_ms / 1e3) / 1e12
+    c3 = a.workload == "c3"
+    if c3:  # FP64 contraction-bound backward sweep: roofline against the DMMA peak
+        roof = {"bound": "tensor", "achieved": fp64_tflops, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
+                "frac": fp64_tflops / FP64_DMMA_TFLOPS, "traffic": ncu_traffic("rr_cta_c3"),
+                "kernel": "rr_cta_kernel<64,32>", "kernel_ms": kern_ms, "dtype_peak": "fp64 DMMA",
+                "alg_flops_per_stage": ALG_FLOPS_PER_STAGE,
+                "peak_source": "K0 probe mma.sync m8n8k4 f64 on this pool (profiles/r01_k0_fp64_probe.txt)",
+                "hbm_gbs_alg": achieved}
+    else:
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic("rr_fused_c2"),
+                "kernel": "rr_fused_kernel<12,4,16>", "kernel_ms": kern_ms,
+                "alg_bytes_per_stage": ALG_BYTES_PER_STAGE, "peak_source": peak_src,
+                "fp64_alg_tflops": fp64_tflops}
     line = {
         "metric": METRIC, "value": solves, "unit": "solves/s", "n_gpus": ws, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2: %d random stable regularized LQR per GPU, n_x=%d n_u=%d N=%d delta=%g, FP64"
-                               % (B, NX, NU, HORIZON, DELTA),
+        "config": {"workload": "%s: %d random stable regularized LQR per GPU, n_x=%d n_u=%d N=%d delta=%g, FP64"
+                               % ("C3" if c3 else "C2", B, NX, NU, HORIZON, DELTA),
                    "global_batch": B * ws, "seq_len": HORIZON, "parallelism": "batch-shard x%d" % ws,
-                   "l2": "inputs 18.7 GB/GPU > 126 MB L2 (no flush needed)"},
+                   "l2": "inputs %.1f GB/GPU > 126 MB L2 (no flush needed)" % (prob.nbytes() / 1e9)},
         "stage_updates_per_s": solves * HORIZON,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic("rr_fused_c2"),
-                     "kernel": "rr_fused_kernel<12,4,16>", "kernel_ms": kern_ms,
-                     "alg_bytes_per_stage": ALG_BYTES_PER_STAGE, "peak_source": peak_src,
-                     "fp64_alg_tflops": ALG_FLOPS_PER_STAGE * B * HORIZON / (kern_ms / 1e3) / 1e12},
+        "roofline": roof,
         "clocks": clk,
         "e2e": e2e,
         "gpu_launches": a.steps,
     }
-    if not a.no_cpu_baseline:
+    if not a.no_cpu_baseline and not c3:
         line["cpu_baseline"] = cpu_baseline(a.cpu_seconds)
     print(json.dumps(line), flush=True)
     barrier(ws)

@@ -317,7 +317,7 @@ template <int NX, int NU>
 struct MmaLayout {
   static constexpr int STG = NX * NX + 2 * NX * NU + NX * (NX + 1) / 2 + NU * (NU + 1) / 2 + 2 * NX + NU;
   static constexpr int STG_PAD = (STG + 1) & ~1;
-  static constexpr int SLOT_B = 2 * STG_PAD + WorkM<NX, NU>::PAD;
+  static constexpr int SLOT_B = STG_PAD + WorkM<NX, NU>::PAD;  // single stage buffer (prefetched mid-stage)
   static constexpr int SLOT_F = 2 * RecM<NX, NU>::PAD + NX;
   static constexpr int SLOT = SLOT_B > SLOT_F ? SLOT_B : SLOT_F;
   static constexpr int SLOT_PAD = (SLOT + 1) & ~1;
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   const int grp = lane >> 4, j = lane & 15, gbase = grp * 16;
   double* slotq[2] = {smem + (warp * 2 + 0) * LY::SLOT_PAD, smem + (warp * 2 + 1) * LY::SLOT_PAD};
   double* slot = grp ? slotq[1] : slotq[0];
-  double* wkq[2] = {slotq[0] + 2 * LY::STG_PAD, slotq[1] + 2 * LY::STG_PAD};
+  double* wkq[2] = {slotq[0] + LY::STG_PAD, slotq[1] + LY::STG_PAD};
   double* wk = grp ? wkq[1] : wkq[0];
 
   const int64_t inst0 = ((int64_t)blockIdx.x * WARPS + warp) * 2;
@@ -397,21 +397,24 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   __syncwarp();
 
   for (int i = N - 1; i >= 0; --i) {
-    const int cur = (N - 1 - i) & 1;
-    const double* sbq[2] = {slotq[0] + cur * LY::STG_PAD, slotq[1] + cur * LY::STG_PAD};
-    if (i > 0) issue_stage(i - 1, slot + (cur ^ 1) * LY::STG_PAD);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncwarp();
+    const double* sbq[2] = {slotq[0], slotq[1]};
     const double* Fq[2] = {sbq[0] + oA, sbq[1] + oA};
     const double* cvq[2] = {sbq[0] + oc, sbq[1] + oc};
     const double* sb = grp ? sbq[1] : sbq[0];
-    const double qj = (j < NX) ? sb[oq + j] : sb[orr + j - NX];
+    auto qjf = [&]() -> double { return (j < NX) ? sb[oq + j] : sb[orr + j - NX]; };
     auto P2 = [&](int q, int s, int t) -> double { return Pat(sbq[q], s, t); };
+    auto wait_inputs = [&]() {
+      cp_async_wait<0>();
+      __syncwarp();
+    };
+    auto prefetch = [&]() {
+      if (i > 0) issue_stage(i - 1, slot);
+      cp_async_commit();
+    };
     double* recq[2] = {rec0q[0] ? rec0q[0] + (int64_t)i * RC::PAD : nullptr,
                        rec0q[1] ? rec0q[1] + (int64_t)i * RC::PAD : nullptr};
     double U[NZ], b[NZ];
-    SM::backward(wkq, Fq, cvq, P2, qj, delta, grp, j, lane, Vc, U, b, recq, i, st);
+    SM::backward(wkq, Fq, cvq, P2, qjf, wait_inputs, prefetch, delta, grp, j, lane, Vc, U, b, recq, i, st);
     if (valid) {
       if (a.f.V != nullptr && j < n) {
         double* Vo = a.f.V + (inst * (sN + 1) + i) * sn;

@@ -42,13 +42,13 @@ struct Work {
   static constexpr int NZ = NX + NU;
   static constexpr int NZP = (NZ + 1) & ~1;
   static constexpr int Si = 0;              // S⁻¹ col-major NX×NX
-  static constexpr int Wb = Si + NX * NX;   // W_i col-major NX×NX
-  static constexpr int pub = Wb + NX * NX;  // 2 × NZP pivot-publish buffers
+  static constexpr int pub = Si + NX * NX;  // 2 × NZP pivot-publish buffers
   static constexpr int pq = pub + 2 * NZP;  // pivot column entries of processed u rows (NU, padded)
   static constexpr int vb = pq + ((NU + 1) & ~1);  // b vector (NZ)
   static constexpr int gb = vb + NZP;       // g_i (NX)
   static constexpr int vs = gb + NX;        // v_{i+1} (NX)
-  static constexpr int SIZE = vs + NX;
+  static constexpr int Wb = vs + NX;        // W_i col-major NX×NX (last: the DMMA stage reuses it)
+  static constexpr int SIZE = Wb + NX * NX;
   static constexpr int PAD = (SIZE + 1) & ~1;
 };
 

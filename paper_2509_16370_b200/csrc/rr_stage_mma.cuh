@@ -46,13 +46,16 @@ struct RecM {
   static constexpr int PAD = (SIZE + 1) & ~1;
 };
 
-// Per-instance work area of the MMA stage (doubles, even offsets).
+// Per-instance work area of the MMA stage (doubles, even offsets).  The SIMT helpers of
+// rr_stage.cuh address Si, pub, pq, vb, gb, vs through Work<NX, NU>; WorkM places X1/X2 over
+// Work's (unused here) Wb slot and beyond so that the whole slot stays small.
 template <int NX, int NU>
 struct WorkM {
   static constexpr int NZ = NX + NU;
-  static constexpr int base = Work<NX, NU>::PAD;  // Si, Wb(unused), pub, pq, vb, gb, vs of Work
-  static constexpr int X1 = base;                 // NX × 16 (ld NX): Vs, then T, then M
-  static constexpr int X2 = X1 + NX * 16;         // 16 × 16 (ld 16 for U; ld NX for W)
+  using W = Work<NX, NU>;
+  static_assert(W::Wb + NX * NX == W::SIZE, "Work<> must end with Wb");
+  static constexpr int X1 = W::Wb;              // NX × 16 (ld NX): [V | Ve], then T, then M
+  static constexpr int X2 = X1 + NX * 16;       // 16 × 16: W (ld NX, NX+1 cols), then U (ld 16)
   static constexpr int SIZE = X2 + 16 * 16;
   static constexpr int PAD = (SIZE + 1) & ~1;
 };
@@ -72,20 +75,24 @@ struct StageMMA {
   using RC = RecM<NX, NU>;
 
   // one backward step for the two instances of the warp.
-  //   wkq[q]: work area of instance q; F_q, cv_q: stage F / c_{i+1} of instance q (in the stage buffers)
-  //   grp/j: this lane's instance and column; Pcol(q, s, t): P_i[s][t] of instance q (padded)
-  template <typename PFun>
+  //   wkq[q]: work area of instance q; Fq/cvq: stage F / c_{i+1} of instance q (stage buffer)
+  //   Pat(q, s, t): P_i[s][t] of instance q;  qjf(): this lane's entry of (q_i; r_i)
+  //   wait_inputs(): waits for this stage's input copies (called after the S⁻¹ sweep, which needs
+  //   none);  prefetch(): issues the next stage's input copies (called once the inputs are dead)
+  template <typename PFun, typename QFun, typename WaitFn, typename PrefFn>
   __device__ static __forceinline__ void backward(double* const (&wkq)[2], const double* const (&Fq)[2],
-                                                  const double* const (&cvq)[2], PFun&& Pat, double qj,
-                                                  double delta, int grp, int j, int lane, double (&Vc)[NX],
-                                                  double (&U)[NZ], double (&b)[NZ], double* const (&recq)[2],
-                                                  int stage, int32_t& st) {
+                                                  const double* const (&cvq)[2], PFun&& Pat, QFun&& qjf,
+                                                  WaitFn&& wait_inputs, PrefFn&& prefetch, double delta, int grp,
+                                                  int j, int lane, double (&Vc)[NX], double (&U)[NZ],
+                                                  double (&b)[NZ], double* const (&recq)[2], int stage,
+                                                  int32_t& st) {
     double* wk = grp ? wkq[1] : wkq[0];
     const double* F = grp ? Fq[1] : Fq[0];
     const double* cv = grp ? cvq[1] : cvq[0];
     const int g = lane >> 2, t = lane & 3;
-    // (1) S⁻¹, and Vs = [V | V e] (V symmetric: (V e)_j = column j · e)
+    // (1) S⁻¹ (no stage input needed), then Vs = [V | V e] (V symmetric: (V e)_j = column j · e)
     ST::invS(Vc, delta, j, wk, stage, st);
+    wait_inputs();
     if (j < NX) {
       ST::store_col(wk + WM::X1 + j * NX, Vc);
       double ve0 = 0.0, ve1 = 0.0;
@@ -97,8 +104,7 @@ struct StageMMA {
       wk[WM::X1 + NX * NX + j] = ve0 + ve1;  // column NX of Vs
     }
     __syncwarp();
-    // (2) [W | W e] = S⁻¹ Vs   (rows < NX, cols <= NX);  keep the S⁻¹ A-fragments for (8)
-    double aS[2][MT][KT];
+    // (2) [W | W e] = S⁻¹ Vs -> X2 (ld NX)
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const double* Si = wkq[q] + WK::Si;
@@ -110,20 +116,21 @@ struct StageMMA {
         for (int nt = 0; nt < CT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
+        double aS[MT];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int r = 8 * mt + g;
-          aS[q][mt][kt] = (r < NX) ? Si[(4 * kt + t) * NX + r] : 0.0;
+          aS[mt] = (r < NX) ? Si[(4 * kt + t) * NX + r] : 0.0;
         }
 #pragma unroll
         for (int nt = 0; nt < CT; ++nt) {
           const int col = 8 * nt + g;
           const double bv = (col <= NX) ? Vs[col * NX + 4 * kt + t] : 0.0;
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aS[q][mt][kt], bv);
+          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aS[mt], bv);
         }
       }
-      double* Wb = wkq[q] + WM::X2;  // W col-major ld NX, column NX = W e
+      double* Wb = wkq[q] + WM::X2;
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -142,7 +149,7 @@ struct StageMMA {
     {
       double gk[NX];
       ST::bcast(wk + WK::gb, gk);
-      double b0 = qj, b1 = 0.0;
+      double b0 = qjf(), b1 = 0.0;
 #pragma unroll
       for (int k = 0; k < NX; k += 2) {
         const double2 f2 = *reinterpret_cast<const double2*>(F + jc * NX + k);
@@ -151,8 +158,7 @@ struct StageMMA {
       }
       if (j < NZ) wk[WK::vb + j] = b0 + b1;
     }
-    // (4) T = W F (NX × NZ) -> X1 (ld NX);  keep F fragments (B of T, A of Fᵀ)
-    double fF[2][ZT][KT];
+    // (4) T = W F (NX × NZ) -> X1 (ld NX)
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const double* Wb = wkq[q] + WM::X2;
@@ -173,12 +179,11 @@ struct StageMMA {
 #pragma unroll
         for (int nt = 0; nt < ZT; ++nt) {
           const int col = 8 * nt + g;
-          fF[q][nt][kt] = (col < NZ) ? Fx[col * NX + 4 * kt + t] : 0.0;
+          const double bF = (col < NZ) ? Fx[col * NX + 4 * kt + t] : 0.0;
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aW[mt], fF[q][nt][kt]);
+          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aW[mt], bF);
         }
       }
-      __syncwarp();  // all lanes done reading Vs (X1) of instance q before T overwrites it
       double* Tb = wkq[q] + WM::X1;
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -191,10 +196,11 @@ struct StageMMA {
           }
     }
     __syncwarp();
-    // (5) U = Fᵀ T + P (NZ × NZ) -> X2 (ld 16)
+    // (5) U = Fᵀ T + P (NZ × NZ) -> X2 (ld 16); A-fragment of Fᵀ = B-fragment layout of F
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const double* Tb = wkq[q] + WM::X1;
+      const double* Fx = Fq[q];
       double c[ZT][ZT][2];
 #pragma unroll
       for (int mt = 0; mt < ZT; ++mt)
@@ -206,14 +212,21 @@ struct StageMMA {
             c[mt][nt][e] = (r < NZ && col < NZ) ? Pat(q, r, col) : 0.0;
           }
 #pragma unroll
-      for (int kt = 0; kt < KT; ++kt)
+      for (int kt = 0; kt < KT; ++kt) {
+        double aF[ZT];
+#pragma unroll
+        for (int mt = 0; mt < ZT; ++mt) {
+          const int col = 8 * mt + g;
+          aF[mt] = (col < NZ) ? Fx[col * NX + 4 * kt + t] : 0.0;
+        }
 #pragma unroll
         for (int nt = 0; nt < ZT; ++nt) {
           const int col = 8 * nt + g;
           const double bT = (col < NZ) ? Tb[col * NX + 4 * kt + t] : 0.0;
 #pragma unroll
-          for (int mt = 0; mt < ZT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], fF[q][mt][kt], bT);
+          for (int mt = 0; mt < ZT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aF[mt], bT);
         }
+      }
       double* Ub = wkq[q] + WM::X2;
 #pragma unroll
       for (int mt = 0; mt < ZT; ++mt)
@@ -227,7 +240,11 @@ struct StageMMA {
     __syncwarp();
     // (6) Gauss-Jordan on the u-block (SIMT, lane j owns column j)
 #pragma unroll
-    for (int s = 0; s < NZ; ++s) U[s] = (j < NZ) ? wk[WM::X2 + jc * 16 + s] : 0.0;
+    for (int s = 0; s < NZ; s += 2) {
+      const double2 u2 = *reinterpret_cast<const double2*>(wk + WM::X2 + jc * 16 + s);
+      U[s] = (j < NZ) ? u2.x : 0.0;
+      U[s + 1] = (j < NZ) ? u2.y : 0.0;
+    }
 #pragma unroll
     for (int s = 0; s < NZ; ++s) b[s] = wk[WK::vb + s];
 #pragma unroll
@@ -280,9 +297,11 @@ struct StageMMA {
       ST::store_col(wk + WM::X1 + j * NX, tcol);
     }
     __syncwarp();
+    prefetch();  // the stage inputs (F, P, q, r, c) are dead from here on
     // (8) [Φ | φ] = S⁻¹ M -> record (row-major, ld NX+2), straight from the C fragments
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
+      const double* Si = wkq[q] + WK::Si;
       const double* Mb = wkq[q] + WM::X1;
       double c[MT][CT][2];
 #pragma unroll
@@ -290,14 +309,21 @@ struct StageMMA {
 #pragma unroll
         for (int nt = 0; nt < CT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
 #pragma unroll
-      for (int kt = 0; kt < KT; ++kt)
+      for (int kt = 0; kt < KT; ++kt) {
+        double aS[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r = 8 * mt + g;
+          aS[mt] = (r < NX) ? Si[(4 * kt + t) * NX + r] : 0.0;
+        }
 #pragma unroll
         for (int nt = 0; nt < CT; ++nt) {
           const int col = 8 * nt + g;
           const double bM = (col <= NX) ? Mb[col * NX + 4 * kt + t] : 0.0;
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aS[q][mt][kt], bM);
+          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aS[mt], bM);
         }
+      }
       double* rec = recq[q];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
