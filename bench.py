@@ -311,7 +311,7 @@ def main():
     else:
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic("rr_fused_c2"),
-                "kernel": "rr_fused_kernel<12,4,16>", "kernel_ms": kern_ms,
+                "kernel": "rr_fused_mma_kernel<12,4> (DMMA stage, TMA loads)", "kernel_ms": kern_ms,
                 "alg_bytes_per_stage": ALG_BYTES_PER_STAGE, "peak_source": peak_src,
                 "fp64_alg_tflops": fp64_tflops}
     line = {

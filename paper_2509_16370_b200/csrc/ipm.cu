@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   using IB = IpmBuf<NX, NU, NG, NC>;
   constexpr int NZ = NX + NU;
   constexpr int IPW = 32 / LG;
-  constexpr int SLOT = ((IB::PAD + WK::PAD + 2 * RC::PAD + NX + 1) & ~1);
+  constexpr int SLOT = ((2 * IB::PAD + WK::PAD + 2 * RC::PAD + NX + 1) & ~1);
   static_assert(NG <= LG && NC <= LG, "constraint count per stage exceeds the lane group");
 
   const int n = a.d.nx, m = a.d.nu, N = a.d.N, w = n + m;
@@ -83,8 +83,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / LG, j = lane % LG, gbase = grp * LG;
   double* slot = smem + (warp * IPW + grp) * SLOT;
-  double* sb = slot;              // IPM stage data (padded)
-  double* wk = slot + IB::PAD;    // Riccati work area
+  double* wk = slot + 2 * IB::PAD;  // Riccati work area (two padded IPM stage buffers before it)
   double* rbuf = wk + WK::PAD;    // one forward record
   double* xs = rbuf + 2 * RC::PAD;
 
@@ -98,106 +97,116 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   int32_t st = 0;
   int nonpos_stage = 0x7fffffff;
 
-  // ---- load stage i (i == N: terminal) of the IPM data into the padded shared layout ----
-  auto load_stage = [&](int i) {
+  // double-buffered stage data: sbuf[0], sbuf[1]; `sb` points at the current one
+  double* sbuf0 = slot;
+  double* sbuf1 = slot + IB::PAD;
+  double* sb = sbuf0;
+  // ---- issue the loads of stage i (i == N: terminal) into the padded shared layout `dst` ----
+  // Real elements travel by cp.async (8-byte LDGSTS, asynchronous); padding is stored directly.
+  // finish_stage() completes Σ, r_z and the positivity check once the copies have landed.
+  auto issue_stage_data = [&](int i, double* dst) {
     const bool term = (i == N);
     const int ww = term ? n : w;
     const int ng = term ? a.d.ngN : a.d.ng;
     const int nc = term ? a.d.ncN : a.d.nc;
     const int64_t si = inst * sN + i;
-    for (int e = j; e < NX * NZ; e += LG) {  // F
+    auto put = [&](int off, const double* src, bool ok, double pad) {
+      if (ok) cp_async8(dst + off, src);
+      else dst[off] = pad;
+    };
+    for (int e = j; e < NX * NZ; e += LG) {  // F = [A B]
       const int k = e % NX, c = e / NX;
-      double v = 0.0;
-      if (!term && k < n) {
-        if (c < NX) v = (c < n) ? a.d_.A[si * n * n + k + c * n] : 0.0;
-        else if (c - NX < m) v = a.d_.B[si * n * m + k + (c - NX) * n];
-      }
-      sb[IB::F + e] = v;
+      const bool okA = !term && k < n && c < n;
+      const bool okB = !term && k < n && c >= NX && c - NX < m;
+      const double* src = okA ? a.d_.A + si * n * n + k + c * n : (okB ? a.d_.B + si * n * m + k + (c - NX) * n : nullptr);
+      put(IB::F + e, src, okA || okB, 0.0);
     }
     for (int e = j; e < NZ * NZ; e += LG) {  // P (padded u-diagonal = 1)
       const int r = e % NZ, c = e / NZ;
-      double v = 0.0;
       const bool rx = r < NX, cx = c < NX;
       const int rr = rx ? r : r - NX, cc = cx ? c : c - NX;
+      const double* src = nullptr;
+      double pad = 0.0;
       if (term) {
-        if (rx && cx && r < n && c < n) v = a.d_.QN[inst * sn + (r >= c ? pidx(n, r, c) : pidx(n, c, r))];
-        else if (!rx && !cx && rr == cc) v = 1.0;
+        if (rx && cx && r < n && c < n) src = a.d_.QN + inst * sn + (r >= c ? pidx(n, r, c) : pidx(n, c, r));
+        else if (!rx && !cx && rr == cc) pad = 1.0;
+      } else if (rx && cx) {
+        if (r < n && c < n) src = a.d_.Q + si * sn + (r >= c ? pidx(n, r, c) : pidx(n, c, r));
+      } else if (rx && !cx) {
+        if (r < n && cc < m) src = a.d_.M + si * n * m + r + cc * n;
+      } else if (!rx && cx) {
+        if (c < n && rr < m) src = a.d_.M + si * n * m + c + rr * n;
       } else {
-        if (rx && cx) {
-          if (r < n && c < n) v = a.d_.Q[si * sn + (r >= c ? pidx(n, r, c) : pidx(n, c, r))];
-        } else if (rx && !cx) {
-          if (r < n && cc < m) v = a.d_.M[si * n * m + r + cc * n];
-        } else if (!rx && cx) {
-          if (c < n && rr < m) v = a.d_.M[si * n * m + c + rr * n];
-        } else {
-          if (rr < m && cc < m) v = a.d_.R[si * sm + (rr >= cc ? pidx(m, rr, cc) : pidx(m, cc, rr))];
-          else if (rr == cc) v = 1.0;
-        }
+        if (rr < m && cc < m) src = a.d_.R + si * sm + (rr >= cc ? pidx(m, rr, cc) : pidx(m, cc, rr));
+        else if (rr == cc) pad = 1.0;
       }
-      sb[IB::P + e] = v;
+      put(IB::P + e, src, src != nullptr, pad);
     }
     for (int e = j; e < NZ; e += LG) {  // ∇f in the padded (x | u) layout
-      double v = 0.0;
+      const double* src = nullptr;
       if (e < NX) {
-        if (e < n) v = term ? a.d_.gradfN[inst * n + e] : a.d_.gradf[si * w + e];
+        if (e < n) src = term ? a.d_.gradfN + inst * n + e : a.d_.gradf + si * w + e;
       } else if (!term && e - NX < m) {
-        v = a.d_.gradf[si * w + n + (e - NX)];
+        src = a.d_.gradf + si * w + n + (e - NX);
       }
-      sb[IB::gf + e] = v;
+      put(IB::gf + e, src, src != nullptr, 0.0);
     }
     for (int e = j; e < NX; e += LG) {
-      sb[IB::cv + e] = (!term && e < n) ? a.d_.dres[si * n + e] : 0.0;
-      sb[IB::yi + e] = (e < n) ? a.it.y[(inst * (sN + 1) + i) * n + e] : 0.0;
-      sb[IB::yn + e] = (!term && e < n) ? a.it.y[(inst * (sN + 1) + i + 1) * n + e] : 0.0;
-      sb[IB::xb + e] = (e < n) ? a.it.x[(inst * (sN + 1) + i) * n + e] : 0.0;
+      put(IB::cv + e, a.d_.dres + si * n + e, !term && e < n, 0.0);
+      put(IB::yi + e, a.it.y + (inst * (sN + 1) + i) * n + e, e < n, 0.0);
+      put(IB::yn + e, a.it.y + (inst * (sN + 1) + i + 1) * n + e, !term && e < n, 0.0);
+      put(IB::xb + e, a.it.x + (inst * (sN + 1) + i) * n + e, e < n, 0.0);
     }
-    for (int e = j; e < NU; e += LG) sb[IB::ub + e] = (!term && e < m) ? a.it.u[si * m + e] : 0.0;
-    // inequalities: G rows over the padded (x | u) columns
+    for (int e = j; e < NU; e += LG) put(IB::ub + e, a.it.u + si * m + e, !term && e < m, 0.0);
     const double* Gsrc = term ? a.d_.GjN + inst * (int64_t)ng * n : a.d_.Gj + si * (int64_t)ng * ww;
     for (int e = j; e < NG * NZ; e += LG) {
       const int q = e % NG, c = e / NG;
-      double v = 0.0;
+      const double* src = nullptr;
       if (q < ng) {
-        if (c < NX) { if (c < n) v = Gsrc[q + (int64_t)c * ng]; }
-        else if (!term && c - NX < m) v = Gsrc[q + (int64_t)(n + c - NX) * ng];
+        if (c < NX) { if (c < n) src = Gsrc + q + (int64_t)c * ng; }
+        else if (!term && c - NX < m) src = Gsrc + q + (int64_t)(n + c - NX) * ng;
       }
-      sb[IB::G + e] = v;
+      put(IB::G + e, src, src != nullptr, 0.0);
     }
     for (int e = j; e < NG; e += LG) {
-      double gvv = 0.0, sv = 1.0, zv = 1.0;
-      if (e < ng) {
-        gvv = term ? a.d_.gvN[inst * ng + e] : a.d_.gv[si * ng + e];
-        sv = term ? a.it.sN[inst * ng + e] : a.it.s[si * ng + e];
-        zv = term ? a.it.zN[inst * ng + e] : a.it.z[si * ng + e];
-        if (!(sv > 0.0) || !(zv > 0.0)) nonpos_stage = min(nonpos_stage, i);
-      }
-      sb[IB::gv + e] = gvv;
-      sb[IB::s + e] = sv;
-      sb[IB::z + e] = zv;
-      // Σ = (s/z + 1/η)⁻¹ and r_z = g + μ/z; padded rows: G row is zero
-      sb[IB::sig + e] = (e < ng) ? 1.0 / (sv / zv + 1.0 / eta) : 0.0;
-      sb[IB::rz + e] = (e < ng) ? gvv + mu / zv : 0.0;
+      const bool ok = e < ng;
+      put(IB::gv + e, term ? a.d_.gvN + inst * ng + e : a.d_.gv + si * ng + e, ok, 0.0);
+      put(IB::s + e, term ? a.it.sN + inst * ng + e : a.it.s + si * ng + e, ok, 1.0);
+      put(IB::z + e, term ? a.it.zN + inst * ng + e : a.it.z + si * ng + e, ok, 1.0);
     }
     const double* Csrc = term ? a.d_.CeN + inst * (int64_t)nc * n : a.d_.Ce + si * (int64_t)nc * ww;
     for (int e = j; e < NC * NZ; e += LG) {
       const int q = e % NC, c = e / NC;
-      double v = 0.0;
+      const double* src = nullptr;
       if (q < nc) {
-        if (c < NX) { if (c < n) v = Csrc[q + (int64_t)c * nc]; }
-        else if (!term && c - NX < m) v = Csrc[q + (int64_t)(n + c - NX) * nc];
+        if (c < NX) { if (c < n) src = Csrc + q + (int64_t)c * nc; }
+        else if (!term && c - NX < m) src = Csrc + q + (int64_t)(n + c - NX) * nc;
       }
-      sb[IB::Ce + e] = v;
+      put(IB::Ce + e, src, src != nullptr, 0.0);
     }
     for (int e = j; e < NC; e += LG) {
-      double cev = 0.0, lv = 0.0;
-      if (e < nc) {
-        cev = term ? a.d_.ceN[inst * nc + e] : a.d_.ce[si * nc + e];
-        lv = term ? a.it.lamN[inst * nc + e] : a.it.lam[si * nc + e];
-      }
-      sb[IB::ce + e] = cev;
-      sb[IB::lam + e] = lv;
+      const bool ok = e < nc;
+      put(IB::ce + e, term ? a.d_.ceN + inst * nc + e : a.d_.ce + si * nc + e, ok, 0.0);
+      put(IB::lam + e, term ? a.it.lamN + inst * nc + e : a.it.lam + si * nc + e, ok, 0.0);
+    }
+  };
+  // after the copies of stage i landed in sb: Σ = (s/z + 1/η)⁻¹, r_z = g + μ/z
+  auto finish_stage = [&](int i) {
+    const int ng = (i == N) ? a.d.ngN : a.d.ng;
+    for (int e = j; e < NG; e += LG) {
+      const double sv = sb[IB::s + e], zv = sb[IB::z + e], gvv = sb[IB::gv + e];
+      if (e < ng && (!(sv > 0.0) || !(zv > 0.0))) nonpos_stage = min(nonpos_stage, i);
+      sb[IB::sig + e] = (e < ng) ? 1.0 / (sv / zv + 1.0 / eta) : 0.0;
+      sb[IB::rz + e] = (e < ng) ? gvv + mu / zv : 0.0;
     }
     __syncwarp();
+  };
+  auto load_stage_now = [&](int i) {  // synchronous variant (terminal stage)
+    issue_stage_data(i, sb);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    finish_stage(i);
   };
 
   // condensed P̃ column j: P + GᵀΣG + η C_eᵀC_e
@@ -227,7 +236,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
 
   // ================= pass 1: backward (condense + Eq.(RR)) =================
   double Vc[NX];
-  load_stage(N);
+  load_stage_now(N);
   {
     // terminal: V_N = Q̃_N (condensed), v_N = q̃_N
 #pragma unroll
@@ -237,8 +246,16 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
     if (j < NX) wk[WK::vs + j] = qj;
     __syncwarp();
   }
+  __syncwarp();
+  if (N > 0) issue_stage_data(N - 1, sbuf1);
+  cp_async_commit();
   for (int i = N - 1; i >= 0; --i) {
-    load_stage(i);
+    sb = ((N - 1 - i) & 1) ? sbuf0 : sbuf1;
+    if (i > 0) issue_stage_data(i - 1, ((N - 1 - i) & 1) ? sbuf1 : sbuf0);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    finish_stage(i);
     auto Pcol = [&](int s) -> double { return Pt(s); };
     const double qj = qt();
     double U[NZ], b[NZ];
@@ -344,15 +361,28 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
     }
   };
 
+  // pipelined loads: stage i+1 data and record i+1 land while stage i computes
+  __syncwarp();
+  if (N > 0) {
+    issue_stage_data(0, sbuf0);
+    copy_async(rbuf, rec0, RC::SIZE, j, LG);
+  } else {
+    issue_stage_data(N, sbuf0);
+  }
+  cp_async_commit();
   for (int i = 0; i < N; ++i) {
-    load_stage(i);
-    // record i -> shared
-    {
-      const double* rg = rec0 + (int64_t)i * RC::PAD;
-      for (int e = j; e < RC::SIZE; e += LG) rbuf[e] = rg[e];
-      __syncwarp();
+    sb = (i & 1) ? sbuf1 : sbuf0;
+    const double* rc = (i & 1) ? rbuf + RC::PAD : rbuf;
+    if (i + 1 < N) {
+      issue_stage_data(i + 1, (i & 1) ? sbuf0 : sbuf1);
+      copy_async((i & 1) ? rbuf : rbuf + RC::PAD, rec0 + (int64_t)(i + 1) * RC::PAD, RC::SIZE, j, LG);
+    } else {
+      issue_stage_data(N, (i & 1) ? sbuf0 : sbuf1);  // terminal data for after the loop
     }
-    const double* rc = rbuf;
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    finish_stage(i);
     double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
     if (j < NX) {
       a0 = rc[RC::phi + j];
@@ -423,7 +453,10 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
     __syncwarp();
   }
   // terminal stage: y_N = Ṽ_N x_N + ṽ_N with the condensed terminal blocks; expansions on x_N
-  load_stage(N);
+  cp_async_wait<0>();
+  __syncwarp();
+  sb = (N & 1) ? sbuf1 : sbuf0;
+  finish_stage(N);
   {
     double dz_full[NZ];
 #pragma unroll
@@ -576,7 +609,7 @@ template <int NX, int NU, int NG, int NC, int LG>
 struct IpmCfg {
   static constexpr int WARPS = 4;
   static constexpr int IPB = WARPS * (32 / LG);
-  static constexpr int SLOT = ((IpmBuf<NX, NU, NG, NC>::PAD + Work<NX, NU>::PAD + 2 * Rec<NX, NU>::PAD + NX + 1) & ~1);
+  static constexpr int SLOT = ((2 * IpmBuf<NX, NU, NG, NC>::PAD + Work<NX, NU>::PAD + 2 * Rec<NX, NU>::PAD + NX + 1) & ~1);
   static size_t smem_bytes() { return sizeof(double) * (size_t)IPB * SLOT; }
   static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * Rec<NX, NU>::PAD; }
   static cudaError_t launch(const IpmArgs& a, cudaStream_t s) {

@@ -134,6 +134,76 @@ __device__ __forceinline__ void cta_sweep(double* A, int lda, double* colbuf, in
   *fail = bad;
 }
 
+// Register-blocked version of cta_sweep for n % 16 == 0 with 256 threads: thread (rb, cb) of a
+// 16 × 16 grid owns the BR × BR block (BR = n/16) in registers; per pivot the column (= row, by
+// symmetry) is published through a double-buffered shared vector, one barrier per pivot.
+template <int n>
+__device__ __forceinline__ void cta_sweep_reg(double* A, int lda, double* colbuf2, int tid, bool* fail) {
+  constexpr int BR = n / 16;
+  static_assert(n % 16 == 0, "register sweep needs n % 16 == 0");
+  const int rb = tid & 15, cb = tid >> 4;  // 256 threads
+  double a[BR][BR];
+#pragma unroll
+  for (int i = 0; i < BR; ++i)
+#pragma unroll
+    for (int k = 0; k < BR; ++k) a[i][k] = A[(rb * BR + i) + (cb * BR + k) * lda];
+  bool bad = false;
+  for (int p = 0; p < n; ++p) {
+    double* cb_ = colbuf2 + (p & 1) * n;
+    const int pb = p / BR, pi = p - pb * BR;
+    if (cb == pb) {
+#pragma unroll
+      for (int k = 0; k < BR; ++k)
+        if (k == pi) {
+#pragma unroll
+          for (int i = 0; i < BR; ++i) cb_[rb * BR + i] = a[i][k];
+        }
+    }
+    __syncthreads();
+    const double d = cb_[p];
+    bad |= !(d > 0.0);
+    const double id = rcp_nr(d);
+    double cr[BR], cc[BR];
+#pragma unroll
+    for (int i = 0; i < BR; ++i) {
+      cr[i] = cb_[rb * BR + i] * id;
+      cc[i] = cb_[cb * BR + i];
+    }
+#pragma unroll
+    for (int i = 0; i < BR; ++i)
+#pragma unroll
+      for (int k = 0; k < BR; ++k) a[i][k] = fma(-cr[i], cc[k], a[i][k]);
+    if (rb == pb) {  // row p: Ã_pc = A_pc / d
+#pragma unroll
+      for (int i = 0; i < BR; ++i)
+        if (i == pi) {
+#pragma unroll
+          for (int k = 0; k < BR; ++k) a[i][k] = cc[k] * id;
+        }
+    }
+    if (cb == pb) {  // column p: Ã_rp = A_rp / d, Ã_pp = −1/d
+#pragma unroll
+      for (int k = 0; k < BR; ++k)
+        if (k == pi) {
+#pragma unroll
+          for (int i = 0; i < BR; ++i) a[i][k] = (rb == pb && i == pi) ? -id : cr[i];
+        }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < BR; ++i)
+#pragma unroll
+    for (int k = 0; k < BR; ++k) A[(rb * BR + i) + (cb * BR + k) * lda] = a[i][k];
+  __syncthreads();
+  *fail = bad;
+}
+
+template <int n, int NTHREADS>
+__device__ __forceinline__ void cta_sweep_any(double* A, int lda, double* colbuf2, int tid, bool* fail) {
+  if constexpr (n % 16 == 0 && NTHREADS == 256) cta_sweep_reg<n>(A, lda, colbuf2, tid, fail);
+  else cta_sweep<n>(A, lda, colbuf2, tid, NTHREADS, fail);
+}
+
 template <int NX, int NU, int NTHREADS>
 __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) {
   using L = CtaLayout<NX, NU>;
@@ -194,14 +264,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
       const int r = e % n, c = e / n;
       sm[L::SI + e] = delta * sm[L::VW + e] + (r == c ? 1.0 : 0.0);
     }
-    for (int r = tid; r < n; r += NTHREADS) {
+    {  // V e with 4 threads per row (NTHREADS >= 4 n)
+      static_assert(NTHREADS >= 4 * NX, "V e matvec layout");
+      const int r = tid >> 2, part = tid & 3;
       double acc = 0.0;
-      for (int k = 0; k < n; ++k) acc = fma(sm[L::VW + r + k * n], sm[L::oc + k] - delta * sm[L::vs + k], acc);
-      sm[L::VW + n * n + r] = acc;
+      if (r < n)
+        for (int k = part; k < n; k += 4) acc = fma(sm[L::VW + r + k * n], sm[L::oc + k] - delta * sm[L::vs + k], acc);
+      acc += __shfl_xor_sync(RR_FULL_MASK, acc, 1);
+      acc += __shfl_xor_sync(RR_FULL_MASK, acc, 2);
+      if (r < n && part == 0) sm[L::VW + n * n + r] = acc;
     }
     __syncthreads();
     bool fail = false;
-    cta_sweep<NX>(sm + L::SI, n, sm + L::pr, tid, NTHREADS, &fail);  // SI = −S⁻¹
+    cta_sweep_any<NX, NTHREADS>(sm + L::SI, n, sm + L::pr, tid, &fail);  // SI = −S⁻¹
     if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, i);
     // [W | We] = S⁻¹ [V | Ve]  -> TT region temporarily (ld NX), then g = v + We
     cta_gemm<NX, NX + 1, NX, false>(
@@ -236,7 +311,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
         warp, NW, lane);
     __syncthreads();
     // G⁻¹ (sweep in place: Uuu = −G⁻¹), K̃ = G⁻¹ [H | h]
-    cta_sweep<NU>(sm + L::Uuu, m, sm + L::pr, tid, NTHREADS, &fail);
+    cta_sweep_any<NU, NTHREADS>(sm + L::Uuu, m, sm + L::pr, tid, &fail);
     if (fail && st == 0) st = mk_status(RR_ST_G_NOT_PD, i);
     cta_gemm<NU, NX + 1, NU, false>(
         [&](int r, int k) { return -sm[L::Uuu + r + k * m]; }, [&](int k, int c) { return sm[L::Uux + k + c * m]; },
@@ -289,7 +364,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
   __syncthreads();
   {
     bool fail = false;
-    cta_sweep<NX>(sm + L::SI, n, sm + L::pr, tid, NTHREADS, &fail);
+    cta_sweep_any<NX, NTHREADS>(sm + L::SI, n, sm + L::pr, tid, &fail);
     if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, 0);
   }
   for (int r = tid; r < n; r += NTHREADS) {

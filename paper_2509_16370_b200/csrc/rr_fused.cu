@@ -319,8 +319,13 @@ struct MmaLayout {
   static constexpr int STG_PAD = (STG + 1) & ~1;
   static constexpr int SLOT_B = STG_PAD + WorkM<NX, NU>::PAD;  // single stage buffer (prefetched mid-stage)
   static constexpr int SLOT_F = 2 * RecM<NX, NU>::PAD + NX;
-  static constexpr int SLOT = SLOT_B > SLOT_F ? SLOT_B : SLOT_F;
+  static constexpr int BAR = ((SLOT_B > SLOT_F ? SLOT_B : SLOT_F) + 1) & ~1;  // 2 mbarriers (TMA completion)
+  static constexpr int SLOT = BAR + 2;
   static constexpr int SLOT_PAD = (SLOT + 1) & ~1;
+  // TMA bulk copies need 16-byte sizes/offsets for every operand block of a stage
+  static constexpr bool BULK = (NX * NX) % 2 == 0 && (NX * NU) % 2 == 0 && (NX * (NX + 1) / 2) % 2 == 0 &&
+                               (NU * (NU + 1) / 2) % 2 == 0 && NX % 2 == 0 && NU % 2 == 0 &&
+                               RecM<NX, NU>::SIZE % 2 == 0;
 };
 
 template <int NX, int NU, int WARPS, int MINB>
@@ -360,16 +365,51 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
                       validq[1] ? a.ws + instq[1] * sN * RC::PAD : nullptr};
   int32_t st = 0;
 
+  // stage inputs: TMA bulk copies issued by lane 0 of the group, completion on bar[0]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(slot + LY::BAR);
+  if (j == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncwarp();
+  uint32_t ph0 = 0, ph1 = 0;
+  constexpr uint32_t STG_BYTES = 8u * (n * n + 2 * n * m + sn + sm + 2 * n + m);
   auto issue_stage = [&](int i, double* dst) {
     const int64_t s = inst * sN + i;
-    copy_async(dst + oA, a.p.A + s * n * n, n * n, j, 16);
-    copy_async(dst + oB, a.p.B + s * n * m, n * m, j, 16);
-    copy_async(dst + oQ, a.p.Q + s * sn, sn, j, 16);
-    copy_async(dst + oM, a.p.M + s * n * m, n * m, j, 16);
-    copy_async(dst + oR, a.p.R + s * sm, sm, j, 16);
-    copy_async(dst + oq, a.p.q + s * n, n, j, 16);
-    copy_async(dst + orr, a.p.r + s * m, m, j, 16);
-    copy_async(dst + oc, a.p.c + s * n, n, j, 16);
+    if constexpr (LY::BULK) {
+      if (j == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&bar[0], STG_BYTES);
+        bulk_g2s(dst + oA, a.p.A + s * n * n, 8 * n * n, &bar[0]);
+        bulk_g2s(dst + oB, a.p.B + s * n * m, 8 * n * m, &bar[0]);
+        bulk_g2s(dst + oQ, a.p.Q + s * sn, 8 * sn, &bar[0]);
+        bulk_g2s(dst + oM, a.p.M + s * n * m, 8 * n * m, &bar[0]);
+        bulk_g2s(dst + oR, a.p.R + s * sm, 8 * sm, &bar[0]);
+        bulk_g2s(dst + oq, a.p.q + s * n, 8 * n, &bar[0]);
+        bulk_g2s(dst + orr, a.p.r + s * m, 8 * m, &bar[0]);
+        bulk_g2s(dst + oc, a.p.c + s * n, 8 * n, &bar[0]);
+      }
+    } else {
+      copy_async(dst + oA, a.p.A + s * n * n, n * n, j, 16);
+      copy_async(dst + oB, a.p.B + s * n * m, n * m, j, 16);
+      copy_async(dst + oQ, a.p.Q + s * sn, sn, j, 16);
+      copy_async(dst + oM, a.p.M + s * n * m, n * m, j, 16);
+      copy_async(dst + oR, a.p.R + s * sm, sm, j, 16);
+      copy_async(dst + oq, a.p.q + s * n, n, j, 16);
+      copy_async(dst + orr, a.p.r + s * m, m, j, 16);
+      copy_async(dst + oc, a.p.c + s * n, n, j, 16);
+      cp_async_commit();
+    }
+  };
+  auto wait_stage = [&]() {
+    if constexpr (LY::BULK) {
+      mbar_wait_parity(&bar[0], ph0);
+      ph0 ^= 1u;
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
   };
   // P = [[Q M]; [Mᵀ R]] of the stage buffer sb (exact shape: no padding inside NZ)
   auto Pat = [&](const double* sb, int s, int t) -> double {
@@ -393,7 +433,6 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     if (valid && a.f.v != nullptr && j < n) a.f.v[(inst * (sN + 1) + N) * n + j] = a.p.qN[inst * n + j];
   }
   if (N > 0) issue_stage(N - 1, slot);
-  cp_async_commit();
   __syncwarp();
 
   for (int i = N - 1; i >= 0; --i) {
@@ -403,13 +442,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     const double* sb = grp ? sbq[1] : sbq[0];
     auto qjf = [&]() -> double { return (j < NX) ? sb[oq + j] : sb[orr + j - NX]; };
     auto P2 = [&](int q, int s, int t) -> double { return Pat(sbq[q], s, t); };
-    auto wait_inputs = [&]() {
-      cp_async_wait<0>();
-      __syncwarp();
-    };
+    auto wait_inputs = [&]() { wait_stage(); };
     auto prefetch = [&]() {
       if (i > 0) issue_stage(i - 1, slot);
-      cp_async_commit();
     };
     double* recq[2] = {rec0q[0] ? rec0q[0] + (int64_t)i * RC::PAD : nullptr,
                        rec0q[1] ? rec0q[1] + (int64_t)i * RC::PAD : nullptr};
@@ -463,9 +498,36 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   double* rbuf0 = slot;
   double* rbuf1 = slot + RC::PAD;
   double* xs = slot + 2 * RC::PAD;
-  auto issue_rec = [&](int i, double* dst) { copy_async(dst, rec0 + (int64_t)i * RC::PAD, RC::SIZE, j, 16); };
-  if (N > 0) issue_rec(0, rbuf0);
-  cp_async_commit();
+  // records were written through the generic proxy; order them before the TMA (async-proxy) reads
+  asm volatile("fence.proxy.async;\n" ::: "memory");
+  __syncwarp();
+  auto issue_rec = [&](int i, double* dst, int b) {
+    if constexpr (LY::BULK) {
+      if (j == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&bar[b], 8u * RC::SIZE);
+        bulk_g2s(dst, rec0 + (int64_t)i * RC::PAD, 8u * RC::SIZE, &bar[b]);
+      }
+    } else {
+      copy_async(dst, rec0 + (int64_t)i * RC::PAD, RC::SIZE, j, 16);
+      cp_async_commit();
+    }
+  };
+  auto wait_rec = [&](int b) {
+    if constexpr (LY::BULK) {
+      if (b == 0) {
+        mbar_wait_parity(&bar[0], ph0);
+        ph0 ^= 1u;
+      } else {
+        mbar_wait_parity(&bar[1], ph1);
+        ph1 ^= 1u;
+      }
+    } else {
+      cp_async_wait<1>();
+    }
+    __syncwarp();
+  };
+  if (N > 0) issue_rec(0, rbuf0, 0);
   {
     double xj = 0.0;
 #pragma unroll
@@ -474,11 +536,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     bad |= (j < n) && !isfinite(xj);
   }
   for (int i = 0; i < N; ++i) {
-    const double* rc = (i & 1) ? rbuf1 : rbuf0;
-    if (i + 1 < N) issue_rec(i + 1, (i & 1) ? rbuf0 : rbuf1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncwarp();
+    const int b = i & 1;
+    const double* rc = b ? rbuf1 : rbuf0;
+    if (i + 1 < N) issue_rec(i + 1, b ? rbuf0 : rbuf1, b ^ 1);
+    else if (!LY::BULK) cp_async_commit();
+    wait_rec(b);
     double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
     if (j < NX) {
       const double* row = rc + RC::PHI + j * RC::LD;
@@ -558,8 +620,8 @@ struct MmaCfg {
 
 // Shape dispatch: exact specialisations for the BASELINE configs, padded fallbacks otherwise.
 // RR_B200_VARIANT (environment, read per call; tuning knob for the 12x4 kernel): 0 = default
-// (SIMT stage kernel, 3 CTAs/SM), 1/2 = SIMT with 2 CTAs/SM / 2-warp CTAs, 3/4 = DMMA stage
-// kernel (rr_stage_mma.cuh) with 3 / 2 CTAs/SM (measured slower: occupancy, profiles/).
+// (DMMA stage kernel rr_stage_mma.cuh, TMA stage loads, 3 CTAs/SM), 1/2 = SIMT stage kernel with
+// 3 / 2 CTAs/SM, 3/4 = DMMA kernel with 2-warp CTAs / 2 CTAs/SM.
 static int variant() {
   const char* v = getenv("RR_B200_VARIANT");
   return v ? atoi(v) : 0;
@@ -569,11 +631,11 @@ template <typename F>
 static bool dispatch_fused(int nx, int nu, F&& f) {
   if (nx == 12 && nu == 4) {
     const int v = variant();
-    if (v == 1) return f(FusedCfg<12, 4, 16, 4, 2, true>{});
-    if (v == 2) return f(FusedCfg<12, 4, 16, 2, 6, true>{});
-    if (v == 3) return f(MmaCfg<12, 4, 4, 3>{});
+    if (v == 1) return f(FusedCfg<12, 4, 16, 4, 3, true>{});
+    if (v == 2) return f(FusedCfg<12, 4, 16, 4, 2, true>{});
+    if (v == 3) return f(MmaCfg<12, 4, 2, 6>{});
     if (v == 4) return f(MmaCfg<12, 4, 4, 2>{});
-    return f(FusedCfg<12, 4, 16, 4, 3, true>{});
+    return f(MmaCfg<12, 4, 4, 3>{});
   }
   if (nx == 4 && nu == 1) return f(FusedCfg<4, 1, 8, 4, 4, true>{});
   if (nx == 2 && nu == 1) return f(FusedCfg<2, 1, 4, 4, 4, true>{});

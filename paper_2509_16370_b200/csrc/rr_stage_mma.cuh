@@ -55,8 +55,9 @@ struct WorkM {
   using W = Work<NX, NU>;
   static_assert(W::Wb + NX * NX == W::SIZE, "Work<> must end with Wb");
   static constexpr int X1 = W::Wb;              // NX × 16 (ld NX): [V | Ve], then T, then M
-  static constexpr int X2 = X1 + NX * 16;       // 16 × 16: W (ld NX, NX+1 cols), then U (ld 16)
-  static constexpr int SIZE = X2 + 16 * 16;
+  static constexpr int X2 = X1 + NX * 16;       // W (ld NX, NX+1 cols), then U (ld ULD)
+  static constexpr int ULD = 18;                // U leading dimension: conflict-free C-fragment stores
+  static constexpr int SIZE = X2 + 16 * ULD;
   static constexpr int PAD = (SIZE + 1) & ~1;
 };
 
@@ -233,15 +234,15 @@ struct StageMMA {
 #pragma unroll
         for (int nt = 0; nt < ZT; ++nt) {
           const int r = 8 * mt + g, col = 8 * nt + 2 * t;
-          Ub[col * 16 + r] = c[mt][nt][0];
-          Ub[(col + 1) * 16 + r] = c[mt][nt][1];
+          Ub[col * WM::ULD + r] = c[mt][nt][0];
+          Ub[(col + 1) * WM::ULD + r] = c[mt][nt][1];
         }
     }
     __syncwarp();
     // (6) Gauss-Jordan on the u-block (SIMT, lane j owns column j)
 #pragma unroll
     for (int s = 0; s < NZ; s += 2) {
-      const double2 u2 = *reinterpret_cast<const double2*>(wk + WM::X2 + jc * 16 + s);
+      const double2 u2 = *reinterpret_cast<const double2*>(wk + WM::X2 + jc * WM::ULD + s);
       U[s] = (j < NZ) ? u2.x : 0.0;
       U[s + 1] = (j < NZ) ? u2.y : 0.0;
     }
