@@ -55,6 +55,16 @@ struct CtaLayout {
   static constexpr int REC = ((rv + NX + 1) & ~1);
 };
 
+// Shared-memory index of element (r, c) of a column-major matrix with leading dimension LD.
+// For LD % 16 == 0 the row index is XOR-swizzled inside 16-element groups (bits 2-3 flipped by a
+// function of the column) so that the DMMA fragment loads (A, Aᵀ, B patterns), the C-fragment
+// stores and 16-byte column copies are bank-conflict free per half-warp; otherwise plain.
+template <int LD>
+__device__ __forceinline__ int swz(int r, int c) {
+  if constexpr (LD % 16 == 0) return c * LD + (r ^ (((c ^ (c >> 2)) & 3) << 2));
+  else return c * LD + r;
+}
+
 // C (rows < Mlim, cols < Nlim) = sign * op(A) · B + Cinit, all column-major in shared memory.
 // op(A) = A (M×K, ld lda) or Aᵀ (A stored K×M, ld lda).  M, N multiples of 8 (padded tiles are
 // computed and masked on store); K multiple of 4.  Warps take 16×16 super-tiles round-robin.
@@ -114,20 +124,20 @@ template <int n>
 __device__ __forceinline__ void cta_sweep(double* A, int lda, double* colbuf, int tid, int nthreads, bool* fail) {
   bool bad = false;
   for (int p = 0; p < n; ++p) {
-    for (int r = tid; r < n; r += nthreads) colbuf[r] = A[r + p * lda];  // column p (= row p)
+    for (int r = tid; r < n; r += nthreads) colbuf[r] = A[swz<n>(r, p)];  // column p (= row p)
     __syncthreads();
     const double d = colbuf[p];
     bad |= !(d > 0.0);
     const double id = rcp_nr(d);
     for (int e = tid; e < n * n; e += nthreads) {
       const int r = e % n, c = e / n;
-      const double arc = A[r + c * lda];
+      const double arc = A[swz<n>(r, c)];
       double v;
       if (r == p && c == p) v = -id;
       else if (r == p) v = colbuf[c] * id;           // row p = column p (symmetric)
       else if (c == p) v = colbuf[r] * id;
       else v = fma(-colbuf[r] * id, colbuf[c], arc);
-      A[r + c * lda] = v;
+      A[swz<n>(r, c)] = v;
     }
     __syncthreads();
   }
@@ -138,7 +148,7 @@ __device__ __forceinline__ void cta_sweep(double* A, int lda, double* colbuf, in
 // 16 × 16 grid owns the BR × BR block (BR = n/16) in registers; per pivot the column (= row, by
 // symmetry) is published through a double-buffered shared vector, one barrier per pivot.
 template <int n>
-__device__ __forceinline__ void cta_sweep_reg(double* A, int lda, double* colbuf2, int tid, bool* fail) {
+__device__ __forceinline__ void cta_sweep_reg(double* A, int /*lda == n*/, double* colbuf2, int tid, bool* fail) {
   constexpr int BR = n / 16;
   static_assert(n % 16 == 0, "register sweep needs n % 16 == 0");
   const int rb = tid & 15, cb = tid >> 4;  // 256 threads
@@ -146,7 +156,7 @@ __device__ __forceinline__ void cta_sweep_reg(double* A, int lda, double* colbuf
 #pragma unroll
   for (int i = 0; i < BR; ++i)
 #pragma unroll
-    for (int k = 0; k < BR; ++k) a[i][k] = A[(rb * BR + i) + (cb * BR + k) * lda];
+    for (int k = 0; k < BR; ++k) a[i][k] = A[swz<n>(rb * BR + i, cb * BR + k)];
   bool bad = false;
   for (int p = 0; p < n; ++p) {
     double* cb_ = colbuf2 + (p & 1) * n;
@@ -193,7 +203,7 @@ __device__ __forceinline__ void cta_sweep_reg(double* A, int lda, double* colbuf
 #pragma unroll
   for (int i = 0; i < BR; ++i)
 #pragma unroll
-    for (int k = 0; k < BR; ++k) A[(rb * BR + i) + (cb * BR + k) * lda] = a[i][k];
+    for (int k = 0; k < BR; ++k) A[swz<n>(rb * BR + i, cb * BR + k)] = a[i][k];
   __syncthreads();
   *fail = bad;
 }
@@ -219,10 +229,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
   double* rec0 = a.ws + inst * sN * L::REC;
   int32_t st = 0;
 
+  auto X = [](int r, int c) { return swz<NX>(r, c); };  // ld NX matrices (F, S⁻¹, V/W/Uxx, T, M)
+  auto Y = [](int r, int c) { return swz<NU>(r, c); };  // ld NU matrices (Uux, Uuu, K̃)
   auto issue_stage = [&](int i) {
     const int64_t s = inst * sN + i;
-    copy_async(sm + L::oA, a.p.A + s * n * n, n * n, tid, NTHREADS);
-    copy_async(sm + L::oB, a.p.B + s * n * m, n * m, tid, NTHREADS);
+    // F = [A B]: 16-byte chunks (rows r, r+1) to their swizzled column positions
+    const double* gA = a.p.A + s * n * n;
+    const double* gB = a.p.B + s * n * m;
+    for (int e = 2 * tid; e < n * NZ; e += 2 * NTHREADS) {
+      const int r = e % n, c = e / n;
+      const double* src = c < NX ? gA + r + c * n : gB + r + (c - NX) * n;
+      cp_async16(sm + L::oA + X(r, c), src);
+    }
     copy_async(sm + L::oQ, a.p.Q + s * L::SN, L::SN, tid, NTHREADS);
     copy_async(sm + L::oM, a.p.M + s * n * m, n * m, tid, NTHREADS);
     copy_async(sm + L::oR, a.p.R + s * L::SMU, L::SMU, tid, NTHREADS);
@@ -236,7 +254,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
     const double* QN = a.p.QN + inst * L::SN;
     for (int e = tid; e < n * n; e += NTHREADS) {
       const int r = e % n, c = e / n;
-      sm[L::VW + e] = r >= c ? QN[pidx(n, r, c)] : QN[pidx(n, c, r)];
+      sm[L::VW + X(r, c)] = r >= c ? QN[pidx(n, r, c)] : QN[pidx(n, c, r)];
     }
     for (int r = tid; r < n; r += NTHREADS) sm[L::vs + r] = a.p.qN[inst * n + r];
     if (a.f.V != nullptr)
@@ -247,7 +265,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
   if (N > 0) issue_stage(N - 1);
   __syncthreads();
 
-  auto Pat = [&](int s, int t) -> double {  // P = [[Q M]; [Mᵀ R]] from the stage input
+  auto Pat = [&](int s, int t) -> double {  // P = [[Q M]; [Mᵀ R]] from the stage input (plain layout)
     if (s < NX && t < NX) return s >= t ? sm[L::oQ + pidx(n, s, t)] : sm[L::oQ + pidx(n, t, s)];
     if (s < NX) return sm[L::oM + s + (t - NX) * n];
     if (t < NX) return sm[L::oM + t + (s - NX) * n];
@@ -262,50 +280,49 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
     // S = I + δV -> SI; column NX of [V | ·] = V e with e = c_{i+1} − δ v_{i+1}
     for (int e = tid; e < n * n; e += NTHREADS) {
       const int r = e % n, c = e / n;
-      sm[L::SI + e] = delta * sm[L::VW + e] + (r == c ? 1.0 : 0.0);
+      sm[L::SI + X(r, c)] = delta * sm[L::VW + X(r, c)] + (r == c ? 1.0 : 0.0);
     }
     {  // V e with 4 threads per row (NTHREADS >= 4 n)
       static_assert(NTHREADS >= 4 * NX, "V e matvec layout");
       const int r = tid >> 2, part = tid & 3;
       double acc = 0.0;
       if (r < n)
-        for (int k = part; k < n; k += 4) acc = fma(sm[L::VW + r + k * n], sm[L::oc + k] - delta * sm[L::vs + k], acc);
+        for (int k = part; k < n; k += 4) acc = fma(sm[L::VW + X(r, k)], sm[L::oc + k] - delta * sm[L::vs + k], acc);
       acc += __shfl_xor_sync(RR_FULL_MASK, acc, 1);
       acc += __shfl_xor_sync(RR_FULL_MASK, acc, 2);
-      if (r < n && part == 0) sm[L::VW + n * n + r] = acc;
+      if (r < n && part == 0) sm[L::VW + X(r, NX)] = acc;
     }
     __syncthreads();
     bool fail = false;
     cta_sweep_any<NX, NTHREADS>(sm + L::SI, n, sm + L::pr, tid, &fail);  // SI = −S⁻¹
     if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, i);
-    // [W | We] = S⁻¹ [V | Ve]  -> TT region temporarily (ld NX), then g = v + We
+    // [W | We] = S⁻¹ [V | Ve]  -> TT region temporarily (same ld/swizzle), then g = v + We
     cta_gemm<NX, NX + 1, NX, false>(
-        [&](int r, int k) { return -sm[L::SI + r + k * n]; }, [&](int k, int c) { return sm[L::VW + k + c * n]; },
-        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::TT + r + c * n] = v; }, warp, NW, lane);
+        [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k, int c) { return sm[L::VW + X(k, c)]; },
+        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::TT + X(r, c)] = v; }, warp, NW, lane);
     __syncthreads();
-    // W -> VW region; g = v + We -> column NZ of [T | g] comes later (keep in pr)
-    for (int e = tid; e < n * n; e += NTHREADS) sm[L::VW + e] = sm[L::TT + e];
-    for (int r = tid; r < n; r += NTHREADS) sm[L::pr + r] = sm[L::vs + r] + sm[L::TT + n * n + r];
+    for (int e = tid; e < n * n; e += NTHREADS) sm[L::VW + e] = sm[L::TT + e];  // same layout: flat copy of W
+    for (int r = tid; r < n; r += NTHREADS) sm[L::pr + r] = sm[L::vs + r] + sm[L::TT + X(r, NX)];
     __syncthreads();
     // [T | g] = [W F | g]   (F = [A B] = stage input columns, ld NX)
     cta_gemm<NX, NZ, NX, false>(
-        [&](int r, int k) { return sm[L::VW + r + k * n]; }, [&](int k, int c) { return sm[L::oA + k + c * n]; },
-        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::TT + r + c * n] = v; }, warp, NW, lane);
-    for (int r = tid; r < n; r += NTHREADS) sm[L::TT + NZ * n + r] = sm[L::pr + r];
+        [&](int r, int k) { return sm[L::VW + X(r, k)]; }, [&](int k, int c) { return sm[L::oA + X(k, c)]; },
+        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::TT + X(r, c)] = v; }, warp, NW, lane);
+    for (int r = tid; r < n; r += NTHREADS) sm[L::TT + X(r, NZ)] = sm[L::pr + r];
     __syncthreads();
     // [U | b] = Fᵀ [T | g] + [P | (q; r)]: rows x -> Uxx|bx (ld NX), rows u -> Uux|bu, Uuu (ld NU)
     cta_gemm<NZ, NZ + 1, NX, true>(
-        [&](int r, int k) { return sm[L::oA + k + r * n]; }, [&](int k, int c) { return sm[L::TT + k + c * n]; },
+        [&](int r, int k) { return sm[L::oA + X(k, r)]; }, [&](int k, int c) { return sm[L::TT + X(k, c)]; },
         [&](int r, int c) { return c < NZ ? Pat(r, c) : (r < NX ? sm[L::oq + r] : sm[L::orr + r - NX]); },
         [&](int r, int c, double v) {
           if (r < NX) {
-            if (c < NX) sm[L::Uxx + r + c * n] = v;
-            else if (c == NZ) sm[L::Uxx + r + NX * n] = v;  // b_x
+            if (c < NX) sm[L::Uxx + X(r, c)] = v;
+            else if (c == NZ) sm[L::Uxx + X(r, NX)] = v;  // b_x
           } else {
             const int u = r - NX;
-            if (c < NX) sm[L::Uux + u + c * m] = v;
-            else if (c == NZ) sm[L::Uux + u + NX * m] = v;  // b_u
-            else sm[L::Uuu + u + (c - NX) * m] = v;          // G
+            if (c < NX) sm[L::Uux + Y(u, c)] = v;
+            else if (c == NZ) sm[L::Uux + Y(u, NX)] = v;  // b_u
+            else sm[L::Uuu + Y(u, c - NX)] = v;            // G
           }
         },
         warp, NW, lane);
@@ -314,52 +331,52 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
     cta_sweep_any<NU, NTHREADS>(sm + L::Uuu, m, sm + L::pr, tid, &fail);
     if (fail && st == 0) st = mk_status(RR_ST_G_NOT_PD, i);
     cta_gemm<NU, NX + 1, NU, false>(
-        [&](int r, int k) { return -sm[L::Uuu + r + k * m]; }, [&](int k, int c) { return sm[L::Uux + k + c * m]; },
-        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::Kt + r + c * m] = v; }, warp, NW, lane);
+        [&](int r, int k) { return -sm[L::Uuu + Y(r, k)]; }, [&](int k, int c) { return sm[L::Uux + Y(k, c)]; },
+        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::Kt + Y(r, c)] = v; }, warp, NW, lane);
     __syncthreads();
     // [V_i | v_i] = [Uxx | bx] − Hᵀ K̃  (in place: each tile reads its own init)
     cta_gemm<NX, NX + 1, NU, true>(
-        [&](int r, int k) { return -sm[L::Uux + k + r * m]; }, [&](int k, int c) { return sm[L::Kt + k + c * m]; },
-        [&](int r, int c) { return sm[L::Uxx + r + c * n]; }, [&](int r, int c, double v) { sm[L::Uxx + r + c * n] = v; },
+        [&](int r, int k) { return -sm[L::Uux + Y(k, r)]; }, [&](int k, int c) { return sm[L::Kt + Y(k, c)]; },
+        [&](int r, int c) { return sm[L::Uxx + X(r, c)]; }, [&](int r, int c, double v) { sm[L::Uxx + X(r, c)] = v; },
         warp, NW, lane);
     // M = [A | c − δ v_{i+1}] − B K̃  (K̃ column NX = G⁻¹h = −k)
     cta_gemm<NX, NX + 1, NU, false>(
-        [&](int r, int k) { return -sm[L::oB + r + k * n]; }, [&](int k, int c) { return sm[L::Kt + k + c * m]; },
-        [&](int r, int c) { return c < NX ? sm[L::oA + r + c * n] : sm[L::oc + r] - delta * sm[L::vs + r]; },
-        [&](int r, int c, double v) { sm[L::MM + r + c * n] = v; }, warp, NW, lane);
+        [&](int r, int k) { return -sm[L::oA + X(r, NX + k)]; }, [&](int k, int c) { return sm[L::Kt + Y(k, c)]; },
+        [&](int r, int c) { return c < NX ? sm[L::oA + X(r, c)] : sm[L::oc + r] - delta * sm[L::vs + r]; },
+        [&](int r, int c, double v) { sm[L::MM + X(r, c)] = v; }, warp, NW, lane);
     __syncthreads();
     // record K = −K̃[:, :NX] (ld NU), k = −K̃[:, NX], V_i (ld NX), v_i; optional factor outputs
-    for (int e = tid; e < m * n; e += NTHREADS) rec[L::rK + e] = -sm[L::Kt + e];
-    for (int u = tid; u < m; u += NTHREADS) rec[L::rk + u] = -sm[L::Kt + u + NX * m];
-    for (int e = tid; e < n * n; e += NTHREADS) rec[L::rV + e] = sm[L::Uxx + e];
-    for (int r = tid; r < n; r += NTHREADS) rec[L::rv + r] = sm[L::Uxx + NX * n + r];
+    for (int e = tid; e < m * n; e += NTHREADS) rec[L::rK + e] = -sm[L::Kt + Y(e % m, e / m)];
+    for (int u = tid; u < m; u += NTHREADS) rec[L::rk + u] = -sm[L::Kt + Y(u, NX)];
+    for (int e = tid; e < n * n; e += NTHREADS) rec[L::rV + e] = sm[L::Uxx + X(e % n, e / n)];
+    for (int r = tid; r < n; r += NTHREADS) rec[L::rv + r] = sm[L::Uxx + X(r, NX)];
     if (a.f.K != nullptr)
-      for (int e = tid; e < m * n; e += NTHREADS) a.f.K[(inst * sN + i) * m * n + e] = -sm[L::Kt + e];
+      for (int e = tid; e < m * n; e += NTHREADS) a.f.K[(inst * sN + i) * m * n + e] = -sm[L::Kt + Y(e % m, e / m)];
     if (a.f.k != nullptr)
-      for (int u = tid; u < m; u += NTHREADS) a.f.k[(inst * sN + i) * m + u] = -sm[L::Kt + u + NX * m];
+      for (int u = tid; u < m; u += NTHREADS) a.f.k[(inst * sN + i) * m + u] = -sm[L::Kt + Y(u, NX)];
     if (a.f.V != nullptr)
       for (int e = tid; e < L::SN; e += NTHREADS) {
         int c = 0, off = e;
         while (off >= n - c) { off -= n - c; ++c; }
-        a.f.V[(inst * (sN + 1) + i) * L::SN + e] = sm[L::Uxx + (c + off) + c * n];
+        a.f.V[(inst * (sN + 1) + i) * L::SN + e] = sm[L::Uxx + X(c + off, c)];
       }
     if (a.f.v != nullptr)
-      for (int r = tid; r < n; r += NTHREADS) a.f.v[(inst * (sN + 1) + i) * n + r] = sm[L::Uxx + NX * n + r];
+      for (int r = tid; r < n; r += NTHREADS) a.f.v[(inst * (sN + 1) + i) * n + r] = sm[L::Uxx + X(r, NX)];
     __syncthreads();
     // stage input is dead: stream the next stage in while [Φ | φ] = S⁻¹ M is formed
     if (i > 0) issue_stage(i - 1);
     cta_gemm<NX, NX + 1, NX, false>(
-        [&](int r, int k) { return -sm[L::SI + r + k * n]; }, [&](int k, int c) { return sm[L::MM + k + c * n]; },
+        [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k, int c) { return sm[L::MM + X(k, c)]; },
         [&](int, int) { return 0.0; }, [&](int r, int c, double v) { rec[L::rPHI + r + c * n] = v; }, warp, NW, lane);
-    // carry: V_i -> VW region (already in place: Uxx == VW with ld NX), v_i -> vs
-    for (int r = tid; r < n; r += NTHREADS) sm[L::vs + r] = sm[L::Uxx + NX * n + r];
+    // carry: V_i -> VW region (already in place: Uxx == VW, same layout), v_i -> vs
+    for (int r = tid; r < n; r += NTHREADS) sm[L::vs + r] = sm[L::Uxx + X(r, NX)];
     __syncthreads();
   }
 
   // x_0 = (I + δV_0)⁻¹ (c_0 − δ v_0)
   for (int e = tid; e < n * n; e += NTHREADS) {
     const int r = e % n, c = e / n;
-    sm[L::SI + e] = delta * sm[L::VW + e] + (r == c ? 1.0 : 0.0);
+    sm[L::SI + X(r, c)] = delta * sm[L::VW + X(r, c)] + (r == c ? 1.0 : 0.0);
   }
   __syncthreads();
   {
@@ -369,7 +386,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
   }
   for (int r = tid; r < n; r += NTHREADS) {
     double acc = 0.0;
-    for (int k = 0; k < n; ++k) acc = fma(-sm[L::SI + r + k * n], a.p.c0[inst * n + k] - delta * sm[L::vs + k], acc);
+    for (int k = 0; k < n; ++k) acc = fma(-sm[L::SI + X(r, k)], a.p.c0[inst * n + k] - delta * sm[L::vs + k], acc);
     sm[L::xs + r] = acc;
   }
   __syncthreads();
