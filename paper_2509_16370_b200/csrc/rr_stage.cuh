@@ -98,10 +98,9 @@ struct Stage {
         if (r != p) A[r] = fma(-col[r], f, A[r]);
       A[p] = (j == p) ? -id : f;
     }
-    if (j < NX) {
+    if (j < NX) {  // S⁻¹ is symmetric: write column j as row j (consecutive lanes, conflict-free)
 #pragma unroll
-      for (int r = 0; r < NX; ++r) A[r] = -A[r];
-      store_col(wk + WK::Si + j * NX, A);
+      for (int r = 0; r < NX; ++r) wk[WK::Si + r * NX + j] = -A[r];
     }
     __syncwarp();
   }

@@ -54,8 +54,10 @@ struct WorkM {
   static constexpr int NZ = NX + NU;
   using W = Work<NX, NU>;
   static_assert(W::Wb + NX * NX == W::SIZE, "Work<> must end with Wb");
-  static constexpr int X1 = W::Wb;              // NX × 16 (ld NX): [V | Ve], then T, then M
-  static constexpr int X2 = X1 + NX * 16;       // W (ld NX, NX+1 cols), then U (ld ULD)
+  static constexpr int MLD = ((NX + 1 + 15) / 16) * 16 + 4;  // row-major ld of M (≡ 4 mod 16: B fragments)
+  static constexpr int X1SZ = (NX * MLD > NX * 16 ? NX * MLD : NX * 16);
+  static constexpr int X1 = W::Wb;              // [V | Ve] (ld NX), then T (ld NX), then M (row-major, ld MLD)
+  static constexpr int X2 = X1 + X1SZ;          // W (ld NX, NX+1 cols), then U (ld ULD)
   static constexpr int ULD = 18;                // U leading dimension: conflict-free C-fragment stores
   static constexpr int SIZE = X2 + 16 * ULD;
   static constexpr int PAD = (SIZE + 1) & ~1;
@@ -95,7 +97,8 @@ struct StageMMA {
     ST::invS(Vc, delta, j, wk, stage, st);
     wait_inputs();
     if (j < NX) {
-      ST::store_col(wk + WM::X1 + j * NX, Vc);
+#pragma unroll
+      for (int r = 0; r < NX; ++r) wk[WM::X1 + r * NX + j] = Vc[r];  // V symmetric: column j as row j
       double ve0 = 0.0, ve1 = 0.0;
 #pragma unroll
       for (int k = 0; k < NX; k += 2) {
@@ -295,7 +298,8 @@ struct StageMMA {
           tcol[r + 1] = fma(f2.y, coef, tcol[r + 1]);
         }
       }
-      ST::store_col(wk + WM::X1 + j * NX, tcol);
+#pragma unroll
+      for (int r = 0; r < NX; ++r) wk[WM::X1 + r * WM::MLD + j] = tcol[r];  // M row-major (ld MLD)
     }
     __syncwarp();
     prefetch();  // the stage inputs (F, P, q, r, c) are dead from here on
@@ -320,7 +324,7 @@ struct StageMMA {
 #pragma unroll
         for (int nt = 0; nt < CT; ++nt) {
           const int col = 8 * nt + g;
-          const double bM = (col <= NX) ? Mb[col * NX + 4 * kt + t] : 0.0;
+          const double bM = (col <= NX) ? Mb[(4 * kt + t) * WM::MLD + col] : 0.0;
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aS[mt], bM);
         }

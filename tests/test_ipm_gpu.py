@@ -99,3 +99,33 @@ def test_ipm_c4_full_batch_sampled():
     g = {k: v[torch.from_numpy(idx).cuda()].cpu().numpy() for k, v in res.items()}
     git = {k: v[torch.from_numpy(idx).cuda()].cpu().numpy() for k, v in p.it.items()}
     assert_ipm_parity(g, git, o, oit)
+
+
+def test_ipm_line_search_failure_status():
+    """RR_ST_LS_FAILED: with max_backtracks = 0 the C4-LS instances that need backtracking fail,
+    keep their iterate, report α_p = 0 -- exactly as the oracle."""
+    p = cartpole_c4(64, seed=7, N=20, variant="C4-LS")
+    g, git, o, oit = run(p, max_backtracks=0)
+    assert np.any(o["status"] == 5) and np.array_equal(g["status"], o["status"])
+    failed = o["status"] == 5
+    assert np.all(g["alpha_p"][failed] == 0.0)
+    np.testing.assert_array_equal(git["x"][failed], p.it["x"][failed].numpy())
+    assert_ipm_parity(g, git, o, oit)
+
+
+def test_ipm_horizon_zero_and_empty_batch():
+    import paper_2509_16370_b200 as rr
+    p = random_lq_ocp(3, 2, 0, 4, seed=8, ng=2, ngN=2, nc=1, ncN=1)
+    assert_ipm_parity(*run(p))
+    e = random_lq_ocp(3, 2, 4, 0, seed=8).to("cuda")
+    res = rr.ipm_step(e)
+    assert res["status"].numel() == 0
+
+
+def test_ipm_invalid_parameters_rejected():
+    import paper_2509_16370_b200 as rr
+    p = random_lq_ocp(3, 2, 4, 2, seed=9).to("cuda")
+    with pytest.raises(rr.RRError):
+        rr.ipm_step(p, tau=1.5)
+    with pytest.raises(rr.RRError):
+        rr.ipm_step(p, beta=0.0)
