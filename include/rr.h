@@ -102,7 +102,7 @@ int64_t rr_workspace_bytes(const rr_dims* dims);
  *   forward sweep: x_0 = (I+δV_0)⁻¹(c_0 - δv_0); u_i = K_i x_i + k_i;
  *     x_{i+1} = (I+δV_{i+1})⁻¹(A_i x_i + B_i u_i + c_{i+1} - δv_{i+1});
  *   dual recovery: y_i = V_i x_i + v_i.
- * prob, sol, status: required.  fac: optional (NULL or any NULL member = not written).
+ * prob, sol, status: required (status may be NULL when batch == 0: the call is then a no-op).  fac: optional (NULL or any NULL member = not written).
  * workspace: device buffer of >= rr_workspace_bytes(dims) bytes, 256-byte aligned; contents
  * are scratch.  Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
  */
@@ -202,7 +202,7 @@ typedef struct {
 /* Bytes of device workspace ipm_step needs (-1 if no kernel covers the dims). */
 int64_t ipm_workspace_bytes(const ipm_dims* dims);
 
-/* One batched regularized-IPM step (rows a1-a8).  status: [b] (RR_ST_NONPOS_SLACK: s or z not > 0
+/* One batched regularized-IPM step (rows a1-a8).  status: [b] (may be NULL when b == 0: no-op) (RR_ST_NONPOS_SLACK: s or z not > 0
  * on entry -> iterate untouched, direction NaN; RR_ST_LS_FAILED: no Armijo point -> iterate
  * untouched, alpha_p = 0; pivot failures as in rr_factor_solve). */
 rr_err ipm_step(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it,

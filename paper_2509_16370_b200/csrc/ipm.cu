@@ -104,6 +104,8 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   // ---- issue the loads of stage i (i == N: terminal) into the padded shared layout `dst` ----
   // Real elements travel by cp.async (8-byte LDGSTS, asynchronous); padding is stored directly.
   // finish_stage() completes Σ, r_z and the positivity check once the copies have landed.
+  // the padded layout equals the global one when the dims are the template dims: contiguous copies
+  const bool exact = (n == NX && m == NU && a.d.ng == NG && a.d.nc == NC);
   auto issue_stage_data = [&](int i, double* dst) {
     const bool term = (i == N);
     const int ww = term ? n : w;
@@ -114,6 +116,36 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
       if (ok) cp_async8(dst + off, src);
       else dst[off] = pad;
     };
+    if (exact && !term) {
+      copy_async(dst + IB::F, a.d_.A + si * NX * NX, NX * NX, j, LG);       // F = [A | B], ld NX
+      copy_async(dst + IB::F + NX * NX, a.d_.B + si * NX * NU, NX * NU, j, LG);
+      for (int e = j; e < NZ * NZ; e += LG) {  // P = [[Q M]; [Mᵀ R]] unpacked
+        const int r = e % NZ, c = e / NZ;
+        const double* src;
+        if (r < NX && c < NX) src = a.d_.Q + si * sn + (r >= c ? pidx(NX, r, c) : pidx(NX, c, r));
+        else if (r < NX) src = a.d_.M + si * NX * NU + r + (c - NX) * NX;
+        else if (c < NX) src = a.d_.M + si * NX * NU + c + (r - NX) * NX;
+        else src = a.d_.R + si * sm + (r >= c ? pidx(NU, r - NX, c - NX) : pidx(NU, c - NX, r - NX));
+        cp_async8(dst + IB::P + e, src);
+      }
+      copy_async(dst + IB::gf, a.d_.gradf + si * NZ, NZ, j, LG);
+      copy_async(dst + IB::cv, a.d_.dres + si * NX, NX, j, LG);
+      copy_async(dst + IB::yi, a.it.y + (inst * (sN + 1) + i) * NX, 2 * NX, j, LG);  // y_i | y_{i+1}
+      copy_async(dst + IB::xb, a.it.x + (inst * (sN + 1) + i) * NX, NX, j, LG);
+      copy_async(dst + IB::ub, a.it.u + si * NU, NU, j, LG);
+      if (NG > 0) {
+        copy_async(dst + IB::G, a.d_.Gj + si * NG * NZ, NG * NZ, j, LG);
+        copy_async(dst + IB::gv, a.d_.gv + si * NG, NG, j, LG);
+        copy_async(dst + IB::s, a.it.s + si * NG, NG, j, LG);
+        copy_async(dst + IB::z, a.it.z + si * NG, NG, j, LG);
+      }
+      if (NC > 0) {
+        copy_async(dst + IB::Ce, a.d_.Ce + si * NC * NZ, NC * NZ, j, LG);
+        copy_async(dst + IB::ce, a.d_.ce + si * NC, NC, j, LG);
+        copy_async(dst + IB::lam, a.it.lam + si * NC, NC, j, LG);
+      }
+      return;
+    }
     for (int e = j; e < NX * NZ; e += LG) {  // F = [A B]
       const int k = e % NX, c = e / NX;
       const bool okA = !term && k < n && c < n;

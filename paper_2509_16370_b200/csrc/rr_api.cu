@@ -35,9 +35,10 @@ rr_err rr_factor_solve(const rr_dims* dims, const rr_problem* prob, const rr_fac
                        const rr_solution* sol, void* workspace, int64_t workspace_bytes,
                        int32_t* status, void* stream) {
   if (!dims_ok(dims)) return set_err(RR_E_INVALID, "rr_factor_solve: invalid dims%s");
-  if (prob == nullptr || sol == nullptr || status == nullptr)
-    return set_err(RR_E_INVALID, "rr_factor_solve: null %s", "prob/sol/status");
-  if (dims->batch == 0) return RR_OK;
+  if (prob == nullptr || sol == nullptr)
+    return set_err(RR_E_INVALID, "rr_factor_solve: null %s", "prob/sol");
+  if (dims->batch == 0) return RR_OK;  // nothing to do; status may be null for an empty batch
+  if (status == nullptr) return set_err(RR_E_INVALID, "rr_factor_solve: null %s", "status");
   const double* req[] = {prob->QN, prob->qN, prob->c0, prob->delta};
   for (const double* p : req)
     if (p == nullptr) return set_err(RR_E_INVALID, "rr_factor_solve: null %s", "terminal/initial operand");
@@ -122,8 +123,9 @@ int64_t ipm_workspace_bytes(const ipm_dims* dims) {
 rr_err ipm_step(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it, const ipm_params* params,
                 const ipm_result* res, void* workspace, int64_t workspace_bytes, int32_t* status, void* stream) {
   if (!ipm_dims_ok(dims)) return set_err(RR_E_INVALID, "ipm_step: invalid dims%s");
-  if (!data || !it || !params || !res || !status) return set_err(RR_E_INVALID, "ipm_step: null %s", "argument");
-  if (dims->batch == 0) return RR_OK;
+  if (!data || !it || !params || !res) return set_err(RR_E_INVALID, "ipm_step: null %s", "argument");
+  if (dims->batch == 0) return RR_OK;  // nothing to do; status may be null for an empty batch
+  if (!status) return set_err(RR_E_INVALID, "ipm_step: null %s", "status");
   if (!(params->tau > 0.0 && params->tau < 1.0) || !(params->armijo_c > 0.0 && params->armijo_c < 0.5) ||
       !(params->beta > 0.0 && params->beta < 1.0) || params->max_backtracks < 0)
     return set_err(RR_E_INVALID, "ipm_step: invalid %s", "line-search parameters");

@@ -14,6 +14,8 @@ TOL = 1e-9
 
 
 def rel_blocks(g, o):
+    if np.asarray(g).size == 0:
+        return 0.0
     g = np.asarray(g).reshape(g.shape[0], -1)
     o = np.asarray(o).reshape(o.shape[0], -1)
     if g.shape[1] == 0:
