@@ -27,10 +27,10 @@ struct IpmBuf {  // padded per-stage IPM data in shared memory (doubles, even of
   static constexpr int NZ = NX + NU;
   static constexpr int E2 = 2;
   static constexpr int F = 0;                         // [A B] col-major NX × NZ
-  static constexpr int P = F + NX * NZ;               // P full NZ × NZ col-major
-  static constexpr int gf = P + NZ * NZ;              // ∇f (NZ)
+  static constexpr int P = F + ((NX * NZ + 1) & ~1);  // P full NZ × NZ col-major
+  static constexpr int gf = P + ((NZ * NZ + 1) & ~1); // ∇f (NZ)
   static constexpr int cv = gf + ((NZ + 1) & ~1);     // dres (NX)
-  static constexpr int G = cv + NX;                   // G col-major NG × NZ
+  static constexpr int G = cv + ((NX + 1) & ~1);      // G col-major NG × NZ
   static constexpr int gv = G + ((NG * NZ + 1) & ~1); // g (NG)
   static constexpr int s = gv + ((NG + 1) & ~1);
   static constexpr int z = s + ((NG + 1) & ~1);
@@ -41,12 +41,45 @@ struct IpmBuf {  // padded per-stage IPM data in shared memory (doubles, even of
   static constexpr int lam = ce + ((NC + 1) & ~1);
   static constexpr int yi = lam + ((NC + 1) & ~1);    // y_i
   static constexpr int yn = yi + NX;                  // y_{i+1}
-  static constexpr int xb = yn + NX;                  // x̄_i
-  static constexpr int ub = xb + NX;                  // ū_i
+  static constexpr int xb = yn + ((NX + 1) & ~1);     // x̄_i
+  static constexpr int ub = xb + ((NX + 1) & ~1);     // ū_i
   static constexpr int du = ub + ((NU + 1) & ~1);     // Δu_i exchange
   static constexpr int SIZE = du + ((NU + 1) & ~1);
   static constexpr int PAD = (SIZE + 1) & ~1;
 };
+
+// Σ log a_e accumulated as a running product m·2^k (frexp renormalisation after every factor, so no
+// overflow/underflow for any positive normal factors), with a single log at the end: the barrier
+// sums of 𝒜 cost one log per lane instead of one per slack.
+struct LogAcc {
+  double m = 1.0;
+  int k = 0;
+  __device__ __forceinline__ void add(double x) {
+    int e;
+    m = frexp(m * x, &e);
+    k += e;
+  }
+  __device__ __forceinline__ double value() const { return log(m) + k * 0.69314718055994530942; }
+};
+
+// x[e] += α d[e] for e < cnt over the LG lanes of a group (lane j), four independent loads in flight
+// per lane before the dependent stores (x and d may not alias, but the compiler cannot know that).
+template <int LG>
+__device__ __forceinline__ void axpy_lanes(double* x, const double* d, double alpha, int64_t cnt, int j) {
+  constexpr int U = 4;
+  int64_t e = j;
+  for (; e + (U - 1) * LG < cnt; e += U * LG) {
+    double xv[U], dv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      xv[u] = x[e + u * LG];
+      dv[u] = d[e + u * LG];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[e + u * LG] = fma(alpha, dv[u], xv[u]);
+  }
+  for (; e < cnt; e += LG) x[e] = fma(alpha, d[e], x[e]);
+}
 
 // cart-pole, explicit Euler (C4); θ from the hanging position, φ = θ − π.
 __device__ __forceinline__ void cartpole_step(const double* prm, const double* x, double u, double* xn) {
@@ -73,7 +106,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   using IB = IpmBuf<NX, NU, NG, NC>;
   constexpr int NZ = NX + NU;
   constexpr int IPW = 32 / LG;
-  constexpr int SLOT = ((2 * IB::PAD + WK::PAD + 2 * RC::PAD + NX + 1) & ~1);
+  constexpr int SLOT = group_stride(2 * IB::PAD + WK::PAD + 2 * RC::PAD + NX, LG);
   static_assert(NG <= LG && NC <= LG, "constraint count per stage exceeds the lane group");
 
   const int n = a.d.nx, m = a.d.nu, N = a.d.N, w = n + m;
@@ -106,6 +139,21 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   // finish_stage() completes Σ, r_z and the positivity check once the copies have landed.
   // the padded layout equals the global one when the dims are the template dims: contiguous copies
   const bool exact = (n == NX && m == NU && a.d.ng == NG && a.d.nc == NC);
+  // per-lane gather table of the unpacked P (exact path): entry e = j + t·LG of the NZ × NZ
+  // col-major P comes from Q (sel 0, packed 'L'), M (sel 1) or R (sel 2, packed); code = off·4 + sel
+  constexpr int PT = (NZ * NZ + LG - 1) / LG;
+  int pg[PT];
+#pragma unroll
+  for (int t = 0; t < PT; ++t) {
+    const int e = j + t * LG, r = e % NZ, c = e / NZ;
+    int code;
+    if (e >= NZ * NZ) code = 3;
+    else if (r < NX && c < NX) code = (r >= c ? pidx(NX, r, c) : pidx(NX, c, r)) * 4;
+    else if (r < NX) code = (r + (c - NX) * NX) * 4 + 1;
+    else if (c < NX) code = (c + (r - NX) * NX) * 4 + 1;
+    else code = (r >= c ? pidx(NU, r - NX, c - NX) : pidx(NU, c - NX, r - NX)) * 4 + 2;
+    pg[t] = code;
+  }
   auto issue_stage_data = [&](int i, double* dst) {
     const bool term = (i == N);
     const int ww = term ? n : w;
@@ -119,14 +167,15 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
     if (exact && !term) {
       copy_async(dst + IB::F, a.d_.A + si * NX * NX, NX * NX, j, LG);       // F = [A | B], ld NX
       copy_async(dst + IB::F + NX * NX, a.d_.B + si * NX * NU, NX * NU, j, LG);
-      for (int e = j; e < NZ * NZ; e += LG) {  // P = [[Q M]; [Mᵀ R]] unpacked
-        const int r = e % NZ, c = e / NZ;
-        const double* src;
-        if (r < NX && c < NX) src = a.d_.Q + si * sn + (r >= c ? pidx(NX, r, c) : pidx(NX, c, r));
-        else if (r < NX) src = a.d_.M + si * NX * NU + r + (c - NX) * NX;
-        else if (c < NX) src = a.d_.M + si * NX * NU + c + (r - NX) * NX;
-        else src = a.d_.R + si * sm + (r >= c ? pidx(NU, r - NX, c - NX) : pidx(NU, c - NX, r - NX));
-        cp_async8(dst + IB::P + e, src);
+      {  // P = [[Q M]; [Mᵀ R]] unpacked through the per-lane gather table
+        const double* bq = a.d_.Q + si * (NX * (NX + 1) / 2);
+        const double* bm = a.d_.M + si * (NX * NU);
+        const double* br = a.d_.R + si * (NU * (NU + 1) / 2);
+#pragma unroll
+        for (int t = 0; t < PT; ++t) {
+          const int code = pg[t], sel = code & 3;
+          if (sel != 3) cp_async8(dst + IB::P + j + t * LG, (sel == 0 ? bq : (sel == 1 ? bm : br)) + (code >> 2));
+        }
       }
       copy_async(dst + IB::gf, a.d_.gradf + si * NZ, NZ, j, LG);
       copy_async(dst + IB::cv, a.d_.dres + si * NX, NX, j, LG);
@@ -228,8 +277,9 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
     for (int e = j; e < NG; e += LG) {
       const double sv = sb[IB::s + e], zv = sb[IB::z + e], gvv = sb[IB::gv + e];
       if (e < ng && (!(sv > 0.0) || !(zv > 0.0))) nonpos_stage = min(nonpos_stage, i);
-      sb[IB::sig + e] = (e < ng) ? 1.0 / (sv / zv + 1.0 / eta) : 0.0;
-      sb[IB::rz + e] = (e < ng) ? gvv + mu / zv : 0.0;
+      // Σ = (s/z + 1/η)⁻¹ = zη / (sη + z); reciprocals by Newton-refined rcp (≤ 1 ulp) for the divides
+      sb[IB::sig + e] = (e < ng) ? zv * eta * rcp_nr(fma(sv, eta, zv)) : 0.0;
+      sb[IB::rz + e] = (e < ng) ? fma(mu, rcp_nr(zv), gvv) : 0.0;
     }
     __syncwarp();
   };
@@ -241,14 +291,25 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
     finish_stage(i);
   };
 
+  // lane j's own column of Σ^{1/2}-weighted G and η-weighted C_e, cached in registers once per stage
+  // (the column-major G / C_e reads at stride NG / NC would otherwise repeat for every column s)
+  constexpr int NGR = NG > 0 ? NG : 1, NCR = NC > 0 ? NC : 1;
+  double gsj[NGR], cej[NCR];
+  auto cache_cols = [&]() {
+    const int jc = j < NZ ? j : 0;
+#pragma unroll
+    for (int e = 0; e < NG; ++e) gsj[e] = sb[IB::sig + e] * sb[IB::G + e + jc * NG];
+#pragma unroll
+    for (int e = 0; e < NC; ++e) cej[e] = eta * sb[IB::Ce + e + jc * NC];
+  };
   // condensed P̃ column j: P + GᵀΣG + η C_eᵀC_e
   auto Pt = [&](int s) -> double {
     if (j >= NZ) return 0.0;
     double v = sb[IB::P + j * NZ + s];
 #pragma unroll
-    for (int e = 0; e < NG; ++e) v = fma(sb[IB::G + e + s * NG] * sb[IB::sig + e], sb[IB::G + e + j * NG], v);
+    for (int e = 0; e < NG; ++e) v = fma(sb[IB::G + e + s * NG], gsj[e], v);
 #pragma unroll
-    for (int e = 0; e < NC; ++e) v = fma(eta * sb[IB::Ce + e + s * NC], sb[IB::Ce + e + j * NC], v);
+    for (int e = 0; e < NC; ++e) v = fma(sb[IB::Ce + e + s * NC], cej[e], v);
     return v;
   };
   // condensed gradient s̃_j = ∇ₓℒ + GᵀΣ r_z + η C_eᵀ c_e, ∇ₓℒ = ∇f + Cᵀy + Gᵀz + C_eᵀλ
@@ -260,15 +321,16 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
     for (int r = 0; r < NX; ++r) v = fma(sb[IB::F + r + j * NX], sb[IB::yn + r], v);
 #pragma unroll
     for (int e = 0; e < NG; ++e)
-      v = fma(sb[IB::G + e + j * NG], sb[IB::z + e] + sb[IB::sig + e] * sb[IB::rz + e], v);
+      v = fma(sb[IB::G + e + j * NG], sb[IB::z + e], fma(gsj[e], sb[IB::rz + e], v));
 #pragma unroll
-    for (int e = 0; e < NC; ++e) v = fma(sb[IB::Ce + e + j * NC], sb[IB::lam + e] + eta * sb[IB::ce + e], v);
+    for (int e = 0; e < NC; ++e) v = fma(sb[IB::Ce + e + j * NC], sb[IB::lam + e], fma(cej[e], sb[IB::ce + e], v));
     return v;
   };
 
   // ================= pass 1: backward (condense + Eq.(RR)) =================
   double Vc[NX];
   load_stage_now(N);
+  cache_cols();
   {
     // terminal: V_N = Q̃_N (condensed), v_N = q̃_N
 #pragma unroll
@@ -288,6 +350,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
     cp_async_wait<1>();
     __syncwarp();
     finish_stage(i);
+    cache_cols();
     auto Pcol = [&](int s) -> double { return Pt(s); };
     const double qj = qt();
     double U[NZ], b[NZ];
@@ -307,7 +370,8 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   ST::mulSinv(xr, wk);
   __syncwarp();
   // per-lane partial sums
-  double sD = 0.0, sK0 = 0.0, sK1 = 0.0, sK2 = 0.0, sLog = 0.0;
+  double sD = 0.0, sK0 = 0.0, sK1 = 0.0, sK2 = 0.0;
+  LogAcc sLog;  // Σ log s as a renormalised running product (one log at the end)
   double sDyn0 = 0.0;  // nonlinear-model dynamics terms of 𝒜 at α = 0 (trial points recompute them)
   double amax = 1.0, admax = 1.0;
   const double tau = a.prm.tau;
@@ -342,15 +406,16 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
       for (int c = 0; c < NZ; ++c) gd = fma(sb[IB::G + j + c * NG], dz_full[c], gd);
       const double s = sb[IB::s + j], z = sb[IB::z + j], g = sb[IB::gv + j];
       const double dzv = sb[IB::sig + j] * (gd + sb[IB::rz + j]);
-      const double dsv = -(s / z) * dzv + mu / z - s;
+      const double iz = rcp_nr(z);
+      const double dsv = fma(-(s * iz), dzv, fma(mu, iz, -s));
       if (dsv < 0.0) amax = fmin(amax, tau * s / (-dsv));
       if (dzv < 0.0) admax = fmin(admax, tau * z / (-dzv));
       const double gs = g + s, bq = gd + dsv;
-      sD += (z + eta * gs) * bq + (-mu / s) * dsv;
+      sD += (z + eta * gs) * bq + (-mu * rcp_nr(s)) * dsv;
       sK0 += z * gs + 0.5 * eta * gs * gs;
       sK1 += z * bq + eta * gs * bq;
       sK2 += 0.5 * eta * bq * bq;
-      sLog += log(s);
+      sLog.add(s);
       if (valid) {
         if (term) {
           a.r.dsN[inst * ng + j] = dsv;
@@ -489,6 +554,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   __syncwarp();
   sb = (N & 1) ? sbuf1 : sbuf0;
   finish_stage(N);
+  cache_cols();
   {
     double dz_full[NZ];
 #pragma unroll
@@ -503,31 +569,33 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
     expand_stage(N, dz_full);
   }
   // ---- reduce the partial sums over the lane group ----
+  // group-masked collectives: pass 3 below runs a data-dependent number of backtracks per instance,
+  // so the lane groups of a warp diverge there and must never wait on each other
+  const unsigned gmask = (LG == 32) ? 0xffffffffu : (((1u << LG) - 1u) << gbase);
   auto gsum = [&](double v) {
 #pragma unroll
-    for (int off = LG / 2; off > 0; off >>= 1) v += __shfl_xor_sync(RR_FULL_MASK, v, off);
+    for (int off = LG / 2; off > 0; off >>= 1) v += __shfl_xor_sync(gmask, v, off);
     return v;
   };
   auto gmin = [&](double v) {
 #pragma unroll
-    for (int off = LG / 2; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(RR_FULL_MASK, v, off));
+    for (int off = LG / 2; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(gmask, v, off));
     return v;
   };
   const double D = gsum(sD);
   const double K0 = gsum(sK0) + a.d_.fval[inst];
   const double K1 = gsum(sK1), K2 = gsum(sK2);
-  const double A0 = K0 + gsum(sDyn0) - mu * gsum(sLog);
+  const double A0 = K0 + gsum(sDyn0) - mu * gsum(sLog.value());
   amax = gmin(amax);
   admax = gmin(admax);
   int32_t status = st;
   int np = nonpos_stage;
 #pragma unroll
   for (int off = LG / 2; off > 0; off >>= 1) {
-    status = max(status, __shfl_xor_sync(RR_FULL_MASK, status, off));
-    np = min(np, __shfl_xor_sync(RR_FULL_MASK, np, off));
+    status = max(status, __shfl_xor_sync(gmask, status, off));
+    np = min(np, __shfl_xor_sync(gmask, np, off));
   }
-  const unsigned gmask = (LG == 32) ? 0xffffffffu : (((1u << LG) - 1u) << gbase);
-  if (status == 0 && (__ballot_sync(RR_FULL_MASK, bad) & gmask)) status = RR_ST_NONFINITE;
+  if (status == 0 && (__ballot_sync(gmask, bad) & gmask)) status = RR_ST_NONFINITE;
   if (np != 0x7fffffff) status = mk_status(RR_ST_NONPOS_SLACK, np);
 
   // ================= pass 3: Armijo backtracking over (x, s) with 𝒜 =================
@@ -536,17 +604,33 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   bool accepted = false;
   if (status == 0) {
     for (nb = 0; nb <= a.prm.max_backtracks; ++nb) {
-      double sl = 0.0, sdyn = 0.0;
+      LogAcc sl;
+      double sdyn = 0.0;
       bool pos = true;
       for (int i = j; i <= N; i += LG) {  // stages distributed over the lanes
         const bool term = (i == N);
         const int ng = term ? a.d.ngN : a.d.ng;
         const double* sp = term ? a.it.sN + inst * ng : a.it.s + (inst * sN + i) * ng;
         const double* dsp = term ? a.r.dsN + inst * ng : a.r.ds + (inst * sN + i) * ng;
-        for (int e = 0; e < ng; ++e) {
-          const double sa = sp[e] + alpha * dsp[e];
-          pos &= sa > 0.0;
-          sl += log(sa);
+        if (ng == NG) {  // all loads of the stage issued before the first use
+          double sv[NG], dv[NG];
+#pragma unroll
+          for (int e = 0; e < NG; ++e) {
+            sv[e] = sp[e];
+            dv[e] = dsp[e];
+          }
+#pragma unroll
+          for (int e = 0; e < NG; ++e) {
+            const double sa = fma(alpha, dv[e], sv[e]);
+            pos &= sa > 0.0;
+            sl.add(sa);
+          }
+        } else {
+          for (int e = 0; e < ng; ++e) {
+            const double sa = fma(alpha, dsp[e], sp[e]);
+            pos &= sa > 0.0;
+            sl.add(sa);
+          }
         }
         if (model == IPM_MODEL_CARTPOLE && !term) {
           double xa[4], xnm[4];
@@ -564,10 +648,10 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
           }
         }
       }
-      sl = gsum(sl);
+      const double slog = gsum(sl.value());
       sdyn = gsum(sdyn);
-      const bool allpos = __all_sync(RR_FULL_MASK, pos);
-      const double At = K0 + alpha * (K1 + alpha * K2) - mu * sl + sdyn;
+      const bool allpos = __ballot_sync(gmask, !pos) == 0;
+      const double At = K0 + alpha * (K1 + alpha * K2) - mu * slog + sdyn;
       if (allpos && At <= A0 + a.prm.armijo_c * alpha * D) {
         Aacc = At;
         accepted = true;
@@ -583,24 +667,19 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   }
 
   // ================= pass 4: update the iterate in place =================
+  auto axpy_group = [&](double* x, const double* d, double al, int64_t cnt, int jj) { axpy_lanes<LG>(x, d, al, cnt, jj); };
   if (valid && accepted) {
     const int64_t nx1 = (sN + 1) * n;
-    for (int64_t e = j; e < nx1; e += LG) {
-      a.it.x[inst * nx1 + e] += alpha * a.r.dx[inst * nx1 + e];
-      a.it.y[inst * nx1 + e] += alpha * a.r.dy[inst * nx1 + e];
-    }
-    for (int64_t e = j; e < sN * m; e += LG) a.it.u[inst * sN * m + e] += alpha * a.r.du[inst * sN * m + e];
+    axpy_group(a.it.x + inst * nx1, a.r.dx + inst * nx1, alpha, nx1, j);
+    axpy_group(a.it.y + inst * nx1, a.r.dy + inst * nx1, alpha, nx1, j);
+    axpy_group(a.it.u + inst * sN * m, a.r.du + inst * sN * m, alpha, sN * m, j);
     const int64_t ngt = sN * a.d.ng, nct = sN * a.d.nc;
-    for (int64_t e = j; e < ngt; e += LG) {
-      a.it.s[inst * ngt + e] += alpha * a.r.ds[inst * ngt + e];
-      a.it.z[inst * ngt + e] += admax * a.r.dz[inst * ngt + e];
-    }
-    for (int e = j; e < a.d.ngN; e += LG) {
-      a.it.sN[inst * a.d.ngN + e] += alpha * a.r.dsN[inst * a.d.ngN + e];
-      a.it.zN[inst * a.d.ngN + e] += admax * a.r.dzN[inst * a.d.ngN + e];
-    }
-    for (int64_t e = j; e < nct; e += LG) a.it.lam[inst * nct + e] += alpha * a.r.dlam[inst * nct + e];
-    for (int e = j; e < a.d.ncN; e += LG) a.it.lamN[inst * a.d.ncN + e] += alpha * a.r.dlamN[inst * a.d.ncN + e];
+    axpy_group(a.it.s + inst * ngt, a.r.ds + inst * ngt, alpha, ngt, j);
+    axpy_group(a.it.z + inst * ngt, a.r.dz + inst * ngt, admax, ngt, j);
+    axpy_group(a.it.sN + inst * a.d.ngN, a.r.dsN + inst * a.d.ngN, alpha, a.d.ngN, j);
+    axpy_group(a.it.zN + inst * a.d.ngN, a.r.dzN + inst * a.d.ngN, admax, a.d.ngN, j);
+    axpy_group(a.it.lam + inst * nct, a.r.dlam + inst * nct, alpha, nct, j);
+    axpy_group(a.it.lamN + inst * a.d.ncN, a.r.dlamN + inst * a.d.ncN, alpha, a.d.ncN, j);
   }
   if (valid && j == 0) {
     a.status[inst] = status;
@@ -641,7 +720,8 @@ template <int NX, int NU, int NG, int NC, int LG>
 struct IpmCfg {
   static constexpr int WARPS = 4;
   static constexpr int IPB = WARPS * (32 / LG);
-  static constexpr int SLOT = ((2 * IpmBuf<NX, NU, NG, NC>::PAD + Work<NX, NU>::PAD + 2 * Rec<NX, NU>::PAD + NX + 1) & ~1);
+  static constexpr int SLOT =
+      group_stride(2 * IpmBuf<NX, NU, NG, NC>::PAD + Work<NX, NU>::PAD + 2 * Rec<NX, NU>::PAD + NX, LG);
   static size_t smem_bytes() { return sizeof(double) * (size_t)IPB * SLOT; }
   static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * Rec<NX, NU>::PAD; }
   static cudaError_t launch(const IpmArgs& a, cudaStream_t s) {

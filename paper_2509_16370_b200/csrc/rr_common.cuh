@@ -10,6 +10,14 @@
 
 namespace rrk {
 
+// Per-instance shared-memory slot stride (doubles) for lane groups of width lg < 16: the 16/lg
+// groups of a half-warp (one 64-bit shared wavefront) start lg double-banks apart, so broadcast
+// reads of the same offset -- and stride-1 / odd-stride column reads -- of different instances
+// fall in disjoint banks instead of serialising.
+__host__ __device__ constexpr int group_stride(int slot, int lg) {
+  return lg >= 16 ? ((slot + 1) & ~1) : ((slot + 1) & ~1) + ((lg - (((slot + 1) & ~1) % 16) + 16) % 16);
+}
+
 // LAPACK 'L' packed index of (r, c) with r >= c in an n×n symmetric matrix.
 __host__ __device__ __forceinline__ int pidx(int n, int r, int c) { return c * (2 * n - c - 1) / 2 + r; }
 

@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_kernel(const FusedA
   extern __shared__ __align__(16) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / LG, j = lane % LG, gbase = grp * LG;
-  double* slot = smem + (warp * IPW + grp) * LY::SLOT_PAD;
+  double* slot = smem + (warp * IPW + grp) * group_stride(LY::SLOT_PAD, LG);
   double* stg0 = slot;
   double* stg1 = slot + LY::STG_PAD;
   double* wk = slot + 2 * LY::STG_PAD;
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_kernel(const FusedA
 template <int NX, int NU, int LG, int WARPS, int MINB, bool EXACT>
 struct FusedCfg {
   static constexpr int IPB = WARPS * (32 / LG);  // instances per block
-  static size_t smem_bytes() { return sizeof(double) * (size_t)IPB * FusedLayout<NX, NU, EXACT>::SLOT_PAD; }
+  static size_t smem_bytes() { return sizeof(double) * (size_t)IPB * group_stride(FusedLayout<NX, NU, EXACT>::SLOT_PAD, LG); }
   static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * Rec<NX, NU>::PAD; }
   static cudaError_t launch(const FusedArgs& a, cudaStream_t s) {
     auto k = rr_fused_kernel<NX, NU, LG, WARPS, MINB, EXACT>;

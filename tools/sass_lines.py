@@ -15,6 +15,7 @@ def main(rep, so, kname):
     so = os.path.abspath(so)
     subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=d, capture_output=True)
     insts = []
+    seen = set()
     for cub in sorted(os.listdir(d)):
         if not cub.endswith(".cubin"):
             continue
@@ -24,6 +25,10 @@ def main(rep, so, kname):
             m = re.match(r"\s*\.text\.(\S+?):\s*$", l)
             if m:
                 cur = m.group(1)
+                if kname in cur:
+                    seen.add(cur)
+                    if len(seen) > 1:
+                        sys.exit("kernel substring %r is ambiguous: %s" % (kname, sorted(seen)))
                 continue
             if cur is None or kname not in cur:
                 continue

@@ -7,13 +7,19 @@ def main(rep, so, kname):
     d = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=d, capture_output=True)
     insts = []
+    seen = set()
     for cub in sorted(os.listdir(d)):
         txt = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True, text=True).stdout
         cur, line = None, None
         for l in txt.splitlines():
             m = re.match(r"\s*\.text\.(\S+?):\s*$", l)
             if m:
-                cur = m.group(1); continue
+                cur = m.group(1)
+                if kname in cur:
+                    seen.add(cur)
+                    if len(seen) > 1:
+                        sys.exit("kernel substring %r is ambiguous: %s" % (kname, sorted(seen)))
+                continue
             if cur is None or kname not in cur:
                 continue
             m = re.search(r'//## File "([^"]+)", line (\d+)', l)
