@@ -208,9 +208,153 @@ __device__ __forceinline__ void cta_sweep_reg(double* A, int /*lda == n*/, doubl
   *fail = bad;
 }
 
+// One 16×16 output tile at (r0, c0) of  C = op_A · B + init  (K multiple of 4) on one warp.
+template <int K, typename LoadA, typename LoadB, typename Init, typename Store>
+__device__ __forceinline__ void warp_tile16(int r0, int c0, LoadA&& la, LoadB&& lb, Init&& init, Store&& store,
+                                            int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  double c[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) c[a][b][e] = init(r0 + 8 * a + g, c0 + 8 * b + 2 * t + e);
+#pragma unroll
+  for (int kt = 0; kt < K / 4; ++kt) {
+    double av[2], bv[2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) av[a] = la(r0 + 8 * a + g, 4 * kt + t);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) bv[b] = lb(4 * kt + t, c0 + 8 * b + g);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) dmma884(c[a][b][0], c[a][b][1], av[a], bv[b]);
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) store(r0 + 8 * a + g, c0 + 8 * b + 2 * t + e, c[a][b][e]);
+}
+
+// Symmetric sweep of a 16×16 diagonal block held in one warp's registers: lane l owns column
+// c = l & 15, rows 8h .. 8h+7 (h = l >> 4).  Pivots 0..15 in order (the scalar sweep of the
+// block); pivot column / row entries travel by shuffles (row k = column k by symmetry).
+__device__ __forceinline__ void warp_sweep16(double (&a)[8], int lane, bool* bad) {
+  const int c = lane & 15, h = lane >> 4;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const double d = __shfl_sync(RR_FULL_MASK, a[k & 7], k + 16 * (k >> 3));
+    const double rowk = __shfl_sync(RR_FULL_MASK, a[k & 7], c + 16 * (k >> 3));  // A[k][c]
+    double colk[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) colk[i] = __shfl_sync(RR_FULL_MASK, a[i], k + 16 * h);  // A[8h+i][k]
+    *bad |= !(d > 0.0);
+    const double id = rcp_nr(d);
+    const double rs = rowk * id;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = 8 * h + i;
+      const double upd = fma(-colk[i], rs, a[i]);
+      a[i] = (r == k) ? ((c == k) ? -id : rs) : ((c == k) ? colk[i] * id : upd);
+    }
+  }
+}
+
+// Block (16-pivot) symmetric sweep of the n×n SPD matrix A (n % 16 == 0, swizzled ld n):
+// A <- −A⁻¹.  Sweeping the pivots of block p at once is the block form of the sweep operator:
+//   Z = A_pp⁻¹:  A_pp <- −Z,  A_rp <- A_rp Z,  A_pc <- Z A_pc,  A_rc <- A_rc − A_rp Z A_pc,
+// identical (up to rounding) to the 16 scalar sweeps of block p.  Per block: warp 0 sweeps A_pp in
+// registers; Y = A_{:,p} Z (DMMA, into `Y`, n × 16); the trailing update A_RC −= Y_R A_pC over the
+// lower tiles R >= C (mirrored to C, R) on DMMA; then column / row block p <- Y / Yᵀ (overlapped
+// with the next block's diagonal sweep).  3 barriers per block instead of 2 per pivot.
+// (A lookahead variant -- warp 0 updating and sweeping tile (p+1, p+1) during the trailing update --
+// measured slower on C3: the dependency chain tile -> sweep -> Y tile is the same length.)
 template <int n, int NTHREADS>
-__device__ __forceinline__ void cta_sweep_any(double* A, int lda, double* colbuf2, int tid, bool* fail) {
-  if constexpr (n % 16 == 0 && NTHREADS == 256) cta_sweep_reg<n>(A, lda, colbuf2, tid, fail);
+__device__ __forceinline__ void cta_sweep_blk(double* A, double* Y, int tid, bool* fail) {
+  constexpr int NB = n / 16;
+  constexpr int NW = NTHREADS / 32;
+  static_assert(n % 16 == 0, "block sweep needs n % 16 == 0");
+  const int lane = tid & 31, warp = tid >> 5;
+  bool bad = false;
+  auto S = [](int r, int c) { return swz<n>(r, c); };
+  for (int p = 0; p < NB; ++p) {
+    const int p0 = 16 * p;
+    if (warp == 0) {
+      double a[8];
+      const int c = lane & 15, h = lane >> 4;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = A[S(p0 + 8 * h + i, p0 + c)];
+      warp_sweep16(a, lane, &bad);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) A[S(p0 + 8 * h + i, p0 + c)] = a[i];  // −Z
+    } else if (p > 0) {
+      // previous block q = p − 1: column block q <- Y, row block q <- Yᵀ (rows outside block q)
+      const int q0 = p0 - 16;
+      for (int e = tid - 32; e < n * 16; e += NTHREADS - 32) {
+        const int r = e % n, cc = e / n;
+        if (r >= q0 && r < q0 + 16) continue;
+        const double v = Y[S(r, cc)];
+        A[S(r, q0 + cc)] = v;
+        A[S(q0 + cc, r)] = v;
+      }
+    }
+    __syncthreads();
+    // Y_R = A_{R,p} Z = −A_{R,p} A'_pp for the row tiles R != p
+    for (int R = warp; R < NB; R += NW) {
+      if (R == p) continue;
+      warp_tile16<16>(
+          16 * R, 0, [&](int r, int k) { return A[S(r, p0 + k)]; }, [&](int k, int c) { return -A[S(p0 + k, p0 + c)]; },
+          [&](int, int) { return 0.0; }, [&](int r, int c, double v) { Y[S(r, c)] = v; }, lane);
+    }
+    __syncthreads();
+    // trailing update of the lower tiles R >= C (R, C != p), mirrored: A_RC −= Y_R A_pC
+    constexpr int NO = NB - 1, NT = NO * (NO + 1) / 2;
+    for (int tt = warp; tt < NT; tt += NW) {
+      int R = 0, C = 0, cnt = tt;  // tt-th pair (R >= C) of the blocks other than p
+      for (int cc = 0; cc < NO; ++cc) {
+        if (cnt < NO - cc) {
+          C = cc;
+          R = cc + cnt;
+          break;
+        }
+        cnt -= NO - cc;
+      }
+      R += (R >= p);
+      C += (C >= p);
+      const int r0 = 16 * R, c0 = 16 * C;
+      warp_tile16<16>(
+          r0, c0, [&](int r, int k) { return -Y[S(r, k)]; }, [&](int k, int c) { return A[S(p0 + k, c)]; },
+          [&](int r, int c) { return A[S(r, c)]; },
+          [&](int r, int c, double v) {
+            A[S(r, c)] = v;
+            if (R != C) A[S(c, r)] = v;
+          },
+          lane);
+    }
+    __syncthreads();
+  }
+  {  // last block's row / column
+    const int q0 = n - 16;
+    for (int e = tid; e < n * 16; e += NTHREADS) {
+      const int r = e % n, cc = e / n;
+      if (r >= q0) continue;
+      const double v = Y[S(r, cc)];
+      A[S(r, q0 + cc)] = v;
+      A[S(q0 + cc, r)] = v;
+    }
+  }
+  __syncthreads();
+  *fail = bad;
+}
+
+template <int n, int NTHREADS>
+__device__ __forceinline__ void cta_sweep_any(double* A, int lda, double* colbuf2, double* ytmp, int tid, bool* fail) {
+  if constexpr (n % 16 == 0 && n >= 32) cta_sweep_blk<n, NTHREADS>(A, ytmp, tid, fail);
+  else if constexpr (n % 16 == 0 && NTHREADS == 256) cta_sweep_reg<n>(A, lda, colbuf2, tid, fail);
   else cta_sweep<n>(A, lda, colbuf2, tid, NTHREADS, fail);
 }
 
@@ -294,7 +438,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
     }
     __syncthreads();
     bool fail = false;
-    cta_sweep_any<NX, NTHREADS>(sm + L::SI, n, sm + L::pr, tid, &fail);  // SI = −S⁻¹
+    cta_sweep_any<NX, NTHREADS>(sm + L::SI, n, sm + L::pr, sm + L::TT, tid, &fail);  // SI = −S⁻¹
     if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, i);
     // [W | We] = S⁻¹ [V | Ve]  -> TT region temporarily (same ld/swizzle), then g = v + We
     cta_gemm<NX, NX + 1, NX, false>(
@@ -328,7 +472,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
         warp, NW, lane);
     __syncthreads();
     // G⁻¹ (sweep in place: Uuu = −G⁻¹), K̃ = G⁻¹ [H | h]
-    cta_sweep_any<NU, NTHREADS>(sm + L::Uuu, m, sm + L::pr, tid, &fail);
+    cta_sweep_any<NU, NTHREADS>(sm + L::Uuu, m, sm + L::pr, sm + L::TT, tid, &fail);
     if (fail && st == 0) st = mk_status(RR_ST_G_NOT_PD, i);
     cta_gemm<NU, NX + 1, NU, false>(
         [&](int r, int k) { return -sm[L::Uuu + Y(r, k)]; }, [&](int k, int c) { return sm[L::Uux + Y(k, c)]; },
@@ -381,7 +525,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
   __syncthreads();
   {
     bool fail = false;
-    cta_sweep_any<NX, NTHREADS>(sm + L::SI, n, sm + L::pr, tid, &fail);
+    cta_sweep_any<NX, NTHREADS>(sm + L::SI, n, sm + L::pr, sm + L::TT, tid, &fail);
     if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, 0);
   }
   for (int r = tid; r < n; r += NTHREADS) {
