@@ -117,6 +117,80 @@ __device__ __forceinline__ void cta_gemm(LoadA&& la, LoadB&& lb, Init&& init, St
   }
 }
 
+// Lower-tile GEMM for a SYMMETRIC M×M result: C = op(A)·B + init over the 16×16 super-tiles
+// (R, C) with R >= C only (masked to M); store(r, c, v, mirror) is told whether the tile is
+// off-diagonal, so the caller can write the transposed entry.  Halves the DMMA work of W, U, V_i.
+template <int M, int K, typename LoadA, typename LoadB, typename Init, typename Store>
+__device__ __forceinline__ void cta_gemm_lower(LoadA&& la, LoadB&& lb, Init&& init, Store&& store, int warp,
+                                               int nwarps, int lane) {
+  constexpr int MT = (M + 15) / 16, NTL = MT * (MT + 1) / 2, KT = K / 4;
+  static_assert(K % 4 == 0, "K must be a multiple of 4");
+  const int g = lane >> 2, t = lane & 3;
+  for (int tile = warp; tile < NTL; tile += nwarps) {
+    int R = 0, rem = tile;
+    while (rem > R) {
+      rem -= R + 1;
+      ++R;
+    }
+    const int C = rem, m0 = 16 * R, n0 = 16 * C;
+    const bool mir = R != C;
+    double c[2][2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = m0 + 8 * a + g, col = n0 + 8 * b + 2 * t + e;
+          c[a][b][e] = (r < M && col < M) ? init(r, col) : 0.0;
+        }
+#pragma unroll 4
+    for (int kt = 0; kt < KT; ++kt) {
+      double av[2], bv[2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int r = m0 + 8 * a + g;
+        av[a] = (r < M) ? la(r, 4 * kt + t) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int col = n0 + 8 * b + g;
+        bv[b] = (col < M) ? lb(4 * kt + t, col) : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma884(c[a][b][0], c[a][b][1], av[a], bv[b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = m0 + 8 * a + g, col = n0 + 8 * b + 2 * t + e;
+          if (r < M && col < M) store(r, col, c[a][b][e], mir);
+        }
+  }
+}
+
+// y = init + A x for an M×K matrix on the SIMT pipe: PARTS adjacent threads per row (power of
+// two), partial sums combined by shuffles.  All NTHREADS threads must call it (uniform loop).
+template <int M, int K, int NTHREADS, typename LoadA, typename LoadX, typename Init, typename Out>
+__device__ __forceinline__ void cta_matvec(LoadA&& la, LoadX&& x, Init&& init, Out&& out, int tid) {
+  constexpr int P0 = NTHREADS / M;
+  constexpr int PARTS = P0 >= 8 ? 8 : (P0 >= 4 ? 4 : (P0 >= 2 ? 2 : 1));
+  for (int base = 0; base < M * PARTS; base += NTHREADS) {
+    const int task = base + tid, row = task / PARTS, part = task % PARTS;
+    double acc = 0.0;
+    if (row < M)
+      for (int k = part; k < K; k += PARTS) acc = fma(la(row, k), x(k), acc);
+#pragma unroll
+    for (int off = PARTS / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(RR_FULL_MASK, acc, off);
+    if (row < M && part == 0) out(row, init(row) + acc);
+  }
+}
+
 // In-place symmetric sweep of the n×n SPD matrix A (ld lda) in shared memory: A <- −A⁻¹.
 // Pivot p: Ã_pp = −1/A_pp, Ã_rp = A_rp/A_pp, Ã_pc = A_pc/A_pp, Ã_rc = A_rc − A_rp A_pc/A_pp.
 // Returns (in *fail) whether a pivot was not > 0 (block-uniform).
@@ -440,54 +514,86 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
     bool fail = false;
     cta_sweep_any<NX, NTHREADS>(sm + L::SI, n, sm + L::pr, sm + L::TT, tid, &fail);  // SI = −S⁻¹
     if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, i);
-    // [W | We] = S⁻¹ [V | Ve]  -> TT region temporarily (same ld/swizzle), then g = v + We
-    cta_gemm<NX, NX + 1, NX, false>(
+    // W = S⁻¹ V (symmetric: S⁻¹ and V commute) -> TT region temporarily (same ld / swizzle), lower
+    // tiles mirrored; g = v_{i+1} + S⁻¹ (V e) on the SIMT pipe in the same phase
+    cta_gemm_lower<NX, NX>(
         [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k, int c) { return sm[L::VW + X(k, c)]; },
-        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::TT + X(r, c)] = v; }, warp, NW, lane);
+        [&](int, int) { return 0.0; },
+        [&](int r, int c, double v, bool mir) {
+          sm[L::TT + X(r, c)] = v;
+          if (mir) sm[L::TT + X(c, r)] = v;
+        },
+        warp, NW, lane);
+    cta_matvec<NX, NX, NTHREADS>(
+        [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k) { return sm[L::VW + X(k, NX)]; },
+        [&](int r) { return sm[L::vs + r]; }, [&](int r, double v) { sm[L::pr + r] = v; }, tid);
     __syncthreads();
     for (int e = tid; e < n * n; e += NTHREADS) sm[L::VW + e] = sm[L::TT + e];  // same layout: flat copy of W
-    for (int r = tid; r < n; r += NTHREADS) sm[L::pr + r] = sm[L::vs + r] + sm[L::TT + X(r, NX)];
     __syncthreads();
-    // [T | g] = [W F | g]   (F = [A B] = stage input columns, ld NX)
+    // T = W F (F = [A B] = stage input columns, ld NX);  b = (q; r) + Fᵀ g  (SIMT, same phase)
     cta_gemm<NX, NZ, NX, false>(
         [&](int r, int k) { return sm[L::VW + X(r, k)]; }, [&](int k, int c) { return sm[L::oA + X(k, c)]; },
         [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::TT + X(r, c)] = v; }, warp, NW, lane);
-    for (int r = tid; r < n; r += NTHREADS) sm[L::TT + X(r, NZ)] = sm[L::pr + r];
+    cta_matvec<NZ, NX, NTHREADS>(
+        [&](int r, int k) { return sm[L::oA + X(k, r)]; }, [&](int k) { return sm[L::pr + k]; },
+        [&](int r) { return r < NX ? sm[L::oq + r] : sm[L::orr + r - NX]; },
+        [&](int r, double v) {
+          if (r < NX) sm[L::Uxx + X(r, NX)] = v;  // b_x (column NX of the V/W region: W uses 0..NX-1)
+          else sm[L::Uux + Y(r - NX, NX)] = v;    // b_u
+        },
+        tid);
     __syncthreads();
-    // [U | b] = Fᵀ [T | g] + [P | (q; r)]: rows x -> Uxx|bx (ld NX), rows u -> Uux|bu, Uuu (ld NU)
-    cta_gemm<NZ, NZ + 1, NX, true>(
+    // U = Fᵀ T + P (symmetric): lower tiles only.  Rows x -> Uxx (lower part suffices: V_i below
+    // reads only its own lower tiles), rows u -> Uux = H and Uuu = G (mirrored: the sweep needs all)
+    cta_gemm_lower<NZ, NX>(
         [&](int r, int k) { return sm[L::oA + X(k, r)]; }, [&](int k, int c) { return sm[L::TT + X(k, c)]; },
-        [&](int r, int c) { return c < NZ ? Pat(r, c) : (r < NX ? sm[L::oq + r] : sm[L::orr + r - NX]); },
-        [&](int r, int c, double v) {
+        [&](int r, int c) { return Pat(r, c); },
+        [&](int r, int c, double v, bool mir) {
           if (r < NX) {
-            if (c < NX) sm[L::Uxx + X(r, c)] = v;
-            else if (c == NZ) sm[L::Uxx + X(r, NX)] = v;  // b_x
+            if (c < NX) sm[L::Uxx + X(r, c)] = v;  // (r < NX, c >= NX: the Hᵀ entry, stored as H)
           } else {
             const int u = r - NX;
-            if (c < NX) sm[L::Uux + Y(u, c)] = v;
-            else if (c == NZ) sm[L::Uux + Y(u, NX)] = v;  // b_u
-            else sm[L::Uuu + Y(u, c - NX)] = v;            // G
+            if (c < NX) {
+              sm[L::Uux + Y(u, c)] = v;
+            } else {
+              sm[L::Uuu + Y(u, c - NX)] = v;
+              if (mir) sm[L::Uuu + Y(c - NX, u)] = v;
+            }
           }
         },
         warp, NW, lane);
     __syncthreads();
-    // G⁻¹ (sweep in place: Uuu = −G⁻¹), K̃ = G⁻¹ [H | h]
+    // G⁻¹ (sweep in place: Uuu = −G⁻¹), K̃ = G⁻¹ H,  k̃ = G⁻¹ h  (= −K_i, −k_i)
     cta_sweep_any<NU, NTHREADS>(sm + L::Uuu, m, sm + L::pr, sm + L::TT, tid, &fail);
     if (fail && st == 0) st = mk_status(RR_ST_G_NOT_PD, i);
-    cta_gemm<NU, NX + 1, NU, false>(
+    cta_gemm<NU, NX, NU, false>(
         [&](int r, int k) { return -sm[L::Uuu + Y(r, k)]; }, [&](int k, int c) { return sm[L::Uux + Y(k, c)]; },
         [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::Kt + Y(r, c)] = v; }, warp, NW, lane);
+    cta_matvec<NU, NU, NTHREADS>(
+        [&](int r, int k) { return -sm[L::Uuu + Y(r, k)]; }, [&](int k) { return sm[L::Uux + Y(k, NX)]; },
+        [&](int) { return 0.0; }, [&](int r, double v) { sm[L::Kt + Y(r, NX)] = v; }, tid);
     __syncthreads();
-    // [V_i | v_i] = [Uxx | bx] − Hᵀ K̃  (in place: each tile reads its own init)
-    cta_gemm<NX, NX + 1, NU, true>(
+    // V_i = Uxx − Hᵀ K̃ (symmetric: lower tiles, mirrored, in place), v_i = b_x − Hᵀ k̃,
+    // M = A − B K̃,  m = c − δ v_{i+1} − B k̃   (M | m: [A | c − δv] − B [K̃ | k̃])
+    cta_gemm_lower<NX, NU>(
         [&](int r, int k) { return -sm[L::Uux + Y(k, r)]; }, [&](int k, int c) { return sm[L::Kt + Y(k, c)]; },
-        [&](int r, int c) { return sm[L::Uxx + X(r, c)]; }, [&](int r, int c, double v) { sm[L::Uxx + X(r, c)] = v; },
+        [&](int r, int c) { return sm[L::Uxx + X(r, c)]; },
+        [&](int r, int c, double v, bool mir) {
+          sm[L::Uxx + X(r, c)] = v;
+          if (mir) sm[L::Uxx + X(c, r)] = v;
+        },
         warp, NW, lane);
-    // M = [A | c − δ v_{i+1}] − B K̃  (K̃ column NX = G⁻¹h = −k)
-    cta_gemm<NX, NX + 1, NU, false>(
+    cta_gemm<NX, NX, NU, false>(
         [&](int r, int k) { return -sm[L::oA + X(r, NX + k)]; }, [&](int k, int c) { return sm[L::Kt + Y(k, c)]; },
-        [&](int r, int c) { return c < NX ? sm[L::oA + X(r, c)] : sm[L::oc + r] - delta * sm[L::vs + r]; },
-        [&](int r, int c, double v) { sm[L::MM + X(r, c)] = v; }, warp, NW, lane);
+        [&](int r, int c) { return sm[L::oA + X(r, c)]; }, [&](int r, int c, double v) { sm[L::MM + X(r, c)] = v; },
+        warp, NW, lane);
+    cta_matvec<NX, NU, NTHREADS>(
+        [&](int r, int k) { return -sm[L::Uux + Y(k, r)]; }, [&](int k) { return sm[L::Kt + Y(k, NX)]; },
+        [&](int r) { return sm[L::Uxx + X(r, NX)]; }, [&](int r, double v) { sm[L::Uxx + X(r, NX)] = v; }, tid);
+    cta_matvec<NX, NU, NTHREADS>(
+        [&](int r, int k) { return -sm[L::oA + X(r, NX + k)]; }, [&](int k) { return sm[L::Kt + Y(k, NX)]; },
+        [&](int r) { return sm[L::oc + r] - delta * sm[L::vs + r]; }, [&](int r, double v) { sm[L::MM + X(r, NX)] = v; },
+        tid);
     __syncthreads();
     // record K = −K̃[:, :NX] (ld NU), k = −K̃[:, NX], V_i (ld NX), v_i; optional factor outputs
     for (int e = tid; e < m * n; e += NTHREADS) rec[L::rK + e] = -sm[L::Kt + Y(e % m, e / m)];
@@ -507,11 +613,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
     if (a.f.v != nullptr)
       for (int r = tid; r < n; r += NTHREADS) a.f.v[(inst * (sN + 1) + i) * n + r] = sm[L::Uxx + X(r, NX)];
     __syncthreads();
-    // stage input is dead: stream the next stage in while [Φ | φ] = S⁻¹ M is formed
+    // stage input is dead: stream the next stage in while [Φ | φ] = S⁻¹ [M | m] is formed
     if (i > 0) issue_stage(i - 1);
-    cta_gemm<NX, NX + 1, NX, false>(
+    cta_gemm<NX, NX, NX, false>(
         [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k, int c) { return sm[L::MM + X(k, c)]; },
         [&](int, int) { return 0.0; }, [&](int r, int c, double v) { rec[L::rPHI + r + c * n] = v; }, warp, NW, lane);
+    cta_matvec<NX, NX, NTHREADS>(
+        [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k) { return sm[L::MM + X(k, NX)]; },
+        [&](int) { return 0.0; }, [&](int r, double v) { rec[L::rPHI + r + NX * n] = v; }, tid);
     // carry: V_i -> VW region (already in place: Uxx == VW, same layout), v_i -> vs
     for (int r = tid; r < n; r += NTHREADS) sm[L::vs + r] = sm[L::Uxx + X(r, NX)];
     __syncthreads();
@@ -608,9 +717,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
   if (tid == 0) a.status[inst] = status;
 }
 
-template <int NX, int NU>
+template <int NX, int NU, int NT_ = 256>
 struct CtaCfg {
-  static constexpr int NTHREADS = 256;
+  static constexpr int NTHREADS = NT_;
   static size_t smem_bytes() { return sizeof(double) * (size_t)CtaLayout<NX, NU>::TOTAL; }
   static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * CtaLayout<NX, NU>::REC; }
   static cudaError_t launch(const FusedArgs& a, cudaStream_t s) {
@@ -625,7 +734,7 @@ struct CtaCfg {
 
 template <typename F>
 static bool dispatch_cta(int nx, int nu, F&& f) {
-  if (nx == 64 && nu == 32) return f(CtaCfg<64, 32>{});
+  if (nx == 64 && nu == 32) return f(CtaCfg<64, 32, 512>{});
   if (nx == 32 && nu == 16) return f(CtaCfg<32, 16>{});
   if (nx == 24 && nu == 8) return f(CtaCfg<24, 8>{});
   return false;
