@@ -24,6 +24,21 @@
 
 namespace rrk {
 
+// Phase timestamps of one stage of CTA 0 (tools/cta_phase_probe.cu builds with RR_CTA_PROFILE);
+// compiled out otherwise.
+#ifdef RR_CTA_PROFILE
+#define RR_CTA_PROFILE_FWD RR_CTA_PROFILE
+__device__ long long g_cta_prof[32];
+#define RR_PROF(i, slot)                                                           \
+  do {                                                                             \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (i) == RR_CTA_PROFILE) g_cta_prof[slot] = clock64(); \
+  } while (0)
+#else
+#define RR_PROF(i, slot) \
+  do {                   \
+  } while (0)
+#endif
+
 template <int NX, int NU>
 struct CtaLayout {
   static constexpr int NZ = NX + NU;
@@ -32,27 +47,39 @@ struct CtaLayout {
   static constexpr int oA = 0, oB = NX * NX, oQ = oB + NX * NU, oM = oQ + SN, oR = oM + NX * NU, oq = oR + SMU,
                        orr = oq + NX, oc = orr + NU;
   static constexpr int IN = ((oc + NX + 1) & ~1);
-  static constexpr int SI = IN;                                   // S⁻¹, NX × NX (ld NX)
-  static constexpr int VW = SI + NX * NX;                         // [V | Ve] / [W | We] (ld NX, NX+1 cols)
-  // U parts (after W is consumed): Uxx | bx (ld NX, NX+1 cols), Uux | bu (ld NU, NX+1 cols), Uuu (ld NU)
-  static constexpr int Uxx = VW;
-  static constexpr int Uux = Uxx + NX * (NX + 1);
-  static constexpr int Uuu = Uux + NU * (NX + 1);
-  static constexpr int VWU_END = Uuu + NU * NU;
-  static constexpr int TT = ((VWU_END + 1) & ~1);                 // [T | g] (ld NX, NZ+1 cols); later K̃, M
-  static constexpr int Kt = TT;                                   // K̃ = G⁻¹[Uux | bu] (ld NU, NX+1 cols)
-  static constexpr int MM = Kt + ((NU * (NX + 1) + 1) & ~1);      // M (ld NX, NX+1 cols)
-  static constexpr int T_END = TT + (NX * (NZ + 1) > (MM - TT) + NX * (NX + 1) ? NX * (NZ + 1) : (MM - TT) + NX * (NX + 1));
-  static constexpr int VEC = ((T_END + 1) & ~1);
-  static constexpr int vs = VEC;         // v_{i+1} (NX)
-  static constexpr int pr = vs + NX;     // pivot column buffer / g / x_{i+1} (2 × NX)
-  static constexpr int xs = pr + 2 * NX;  // x (NX)
-  static constexpr int TOTAL = xs + NX;
-  static constexpr int red = TT;          // forward-pass partial sums (4 × (2NX+NU)), TT is dead then
-  static_assert(4 * (2 * NX + NU) <= T_END - TT, "partial-sum buffer does not fit the T region");
-  // forward record (global, per stage): Φ̃ (ld NX, NX+1 cols) | K (ld NU, NX cols) | k | V (ld NX) | v
-  static constexpr int rPHI = 0, rK = NX * (NX + 1), rk = rK + NU * NX, rV = rk + NU, rv = rV + NX * NX;
-  static constexpr int REC = ((rv + NX + 1) & ~1);
+  // SI: S = I + δV -> −S⁻¹ (ld NX); after the S⁻¹ record is out: Uuu = G (ld NU) | K̃ (ld NU, NX cols)
+  static constexpr int SI = IN;
+  static constexpr int Uuu = SI, Kt = SI + NU * NU;
+  static constexpr int SI_SZ = (NX * NX > NU * NU + NU * NX) ? NX * NX : NU * NU + NU * NX;
+  // R1: V_{i+1} (ld NX) + sweep scratch | T = S⁻¹(V F) (ld NX, NZ cols) | G-sweep scratch | V_i
+  static constexpr int R1 = SI + ((SI_SZ + 1) & ~1);
+  static constexpr int YS = R1 + NX * NX;  // S-sweep scratch (NX × 16) behind V
+  static constexpr int R1_SZ = (NX * NZ > NX * NX + NX * 16) ? NX * NZ : NX * NX + NX * 16;
+  // R2: V F (ld NX, NZ cols) | Uxx (ld NX) + Uux = H (ld NU, NX cols)
+  static constexpr int R2 = R1 + ((R1_SZ + 1) & ~1);
+  static constexpr int Uxx = R2, Uux = R2 + NX * NX;
+  static constexpr int R2_SZ = NX * NZ;
+  static constexpr int VEC = R2 + ((R2_SZ + 1) & ~1);
+  static constexpr int vs = VEC;       // v_{i+1}, then v_i (NX)
+  static constexpr int ve = vs + NX;   // V e (NX)
+  static constexpr int ee = ve + NX;   // e = c_{i+1} − δ v_{i+1} (NX)
+  static constexpr int gg = ee + NX;   // g = v_{i+1} + S⁻¹ V e (NX)
+  static constexpr int bb = gg + NX;   // b = (q; r) + Fᵀ g (NZ)
+  static constexpr int kt = bb + NZ;   // k̃ = G⁻¹ b_u (NU)
+  static constexpr int xs = kt + NU;   // forward: x_i (NX)
+  static constexpr int us = xs + NX;   // forward: u_i (NU)
+  static constexpr int ws = us + NU;   // forward: z = A x + e (NX)
+  static constexpr int pr2 = ws + NX;  // forward: w = z + B u (NX)
+  static constexpr int TOTAL = pr2 + NX;
+  // forward record (global, per stage i): K_i (ld NU, NX cols) | k_i | V_i (packed 'L') | v_i |
+  // e_i = c_{i+1} − δ v_{i+1} | S⁻¹_{i+1} = (I + δV_{i+1})⁻¹ (packed 'L')
+  static constexpr int rK = 0, rk = rK + NU * NX, rV = rk + NU, rv = rV + SN, re = rv + NX, rS = re + NX;
+  static constexpr int REC = ((rS + SN + 1) & ~1);
+  // forward sweep: two TMA-filled stage buffers [record | A_i | B_i] over the dead backward regions
+  static constexpr int FA = REC, FB = FA + NX * NX;
+  static constexpr int FBUF = ((FB + NX * NU + 1) & ~1);
+  static constexpr int zs = ws;  // forward: z = A x + e, then w = z + B u (reuses ws)
+  static_assert(2 * FBUF <= VEC, "forward stage buffers overlap the vectors");
 };
 
 // Shared-memory index of element (r, c) of a column-major matrix with leading dimension LD.
@@ -314,28 +341,61 @@ __device__ __forceinline__ void warp_tile16(int r0, int c0, LoadA&& la, LoadB&& 
       for (int e = 0; e < 2; ++e) store(r0 + 8 * a + g, c0 + 8 * b + 2 * t + e, c[a][b][e]);
 }
 
-// Symmetric sweep of a 16×16 diagonal block held in one warp's registers: lane l owns column
-// c = l & 15, rows 8h .. 8h+7 (h = l >> 4).  Pivots 0..15 in order (the scalar sweep of the
-// block); pivot column / row entries travel by shuffles (row k = column k by symmetry).
-__device__ __forceinline__ void warp_sweep16(double (&a)[8], int lane, bool* bad) {
-  const int c = lane & 15, h = lane >> 4;
+// Symmetric sweep of an n×n block held in one warp's registers (n = 16 or 32).  The 32 lanes form
+// a 4 × 8 grid of row groups × column groups: lane l = 8·rg + cg owns rows R·rg .. R·rg+R−1 and
+// columns C·cg .. C·cg+C−1 (R = n/4, C = n/8), a[i][j] = A[R·rg+i][C·cg+j].  Pivots 0..n−1 in order;
+// per pivot the diagonal entry, the pivot column at the lane's R rows and the pivot row at its C
+// columns travel by R + C + 1 shuffles (row k = column k by symmetry).  The 4 × 8 grid needs 30 %
+// fewer shuffles than a column-per-lane layout (measured 1772 vs 2316 cycles for n = 16).
+template <int n>
+__device__ __forceinline__ void warp_sweep_reg(double (&a)[n / 4][n / 8], int lane, bool* bad) {
+  constexpr int R = n / 4, C = n / 8;
+  const int rg = lane >> 3, cg = lane & 7;
+  // outer loop over the 4 pivot row groups kept rolled (code size: the unrolled body covers R
+  // pivots, whose register positions ki = kk, kj = kk % C are compile-time)
+#pragma unroll 1
+  for (int kr = 0; kr < 4; ++kr) {
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const double d = __shfl_sync(RR_FULL_MASK, a[k & 7], k + 16 * (k >> 3));
-    const double rowk = __shfl_sync(RR_FULL_MASK, a[k & 7], c + 16 * (k >> 3));  // A[k][c]
-    double colk[8];
+    for (int kk = 0; kk < R; ++kk) {
+      const int k = kr * R + kk, ki = kk, kj = kk % C, kc = k / C;
+      const double d = __shfl_sync(RR_FULL_MASK, a[ki][kj], kr * 8 + kc);
+      double colk[R], rowk[C];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) colk[i] = __shfl_sync(RR_FULL_MASK, a[i], k + 16 * h);  // A[8h+i][k]
-    *bad |= !(d > 0.0);
-    const double id = rcp_nr(d);
-    const double rs = rowk * id;
+      for (int i = 0; i < R; ++i) colk[i] = __shfl_sync(RR_FULL_MASK, a[i][kj], rg * 8 + kc);  // A[R·rg+i][k]
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = 8 * h + i;
-      const double upd = fma(-colk[i], rs, a[i]);
-      a[i] = (r == k) ? ((c == k) ? -id : rs) : ((c == k) ? colk[i] * id : upd);
+      for (int j = 0; j < C; ++j) rowk[j] = __shfl_sync(RR_FULL_MASK, a[ki][j], kr * 8 + cg);  // A[k][C·cg+j]
+      *bad |= !(d > 0.0);
+      const double id = rcp_nr(d);
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        const int c = C * cg + j;
+        const double rs = rowk[j] * id;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int r = R * rg + i;
+          const double upd = fma(-colk[i], rs, a[i][j]);
+          a[i][j] = (r == k) ? ((c == k) ? -id : rs) : ((c == k) ? colk[i] * id : upd);
+        }
+      }
     }
   }
+}
+
+// A (n×n at (q0, q0) of a swizzled ld-LD matrix in shared memory) <- its sweep, on one warp.
+template <int n, int LD>
+__device__ __forceinline__ void warp_sweep_smem(double* A, int q0, int lane, bool* bad) {
+  constexpr int R = n / 4, C = n / 8;
+  const int rg = lane >> 3, cg = lane & 7;
+  double a[R][C];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < C; ++j) a[i][j] = A[swz<LD>(q0 + R * rg + i, q0 + C * cg + j)];
+  warp_sweep_reg<n>(a, lane, bad);
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < C; ++j) A[swz<LD>(q0 + R * rg + i, q0 + C * cg + j)] = a[i][j];
 }
 
 // Block (16-pivot) symmetric sweep of the n×n SPD matrix A (n % 16 == 0, swizzled ld n):
@@ -344,11 +404,13 @@ __device__ __forceinline__ void warp_sweep16(double (&a)[8], int lane, bool* bad
 // identical (up to rounding) to the 16 scalar sweeps of block p.  Per block: warp 0 sweeps A_pp in
 // registers; Y = A_{:,p} Z (DMMA, into `Y`, n × 16); the trailing update A_RC −= Y_R A_pC over the
 // lower tiles R >= C (mirrored to C, R) on DMMA; then column / row block p <- Y / Yᵀ (overlapped
-// with the next block's diagonal sweep).  3 barriers per block instead of 2 per pivot.
+// with the next block's diagonal sweep).  3 barriers per block instead of 2 per pivot.  While warp 0
+// sweeps, the other warps also run side(p, NB, slot, nslots): caller work independent of A.
 // (A lookahead variant -- warp 0 updating and sweeping tile (p+1, p+1) during the trailing update --
 // measured slower on C3: the dependency chain tile -> sweep -> Y tile is the same length.)
-template <int n, int NTHREADS>
-__device__ __forceinline__ void cta_sweep_blk(double* A, double* Y, int tid, bool* fail) {
+template <int n, int NTHREADS, typename Side>
+__device__ __forceinline__ void cta_sweep_blk(double* A, double* Y, int tid, bool* fail, Side&& side,
+                                              int prof = -1) {
   constexpr int NB = n / 16;
   constexpr int NW = NTHREADS / 32;
   static_assert(n % 16 == 0, "block sweep needs n % 16 == 0");
@@ -357,14 +419,11 @@ __device__ __forceinline__ void cta_sweep_blk(double* A, double* Y, int tid, boo
   auto S = [](int r, int c) { return swz<n>(r, c); };
   for (int p = 0; p < NB; ++p) {
     const int p0 = 16 * p;
+#ifdef RR_CTA_PROFILE
+    if (prof >= 0 && tid == 32) g_cta_prof[prof + 3 * p] = clock64();
+#endif
     if (warp == 0) {
-      double a[8];
-      const int c = lane & 15, h = lane >> 4;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = A[S(p0 + 8 * h + i, p0 + c)];
-      warp_sweep16(a, lane, &bad);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) A[S(p0 + 8 * h + i, p0 + c)] = a[i];  // −Z
+      warp_sweep_smem<16, n>(A, p0, lane, &bad);  // A_pp <- −Z
     } else if (p > 0) {
       // previous block q = p − 1: column block q <- Y, row block q <- Yᵀ (rows outside block q)
       const int q0 = p0 - 16;
@@ -376,7 +435,11 @@ __device__ __forceinline__ void cta_sweep_blk(double* A, double* Y, int tid, boo
         A[S(q0 + cc, r)] = v;
       }
     }
+    if (warp != 0) side(p, NB, warp - 1, NW - 1);  // independent work of the caller, hidden behind warp 0
     __syncthreads();
+#ifdef RR_CTA_PROFILE
+    if (prof >= 0 && tid == 32) g_cta_prof[prof + 3 * p + 1] = clock64();
+#endif
     // Y_R = A_{R,p} Z = −A_{R,p} A'_pp for the row tiles R != p
     for (int R = warp; R < NB; R += NW) {
       if (R == p) continue;
@@ -385,6 +448,9 @@ __device__ __forceinline__ void cta_sweep_blk(double* A, double* Y, int tid, boo
           [&](int, int) { return 0.0; }, [&](int r, int c, double v) { Y[S(r, c)] = v; }, lane);
     }
     __syncthreads();
+#ifdef RR_CTA_PROFILE
+    if (prof >= 0 && tid == 32) g_cta_prof[prof + 3 * p + 2] = clock64();
+#endif
     // trailing update of the lower tiles R >= C (R, C != p), mirrored: A_RC −= Y_R A_pC
     constexpr int NO = NB - 1, NT = NO * (NO + 1) / 2;
     for (int tt = warp; tt < NT; tt += NW) {
@@ -425,11 +491,73 @@ __device__ __forceinline__ void cta_sweep_blk(double* A, double* Y, int tid, boo
   *fail = bad;
 }
 
-template <int n, int NTHREADS>
-__device__ __forceinline__ void cta_sweep_any(double* A, int lda, double* colbuf2, double* ytmp, int tid, bool* fail) {
-  if constexpr (n % 16 == 0 && n >= 32) cta_sweep_blk<n, NTHREADS>(A, ytmp, tid, fail);
-  else if constexpr (n % 16 == 0 && NTHREADS == 256) cta_sweep_reg<n>(A, lda, colbuf2, tid, fail);
-  else cta_sweep<n>(A, lda, colbuf2, tid, NTHREADS, fail);
+// A <- −A⁻¹ by the block sweep when n is a multiple of 16 (>= 32), else the register / scalar
+// sweep; side(p, nphases, slot, nslots) is run by warps 1.. alongside (blocked) or before it.
+template <int n, int NTHREADS, typename Side>
+__device__ __forceinline__ void cta_sweep_any(double* A, int lda, double* scratch, int tid, bool* fail, Side&& side,
+                                              int prof = -1) {
+  const int warp = tid >> 5;
+  constexpr int NW = NTHREADS / 32;
+  if constexpr (n == 32) {  // one warp sweeps the whole matrix in registers; the others run `side`
+    bool bad = false;
+    if (warp == 0) warp_sweep_smem<32, n>(A, 0, tid & 31, &bad);
+    else side(0, 1, warp - 1, NW - 1);
+    __syncthreads();
+    *fail = bad;
+  } else if constexpr (n % 16 == 0 && n >= 32) {
+    cta_sweep_blk<n, NTHREADS>(A, scratch, tid, fail, side, prof);
+  } else {
+    side(0, 1, warp, NW);
+    __syncthreads();
+    if constexpr (n % 16 == 0 && NTHREADS == 256) cta_sweep_reg<n>(A, lda, scratch, tid, fail);
+    else cta_sweep<n>(A, lda, scratch, tid, NTHREADS, fail);
+  }
+}
+
+// One 16×16 super-tile (tile index tt of an M×N result, column-major tile order) of
+// C = op_A · B + init on one warp, masked to M × N.
+template <int M, int N, int K, typename LoadA, typename LoadB, typename Init, typename Store>
+__device__ __forceinline__ void warp_tile_mn(int tt, LoadA&& la, LoadB&& lb, Init&& init, Store&& store, int lane) {
+  constexpr int MT = (M + 15) / 16;
+  const int g = lane >> 2, t = lane & 3;
+  const int m0 = (tt % MT) * 16, n0 = (tt / MT) * 16;
+  double c[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = m0 + 8 * a + g, col = n0 + 8 * b + 2 * t + e;
+        c[a][b][e] = (r < M && col < N) ? init(r, col) : 0.0;
+      }
+#pragma unroll 4
+  for (int kt = 0; kt < K / 4; ++kt) {
+    double av[2], bv[2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int r = m0 + 8 * a + g;
+      av[a] = (r < M) ? la(r, 4 * kt + t) : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int col = n0 + 8 * b + g;
+      bv[b] = (col < N) ? lb(4 * kt + t, col) : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) dmma884(c[a][b][0], c[a][b][1], av[a], bv[b]);
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = m0 + 8 * a + g, col = n0 + 8 * b + 2 * t + e;
+        if (r < M && col < N) store(r, col, c[a][b][e]);
+      }
 }
 
 template <int NX, int NU, int NTHREADS>
@@ -447,8 +575,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
   double* rec0 = a.ws + inst * sN * L::REC;
   int32_t st = 0;
 
-  auto X = [](int r, int c) { return swz<NX>(r, c); };  // ld NX matrices (F, S⁻¹, V/W/Uxx, T, M)
-  auto Y = [](int r, int c) { return swz<NU>(r, c); };  // ld NU matrices (Uux, Uuu, K̃)
+  auto X = [](int r, int c) { return swz<NX>(r, c); };  // ld NX matrices (F, S⁻¹, V, T, Uxx)
+  auto Y = [](int r, int c) { return swz<NU>(r, c); };  // ld NU matrices (Uux = H, Uuu = G, K̃)
   auto issue_stage = [&](int i) {
     const int64_t s = inst * sN + i;
     // F = [A B]: 16-byte chunks (rows r, r+1) to their swizzled column positions
@@ -467,12 +595,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
     copy_async(sm + L::oc, a.p.c + s * n, n, tid, NTHREADS);
     cp_async_commit();
   };
-  // V_N = Q_N -> [V | ·] region (ld NX), v_N = q_N
+  // V_N = Q_N -> R1 (ld NX), v_N = q_N
   {
     const double* QN = a.p.QN + inst * L::SN;
     for (int e = tid; e < n * n; e += NTHREADS) {
       const int r = e % n, c = e / n;
-      sm[L::VW + X(r, c)] = r >= c ? QN[pidx(n, r, c)] : QN[pidx(n, c, r)];
+      sm[L::R1 + X(r, c)] = r >= c ? QN[pidx(n, r, c)] : QN[pidx(n, c, r)];
     }
     for (int r = tid; r < n; r += NTHREADS) sm[L::vs + r] = a.p.qN[inst * n + r];
     if (a.f.V != nullptr)
@@ -490,63 +618,67 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
     const int u = s - NX, w = t - NX;
     return u >= w ? sm[L::oR + pidx(m, u, w)] : sm[L::oR + pidx(m, w, u)];
   };
+  constexpr int NT_VF = ((NX + 15) / 16) * ((NZ + 15) / 16);  // tiles of V F
+  auto no_side = [](int, int, int, int) {};
 
   for (int i = N - 1; i >= 0; --i) {
     cp_async_wait<0>();
     __syncthreads();
+    RR_PROF(i, 0);
     double* rec = rec0 + (int64_t)i * L::REC;
-    // S = I + δV -> SI; column NX of [V | ·] = V e with e = c_{i+1} − δ v_{i+1}
+    // S = I + δV_{i+1} -> SI;  e = c_{i+1} − δ v_{i+1};  V e
     for (int e = tid; e < n * n; e += NTHREADS) {
       const int r = e % n, c = e / n;
-      sm[L::SI + X(r, c)] = delta * sm[L::VW + X(r, c)] + (r == c ? 1.0 : 0.0);
+      sm[L::SI + X(r, c)] = delta * sm[L::R1 + X(r, c)] + (r == c ? 1.0 : 0.0);
     }
-    {  // V e with 4 threads per row (NTHREADS >= 4 n)
-      static_assert(NTHREADS >= 4 * NX, "V e matvec layout");
-      const int r = tid >> 2, part = tid & 3;
-      double acc = 0.0;
-      if (r < n)
-        for (int k = part; k < n; k += 4) acc = fma(sm[L::VW + X(r, k)], sm[L::oc + k] - delta * sm[L::vs + k], acc);
-      acc += __shfl_xor_sync(RR_FULL_MASK, acc, 1);
-      acc += __shfl_xor_sync(RR_FULL_MASK, acc, 2);
-      if (r < n && part == 0) sm[L::VW + X(r, NX)] = acc;
+    for (int r = tid; r < n; r += NTHREADS) {
+      const double ev = sm[L::oc + r] - delta * sm[L::vs + r];
+      sm[L::ee + r] = ev;
+      rec[L::re + r] = ev;
     }
     __syncthreads();
-    bool fail = false;
-    cta_sweep_any<NX, NTHREADS>(sm + L::SI, n, sm + L::pr, sm + L::TT, tid, &fail);  // SI = −S⁻¹
-    if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, i);
-    // W = S⁻¹ V (symmetric: S⁻¹ and V commute) -> TT region temporarily (same ld / swizzle), lower
-    // tiles mirrored; g = v_{i+1} + S⁻¹ (V e) on the SIMT pipe in the same phase
-    cta_gemm_lower<NX, NX>(
-        [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k, int c) { return sm[L::VW + X(k, c)]; },
-        [&](int, int) { return 0.0; },
-        [&](int r, int c, double v, bool mir) {
-          sm[L::TT + X(r, c)] = v;
-          if (mir) sm[L::TT + X(c, r)] = v;
-        },
-        warp, NW, lane);
     cta_matvec<NX, NX, NTHREADS>(
-        [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k) { return sm[L::VW + X(k, NX)]; },
-        [&](int r) { return sm[L::vs + r]; }, [&](int r, double v) { sm[L::pr + r] = v; }, tid);
-    __syncthreads();
-    for (int e = tid; e < n * n; e += NTHREADS) sm[L::VW + e] = sm[L::TT + e];  // same layout: flat copy of W
-    __syncthreads();
-    // T = W F (F = [A B] = stage input columns, ld NX);  b = (q; r) + Fᵀ g  (SIMT, same phase)
-    cta_gemm<NX, NZ, NX, false>(
-        [&](int r, int k) { return sm[L::VW + X(r, k)]; }, [&](int k, int c) { return sm[L::oA + X(k, c)]; },
-        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::TT + X(r, c)] = v; }, warp, NW, lane);
-    cta_matvec<NZ, NX, NTHREADS>(
-        [&](int r, int k) { return sm[L::oA + X(k, r)]; }, [&](int k) { return sm[L::pr + k]; },
-        [&](int r) { return r < NX ? sm[L::oq + r] : sm[L::orr + r - NX]; },
-        [&](int r, double v) {
-          if (r < NX) sm[L::Uxx + X(r, NX)] = v;  // b_x (column NX of the V/W region: W uses 0..NX-1)
-          else sm[L::Uux + Y(r - NX, NX)] = v;    // b_u
+        [&](int r, int k) { return sm[L::R1 + X(r, k)]; }, [&](int k) { return sm[L::ee + k]; },
+        [&](int) { return 0.0; }, [&](int r, double v) { sm[L::ve + r] = v; }, tid);
+    // S⁻¹ by the block sweep (SI = −S⁻¹, scratch behind V in R1); meanwhile the idle warps form
+    // V F -> R2 (independent of S⁻¹):  T = W F = S⁻¹ (V F) below needs no W
+    RR_PROF(i, 1);
+    bool fail = false;
+    cta_sweep_any<NX, NTHREADS>(
+        sm + L::SI, n, sm + L::YS, tid, &fail,
+        [&](int p, int nph, int slot, int nslots) {
+          const int t0 = p * NT_VF / nph, t1 = (p + 1) * NT_VF / nph;
+          for (int tt = t0 + slot; tt < t1; tt += nslots)
+            warp_tile_mn<NX, NZ, NX>(
+                tt, [&](int r, int k) { return sm[L::R1 + X(r, k)]; },
+                [&](int k, int c) { return sm[L::oA + X(k, c)]; }, [&](int, int) { return 0.0; },
+                [&](int r, int c, double v) { sm[L::R2 + X(r, c)] = v; }, lane);
         },
-        tid);
+#ifdef RR_CTA_PROFILE
+        (blockIdx.x == 0 && i == RR_CTA_PROFILE) ? 12 : -1
+#else
+        -1
+#endif
+    );
+    if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, i);
+    RR_PROF(i, 2);
+    // T = S⁻¹ (V F) -> R1 (V is dead);  g = v_{i+1} + S⁻¹ V e;  record S⁻¹ (for the forward sweep)
+    cta_gemm<NX, NZ, NX, false>(
+        [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k, int c) { return sm[L::R2 + X(k, c)]; },
+        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::R1 + X(r, c)] = v; }, warp, NW, lane);
+    cta_matvec<NX, NX, NTHREADS>(
+        [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k) { return sm[L::ve + k]; },
+        [&](int r) { return sm[L::vs + r]; }, [&](int r, double v) { sm[L::gg + r] = v; }, tid);
+    for (int e = tid; e < n * n; e += NTHREADS) {
+      const int r = e % n, c = e / n;
+      if (r >= c) rec[L::rS + pidx(n, r, c)] = -sm[L::SI + X(r, c)];
+    }
     __syncthreads();
-    // U = Fᵀ T + P (symmetric): lower tiles only.  Rows x -> Uxx (lower part suffices: V_i below
-    // reads only its own lower tiles), rows u -> Uux = H and Uuu = G (mirrored: the sweep needs all)
+    RR_PROF(i, 3);
+    // U = Fᵀ T + P (symmetric, lower tiles): Uxx (lower part suffices) and H = Uux -> R2 (V F dead),
+    // G = Uuu -> SI (S⁻¹ is recorded), mirrored for the sweep;  b = (q; r) + Fᵀ g
     cta_gemm_lower<NZ, NX>(
-        [&](int r, int k) { return sm[L::oA + X(k, r)]; }, [&](int k, int c) { return sm[L::TT + X(k, c)]; },
+        [&](int r, int k) { return sm[L::oA + X(k, r)]; }, [&](int k, int c) { return sm[L::R1 + X(k, c)]; },
         [&](int r, int c) { return Pat(r, c); },
         [&](int r, int c, double v, bool mir) {
           if (r < NX) {
@@ -562,88 +694,84 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
           }
         },
         warp, NW, lane);
+    cta_matvec<NZ, NX, NTHREADS>(
+        [&](int r, int k) { return sm[L::oA + X(k, r)]; }, [&](int k) { return sm[L::gg + k]; },
+        [&](int r) { return r < NX ? sm[L::oq + r] : sm[L::orr + r - NX]; }, [&](int r, double v) { sm[L::bb + r] = v; },
+        tid);
     __syncthreads();
-    // G⁻¹ (sweep in place: Uuu = −G⁻¹), K̃ = G⁻¹ H,  k̃ = G⁻¹ h  (= −K_i, −k_i)
-    cta_sweep_any<NU, NTHREADS>(sm + L::Uuu, m, sm + L::pr, sm + L::TT, tid, &fail);
+    RR_PROF(i, 4);
+    // the stage input is dead: stream the next stage in behind the rest of this one
+    if (i > 0) issue_stage(i - 1);
+    // G⁻¹ (sweep in place: Uuu = −G⁻¹; scratch in R1, T is dead), K̃ = G⁻¹ H, k̃ = G⁻¹ b_u (= −K_i, −k_i)
+    cta_sweep_any<NU, NTHREADS>(sm + L::Uuu, m, sm + L::R1, tid, &fail, no_side);
     if (fail && st == 0) st = mk_status(RR_ST_G_NOT_PD, i);
+    RR_PROF(i, 5);
     cta_gemm<NU, NX, NU, false>(
         [&](int r, int k) { return -sm[L::Uuu + Y(r, k)]; }, [&](int k, int c) { return sm[L::Uux + Y(k, c)]; },
         [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::Kt + Y(r, c)] = v; }, warp, NW, lane);
     cta_matvec<NU, NU, NTHREADS>(
-        [&](int r, int k) { return -sm[L::Uuu + Y(r, k)]; }, [&](int k) { return sm[L::Uux + Y(k, NX)]; },
-        [&](int) { return 0.0; }, [&](int r, double v) { sm[L::Kt + Y(r, NX)] = v; }, tid);
+        [&](int r, int k) { return -sm[L::Uuu + Y(r, k)]; }, [&](int k) { return sm[L::bb + NX + k]; },
+        [&](int) { return 0.0; }, [&](int r, double v) { sm[L::kt + r] = v; }, tid);
     __syncthreads();
-    // V_i = Uxx − Hᵀ K̃ (symmetric: lower tiles, mirrored, in place), v_i = b_x − Hᵀ k̃,
-    // M = A − B K̃,  m = c − δ v_{i+1} − B k̃   (M | m: [A | c − δv] − B [K̃ | k̃])
+    RR_PROF(i, 6);
+    // V_i = Uxx − Hᵀ K̃ -> R1 (symmetric: lower tiles, mirrored);  v_i = b_x − Hᵀ k̃ -> vs
     cta_gemm_lower<NX, NU>(
         [&](int r, int k) { return -sm[L::Uux + Y(k, r)]; }, [&](int k, int c) { return sm[L::Kt + Y(k, c)]; },
         [&](int r, int c) { return sm[L::Uxx + X(r, c)]; },
         [&](int r, int c, double v, bool mir) {
-          sm[L::Uxx + X(r, c)] = v;
-          if (mir) sm[L::Uxx + X(c, r)] = v;
+          sm[L::R1 + X(r, c)] = v;
+          if (mir) sm[L::R1 + X(c, r)] = v;
         },
         warp, NW, lane);
-    cta_gemm<NX, NX, NU, false>(
-        [&](int r, int k) { return -sm[L::oA + X(r, NX + k)]; }, [&](int k, int c) { return sm[L::Kt + Y(k, c)]; },
-        [&](int r, int c) { return sm[L::oA + X(r, c)]; }, [&](int r, int c, double v) { sm[L::MM + X(r, c)] = v; },
-        warp, NW, lane);
     cta_matvec<NX, NU, NTHREADS>(
-        [&](int r, int k) { return -sm[L::Uux + Y(k, r)]; }, [&](int k) { return sm[L::Kt + Y(k, NX)]; },
-        [&](int r) { return sm[L::Uxx + X(r, NX)]; }, [&](int r, double v) { sm[L::Uxx + X(r, NX)] = v; }, tid);
-    cta_matvec<NX, NU, NTHREADS>(
-        [&](int r, int k) { return -sm[L::oA + X(r, NX + k)]; }, [&](int k) { return sm[L::Kt + Y(k, NX)]; },
-        [&](int r) { return sm[L::oc + r] - delta * sm[L::vs + r]; }, [&](int r, double v) { sm[L::MM + X(r, NX)] = v; },
-        tid);
+        [&](int r, int k) { return -sm[L::Uux + Y(k, r)]; }, [&](int k) { return sm[L::kt + k]; },
+        [&](int r) { return sm[L::bb + r]; }, [&](int r, double v) { sm[L::vs + r] = v; }, tid);
     __syncthreads();
-    // record K = −K̃[:, :NX] (ld NU), k = −K̃[:, NX], V_i (ld NX), v_i; optional factor outputs
+    RR_PROF(i, 7);
+    // record K = −K̃ (ld NU), k = −k̃, V_i (ld NX), v_i; optional factor outputs
     for (int e = tid; e < m * n; e += NTHREADS) rec[L::rK + e] = -sm[L::Kt + Y(e % m, e / m)];
-    for (int u = tid; u < m; u += NTHREADS) rec[L::rk + u] = -sm[L::Kt + Y(u, NX)];
-    for (int e = tid; e < n * n; e += NTHREADS) rec[L::rV + e] = sm[L::Uxx + X(e % n, e / n)];
-    for (int r = tid; r < n; r += NTHREADS) rec[L::rv + r] = sm[L::Uxx + X(r, NX)];
+    for (int u = tid; u < m; u += NTHREADS) rec[L::rk + u] = -sm[L::kt + u];
+    {
+      double* fV = a.f.V != nullptr ? a.f.V + (inst * (sN + 1) + i) * L::SN : nullptr;
+      for (int e = tid; e < n * n; e += NTHREADS) {
+        const int r = e % n, c = e / n;
+        if (r >= c) {
+          const double v = sm[L::R1 + X(r, c)];
+          rec[L::rV + pidx(n, r, c)] = v;
+          if (fV != nullptr) fV[pidx(n, r, c)] = v;
+        }
+      }
+    }
+    for (int r = tid; r < n; r += NTHREADS) rec[L::rv + r] = sm[L::vs + r];
     if (a.f.K != nullptr)
       for (int e = tid; e < m * n; e += NTHREADS) a.f.K[(inst * sN + i) * m * n + e] = -sm[L::Kt + Y(e % m, e / m)];
     if (a.f.k != nullptr)
-      for (int u = tid; u < m; u += NTHREADS) a.f.k[(inst * sN + i) * m + u] = -sm[L::Kt + Y(u, NX)];
-    if (a.f.V != nullptr)
-      for (int e = tid; e < L::SN; e += NTHREADS) {
-        int c = 0, off = e;
-        while (off >= n - c) { off -= n - c; ++c; }
-        a.f.V[(inst * (sN + 1) + i) * L::SN + e] = sm[L::Uxx + X(c + off, c)];
-      }
+      for (int u = tid; u < m; u += NTHREADS) a.f.k[(inst * sN + i) * m + u] = -sm[L::kt + u];
     if (a.f.v != nullptr)
-      for (int r = tid; r < n; r += NTHREADS) a.f.v[(inst * (sN + 1) + i) * n + r] = sm[L::Uxx + X(r, NX)];
-    __syncthreads();
-    // stage input is dead: stream the next stage in while [Φ | φ] = S⁻¹ [M | m] is formed
-    if (i > 0) issue_stage(i - 1);
-    cta_gemm<NX, NX, NX, false>(
-        [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k, int c) { return sm[L::MM + X(k, c)]; },
-        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { rec[L::rPHI + r + c * n] = v; }, warp, NW, lane);
-    cta_matvec<NX, NX, NTHREADS>(
-        [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k) { return sm[L::MM + X(k, NX)]; },
-        [&](int) { return 0.0; }, [&](int r, double v) { rec[L::rPHI + r + NX * n] = v; }, tid);
-    // carry: V_i -> VW region (already in place: Uxx == VW, same layout), v_i -> vs
-    for (int r = tid; r < n; r += NTHREADS) sm[L::vs + r] = sm[L::Uxx + X(r, NX)];
-    __syncthreads();
+      for (int r = tid; r < n; r += NTHREADS) a.f.v[(inst * (sN + 1) + i) * n + r] = sm[L::vs + r];
+    // (the next iteration's leading barrier orders these reads before R1 / vs are rewritten)
   }
+  cp_async_wait<0>();
+  __syncthreads();
+  RR_PROF(RR_CTA_PROFILE_FWD, 8);
 
   // x_0 = (I + δV_0)⁻¹ (c_0 − δ v_0)
   for (int e = tid; e < n * n; e += NTHREADS) {
     const int r = e % n, c = e / n;
-    sm[L::SI + X(r, c)] = delta * sm[L::VW + X(r, c)] + (r == c ? 1.0 : 0.0);
+    sm[L::SI + X(r, c)] = delta * sm[L::R1 + X(r, c)] + (r == c ? 1.0 : 0.0);
   }
+  for (int r = tid; r < n; r += NTHREADS) sm[L::ee + r] = a.p.c0[inst * n + r] - delta * sm[L::vs + r];
   __syncthreads();
   {
     bool fail = false;
-    cta_sweep_any<NX, NTHREADS>(sm + L::SI, n, sm + L::pr, sm + L::TT, tid, &fail);
+    cta_sweep_any<NX, NTHREADS>(sm + L::SI, n, sm + L::YS, tid, &fail, no_side);
     if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, 0);
   }
-  for (int r = tid; r < n; r += NTHREADS) {
-    double acc = 0.0;
-    for (int k = 0; k < n; ++k) acc = fma(-sm[L::SI + X(r, k)], a.p.c0[inst * n + k] - delta * sm[L::vs + k], acc);
-    sm[L::xs + r] = acc;
-  }
+  cta_matvec<NX, NX, NTHREADS>(
+      [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k) { return sm[L::ee + k]; }, [&](int) { return 0.0; },
+      [&](int r, double v) { sm[L::xs + r] = v; }, tid);
   __syncthreads();
-  // block-wide status: any thread's failure (same value on all threads of a block in practice)
+  // block-wide status: any thread's failure
   __shared__ int sst;
   if (tid == 0) sst = 0;
   __syncthreads();
@@ -656,56 +784,87 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
   double* yo = a.s.y + inst * (sN + 1) * n;
   for (int r = tid; r < n; r += NTHREADS) xo[r] = sm[L::xs + r];
   bool bad = false;
-  // forward: thread (row, part): row = tid % NZ-ish split; 4 partial sums per output row
-  constexpr int PARTS = NTHREADS / 64 > 4 ? 4 : NTHREADS / 64;
+  RR_PROF(RR_CTA_PROFILE_FWD, 9);
+  // forward: u_i = K_i x_i + k_i,  y_i = V_i x_i + v_i,
+  //   x_{i+1} = (I + δV_{i+1})⁻¹ (A_i x_i + B_i u_i + c_{i+1} − δ v_{i+1}).
+  // Stage data (record | A_i | B_i) streams into two shared buffers by TMA bulk copies, one stage ahead.
+  __shared__ __align__(8) uint64_t fbar[2];
+  auto issue_fwd = [&](int i) {  // one thread
+    double* dst = sm + (i & 1) * L::FBUF;
+    const int64_t s = inst * sN + i;
+    constexpr uint32_t brec = 8u * L::REC, bA = 8u * NX * NX, bB = 8u * NX * NU;
+    fence_proxy_async();  // order the CTA's earlier generic accesses of the buffer (after a barrier) before the TMA writes
+    mbar_arrive_expect_tx(&fbar[i & 1], brec + bA + bB);
+    bulk_g2s(dst, rec0 + (int64_t)i * L::REC, brec, &fbar[i & 1]);
+    bulk_g2s(dst + L::FA, a.p.A + s * n * n, bA, &fbar[i & 1]);
+    bulk_g2s(dst + L::FB, a.p.B + s * n * m, bB, &fbar[i & 1]);
+  };
+  if (tid == 0) {
+    mbar_init(&fbar[0], 1);
+    mbar_init(&fbar[1], 1);
+  }
+  __syncthreads();
+  if (tid == 0 && N > 0) issue_fwd(0);
   for (int i = 0; i < N; ++i) {
-    const double* rec = rec0 + (int64_t)i * L::REC;
-    for (int task = tid; task < PARTS * (2 * NX + NU); task += NTHREADS) {
-      const int part = task / (2 * NX + NU), row = task % (2 * NX + NU);
-      const int k0 = part * (NX / PARTS), k1 = k0 + NX / PARTS;
-      double acc = 0.0;
-      if (row < NX) {  // x_{i+1} row
-        for (int k = k0; k < k1; ++k) acc = fma(rec[L::rPHI + row + k * n], sm[L::xs + k], acc);
-      } else if (row < 2 * NX) {  // y_i row
-        const int rr = row - NX;
-        for (int k = k0; k < k1; ++k) acc = fma(rec[L::rV + rr + k * n], sm[L::xs + k], acc);
-      } else {  // u_i row
-        const int u = row - 2 * NX;
-        for (int k = k0; k < k1; ++k) acc = fma(rec[L::rK + u + k * m], sm[L::xs + k], acc);
-      }
-      sm[L::red + part * (2 * NX + NU) + row] = acc;
-    }
+    const double* fb = sm + (i & 1) * L::FBUF;
+    mbar_wait_parity(&fbar[i & 1], (i >> 1) & 1);
+    if (tid == 0 && i + 1 < N) issue_fwd(i + 1);  // its buffer was last read by stage i−1 (barriers since)
+    // [u_i; y_i; z] = [K_i; V_i; A_i] x_i + [k_i; v_i; e_i]
+    cta_matvec<NU + 2 * NX, NX, NTHREADS>(
+        [&](int r, int k) {
+          if (r < NU) return fb[L::rK + r + k * m];
+          if (r < NU + NX) {
+            const int rr = r - NU;
+            return fb[L::rV + (rr >= k ? pidx(n, rr, k) : pidx(n, k, rr))];
+          }
+          return fb[L::FA + (r - NU - NX) + k * n];
+        },
+        [&](int k) { return sm[L::xs + k]; },
+        [&](int r) { return r < NU ? fb[L::rk + r] : (r < NU + NX ? fb[L::rv + r - NU] : fb[L::re + r - NU - NX]); },
+        [&](int r, double v) {
+          if (r < NU) {
+            sm[L::us + r] = v;
+            uo[(int64_t)i * m + r] = v;
+            bad |= !isfinite(v);
+          } else if (r < NU + NX) {
+            yo[(int64_t)i * n + r - NU] = v;
+            bad |= !isfinite(v);
+          } else {
+            sm[L::zs + r - NU - NX] = v;
+          }
+        },
+        tid);
     __syncthreads();
-    for (int row = tid; row < 2 * NX + NU; row += NTHREADS) {
-      double acc = 0.0;
-      for (int p = 0; p < PARTS; ++p) acc += sm[L::red + p * (2 * NX + NU) + row];
-      if (row < NX) {
-        acc += rec[L::rPHI + row + NX * n];
-        xo[(int64_t)(i + 1) * n + row] = acc;
-        sm[L::pr + row] = acc;
-      } else if (row < 2 * NX) {
-        acc += rec[L::rv + row - NX];
-        yo[(int64_t)i * n + row - NX] = acc;
-      } else {
-        acc += rec[L::rk + row - 2 * NX];
-        uo[(int64_t)i * m + row - 2 * NX] = acc;
-      }
-      bad |= !isfinite(acc);
-    }
+    // w = z + B_i u_i
+    cta_matvec<NX, NU, NTHREADS>(
+        [&](int r, int k) { return fb[L::FB + r + k * n]; }, [&](int k) { return sm[L::us + k]; },
+        [&](int r) { return sm[L::zs + r]; }, [&](int r, double v) { sm[L::pr2 + r] = v; }, tid);
     __syncthreads();
-    for (int r = tid; r < n; r += NTHREADS) sm[L::xs + r] = sm[L::pr + r];
+    // x_{i+1} = S⁻¹_{i+1} w
+    cta_matvec<NX, NX, NTHREADS>(
+        [&](int r, int k) { return fb[L::rS + (r >= k ? pidx(n, r, k) : pidx(n, k, r))]; },
+        [&](int k) { return sm[L::pr2 + k]; }, [&](int) { return 0.0; },
+        [&](int r, double v) {
+          sm[L::xs + r] = v;
+          xo[(int64_t)(i + 1) * n + r] = v;
+          bad |= !isfinite(v);
+        },
+        tid);
     __syncthreads();
   }
   {  // y_N = Q_N x_N + q_N
     const double* QN = a.p.QN + inst * L::SN;
-    for (int r = tid; r < n; r += NTHREADS) {
-      double acc = a.p.qN[inst * n + r];
-      for (int k = 0; k < n; ++k) acc = fma(k >= r ? QN[pidx(n, k, r)] : QN[pidx(n, r, k)], sm[L::xs + k], acc);
-      yo[sN * n + r] = acc;
-      bad |= !isfinite(acc);
-    }
+    cta_matvec<NX, NX, NTHREADS>(
+        [&](int r, int k) { return k >= r ? QN[pidx(n, k, r)] : QN[pidx(n, r, k)]; }, [&](int k) { return sm[L::xs + k]; },
+        [&](int r) { return a.p.qN[inst * n + r]; },
+        [&](int r, double v) {
+          yo[sN * n + r] = v;
+          bad |= !isfinite(v);
+        },
+        tid);
   }
   if (__syncthreads_or(bad) && status == 0) status = RR_ST_NONFINITE;
+  RR_PROF(RR_CTA_PROFILE_FWD, 10);
   if (status != 0) {
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
     for (int64_t e = tid; e < (sN + 1) * n; e += NTHREADS) {
