@@ -47,18 +47,21 @@ struct CtaLayout {
   static constexpr int oA = 0, oB = NX * NX, oQ = oB + NX * NU, oM = oQ + SN, oR = oM + NX * NU, oq = oR + SMU,
                        orr = oq + NX, oc = orr + NU;
   static constexpr int IN = ((oc + NX + 1) & ~1);
-  // SI: S = I + δV -> −S⁻¹ (ld NX); after the S⁻¹ record is out: Uuu = G (ld NU) | K̃ (ld NU, NX cols)
+  // SI: S = I + δV -> −S⁻¹ (ld NX); once T is formed: K̃ (ld NU, NX cols)
   static constexpr int SI = IN;
-  static constexpr int Uuu = SI, Kt = SI + NU * NU;
-  static constexpr int SI_SZ = (NX * NX > NU * NU + NU * NX) ? NX * NX : NU * NU + NU * NX;
-  // R1: V_{i+1} (ld NX) + sweep scratch | T = S⁻¹(V F) (ld NX, NZ cols) | G-sweep scratch | V_i
+  static constexpr int Kt = SI;
+  static constexpr int SI_SZ = NX * NX;
+  // R1: V_{i+1} (ld NX) + S-sweep scratch | T = S⁻¹(V F) (ld NX, NZ cols) | T_A + H = Uux (ld NU, NX
+  // cols, over T_B) | V_i
   static constexpr int R1 = SI + ((SI_SZ + 1) & ~1);
   static constexpr int YS = R1 + NX * NX;  // S-sweep scratch (NX × 16) behind V
+  static constexpr int Uux = R1 + NX * NX;
   static constexpr int R1_SZ = (NX * NZ > NX * NX + NX * 16) ? NX * NZ : NX * NX + NX * 16;
-  // R2: V F (ld NX, NZ cols) | Uxx (ld NX) + Uux = H (ld NU, NX cols)
+  // R2: V F (ld NX, NZ cols) | Uxx (ld NX) + G = Uuu (ld NU, over (V F)_B)
   static constexpr int R2 = R1 + ((R1_SZ + 1) & ~1);
-  static constexpr int Uxx = R2, Uux = R2 + NX * NX;
+  static constexpr int Uxx = R2, Uuu = R2 + NX * NX;
   static constexpr int R2_SZ = NX * NZ;
+  static_assert(NU <= NX && NU * NX <= SI_SZ, "C3 layout assumes n_u <= n_x");
   static constexpr int VEC = R2 + ((R2_SZ + 1) & ~1);
   static constexpr int vs = VEC;       // v_{i+1}, then v_i (NX)
   static constexpr int ve = vs + NX;   // V e (NX)
@@ -66,7 +69,8 @@ struct CtaLayout {
   static constexpr int gg = ee + NX;   // g = v_{i+1} + S⁻¹ V e (NX)
   static constexpr int bb = gg + NX;   // b = (q; r) + Fᵀ g (NZ)
   static constexpr int kt = bb + NZ;   // k̃ = G⁻¹ b_u (NU)
-  static constexpr int xs = kt + NU;   // forward: x_i (NX)
+  static constexpr int gpb = kt + NU;  // G-sweep pivot buffer (2 NU)
+  static constexpr int xs = gpb + 2 * NU;  // forward: x_i (NX)
   static constexpr int us = xs + NX;   // forward: u_i (NU)
   static constexpr int ws = us + NU;   // forward: z = A x + e (NX)
   static constexpr int pr2 = ws + NX;  // forward: w = z + B u (NX)
@@ -579,13 +583,11 @@ __device__ __forceinline__ void cta_sweep_any(double* A, int lda, double* scratc
   }
 }
 
-// One 16×16 super-tile (tile index tt of an M×N result, column-major tile order) of
-// C = op_A · B + init on one warp, masked to M × N.
+// One 16×16 super-tile at (m0, n0) of C = op_A · B + init (K multiple of 4) on one warp, masked to M × N.
 template <int M, int N, int K, typename LoadA, typename LoadB, typename Init, typename Store>
-__device__ __forceinline__ void warp_tile_mn(int tt, LoadA&& la, LoadB&& lb, Init&& init, Store&& store, int lane) {
-  constexpr int MT = (M + 15) / 16;
+__device__ __forceinline__ void warp_tile_at(int m0, int n0, LoadA&& la, LoadB&& lb, Init&& init, Store&& store,
+                                             int lane) {
   const int g = lane >> 2, t = lane & 3;
-  const int m0 = (tt % MT) * 16, n0 = (tt / MT) * 16;
   double c[2][2][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -623,6 +625,23 @@ __device__ __forceinline__ void warp_tile_mn(int tt, LoadA&& la, LoadB&& lb, Ini
         const int r = m0 + 8 * a + g, col = n0 + 8 * b + 2 * t + e;
         if (r < M && col < N) store(r, col, c[a][b][e]);
       }
+}
+
+// Tile index tt (column-major tile order) of an M×N result.
+template <int M, int N, int K, typename LoadA, typename LoadB, typename Init, typename Store>
+__device__ __forceinline__ void warp_tile_mn(int tt, LoadA&& la, LoadB&& lb, Init&& init, Store&& store, int lane) {
+  constexpr int MT = (M + 15) / 16;
+  warp_tile_at<M, N, K>((tt % MT) * 16, (tt / MT) * 16, la, lb, init, store, lane);
+}
+
+// (R, C) of the t-th lower tile (R >= C) in row-major lower order.
+__device__ __forceinline__ void lower_tile(int t, int& R, int& C) {
+  R = 0;
+  while (t > R) {
+    t -= R + 1;
+    ++R;
+  }
+  C = t;
 }
 
 template <int NX, int NU, int NTHREADS>
@@ -727,10 +746,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
     );
     if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, i);
     RR_PROF(i, 2);
-    // T = S⁻¹ (V F) -> R1 (V is dead);  g = v_{i+1} + S⁻¹ V e;  record S⁻¹ (for the forward sweep)
-    cta_gemm<NX, NZ, NX, false>(
-        [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k, int c) { return sm[L::R2 + X(k, c)]; },
-        [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::R1 + X(r, c)] = v; }, warp, NW, lane);
+    // T = S⁻¹ (V F) -> R1 (V is dead), U = Fᵀ T + P, scheduled so that G = Uuu is ready first and
+    // the rest of U runs beside the G⁻¹ sweep:
+    //   P1: the T tiles holding B columns (T_B) + the first T_A tiles;  g = v_{i+1} + S⁻¹ V e;  record S⁻¹
+    //   P2: G = Bᵀ T_B + R (lower tiles) + the remaining T_A tiles;  b = (q; r) + Fᵀ g
+    //   P3: G⁻¹ sweep  ‖  H = Uux = Bᵀ T_A + Mᵀ and Uxx = Aᵀ T_A + Q (lower tiles) on the other warps
+    constexpr int MT_T = (NX + 15) / 16, NT_T = MT_T * ((NZ + 15) / 16), CTB = NX / 16;
+    constexpr int NB_T = MT_T * (((NZ + 15) / 16) - CTB);  // T tiles holding B columns (first in order)
+    static_assert(NB_T <= NW, "T_B tiles must fit one round");
+    auto t_tile = [&](int o) {  // o-th T tile in the order: B-column tiles first
+      const int tt = (o + MT_T * CTB) % NT_T;
+      warp_tile_mn<NX, NZ, NX>(
+          tt, [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k, int c) { return sm[L::R2 + X(k, c)]; },
+          [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::R1 + X(r, c)] = v; }, lane);
+    };
+    constexpr int P1T = NT_T < NW ? NT_T : NW;
+    for (int o = warp; o < P1T; o += NW) t_tile(o);
     cta_matvec<NX, NX, NTHREADS>(
         [&](int r, int k) { return -sm[L::SI + X(r, k)]; }, [&](int k) { return sm[L::ve + k]; },
         [&](int r) { return sm[L::vs + r]; }, [&](int r, double v) { sm[L::gg + r] = v; }, tid);
@@ -740,37 +771,57 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
     }
     __syncthreads();
     RR_PROF(i, 3);
-    // U = Fᵀ T + P (symmetric, lower tiles): Uxx (lower part suffices) and H = Uux -> R2 (V F dead),
-    // G = Uuu -> SI (S⁻¹ is recorded), mirrored for the sweep;  b = (q; r) + Fᵀ g
-    cta_gemm_lower<NZ, NX>(
-        [&](int r, int k) { return sm[L::oA + X(k, r)]; }, [&](int k, int c) { return sm[L::R1 + X(k, c)]; },
-        [&](int r, int c) { return Pat(r, c); },
-        [&](int r, int c, double v, bool mir) {
-          if (r < NX) {
-            if (c < NX) sm[L::Uxx + X(r, c)] = v;  // (r < NX, c >= NX: the Hᵀ entry, stored as H)
-          } else {
-            const int u = r - NX;
-            if (c < NX) {
-              sm[L::Uux + Y(u, c)] = v;
-            } else {
-              sm[L::Uuu + Y(u, c - NX)] = v;
-              if (mir) sm[L::Uuu + Y(c - NX, u)] = v;
-            }
-          }
-        },
-        warp, NW, lane);
+    {
+      constexpr int MTU = (NU + 15) / 16, NGT = MTU * (MTU + 1) / 2;  // lower tiles of G
+      for (int task = warp; task < NGT + (NT_T - P1T); task += NW) {
+        if (task < NGT) {
+          int R, C;
+          lower_tile(task, R, C);
+          const bool mir = R != C;
+          warp_tile_at<NU, NU, NX>(
+              16 * R, 16 * C, [&](int r, int k) { return sm[L::oA + X(k, NX + r)]; },
+              [&](int k, int c) { return sm[L::R1 + X(k, NX + c)]; }, [&](int r, int c) { return Pat(NX + r, NX + c); },
+              [&](int r, int c, double v) {
+                sm[L::Uuu + Y(r, c)] = v;
+                if (mir) sm[L::Uuu + Y(c, r)] = v;
+              },
+              lane);
+        } else {
+          t_tile(P1T + task - NGT);
+        }
+      }
+    }
     cta_matvec<NZ, NX, NTHREADS>(
         [&](int r, int k) { return sm[L::oA + X(k, r)]; }, [&](int k) { return sm[L::gg + k]; },
         [&](int r) { return r < NX ? sm[L::oq + r] : sm[L::orr + r - NX]; }, [&](int r, double v) { sm[L::bb + r] = v; },
         tid);
     __syncthreads();
     RR_PROF(i, 4);
-    // the stage input is dead: stream the next stage in behind the rest of this one
-    if (i > 0) issue_stage(i - 1);
-    // G⁻¹ (sweep in place: Uuu = −G⁻¹; scratch in R1, T is dead), K̃ = G⁻¹ H, k̃ = G⁻¹ b_u (= −K_i, −k_i)
-    cta_sweep_any<NU, NTHREADS>(sm + L::Uuu, m, sm + L::R1, tid, &fail, no_side);
+    // P3: G⁻¹ (sweep in place: Uuu = −G⁻¹)  ‖  H and Uxx
+    cta_sweep_any<NU, NTHREADS>(sm + L::Uuu, m, sm + L::gpb, tid, &fail, [&](int, int, int slot, int nslots) {
+      constexpr int MTX = (NX + 15) / 16, MTU = (NU + 15) / 16;
+      constexpr int NH = MTU * MTX, NXX = MTX * (MTX + 1) / 2;
+      for (int task = slot; task < NH + NXX; task += nslots) {
+        if (task < NH) {  // H = Uux (u, c) = Σ_k F[k][NX+u] T[k][c] + M[c][u]
+          warp_tile_mn<NU, NX, NX>(
+              task, [&](int r, int k) { return sm[L::oA + X(k, NX + r)]; },
+              [&](int k, int c) { return sm[L::R1 + X(k, c)]; }, [&](int r, int c) { return Pat(NX + r, c); },
+              [&](int r, int c, double v) { sm[L::Uux + Y(r, c)] = v; }, lane);
+        } else {  // Uxx lower tiles (the lower part is all V_i below reads)
+          int R, C;
+          lower_tile(task - NH, R, C);
+          warp_tile_at<NX, NX, NX>(
+              16 * R, 16 * C, [&](int r, int k) { return sm[L::oA + X(k, r)]; },
+              [&](int k, int c) { return sm[L::R1 + X(k, c)]; }, [&](int r, int c) { return Pat(r, c); },
+              [&](int r, int c, double v) { sm[L::Uxx + X(r, c)] = v; }, lane);
+        }
+      }
+    });
     if (fail && st == 0) st = mk_status(RR_ST_G_NOT_PD, i);
     RR_PROF(i, 5);
+    // the stage input is dead: stream the next stage in behind the rest of this one
+    if (i > 0) issue_stage(i - 1);
+    // K̃ = G⁻¹ H, k̃ = G⁻¹ b_u (= −K_i, −k_i) -> SI region (S⁻¹ is dead)
     cta_gemm<NU, NX, NU, false>(
         [&](int r, int k) { return -sm[L::Uuu + Y(r, k)]; }, [&](int k, int c) { return sm[L::Uux + Y(k, c)]; },
         [&](int, int) { return 0.0; }, [&](int r, int c, double v) { sm[L::Kt + Y(r, c)] = v; }, warp, NW, lane);

@@ -64,8 +64,8 @@ int main() {
   for (auto v : st) nbad += v != 0;
   printf("err=%s  one wave (148 instances, N=%d): %.3f ms = %.1f us/stage  status!=0: %d\n", cudaGetErrorString(err),
          N, ms, ms * 1e3 / N, nbad);
-  const char* names[] = {"S=I+dV, e, Ve", "S sweep (+V F side work)", "T=S^-1(VF), g, rec S^-1", "U=F'T+P, b",
-                         "G sweep", "K~, k~", "V_i, v_i", "records (to next stage)"};
+  const char* names[] = {"S=I+dV, e, Ve", "S sweep (+V F side work)", "P1: T_B + T_A half, g, rec", "P2: G tiles + T_A rest, b",
+                         "P3: G sweep | H, Uxx", "K~, k~", "V_i, v_i", "records (to next stage)"};
   for (int k = 0; k < 7; ++k) printf("  %-28s %7lld cyc\n", names[k], t[k + 1] - t[k]);
   printf("  stage total (slot 0..7)      %7lld cyc\n", t[7] - t[0]);
   for (int p = 0; p < 4; ++p)
