@@ -122,6 +122,59 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* prob_host, co
                             int32_t* status_host, const rr_problem* prob_dev, const rr_solution* sol_dev,
                             int32_t* status_dev, void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ============================ factorization / solve split (rows a2 | a3-a5) ============================
+ * The paper's solver plugs problem-specific "KKT system factorization" and "KKT system solve"
+ * callbacks into a shared backend.  rr_factor is the matrix half of Eq.(RR),
+ * which depends only on (A, B, Q, M, R, Q_N, δ); rr_solve is the vector half plus the forward sweep
+ * and dual recovery for one right-hand side (q, r, c, q_N, c_0).  One rr_factor serves any number of
+ * rr_solve calls with different right-hand sides (iterative refinement, corrector steps).
+ *
+ * FACTOR RECORD (device memory written by rr_factor, read by rr_solve; [batch][N+1][R] doubles,
+ * R = rr_factor_record_doubles(n, m) = n(n+1) + nm + m(m+1)/2 rounded up to even).  Record i:
+ *     [0, s)            V_i                 packed lower (s = n(n+1)/2; V_N = Q_N)
+ *     [s, 2s)           S_i⁻¹ = (I + δV_i)⁻¹  packed lower (the (I+δV)⁻¹ of P:616)
+ *     [2s, 2s+nm)       K_i                 m×n column-major   (record N: unused)
+ *     [2s+nm, +m(m+1)/2) G_i⁻¹ = (BᵀW_iB + R_i)⁻¹ packed lower (record N: unused)
+ * An instance whose factorization failed (status != 0) has its records NaN-filled.
+ */
+int32_t rr_factor_record_doubles(int32_t n, int32_t m);
+
+/* Bytes of the factor record array for `dims` (batch * (N+1) * R * 8), or -1 if no kernel covers
+ * (nx, nu) (rr_factor / rr_solve are compiled for nx, nu <= 16). */
+int64_t rr_factor_bytes(const rr_dims* dims);
+
+/*
+ * rr_factor: backward matrix sweep i = N-1..0 (row a2), V_N = Q_N:
+ *     S_{i+1}⁻¹ = (I + δV_{i+1})⁻¹; W_i = S⁻¹V_{i+1}; G_i = BᵀWB + R; H_i = BᵀWA + Mᵀ;
+ *     K_i = −G_i⁻¹H_i; V_i = AᵀWA + Q + K_iᵀH_i;   then S_0⁻¹ = (I + δV_0)⁻¹.
+ * prob: A, B, Q, M, R, QN, delta are read (q, r, c, qN, c0 ignored, may be NULL).
+ * factor: device buffer of >= rr_factor_bytes(dims) bytes, 16-byte aligned (output, layout above).
+ * fac: optional (NULL or NULL members): V [batch][N+1][sym n] and K [batch][N][m*n] copies.
+ * status: [batch] device int32 (RR_ST_S_NOT_PD / RR_ST_G_NOT_PD | stage << 8, as rr_factor_solve).
+ */
+rr_err rr_factor(const rr_dims* dims, const rr_problem* prob, void* factor, int64_t factor_bytes,
+                 const rr_factor_buf* fac, int32_t* status, void* stream);
+
+/* Bytes of device scratch rr_solve needs (batch * N * (n+m) * 8 + 256), or -1 if unsupported. */
+int64_t rr_solve_workspace_bytes(const rr_dims* dims);
+
+/*
+ * rr_solve: rows a3-a5 for the right-hand side (q, r, c, q_N, c_0) of prob, given rr_factor's records:
+ *   backward vector sweep: g_i = v_{i+1} + W_i(c_{i+1} − δv_{i+1}) (evaluated as
+ *     S_{i+1}⁻¹(v_{i+1} + V_{i+1}c_{i+1}), the same quantity since S⁻¹ = I − δW), h_i = r + Bᵀg,
+ *     k_i = −G_i⁻¹h_i, v_i = q + Aᵀg + K_iᵀh_i  (v_N = q_N);
+ *   forward sweep: x_0 = S_0⁻¹(c_0 − δv_0), u_i = K_i x_i + k_i,
+ *     x_{i+1} = S_{i+1}⁻¹(A_i x_i + B_i u_i + c_{i+1} − δv_{i+1});  duals y_i = V_i x_i + v_i.
+ * prob: A, B, q, r, c, qN, c0, delta are read (Q, M, R, QN ignored: the factor carries them).
+ *   A, B and delta must be the ones the factor was computed with.
+ * fac: optional v [batch][N+1][n] and k [batch][N][m] copies (V, K members ignored).
+ * status: [batch] device int32, 0 or RR_ST_NONFINITE (e.g. the instance's factor failed: see
+ *   rr_factor's status for the reason); outputs of a non-finite instance are NaN-filled.
+ */
+rr_err rr_solve(const rr_dims* dims, const rr_problem* prob, const void* factor, int64_t factor_bytes,
+                const rr_factor_buf* fac, const rr_solution* sol, void* workspace, int64_t workspace_bytes,
+                int32_t* status, void* stream);
+
 /* ================================ regularized IPM step (rows a1-a8) ================================
  * One iteration of the regularized interior point method of §1.2 on the stagewise OCP of
  * §1.1, per instance, with the Newton system solved stagewise (§1.3):

@@ -84,6 +84,17 @@ def lib():
                                                ctypes.POINTER(rr_solution), ctypes.c_void_p,
                                                ctypes.POINTER(rr_problem), ctypes.POINTER(rr_solution),
                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+            L.rr_factor_bytes.restype = ctypes.c_int64
+            L.rr_factor_bytes.argtypes = [ctypes.POINTER(rr_dims)]
+            L.rr_solve_workspace_bytes.restype = ctypes.c_int64
+            L.rr_solve_workspace_bytes.argtypes = [ctypes.POINTER(rr_dims)]
+            L.rr_factor.restype = ctypes.c_int32
+            L.rr_factor.argtypes = [ctypes.POINTER(rr_dims), ctypes.POINTER(rr_problem), ctypes.c_void_p,
+                                    ctypes.c_int64, ctypes.POINTER(rr_factor_buf), ctypes.c_void_p, ctypes.c_void_p]
+            L.rr_solve.restype = ctypes.c_int32
+            L.rr_solve.argtypes = [ctypes.POINTER(rr_dims), ctypes.POINTER(rr_problem), ctypes.c_void_p,
+                                   ctypes.c_int64, ctypes.POINTER(rr_factor_buf), ctypes.POINTER(rr_solution),
+                                   ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
             L.ipm_workspace_bytes.restype = ctypes.c_int64
             L.ipm_workspace_bytes.argtypes = [ctypes.POINTER(ipm_dims)]
             L.ipm_step.restype = ctypes.c_int32

@@ -6,6 +6,7 @@
 #include "rr.h"
 #include "ipm.cuh"
 #include "rr_fused.cuh"
+#include "rr_split.cuh"
 
 namespace {
 thread_local char g_err[512] = "";
@@ -109,6 +110,101 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* ph, const rr_
   return RR_OK;
 }
 
+
+int32_t rr_factor_record_doubles(int32_t n, int32_t m) { return rrk::frec_doubles(n, m); }
+
+int64_t rr_factor_bytes(const rr_dims* dims) {
+  if (!dims_ok(dims) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
+  return dims->batch * (int64_t)(dims->N + 1) * rrk::frec_doubles(dims->nx, dims->nu) * 8;
+}
+
+int64_t rr_solve_workspace_bytes(const rr_dims* dims) {
+  if (!dims_ok(dims) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
+  return dims->batch * (int64_t)dims->N * (dims->nx + dims->nu) * 8 + 256;
+}
+
+rr_err rr_factor(const rr_dims* dims, const rr_problem* prob, void* factor, int64_t factor_bytes,
+                 const rr_factor_buf* fac, int32_t* status, void* stream) {
+  if (!dims_ok(dims)) return set_err(RR_E_INVALID, "rr_factor: invalid dims%s");
+  if (prob == nullptr) return set_err(RR_E_INVALID, "rr_factor: null %s", "prob");
+  if (dims->batch == 0) return RR_OK;
+  if (status == nullptr) return set_err(RR_E_INVALID, "rr_factor: null %s", "status");
+  if (prob->QN == nullptr || prob->delta == nullptr)
+    return set_err(RR_E_INVALID, "rr_factor: null %s", "QN/delta");
+  if (dims->N > 0) {
+    const double* req[] = {prob->A, prob->B, prob->Q, prob->M, prob->R};
+    for (const double* p : req)
+      if (p == nullptr) return set_err(RR_E_INVALID, "rr_factor: null %s", "stage operand (A, B, Q, M, R)");
+  }
+  const int64_t need = rr_factor_bytes(dims);
+  if (need < 0) return set_err(RR_E_UNSUPPORTED, "rr_factor: no kernel compiled for this (nx, nu)%s");
+  if (factor == nullptr || factor_bytes < need)
+    return set_err(RR_E_INVALID, "rr_factor: factor buffer missing or smaller than %s", "rr_factor_bytes()");
+  if ((reinterpret_cast<uintptr_t>(factor) & 15u) != 0)
+    return set_err(RR_E_INVALID, "rr_factor: factor buffer not %s", "16-byte aligned");
+  rrk::SplitArgs a{};
+  a.nx = dims->nx;
+  a.nu = dims->nu;
+  a.N = dims->N;
+  a.batch = dims->batch;
+  a.p = *prob;
+  rr_factor_buf none = {nullptr, nullptr, nullptr, nullptr};
+  a.f = fac ? *fac : none;
+  a.f.v = nullptr;
+  a.f.k = nullptr;
+  a.fr = static_cast<double*>(factor);
+  a.status = status;
+  bool supported = false;
+  cudaError_t e = rrk::factor_launch(a, static_cast<cudaStream_t>(stream), &supported);
+  if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_factor: unsupported shape%s");
+  if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_factor: CUDA error %s", cudaGetErrorString(e));
+  return RR_OK;
+}
+
+rr_err rr_solve(const rr_dims* dims, const rr_problem* prob, const void* factor, int64_t factor_bytes,
+                const rr_factor_buf* fac, const rr_solution* sol, void* workspace, int64_t workspace_bytes,
+                int32_t* status, void* stream) {
+  if (!dims_ok(dims)) return set_err(RR_E_INVALID, "rr_solve: invalid dims%s");
+  if (prob == nullptr || sol == nullptr) return set_err(RR_E_INVALID, "rr_solve: null %s", "prob/sol");
+  if (dims->batch == 0) return RR_OK;
+  if (status == nullptr) return set_err(RR_E_INVALID, "rr_solve: null %s", "status");
+  if (prob->qN == nullptr || prob->c0 == nullptr || prob->delta == nullptr)
+    return set_err(RR_E_INVALID, "rr_solve: null %s", "qN/c0/delta");
+  if (dims->N > 0) {
+    const double* req[] = {prob->A, prob->B, prob->q, prob->r, prob->c};
+    for (const double* p : req)
+      if (p == nullptr) return set_err(RR_E_INVALID, "rr_solve: null %s", "stage operand (A, B, q, r, c)");
+  }
+  if (sol->x == nullptr || sol->y == nullptr || (dims->N > 0 && sol->u == nullptr))
+    return set_err(RR_E_INVALID, "rr_solve: null %s", "solution pointer");
+  const int64_t need_f = rr_factor_bytes(dims), need_w = rr_solve_workspace_bytes(dims);
+  if (need_f < 0 || need_w < 0) return set_err(RR_E_UNSUPPORTED, "rr_solve: no kernel compiled for this (nx, nu)%s");
+  if (factor == nullptr || factor_bytes < need_f)
+    return set_err(RR_E_INVALID, "rr_solve: factor buffer missing or smaller than %s", "rr_factor_bytes()");
+  if ((reinterpret_cast<uintptr_t>(factor) & 15u) != 0)
+    return set_err(RR_E_INVALID, "rr_solve: factor buffer not %s", "16-byte aligned");
+  if (dims->N > 0 && (workspace == nullptr || workspace_bytes < need_w))
+    return set_err(RR_E_INVALID, "rr_solve: workspace missing or smaller than %s", "rr_solve_workspace_bytes()");
+  rrk::SplitArgs a{};
+  a.nx = dims->nx;
+  a.nu = dims->nu;
+  a.N = dims->N;
+  a.batch = dims->batch;
+  a.p = *prob;
+  rr_factor_buf none = {nullptr, nullptr, nullptr, nullptr};
+  a.f = fac ? *fac : none;
+  a.f.V = nullptr;
+  a.f.K = nullptr;
+  a.s = *sol;
+  a.frc = static_cast<const double*>(factor);
+  a.ws = static_cast<double*>(workspace);
+  a.status = status;
+  bool supported = false;
+  cudaError_t e = rrk::solve_launch(a, static_cast<cudaStream_t>(stream), &supported);
+  if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_solve: unsupported shape%s");
+  if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_solve: CUDA error %s", cudaGetErrorString(e));
+  return RR_OK;
+}
 
 static bool ipm_dims_ok(const ipm_dims* d) {
   return d != nullptr && d->nx >= 1 && d->nu >= 1 && d->N >= 0 && d->batch >= 0 && d->ng >= 0 && d->ngN >= 0 &&

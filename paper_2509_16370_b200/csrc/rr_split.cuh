@@ -1,0 +1,31 @@
+// rr_split.cuh -- internal launch interface of the rr_factor / rr_solve kernels (rr_split.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rr.h"
+
+namespace rrk {
+
+struct SplitArgs {
+  int nx, nu, N;
+  int64_t batch;
+  rr_problem p;
+  rr_factor_buf f;   // optional user copies (rr_factor: V, K; rr_solve: v, k)
+  rr_solution s;     // rr_solve outputs
+  double* fr;        // rr_factor: factor records [batch][N+1][frec_doubles]
+  const double* frc; // rr_solve: the same records, read only
+  double* ws;        // rr_solve scratch: [batch][N][n+m] (v_i | k_i)
+  int32_t* status;
+};
+
+// doubles per factor record: V (packed n) | S⁻¹ (packed n) | K (m×n) | G⁻¹ (packed m), even
+__host__ __device__ inline int frec_doubles(int n, int m) {
+  return (n * (n + 1) + n * m + m * (m + 1) / 2 + 1) & ~1;
+}
+
+bool split_supported(int nx, int nu);
+cudaError_t factor_launch(const SplitArgs& a, cudaStream_t s, bool* supported);
+cudaError_t solve_launch(const SplitArgs& a, cudaStream_t s, bool* supported);
+
+}  // namespace rrk

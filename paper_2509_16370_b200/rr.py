@@ -95,6 +95,71 @@ def rr_factor_solve(prob, want_factor: bool = False, out=None, fac=None, workspa
     return res
 
 
+def factor_record_doubles(nx: int, nu: int) -> int:
+    """Doubles per factor record (include/rr.h rr_factor_record_doubles)."""
+    return (nx * (nx + 1) + nx * nu + nu * (nu + 1) // 2 + 1) & ~1
+
+
+def factor_bytes(nx: int, nu: int, N: int, batch: int) -> int:
+    nb = lib().rr_factor_bytes(ctypes.byref(rr_dims(nx, nu, N, 0, batch)))
+    if nb < 0:
+        raise RRError("rr_factor: no kernel compiled for nx=%d nu=%d" % (nx, nu))
+    return int(nb)
+
+
+def solve_workspace_bytes(nx: int, nu: int, N: int, batch: int) -> int:
+    nb = lib().rr_solve_workspace_bytes(ctypes.byref(rr_dims(nx, nu, N, 0, batch)))
+    if nb < 0:
+        raise RRError("rr_solve: no kernel compiled for nx=%d nu=%d" % (nx, nu))
+    return int(nb)
+
+
+def _stream(stream, device):
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def rr_factor(prob, factor=None, fac=None, status=None, stream=None):
+    """Row a2 (matrix half of Eq.(RR)): returns (factor, status), factor a CUDA float64 tensor
+    [batch, N+1, rr_factor_record_doubles] in the include/rr.h record layout
+    (V_i | S_i^-1 | K_i | G_i^-1).  fac: optional dict with V / K tensors to receive copies."""
+    if not prob.delta.is_cuda:
+        raise RRError("rr_factor needs CUDA tensors (no CPU fallback)")
+    dev = prob.delta.device
+    factor_bytes(prob.nx, prob.nu, prob.N, prob.batch)  # raises if no kernel covers the shape
+    if factor is None:
+        factor = torch.empty(prob.batch, prob.N + 1, factor_record_doubles(prob.nx, prob.nu),
+                             dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.empty(prob.batch, dtype=torch.int32, device=dev)
+    p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
+    f = rr_factor_buf(*[_p(fac.get(k)) if fac is not None else None for k in ("V", "v", "K", "k")])
+    rc = lib().rr_factor(ctypes.byref(dims_of(prob)), ctypes.byref(p), _p(factor), factor.numel() * 8,
+                         ctypes.byref(f), _p(status), _stream(stream, dev))
+    check(rc, "rr_factor")
+    return factor, status
+
+
+def rr_solve(prob, factor, out=None, fac=None, workspace=None, stream=None):
+    """Rows a3-a5 for the right-hand side (q, r, c, qN, c0) of `prob` with rr_factor's records.
+    Returns dict x, u, y, status (status: 0 or RR_ST_NONFINITE)."""
+    if not prob.delta.is_cuda:
+        raise RRError("rr_solve needs CUDA tensors (no CPU fallback)")
+    dev = prob.delta.device
+    sol = out if out is not None else alloc_solution(prob)
+    if workspace is None:
+        nb = solve_workspace_bytes(prob.nx, prob.nu, prob.N, prob.batch)
+        workspace = torch.empty((nb + 7) // 8, dtype=torch.float64, device=dev)
+    p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
+    f = rr_factor_buf(*[_p(fac.get(k)) if fac is not None else None for k in ("V", "v", "K", "k")])
+    s = rr_solution(_p(sol["x"]), _p(sol["u"]), _p(sol["y"]))
+    rc = lib().rr_solve(ctypes.byref(dims_of(prob)), ctypes.byref(p), _p(factor), factor.numel() * 8,
+                        ctypes.byref(f), ctypes.byref(s), _p(workspace), workspace.numel() * 8,
+                        _p(sol["status"]), _stream(stream, dev))
+    check(rc, "rr_solve")
+    return sol
+
+
 def version() -> str:
     return lib().rr_version().decode()
 
