@@ -42,9 +42,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample wall time")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
                     help="c2 (default, BASELINE configs[1]); c3 = 4,096 dense n64 m32 N50 (configs[2]); "
-                         "c4 = ipm_step on 16,384 cart-pole instances (configs[3])")
+                         "c4 = ipm_step on 16,384 cart-pole instances (configs[3]); c5 = 1,048,576 "
+                         "quadrotor n12 m4 N200 sharded over the ranks, chunks of 65,536 (configs[4])")
+    ap.add_argument("--c5-total", type=int, default=1048576, help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -216,6 +218,8 @@ def main():
     dev = torch.device("cuda", local)
     if a.workload == "c4":
         return run_c4(a, ws, rank, local)
+    if a.workload == "c5":
+        return run_c5(a, ws, rank, local)
     global NX, NU, HORIZON, BATCH, SEED, ALG_BYTES_PER_STAGE, ALG_FLOPS_PER_STAGE
     if a.workload == "c3":
         # 206,208 B and 2.42M flop per stage (algorithmic)
@@ -389,6 +393,96 @@ def run_c4(a, ws, rank, local):
                          "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": ncu_traffic("ipm_c4"),
                          "alg_bytes_per_stage": 1900, "peak_source": src},
             "gpu_launches": a.steps}), flush=True)
+
+
+def run_c5(a, ws, rank, local):
+    """BASELINE configs[4]: 1,048,576 quadrotor instances (n=12, m=4, N=200) split over the ranks
+    (strong scaling: total work fixed), rr_factor_solve in resident chunks of 65,536 instances
+    (inputs 37 GB + policy records 31 GB per chunk; the whole batch is ~600 GB of inputs, more than
+    one GPU holds).  Every chunk is generated on the device (untimed), then solved W times untimed
+    and K times timed with CUDA events; the step time is the sum over the rank's chunks of the
+    mean chunk time (each chunk's inputs exceed L2, so re-solving a resident chunk is not cached),
+    plus the timed NCCL gather of the per-instance summaries (status, u_0) to rank 0.  Reported
+    time = max over ranks."""
+    import torch
+    import synth
+    import paper_2509_16370_b200 as rr
+    from paper_2509_16370_b200.shard import shard_range, gather_summaries
+    dev = torch.device("cuda", local)
+    n, m, Nh, CH = 12, 4, 200, 65536
+    total = a.c5_total
+    b0, b1 = shard_range(rank, ws, total)
+    mine = b1 - b0
+    CH = min(CH, max(mine, 1))
+    prob = synth.empty_problem(n, m, Nh, CH, device=dev)
+    sol = rr.alloc_solution(prob)
+    call = rr.Marshalled(prob, sol)
+    stream = torch.cuda.current_stream(dev)
+    summ = {"status": torch.empty(mine, dtype=torch.int32, device=dev),
+            "u0": torch.empty(mine, m, dtype=torch.float64, device=dev)}
+    chunk_ms, gen_s = [], 0.0
+    clocks = ClockSampler(local)
+    clocks.start()
+    for s in range(b0, b1, CH):
+        e = min(b1, s + CH)
+        t0 = time.perf_counter()
+        if e - s != CH:  # ragged last chunk: its own buffers
+            prob = synth.empty_problem(n, m, Nh, e - s, device=dev)
+            sol = rr.alloc_solution(prob)
+            call = rr.Marshalled(prob, sol, ws=call.ws)
+        for g in range(s, e, 4096):
+            ge = min(e, g + 4096)
+            p = synth.quadrotor_c5(ge - g, first=g, device=dev)
+            for f in synth.RRProblem.FIELDS:
+                getattr(prob, f)[g - s:ge - s].copy_(getattr(p, f))
+            del p
+        torch.cuda.synchronize()
+        gen_s += time.perf_counter() - t0
+        for _ in range(max(3, a.warmup) if s == b0 else 1):
+            call.launch(stream)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+        for k in range(a.steps):
+            ev[k][0].record(stream)
+            call.launch(stream)
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        chunk_ms.append(statistics.mean(x.elapsed_time(y) for x, y in ev))
+        summ["status"][s - b0:e - b0].copy_(sol["status"])
+        summ["u0"][s - b0:e - b0].copy_(sol["u"][:, 0, :])
+    barrier(ws)
+    torch.cuda.synchronize()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    gathered = gather_summaries(summ, rank, ws, total)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    solve_ms = max_over_ranks(sum(chunk_ms), ws)
+    gather_ms = max_over_ranks(g0.elapsed_time(g1), ws)
+    if rank != 0:
+        return
+    nbad = int((gathered["status"] != 0).sum())
+    ms = solve_ms + gather_ms
+    kern_ms_chunk = statistics.mean(chunk_ms)
+    alg = ALG_BYTES_PER_STAGE * total * Nh / ws
+    peak, src = measured_peaks()
+    ach = alg / (solve_ms / 1e3) / 1e9
+    print(json.dumps({
+        "metric": METRIC, "value": total / (ms / 1e3), "unit": "solves/s", "n_gpus": ws, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C5: %d quadrotor regularized LQR (n_x=12 n_u=4 N=200 delta=1e-4) over %d GPU(s), "
+                               "chunks of %d, FP64" % (total, ws, CH),
+                   "global_batch": total, "seq_len": Nh, "parallelism": "batch-shard x%d" % ws,
+                   "l2": "chunk inputs 37 GB > 126 MB L2 (no flush needed)",
+                   "timing": "sum over the rank's chunks of the mean event-timed rr_factor_solve launch, "
+                             "+ summary gather; max over ranks; generation untimed (%.1f s)" % gen_s},
+        "stage_updates_per_s": total * Nh / (ms / 1e3), "solve_ms": solve_ms, "gather_ms": gather_ms,
+        "chunks_per_rank": len(chunk_ms), "status_nonzero": nbad,
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": None, "kernel": "rr_fused_mma_kernel<12,4>", "kernel_ms_per_chunk": kern_ms_chunk,
+                     "alg_bytes_per_stage": ALG_BYTES_PER_STAGE, "peak_source": src},
+        "clocks": clk, "e2e": None, "gpu_launches": a.steps * len(chunk_ms)}), flush=True)
 
 
 if __name__ == "__main__":

@@ -1,6 +1,8 @@
 """Batch sharding across GPUs (row e): instances are independent, so ranks own contiguous
 global-id ranges and no collective touches the data path.  torch.distributed is used only to
-reduce the timing (max over ranks) and for barriers."""
+reduce the timing (max over ranks), for barriers, and for the final gather of per-instance
+summaries (status, u_0) to rank 0 after the solve; full trajectories stay on
+their device."""
 from __future__ import annotations
 
 from typing import Tuple
@@ -25,3 +27,29 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gather_summaries(parts, rank: int, world: int, total: int):
+    """Gather per-instance summary tensors of every rank's shard to rank 0 (after the solve).
+
+    parts: dict name -> tensor [shard_size, ...] (this rank's contiguous shard, shard_range order).
+    Returns, on rank 0, dict name -> tensor [total, ...] in global-id order; None on other ranks.
+    Shards differ in size by at most one, so every rank pads to the largest shard and one
+    all_gather per tensor moves them (NCCL over NVLink/NVSwitch on GPUs, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1 or not (dist.is_available() and dist.is_initialized()):
+        return dict(parts)
+    sizes = [e - b for b, e in (shard_range(r, world, total) for r in range(world))]
+    mx = max(sizes)
+    out = {}
+    for name, t in parts.items():
+        if t.shape[0] != sizes[rank]:
+            raise ValueError("summary %s has %d rows, shard has %d" % (name, t.shape[0], sizes[rank]))
+        pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[:t.shape[0]].copy_(t)
+        bufs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(bufs, pad)
+        if rank == 0:
+            out[name] = torch.cat([bufs[r][:sizes[r]] for r in range(world)], dim=0)
+    return out if rank == 0 else None

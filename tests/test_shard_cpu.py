@@ -70,3 +70,37 @@ def test_gloo_world2_shards_equal_unsharded():
     for b, e, x, A in obj:
         assert np.array_equal(A, full.A[b:e].numpy())     # generator keyed by global id
         assert np.array_equal(x, of["x"][b:e])
+
+
+def _gather_worker(rank, world, port, total, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2509_16370_b200.shard import gather_summaries
+    b, e = shard_range(rank, world, total)
+    ids = torch.arange(b, e, dtype=torch.int64)
+    parts = {"status": (ids % 7).to(torch.int32), "u0": torch.stack([ids.double(), -ids.double()], dim=1)}
+    g = gather_summaries(parts, rank, world, total)
+    if rank == 0:
+        out.put({k: v.numpy() for k, v in g.items()})
+    else:
+        assert g is None
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,total", [(2, 11), (3, 10)])
+def test_gloo_summary_gather_global_order(world, total):
+    """Per-instance summaries of uneven shards arrive on rank 0 in global-id order (row e)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    g = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    ids = np.arange(total)
+    assert np.array_equal(g["status"], (ids % 7).astype(np.int32))
+    assert np.array_equal(g["u0"], np.stack([ids, -ids], axis=1).astype(np.float64))
