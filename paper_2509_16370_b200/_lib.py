@@ -7,7 +7,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librr_b200.so")
+# RR_B200_LIB: alternate in-tree build of the same library (kernel A/B experiments only)
+LIB_PATH = os.environ.get("RR_B200_LIB") or os.path.join(HERE, "librr_b200.so")
 _lock = threading.Lock()
 _lib = None
 

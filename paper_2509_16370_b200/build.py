@@ -22,14 +22,17 @@ def deps():
         sorted(glob.glob(os.path.join(ROOT, "include", "*.h"))) + [os.path.abspath(__file__)]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Build librr_b200.so (or, for kernel A/B experiments, `out` with extra -D `defines`)."""
+    lib = out or LIB
     newest = max(os.path.getmtime(p) for p in deps())
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= newest:
+        return lib
+    tmp = lib + ".tmp%d" % os.getpid()
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
            "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
-           "-Xptxas", "-v" if verbose else "-O3", "-o", tmp, *sources(), "-lcudart"]
+           "-Xptxas", "-v" if verbose else "-O3", *["-D" + d for d in defines], "-o", tmp, *sources(),
+           "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -37,8 +40,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         with open(os.path.join(HERE, "ptxas.log"), "w") as f:
             f.write(r.stdout + r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -323,6 +323,10 @@ struct MmaLayout {
   static constexpr int SLOT = BAR + 2;
   static constexpr int SLOT_PAD = (SLOT + 1) & ~1;
   // TMA bulk copies need 16-byte sizes/offsets for every operand block of a stage
+  // P-gather table: per lane, the stage-buffer offset of each P_i element of its U C-fragments
+  // (ZT × ZT tiles × 2 values), -1 outside NZ; stage independent, built once per CTA
+  static constexpr int ZT = (NX + NU + 7) / 8;
+  static constexpr int PTAB = ZT * ZT * 2;
   static constexpr bool BULK = (NX * NX) % 2 == 0 && (NX * NU) % 2 == 0 && (NX * (NX + 1) / 2) % 2 == 0 &&
                                (NU * (NU + 1) / 2) % 2 == 0 && NX % 2 == 0 && NU % 2 == 0 &&
                                RecM<NX, NU>::SIZE % 2 == 0;
@@ -348,6 +352,26 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   double* slotq[2] = {smem + (warp * 2 + 0) * LY::SLOT_PAD, smem + (warp * 2 + 1) * LY::SLOT_PAD};
   double* slot = grp ? slotq[1] : slotq[0];
   double* wkq[2] = {slotq[0] + LY::STG_PAD, slotq[1] + LY::STG_PAD};
+#ifndef RR_NO_PTAB
+  int* ptab = reinterpret_cast<int*>(smem + WARPS * 2 * LY::SLOT_PAD);
+  if (warp == 0) {
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int k = 0; k < LY::PTAB; ++k) {
+      const int e = k & 1, nt = (k >> 1) % LY::ZT, mt = (k >> 1) / LY::ZT;
+      const int s = 8 * mt + g, c = 8 * nt + 2 * t + e;
+      int off = -1;
+      if (s < NZ && c < NZ) {
+        if (s < NX && c < NX) off = oQ + (s >= c ? pidx(n, s, c) : pidx(n, c, s));
+        else if (s < NX) off = oM + s + (c - NX) * n;
+        else if (c < NX) off = oM + c + (s - NX) * n;
+        else off = oR + (s >= c ? pidx(m, s - NX, c - NX) : pidx(m, c - NX, s - NX));
+      }
+      ptab[lane * LY::PTAB + k] = off;
+    }
+  }
+  __syncthreads();
+#endif
   double* wk = grp ? wkq[1] : wkq[0];
 
   const int64_t inst0 = ((int64_t)blockIdx.x * WARPS + warp) * 2;
@@ -441,7 +465,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     const double* cvq[2] = {sbq[0] + oc, sbq[1] + oc};
     const double* sb = grp ? sbq[1] : sbq[0];
     auto qjf = [&]() -> double { return (j < NX) ? sb[oq + j] : sb[orr + j - NX]; };
+#ifdef RR_NO_PTAB
     auto P2 = [&](int q, int s, int t) -> double { return Pat(sbq[q], s, t); };
+#else
+    auto P2 = [&](int q, int k) -> double {
+      const int off = ptab[lane * LY::PTAB + k];
+      return off >= 0 ? sbq[q][off] : 0.0;
+    };
+    (void)Pat;
+#endif
     auto wait_inputs = [&]() { wait_stage(); };
     auto prefetch = [&]() {
       if (i > 0) issue_stage(i - 1, slot);
@@ -605,7 +637,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
 template <int NX, int NU, int WARPS, int MINB>
 struct MmaCfg {
   static constexpr int IPB = WARPS * 2;
-  static size_t smem_bytes() { return sizeof(double) * (size_t)IPB * MmaLayout<NX, NU>::SLOT_PAD; }
+  static size_t smem_bytes() {
+    return sizeof(double) * (size_t)IPB * MmaLayout<NX, NU>::SLOT_PAD + sizeof(int) * 32 * MmaLayout<NX, NU>::PTAB;
+  }
   static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * RecM<NX, NU>::PAD; }
   static cudaError_t launch(const FusedArgs& a, cudaStream_t s) {
     auto k = rr_fused_mma_kernel<NX, NU, WARPS, MINB>;

@@ -82,6 +82,7 @@ struct Stage {
     double A[NX];
 #pragma unroll
     for (int r = 0; r < NX; ++r) A[r] = delta * Vc[r] + (r == j ? 1.0 : 0.0);
+    bool notpd = false;
 #pragma unroll
     for (int p = 0; p < NX; ++p) {
       double* pb = wk + WK::pub + (p & 1) * WK::NZP;
@@ -90,7 +91,7 @@ struct Stage {
       double col[NX];
       bcast(pb, col);
       const double d = col[p];
-      if (!(d > 0.0) && st == 0) st = mk_status(RR_ST_S_NOT_PD, stage);
+      notpd |= !(d > 0.0);
       const double id = rcp_nr(d);
       const double f = (A[p] - (j == p ? 1.0 : 0.0)) * id;
 #pragma unroll
@@ -98,6 +99,7 @@ struct Stage {
         if (r != p) A[r] = fma(-col[r], f, A[r]);
       A[p] = (j == p) ? -id : f;
     }
+    if (notpd && st == 0) st = mk_status(RR_ST_S_NOT_PD, stage);
     if (j < NX) {  // S⁻¹ is symmetric: write column j as row j (consecutive lanes, conflict-free)
 #pragma unroll
       for (int r = 0; r < NX; ++r) wk[WK::Si + r * NX + j] = -A[r];

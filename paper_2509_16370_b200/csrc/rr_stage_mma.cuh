@@ -28,9 +28,16 @@
 namespace rrk {
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+#ifdef RR_DMMA_VOLATILE
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
+#else
+  // not volatile: a pure register operation, so the compiler may interleave independent chains
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+#endif
 }
 
 // Workspace record of the MMA kernel: PhiT row-major NX × (NX+2) (column NX = φ) | K | k | V packed | v
@@ -59,7 +66,8 @@ struct WorkM {
   static constexpr int X1 = W::Wb;              // [V | Ve] (ld NX), then T (ld NX), then M (row-major, ld MLD)
   static constexpr int X2 = X1 + X1SZ;          // W (ld NX, NX+1 cols), then U (ld ULD)
   static constexpr int ULD = 18;                // U leading dimension: conflict-free C-fragment stores
-  static constexpr int SIZE = X2 + 16 * ULD;
+  static constexpr int E = X2 + 16 * ULD;       // e = c_{i+1} − δ v_{i+1} (NX, even)
+  static constexpr int SIZE = E + ((NX + 1) & ~1);
   static constexpr int PAD = (SIZE + 1) & ~1;
 };
 
@@ -96,14 +104,18 @@ struct StageMMA {
     // (1) S⁻¹ (no stage input needed), then Vs = [V | V e] (V symmetric: (V e)_j = column j · e)
     ST::invS(Vc, delta, j, wk, stage, st);
     wait_inputs();
+    if (j < NX) wk[WM::E + j] = cv[j] - delta * wk[WK::vs + j];  // e = c_{i+1} − δ v_{i+1}
+    __syncwarp();
     if (j < NX) {
 #pragma unroll
       for (int r = 0; r < NX; ++r) wk[WM::X1 + r * NX + j] = Vc[r];  // V symmetric: column j as row j
+      double ek[NX];
+      ST::bcast(wk + WM::E, ek);
       double ve0 = 0.0, ve1 = 0.0;
 #pragma unroll
       for (int k = 0; k < NX; k += 2) {
-        ve0 = fma(Vc[k], cv[k] - delta * wk[WK::vs + k], ve0);
-        ve1 = fma(Vc[k + 1], cv[k + 1] - delta * wk[WK::vs + k + 1], ve1);
+        ve0 = fma(Vc[k], ek[k], ve0);
+        ve1 = fma(Vc[k + 1], ek[k + 1], ve1);
       }
       wk[WM::X1 + NX * NX + j] = ve0 + ve1;  // column NX of Vs
     }
@@ -212,8 +224,12 @@ struct StageMMA {
         for (int nt = 0; nt < ZT; ++nt)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
+#ifdef RR_NO_PTAB
             const int r = 8 * mt + g, col = 8 * nt + 2 * t + e;
             c[mt][nt][e] = (r < NZ && col < NZ) ? Pat(q, r, col) : 0.0;
+#else
+            c[mt][nt][e] = Pat(q, (mt * ZT + nt) * 2 + e);  // P-gather table (kernel)
+#endif
           }
 #pragma unroll
       for (int kt = 0; kt < KT; ++kt) {
@@ -281,12 +297,7 @@ struct StageMMA {
     // (7) M = [A + B K | B k + c − δ v] -> X1 (ld NX, NX+1 columns)
     if (j <= NX) {
       double tcol[NX];
-#pragma unroll
-      for (int r = 0; r < NX; r += 2) {
-        const double2 f2 = *reinterpret_cast<const double2*>(F + jc * NX + r);
-        tcol[r] = (j < NX) ? f2.x : cv[r] - delta * wk[WK::vs + r];
-        tcol[r + 1] = (j < NX) ? f2.y : cv[r + 1] - delta * wk[WK::vs + r + 1];
-      }
+      ST::bcast((j < NX) ? F + jc * NX : wk + WM::E, tcol);  // column j of A, or e for the φ column
 #pragma unroll
       for (int u = 0; u < NU; ++u) {
         const double coef = (j < NX) ? -U[NX + u] : -b[NX + u];
