@@ -10,8 +10,10 @@ Tiers:
   T2 (rr_oracle.c)   the paper's recursion Eq.(RR), forward pass and dual
                      recovery (P:496-509, P:627-650), literally, in plain C loops;
                      pinned to T1 and to the textbook pins in tests/.
+  R  (residual.py)   the KKT residual K[x; y] + [s; c] (the paper's third callback).
   IPM (ipm.py)       condense (P:277-300) -> T2 -> expand (P:224-227), merit (P:61-66),
                      directional derivative, line search (P:221-222 + reading R12).
 """
 from .rr import build_oracle, rr_solve_t2, load_oracle  # noqa: F401
 from .dense import assemble_reglqr, rr_solve_dense, unpack_solution  # noqa: F401
+from .residual import residual_dense, residual_blocks  # noqa: F401,E402
