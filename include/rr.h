@@ -45,11 +45,16 @@ typedef int32_t rr_err;
 #define RR_ST_NONPOS_SLACK 4 /* ipm_step: s <= 0 or z <= 0 on entry (P:53-59 needs log s)  */
 #define RR_ST_LS_FAILED 5    /* ipm_step: no Armijo point within max_backtracks           */
 
+/* rr_dims.flags: RR_FLAG_ACCUMULATE makes rr_solve ADD its solution to sol (x += Δx, u += Δu,
+ * y += Δy) instead of overwriting it -- the update step of iterative refinement with rr_residual.
+ * Every other entry point requires flags == 0. */
+#define RR_FLAG_ACCUMULATE 1
+
 typedef struct {
   int32_t nx;    /* state dimension n   (1 <= nx)            */
   int32_t nu;    /* control dimension m (1 <= nu)            */
   int32_t N;     /* horizon (number of stages, N >= 0)       */
-  int32_t flags; /* reserved, must be 0                      */
+  int32_t flags; /* 0, or RR_FLAG_ACCUMULATE for rr_solve     */
   int64_t batch; /* number of independent instances (>= 0)  */
 } rr_dims;
 
@@ -170,10 +175,37 @@ int64_t rr_solve_workspace_bytes(const rr_dims* dims);
  * fac: optional v [batch][N+1][n] and k [batch][N][m] copies (V, K members ignored).
  * status: [batch] device int32, 0 or RR_ST_NONFINITE (e.g. the instance's factor failed: see
  *   rr_factor's status for the reason); outputs of a non-finite instance are NaN-filled.
+ * dims->flags: 0 (sol = solution) or RR_FLAG_ACCUMULATE (sol += solution; see rr_residual).
  */
 rr_err rr_solve(const rr_dims* dims, const rr_problem* prob, const void* factor, int64_t factor_bytes,
                 const rr_factor_buf* fac, const rr_solution* sol, void* workspace, int64_t workspace_bytes,
                 int32_t* status, void* stream);
+
+/* ================================ KKT residual (the paper's third callback) ================================
+ * rr_residual: r = K [x; y] + [s; c] for the §1.4 system K [x; y] = −[s; c], i.e. the
+ * paper's "KKT system residual computation callback", block by block:
+ *   stationarity  x_i: Q_i x_i + M_i u_i + q_i − y_i + A_iᵀ y_{i+1}      (i < N)
+ *                 u_i: M_iᵀ x_i + R_i u_i + r_i + B_iᵀ y_{i+1}
+ *                 x_N: Q_N x_N + q_N − y_N
+ *   primal   row 0:    −x_0 − δ y_0 + c_0
+ *            row i+1:  A_i x_i + B_i u_i − x_{i+1} − δ y_{i+1} + c_{i+1}
+ * The blocks are written into the right-hand-side slots of an rr_problem (q, r, c, q_N, c_0 layouts),
+ * so {A, B, delta, res} is directly the right-hand side of the correction system: rr_solve on it with
+ * RR_FLAG_ACCUMULATE performs one step of iterative refinement (x, u, y) += K⁻¹(−r).
+ * res: optional (NULL or NULL members: not written).  norms: optional device [batch][2] =
+ * (max |stationarity|, max |primal|) per instance (NaN if any residual entry is non-finite).
+ * prob: every operand read.  sol: x, u, y read.  Same shape support as rr_factor.
+ */
+typedef struct {
+  double* q;  /* [batch][N][n]  stationarity rows x_i  */
+  double* r;  /* [batch][N][m]  stationarity rows u_i  */
+  double* c;  /* [batch][N][n]  primal rows i+1        */
+  double* qN; /* [batch][n]     stationarity rows x_N  */
+  double* c0; /* [batch][n]     primal row 0           */
+} rr_residual_buf;
+
+rr_err rr_residual(const rr_dims* dims, const rr_problem* prob, const rr_solution* sol, const rr_residual_buf* res,
+                   double* norms, void* stream);
 
 /* ================================ regularized IPM step (rows a1-a8) ================================
  * One iteration of the regularized interior point method of §1.2 on the stagewise OCP of

@@ -4,7 +4,8 @@ this package only marshals torch CUDA tensors into the C-ABI.  There is no CPU f
 from ._lib import RRError, LIB_PATH  # noqa: F401
 from .rr import (rr_factor_solve, alloc_solution, alloc_factor, alloc_workspace,  # noqa: F401
                  workspace_bytes, Marshalled, HostMarshalled, version,
-                 rr_factor, rr_solve, factor_bytes, factor_record_doubles, solve_workspace_bytes)
+                 rr_factor, rr_solve, factor_bytes, factor_record_doubles, solve_workspace_bytes,
+                 rr_residual, rr_refine)
 
 from .ipm import ipm_step, IpmCall  # noqa: F401,E402
 

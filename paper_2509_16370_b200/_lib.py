@@ -34,6 +34,13 @@ class rr_solution(ctypes.Structure):
     _fields_ = [(f, ctypes.c_void_p) for f in ("x", "u", "y")]
 
 
+class rr_residual_buf(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in ("q", "r", "c", "qN", "c0")]
+
+
+RR_FLAG_ACCUMULATE = 1
+
+
 class ipm_dims(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int32) for f in ("nx", "nu", "N", "ng", "ngN", "nc", "ncN", "model")] + \
                [("batch", ctypes.c_int64)]
@@ -96,6 +103,9 @@ def lib():
             L.rr_solve.argtypes = [ctypes.POINTER(rr_dims), ctypes.POINTER(rr_problem), ctypes.c_void_p,
                                    ctypes.c_int64, ctypes.POINTER(rr_factor_buf), ctypes.POINTER(rr_solution),
                                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+            L.rr_residual.restype = ctypes.c_int32
+            L.rr_residual.argtypes = [ctypes.POINTER(rr_dims), ctypes.POINTER(rr_problem), ctypes.POINTER(rr_solution),
+                                      ctypes.POINTER(rr_residual_buf), ctypes.c_void_p, ctypes.c_void_p]
             L.ipm_workspace_bytes.restype = ctypes.c_int64
             L.ipm_workspace_bytes.argtypes = [ctypes.POINTER(ipm_dims)]
             L.ipm_step.restype = ctypes.c_int32

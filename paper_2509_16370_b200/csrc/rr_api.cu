@@ -16,8 +16,8 @@ rr_err set_err(rr_err code, const char* fmt, const char* what = "") {
   return code;
 }
 
-bool dims_ok(const rr_dims* d) {
-  return d != nullptr && d->nx >= 1 && d->nu >= 1 && d->N >= 0 && d->batch >= 0 && d->flags == 0;
+bool dims_ok(const rr_dims* d, int allowed_flags = 0) {
+  return d != nullptr && d->nx >= 1 && d->nu >= 1 && d->N >= 0 && d->batch >= 0 && (d->flags & ~allowed_flags) == 0;
 }
 }  // namespace
 
@@ -114,12 +114,12 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* ph, const rr_
 int32_t rr_factor_record_doubles(int32_t n, int32_t m) { return rrk::frec_doubles(n, m); }
 
 int64_t rr_factor_bytes(const rr_dims* dims) {
-  if (!dims_ok(dims) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
+  if (!dims_ok(dims, RR_FLAG_ACCUMULATE) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
   return dims->batch * (int64_t)(dims->N + 1) * rrk::frec_doubles(dims->nx, dims->nu) * 8;
 }
 
 int64_t rr_solve_workspace_bytes(const rr_dims* dims) {
-  if (!dims_ok(dims) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
+  if (!dims_ok(dims, RR_FLAG_ACCUMULATE) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
   return dims->batch * (int64_t)dims->N * (dims->nx + dims->nu) * 8 + 256;
 }
 
@@ -164,7 +164,7 @@ rr_err rr_factor(const rr_dims* dims, const rr_problem* prob, void* factor, int6
 rr_err rr_solve(const rr_dims* dims, const rr_problem* prob, const void* factor, int64_t factor_bytes,
                 const rr_factor_buf* fac, const rr_solution* sol, void* workspace, int64_t workspace_bytes,
                 int32_t* status, void* stream) {
-  if (!dims_ok(dims)) return set_err(RR_E_INVALID, "rr_solve: invalid dims%s");
+  if (!dims_ok(dims, RR_FLAG_ACCUMULATE)) return set_err(RR_E_INVALID, "rr_solve: invalid dims%s");
   if (prob == nullptr || sol == nullptr) return set_err(RR_E_INVALID, "rr_solve: null %s", "prob/sol");
   if (dims->batch == 0) return RR_OK;
   if (status == nullptr) return set_err(RR_E_INVALID, "rr_solve: null %s", "status");
@@ -199,10 +199,43 @@ rr_err rr_solve(const rr_dims* dims, const rr_problem* prob, const void* factor,
   a.frc = static_cast<const double*>(factor);
   a.ws = static_cast<double*>(workspace);
   a.status = status;
+  a.accumulate = (dims->flags & RR_FLAG_ACCUMULATE) != 0;
   bool supported = false;
   cudaError_t e = rrk::solve_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_solve: unsupported shape%s");
   if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_solve: CUDA error %s", cudaGetErrorString(e));
+  return RR_OK;
+}
+
+rr_err rr_residual(const rr_dims* dims, const rr_problem* prob, const rr_solution* sol, const rr_residual_buf* res,
+                   double* norms, void* stream) {
+  if (!dims_ok(dims)) return set_err(RR_E_INVALID, "rr_residual: invalid dims%s");
+  if (prob == nullptr || sol == nullptr) return set_err(RR_E_INVALID, "rr_residual: null %s", "prob/sol");
+  if (dims->batch == 0) return RR_OK;
+  const double* req[] = {prob->QN, prob->qN, prob->c0, prob->delta, sol->x, sol->y};
+  for (const double* p : req)
+    if (p == nullptr) return set_err(RR_E_INVALID, "rr_residual: null %s", "terminal operand or solution");
+  if (dims->N > 0) {
+    const double* req2[] = {prob->A, prob->B, prob->Q, prob->M, prob->R, prob->q, prob->r, prob->c, sol->u};
+    for (const double* p : req2)
+      if (p == nullptr) return set_err(RR_E_INVALID, "rr_residual: null %s", "stage operand or u");
+  }
+  if (!rrk::split_supported(dims->nx, dims->nu))
+    return set_err(RR_E_UNSUPPORTED, "rr_residual: no kernel compiled for this (nx, nu)%s");
+  rrk::ResArgs a{};
+  a.nx = dims->nx;
+  a.nu = dims->nu;
+  a.N = dims->N;
+  a.batch = dims->batch;
+  a.p = *prob;
+  a.s = *sol;
+  rr_residual_buf none = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  a.r = res ? *res : none;
+  a.norms = norms;
+  bool supported = false;
+  cudaError_t e = rrk::residual_launch(a, static_cast<cudaStream_t>(stream), &supported);
+  if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_residual: unsupported shape%s");
+  if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_residual: CUDA error %s", cudaGetErrorString(e));
   return RR_OK;
 }
 

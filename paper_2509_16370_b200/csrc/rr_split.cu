@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
   double* kv = a.ws + inst * sN * (n + m);  // per stage: v_i (n) | k_i (m)
   const int ui = j - NX;                     // control row of this lane (0 <= ui < m)
   const bool xl = j < n, ul = ui >= 0 && ui < m;
+  const bool acc = a.accumulate;             // RR_FLAG_ACCUMULATE: sol += solution (refinement)
 
   auto issue_stage = [&](int i) {
     const int64_t s = inst * sN + i;
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
     }
     const double xv = x0 + x1;
     xb(0)[j] = xv;
-    if (valid) xo[j] = xv;
+    if (valid) xo[j] = acc ? xo[j] + xv : xv;
     bad |= !isfinite(xv);
   }
   __syncwarp();
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
         if (k + 1 < n) y1 = fma(R0[sidx(n, j, k + 1)], xc[k + 1], y1);
       }
       const double yv = y0 + y1;
-      if (valid) yo[(int64_t)i * n + j] = yv;
+      if (valid) yo[(int64_t)i * n + j] = acc ? yo[(int64_t)i * n + j] + yv : yv;
       bad |= !isfinite(yv);
     } else if (ul) {
       double u0 = kv[(int64_t)i * (n + m) + n + ui], u1 = 0.0;
@@ -475,7 +476,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
       }
       const double uv = u0 + u1;
       hb[ui] = uv;
-      if (valid) uo[(int64_t)i * m + ui] = uv;
+      if (valid) uo[(int64_t)i * m + ui] = acc ? uo[(int64_t)i * m + ui] + uv : uv;
       bad |= !isfinite(uv);
     }
     __syncwarp();
@@ -504,7 +505,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
       }
       const double xv = x0 + x1;
       xn[j] = xv;
-      if (valid) xo[(int64_t)(i + 1) * n + j] = xv;
+      if (valid) xo[(int64_t)(i + 1) * n + j] = acc ? xo[(int64_t)(i + 1) * n + j] + xv : xv;
       bad |= !isfinite(xv);
     }
     __syncwarp();
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
       if (k + 1 < n) y1 = fma(RN[sidx(n, j, k + 1)], xc[k + 1], y1);
     }
     const double yv = y0 + y1;
-    if (valid) yo[sN * n + j] = yv;
+    if (valid) yo[sN * n + j] = acc ? yo[sN * n + j] + yv : yv;
     bad |= !isfinite(yv);
   }
   const unsigned anybad = __ballot_sync(RR_FULL_MASK, bad);
@@ -538,11 +539,166 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
 }
 
 // ------------------------------------------------------------------------------------------
+// rr_residual kernel: r = K [x; y] + [s; c] of the §1.4 system, block by block
+// (the paper's residual callback):
+//   rq_i = Q_i x_i + M_i u_i + q_i − y_i + A_iᵀ y_{i+1}     rr_i = M_iᵀ x_i + R_i u_i + r_i + B_iᵀ y_{i+1}
+//   rqN  = Q_N x_N + q_N − y_N                              rc0  = −x_0 − δ y_0 + c_0
+//   rc_i = A_i x_i + B_i u_i − x_{i+1} − δ y_{i+1} + c_{i+1}
+// Written into the right-hand-side slots (q, r, c, q_N, c_0) so rr_solve can refine with it.
+template <int NX, int NU>
+struct ResLayout {
+  static constexpr int STG = NX * NX + 2 * NX * NU + symn(NX) + symn(NU) + 2 * NX + NU;
+  // stage buffer: stage data | x_i | x_{i+1} | u_i | y_i | y_{i+1}
+  static constexpr int BUF = ((STG + 1) & ~1) + 4 * ((NX + 1) & ~1) + ((NU + 1) & ~1);
+  static constexpr int SLOT_PAD = 2 * BUF;
+};
+
+template <int NX, int NU, int LG, int WARPS, int MINB, bool EXACT>
+__global__ void __launch_bounds__(WARPS * 32, MINB) rr_residual_kernel(const ResArgs a) {
+  using LY = ResLayout<NX, NU>;
+  constexpr int IPW = 32 / LG;
+  static_assert(NX + NU <= LG, "lane group narrower than n+m");
+  const int n = EXACT ? NX : a.nx;
+  const int m = EXACT ? NU : a.nu;
+  const int N = a.N;
+  const int sn = symn(n), sm = symn(m);
+  const int oA = 0, oB = n * n, oQ = oB + n * m, oM = oQ + sn, oR = oM + n * m, oq = oR + sm, orr = oq + n,
+            oc = orr + m, STGP = (oc + n + 1) & ~1;
+  const int ox0 = STGP, ox1 = ox0 + ((n + 1) & ~1), ou = ox1 + ((n + 1) & ~1), oy0 = ou + ((m + 1) & ~1),
+            oy1 = oy0 + ((n + 1) & ~1);
+
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / LG, j = lane % LG, gbase = grp * LG;
+  double* slot = smem + (warp * IPW + grp) * group_stride(LY::SLOT_PAD, LG);
+  auto buf = [&](int i) { return slot + (i & 1) * LY::BUF; };
+
+  int64_t inst = ((int64_t)blockIdx.x * WARPS + warp) * IPW + grp;
+  const bool valid = inst < a.batch;
+  if (!valid) inst = a.batch - 1;
+  const double delta = a.p.delta[inst];
+  const int64_t sN = (int64_t)N;
+  const double* xg = a.s.x + inst * (sN + 1) * n;
+  const double* ug = a.s.u + inst * sN * m;
+  const double* yg = a.s.y + inst * (sN + 1) * n;
+  const int ui = j - NX;
+  const bool xl = j < n, ul = ui >= 0 && ui < m;
+
+  auto issue = [&](int i) {
+    const int64_t s = inst * sN + i;
+    double* d = buf(i);
+    copy_async(d + oA, a.p.A + s * n * n, n * n, j, LG);
+    copy_async(d + oB, a.p.B + s * n * m, n * m, j, LG);
+    copy_async(d + oQ, a.p.Q + s * sn, sn, j, LG);
+    copy_async(d + oM, a.p.M + s * n * m, n * m, j, LG);
+    copy_async(d + oR, a.p.R + s * sm, sm, j, LG);
+    copy_async(d + oq, a.p.q + s * n, n, j, LG);
+    copy_async(d + orr, a.p.r + s * m, m, j, LG);
+    copy_async(d + oc, a.p.c + s * n, n, j, LG);
+    copy_async(d + ox0, xg + (int64_t)i * n, n, j, LG);
+    copy_async(d + ox1, xg + (int64_t)(i + 1) * n, n, j, LG);
+    copy_async(d + ou, ug + (int64_t)i * m, m, j, LG);
+    copy_async(d + oy0, yg + (int64_t)i * n, n, j, LG);
+    copy_async(d + oy1, yg + (int64_t)(i + 1) * n, n, j, LG);
+  };
+  double nst = 0.0, npr = 0.0;  // running max |stationarity|, |primal| of this lane
+  bool bad = false;
+  auto upd = [&](double& nm, double r) {
+    bad |= !isfinite(r);
+    nm = fmax(nm, fabs(r));
+  };
+  if (N > 0) issue(0);
+  cp_async_commit();
+  for (int i = 0; i < N; ++i) {
+    if (i + 1 < N) issue(i + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const double* S = buf(i);
+    const int64_t s = inst * sN + i;
+    if (xl) {
+      double a0 = S[oq + j] - S[oy0 + j], a1 = 0.0;  // stationarity row x_i[j]
+      double p0 = S[oc + j] - S[ox1 + j] - delta * S[oy1 + j], p1 = 0.0;  // primal row i+1, entry j
+#pragma unroll
+      for (int k = 0; k < NX; ++k)
+        if (k < n) {
+          a0 = fma(S[oQ + sidx(n, j, k)], S[ox0 + k], a0);
+          a1 = fma(S[oA + k + j * n], S[oy1 + k], a1);
+          p0 = fma(S[oA + j + k * n], S[ox0 + k], p0);
+        }
+#pragma unroll
+      for (int u = 0; u < NU; ++u)
+        if (u < m) {
+          a1 = fma(S[oM + j + u * n], S[ou + u], a1);
+          p1 = fma(S[oB + j + u * n], S[ou + u], p1);
+        }
+      const double rq = a0 + a1, rc = p0 + p1;
+      upd(nst, rq);
+      upd(npr, rc);
+      if (valid) {
+        if (a.r.q) a.r.q[s * n + j] = rq;
+        if (a.r.c) a.r.c[s * n + j] = rc;
+      }
+    } else if (ul) {
+      double a0 = S[orr + ui], a1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < NX; ++k)
+        if (k < n) {
+          a0 = fma(S[oM + k + ui * n], S[ox0 + k], a0);
+          a1 = fma(S[oB + k + ui * n], S[oy1 + k], a1);
+        }
+#pragma unroll
+      for (int w = 0; w < NU; ++w)
+        if (w < m) a0 = fma(S[oR + sidx(m, ui, w)], S[ou + w], a0);
+      const double rr = a0 + a1;
+      upd(nst, rr);
+      if (valid && a.r.r) a.r.r[s * m + ui] = rr;
+    }
+    __syncwarp();  // buffer i is refilled by issue(i + 2)
+  }
+  // terminal stationarity and the initial-state row
+  if (xl) {
+    const double* QN = a.p.QN + inst * sn;
+    const double* xN = xg + sN * n;
+    double a0 = a.p.qN[inst * n + j] - yg[sN * n + j];
+    for (int k = 0; k < n; ++k) a0 = fma(QN[sidx(n, j, k)], xN[k], a0);
+    const double r0 = -xg[j] - delta * yg[j] + a.p.c0[inst * n + j];
+    upd(nst, a0);
+    upd(npr, r0);
+    if (valid) {
+      if (a.r.qN) a.r.qN[inst * n + j] = a0;
+      if (a.r.c0) a.r.c0[inst * n + j] = r0;
+    }
+  }
+#pragma unroll
+  for (int off = LG / 2; off > 0; off >>= 1) {
+    nst = fmax(nst, __shfl_xor_sync(RR_FULL_MASK, nst, off));
+    npr = fmax(npr, __shfl_xor_sync(RR_FULL_MASK, npr, off));
+  }
+  const unsigned anybad = __ballot_sync(RR_FULL_MASK, bad);
+  const unsigned gmask = (LG == 32) ? 0xffffffffu : (((1u << LG) - 1u) << gbase);
+  if (valid && j == 0 && a.norms != nullptr) {
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    a.norms[2 * inst] = (anybad & gmask) ? nan : nst;
+    a.norms[2 * inst + 1] = (anybad & gmask) ? nan : npr;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 template <int NX, int NU, int LG, int WARPS, int MINB, bool EXACT, int MINB_F = MINB>
 struct SplitCfg {
   static constexpr int IPB = WARPS * (32 / LG);
   static size_t fac_smem() { return sizeof(double) * (size_t)IPB * group_stride(FacLayout<NX, NU, EXACT>::SLOT_PAD, LG); }
   static size_t sol_smem() { return sizeof(double) * (size_t)IPB * group_stride(SolLayout<NX, NU>::SLOT_PAD, LG); }
+  static size_t res_smem() { return sizeof(double) * (size_t)IPB * group_stride(ResLayout<NX, NU>::SLOT_PAD, LG); }
+  static cudaError_t residual(const ResArgs& a, cudaStream_t s) {
+    auto k = rr_residual_kernel<NX, NU, LG, WARPS, MINB, EXACT>;
+    const size_t sm = res_smem();
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k<<<(unsigned)((a.batch + IPB - 1) / IPB), WARPS * 32, sm, s>>>(a);
+    return cudaGetLastError();
+  }
   static cudaError_t factor(const SplitArgs& a, cudaStream_t s) {
     auto k = rr_factor_kernel<NX, NU, LG, WARPS, MINB_F, EXACT>;
     const size_t sm = fac_smem();
@@ -595,4 +751,15 @@ cudaError_t solve_launch(const SplitArgs& a, cudaStream_t s, bool* supported) {
   return err;
 }
 
+}  // namespace rrk
+
+namespace rrk {
+cudaError_t residual_launch(const ResArgs& a, cudaStream_t s, bool* supported) {
+  cudaError_t err = cudaSuccess;
+  *supported = dispatch_split(a.nx, a.nu, [&](auto cfg) {
+    err = decltype(cfg)::residual(a, s);
+    return true;
+  });
+  return err;
+}
 }  // namespace rrk

@@ -17,6 +17,16 @@ struct SplitArgs {
   const double* frc; // rr_solve: the same records, read only
   double* ws;        // rr_solve scratch: [batch][N][n+m] (v_i | k_i)
   int32_t* status;
+  int accumulate;    // rr_solve: RR_FLAG_ACCUMULATE (sol += solution)
+};
+
+struct ResArgs {
+  int nx, nu, N;
+  int64_t batch;
+  rr_problem p;
+  rr_solution s;     // candidate (read)
+  rr_residual_buf r; // residual blocks (any member may be null)
+  double* norms;     // [batch][2] or null
 };
 
 // doubles per factor record: V (packed n) | S⁻¹ (packed n) | K (m×n) | G⁻¹ (packed m), even
@@ -27,5 +37,6 @@ __host__ __device__ inline int frec_doubles(int n, int m) {
 bool split_supported(int nx, int nu);
 cudaError_t factor_launch(const SplitArgs& a, cudaStream_t s, bool* supported);
 cudaError_t solve_launch(const SplitArgs& a, cudaStream_t s, bool* supported);
+cudaError_t residual_launch(const ResArgs& a, cudaStream_t s, bool* supported);
 
 }  // namespace rrk

@@ -9,7 +9,8 @@ from typing import Optional
 
 import torch
 
-from ._lib import RRError, check, lib, rr_dims, rr_factor_buf, rr_problem, rr_solution
+from ._lib import (RR_FLAG_ACCUMULATE, RRError, check, lib, rr_dims, rr_factor_buf, rr_problem, rr_residual_buf,
+                   rr_solution)
 
 PROBLEM_FIELDS = ("A", "B", "Q", "M", "R", "q", "r", "c", "QN", "qN", "c0", "delta")
 
@@ -140,9 +141,10 @@ def rr_factor(prob, factor=None, fac=None, status=None, stream=None):
     return factor, status
 
 
-def rr_solve(prob, factor, out=None, fac=None, workspace=None, stream=None):
+def rr_solve(prob, factor, out=None, fac=None, workspace=None, stream=None, accumulate=False):
     """Rows a3-a5 for the right-hand side (q, r, c, qN, c0) of `prob` with rr_factor's records.
-    Returns dict x, u, y, status (status: 0 or RR_ST_NONFINITE)."""
+    Returns dict x, u, y, status (status: 0 or RR_ST_NONFINITE).  accumulate: add the solution
+    to `out` (RR_FLAG_ACCUMULATE, the refinement update) instead of overwriting it."""
     if not prob.delta.is_cuda:
         raise RRError("rr_solve needs CUDA tensors (no CPU fallback)")
     dev = prob.delta.device
@@ -153,11 +155,53 @@ def rr_solve(prob, factor, out=None, fac=None, workspace=None, stream=None):
     p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
     f = rr_factor_buf(*[_p(fac.get(k)) if fac is not None else None for k in ("V", "v", "K", "k")])
     s = rr_solution(_p(sol["x"]), _p(sol["u"]), _p(sol["y"]))
-    rc = lib().rr_solve(ctypes.byref(dims_of(prob)), ctypes.byref(p), _p(factor), factor.numel() * 8,
+    d = dims_of(prob)
+    if accumulate:
+        if out is None:
+            raise RRError("rr_solve(accumulate=True) needs `out` (the solution to update)")
+        d.flags = RR_FLAG_ACCUMULATE
+    rc = lib().rr_solve(ctypes.byref(d), ctypes.byref(p), _p(factor), factor.numel() * 8,
                         ctypes.byref(f), ctypes.byref(s), _p(workspace), workspace.numel() * 8,
                         _p(sol["status"]), _stream(stream, dev))
     check(rc, "rr_solve")
     return sol
+
+
+RESIDUAL_FIELDS = ("q", "r", "c", "qN", "c0")
+
+
+def rr_residual(prob, sol, res=None, norms=None, stream=None):
+    """KKT residual r = K[x; y] + [s; c] (the paper's residual callback) of `sol` (dict x, u, y).
+    Returns (res, norms): res a dict q, r, c, qN, c0 in the right-hand-side layouts of `prob`,
+    norms [batch, 2] = (max |stationarity|, max |primal|)."""
+    if not prob.delta.is_cuda:
+        raise RRError("rr_residual needs CUDA tensors (no CPU fallback)")
+    dev = prob.delta.device
+    if res is None:
+        res = {f: torch.empty_like(getattr(prob, f)) for f in RESIDUAL_FIELDS}
+    if norms is None:
+        norms = torch.empty(prob.batch, 2, dtype=torch.float64, device=dev)
+    p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
+    s = rr_solution(_p(sol["x"]), _p(sol["u"]), _p(sol["y"]))
+    r = rr_residual_buf(*[_p(res.get(f)) for f in RESIDUAL_FIELDS])
+    rc = lib().rr_residual(ctypes.byref(dims_of(prob)), ctypes.byref(p), ctypes.byref(s), ctypes.byref(r),
+                           _p(norms), _stream(stream, dev))
+    check(rc, "rr_residual")
+    return res, norms
+
+
+def rr_refine(prob, factor, sol, iters: int = 1, workspace=None, stream=None):
+    """Iterative refinement of `sol` in place: iters x (rr_residual -> rr_solve(accumulate)).
+    The correction system has the same matrix (A, B, Q, M, R, Q_N, δ -- the factor) and the
+    residual as its right-hand side.  Returns the norms of the residual before the last update."""
+    norms = None
+    res = None
+    for _ in range(iters):
+        res, norms = rr_residual(prob, sol, res=res, stream=stream)
+        corr = type(prob)(prob.nx, prob.nu, prob.N, **{f: (res[f] if f in res else getattr(prob, f))
+                                                      for f in PROBLEM_FIELDS})
+        rr_solve(corr, factor, out=sol, workspace=workspace, stream=stream, accumulate=True)
+    return norms
 
 
 def version() -> str:
