@@ -42,10 +42,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample wall time")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5", "split"],
                     help="c2 (default, BASELINE configs[1]); c3 = 4,096 dense n64 m32 N50 (configs[2]); "
                          "c4 = ipm_step on 16,384 cart-pole instances (configs[3]); c5 = 1,048,576 "
-                         "quadrotor n12 m4 N200 sharded over the ranks, chunks of 65,536 (configs[4])")
+                         "quadrotor n12 m4 N200 sharded over the ranks, chunks of 65,536 (configs[4]); split = "
+                         "rr_factor + rr_solve + rr_residual on the C2 workload, each kernel timed")
     ap.add_argument("--c5-total", type=int, default=1048576, help=argparse.SUPPRESS)
     return ap.parse_args()
 
@@ -220,6 +221,8 @@ def main():
         return run_c4(a, ws, rank, local)
     if a.workload == "c5":
         return run_c5(a, ws, rank, local)
+    if a.workload == "split":
+        return run_split(a, ws, rank, local)
     global NX, NU, HORIZON, BATCH, SEED, ALG_BYTES_PER_STAGE, ALG_FLOPS_PER_STAGE
     if a.workload == "c3":
         # 206,208 B and 2.42M flop per stage (algorithmic)
@@ -483,6 +486,90 @@ def run_c5(a, ws, rank, local):
                      "traffic": None, "kernel": "rr_fused_mma_kernel<12,4>", "kernel_ms_per_chunk": kern_ms_chunk,
                      "alg_bytes_per_stage": ALG_BYTES_PER_STAGE, "peak_source": src},
         "clocks": clk, "e2e": None, "gpu_launches": a.steps * len(chunk_ms)}), flush=True)
+
+
+def run_split(a, ws, rank, local):
+    """Extra line: the factorization / solve / residual callbacks (rr_factor, rr_solve, rr_residual)
+    on the C2 workload, one step = factor + solve (the residual timed beside it).  Each kernel is
+    timed with CUDA events on the launching stream and reported against its own algorithmic bytes
+    per (instance, stage):  rr_factor reads A,B,Q,M,R and writes the record
+    (328 + 214 doubles); rr_solve reads A,B,c,q,r + record in the backward sweep, record + A,B,c in
+    the forward sweep, writes/reads v,k and writes x,u,y (220+214+16 + 214+204+16+28 doubles);
+    rr_residual reads the stage data + x,u,y once and writes the residual (356+28+28 doubles)."""
+    import torch
+    import synth
+    import paper_2509_16370_b200 as rr
+    dev = torch.device("cuda", local)
+    B = a.batch
+    prob = synth.empty_problem(NX, NU, HORIZON, B, device=dev)
+    for s in range(0, B, 4096):
+        e = min(B, s + 4096)
+        p = synth.random_stable_lqr(NX, NU, HORIZON, e - s, SEED, DELTA, first=rank * B + s, device=dev)
+        for f in synth.RRProblem.FIELDS:
+            getattr(prob, f)[s:e].copy_(getattr(p, f))
+        del p
+    stream = torch.cuda.current_stream(dev)
+    F, st = rr.rr_factor(prob)
+    sol = rr.rr_solve(prob, F)
+    nbs = rr.solve_workspace_bytes(NX, NU, HORIZON, B)
+    wsb = torch.empty((nbs + 7) // 8, dtype=torch.float64, device=dev)
+    res, norms = rr.rr_residual(prob, sol)
+    for _ in range(max(3, a.warmup)):
+        rr.rr_factor(prob, factor=F, status=st)
+        rr.rr_solve(prob, F, out=sol, workspace=wsb)
+        rr.rr_residual(prob, sol, res=res, norms=norms)
+    torch.cuda.synchronize()
+    assert int((st != 0).sum()) == 0 and int((sol["status"] != 0).sum()) == 0
+    E = lambda: torch.cuda.Event(enable_timing=True)
+    ev = {k: [(E(), E()) for _ in range(a.steps)] for k in ("factor", "solve", "residual")}
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier(ws)
+    torch.cuda.synchronize()
+    t0, t1 = E(), E()
+    t0.record(stream)
+    for k in range(a.steps):
+        ev["factor"][k][0].record(stream)
+        rr.rr_factor(prob, factor=F, status=st)
+        ev["factor"][k][1].record(stream)
+        ev["solve"][k][0].record(stream)
+        rr.rr_solve(prob, F, out=sol, workspace=wsb)
+        ev["solve"][k][1].record(stream)
+    t1.record(stream)
+    for k in range(a.steps):
+        ev["residual"][k][0].record(stream)
+        rr.rr_residual(prob, sol, res=res, norms=norms)
+        ev["residual"][k][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = clocks.stop()
+    ms = max_over_ranks(t0.elapsed_time(t1) / a.steps, ws)
+    kms = {k: statistics.mean(x.elapsed_time(y) for x, y in v) for k, v in ev.items()}
+    if rank != 0:
+        return
+    peak, src = measured_peaks()
+    per_stage = {"factor": 8 * (328 + 214), "solve": 8 * (220 + 214 + 16 + 214 + 204 + 16 + 28),
+                 "residual": 8 * (356 + 28 + 28)}
+    kern = {}
+    for k, b in per_stage.items():
+        ach = b * B * HORIZON / (kms[k] / 1e3) / 1e9
+        kern[k] = {"ms": kms[k], "alg_bytes_per_stage": b, "achieved_gbs": ach, "frac": ach / peak,
+                   "traffic": ncu_traffic("rr_split_%s_c2" % k)}
+    tot_b = (per_stage["factor"] + per_stage["solve"]) * B * HORIZON
+    ach = tot_b / (ms / 1e3) / 1e9
+    print(json.dumps({
+        "metric": METRIC + " (split API: rr_factor + rr_solve)", "value": B * ws / (ms / 1e3), "unit": "solves/s",
+        "n_gpus": ws, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 via rr_factor + rr_solve: %d random stable regularized LQR per GPU, n_x=%d n_u=%d "
+                               "N=%d delta=%g, FP64" % (B, NX, NU, HORIZON, DELTA),
+                   "l2": "inputs %.1f GB/GPU > 126 MB L2 (no flush needed)" % (prob.nbytes() / 1e9)},
+        "stage_updates_per_s": B * ws * HORIZON / (ms / 1e3),
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": None, "kernel": "rr_factor_kernel<12,4> + rr_solve_kernel<12,4>",
+                     "peak_source": src, "kernels": kern},
+        "clocks": clk, "e2e": None, "gpu_launches": 2 * a.steps}), flush=True)
 
 
 if __name__ == "__main__":
