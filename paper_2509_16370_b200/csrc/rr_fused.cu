@@ -347,7 +347,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   const int N = a.N;
 
   extern __shared__ __align__(16) double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle from lane 0: provably warp-uniform, so the TMA issue below
+  // (addresses from blockIdx, warp, stage) runs on uniform registers without a per-lane loop
+  const int warp = __shfl_sync(RR_FULL_MASK, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int grp = lane >> 4, j = lane & 15, gbase = grp * 16;
   double* slotq[2] = {smem + (warp * 2 + 0) * LY::SLOT_PAD, smem + (warp * 2 + 1) * LY::SLOT_PAD};
   double* slot = grp ? slotq[1] : slotq[0];
@@ -389,8 +391,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
                       validq[1] ? a.ws + instq[1] * sN * RC::PAD : nullptr};
   int32_t st = 0;
 
-  // stage inputs: TMA bulk copies issued by lane 0 of the group, completion on bar[0]
+  // stage inputs: TMA bulk copies for BOTH instances of the warp issued by lane 0, completion on
+  // each instance's bar[0] (records in the forward sweep: bar[0] / bar[1] by buffer)
   uint64_t* bar = reinterpret_cast<uint64_t*>(slot + LY::BAR);
+  uint64_t* barq[2] = {reinterpret_cast<uint64_t*>(slotq[0] + LY::BAR),
+                       reinterpret_cast<uint64_t*>(slotq[1] + LY::BAR)};
   if (j == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -402,18 +407,26 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   auto issue_stage = [&](int i, double* dst) {
     const int64_t s = inst * sN + i;
     if constexpr (LY::BULK) {
-      if (j == 0) {
+      if (lane == 0) {
         fence_proxy_async();
-        mbar_arrive_expect_tx(&bar[0], STG_BYTES);
-        bulk_g2s(dst + oA, a.p.A + s * n * n, 8 * n * n, &bar[0]);
-        bulk_g2s(dst + oB, a.p.B + s * n * m, 8 * n * m, &bar[0]);
-        bulk_g2s(dst + oQ, a.p.Q + s * sn, 8 * sn, &bar[0]);
-        bulk_g2s(dst + oM, a.p.M + s * n * m, 8 * n * m, &bar[0]);
-        bulk_g2s(dst + oR, a.p.R + s * sm, 8 * sm, &bar[0]);
-        bulk_g2s(dst + oq, a.p.q + s * n, 8 * n, &bar[0]);
-        bulk_g2s(dst + orr, a.p.r + s * m, 8 * m, &bar[0]);
-        bulk_g2s(dst + oc, a.p.c + s * n, 8 * n, &bar[0]);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int64_t sq = instq[q] * sN + i;
+          double* d = slotq[q];
+          uint64_t* bq = barq[q];
+          mbar_arrive_expect_tx(bq, STG_BYTES);
+          bulk_g2s(d + oA, a.p.A + sq * n * n, 8 * n * n, bq);
+          bulk_g2s(d + oB, a.p.B + sq * n * m, 8 * n * m, bq);
+          bulk_g2s(d + oQ, a.p.Q + sq * sn, 8 * sn, bq);
+          bulk_g2s(d + oM, a.p.M + sq * n * m, 8 * n * m, bq);
+          bulk_g2s(d + oR, a.p.R + sq * sm, 8 * sm, bq);
+          bulk_g2s(d + oq, a.p.q + sq * n, 8 * n, bq);
+          bulk_g2s(d + orr, a.p.r + sq * m, 8 * m, bq);
+          bulk_g2s(d + oc, a.p.c + sq * n, 8 * n, bq);
+        }
       }
+      (void)s;
+      (void)dst;
     } else {
       copy_async(dst + oA, a.p.A + s * n * n, n * n, j, 16);
       copy_async(dst + oB, a.p.B + s * n * m, n * m, j, 16);
@@ -535,11 +548,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   __syncwarp();
   auto issue_rec = [&](int i, double* dst, int b) {
     if constexpr (LY::BULK) {
-      if (j == 0) {
+      if (lane == 0) {
         fence_proxy_async();
-        mbar_arrive_expect_tx(&bar[b], 8u * RC::SIZE);
-        bulk_g2s(dst, rec0 + (int64_t)i * RC::PAD, 8u * RC::SIZE, &bar[b]);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          mbar_arrive_expect_tx(&barq[q][b], 8u * RC::SIZE);
+          bulk_g2s(slotq[q] + b * RC::PAD, a.ws + (instq[q] * sN + i) * RC::PAD, 8u * RC::SIZE, &barq[q][b]);
+        }
       }
+      (void)dst;
     } else {
       copy_async(dst, rec0 + (int64_t)i * RC::PAD, RC::SIZE, j, 16);
       cp_async_commit();
