@@ -44,6 +44,7 @@ typedef int32_t rr_err;
 #define RR_ST_NONFINITE 3    /* non-finite output without a pivot failure                 */
 #define RR_ST_NONPOS_SLACK 4 /* ipm_step: s <= 0 or z <= 0 on entry (P:53-59 needs log s)  */
 #define RR_ST_LS_FAILED 5    /* ipm_step: no Armijo point within max_backtracks           */
+#define RR_ST_MAXITER 6      /* ipm_solve: not converged within max_iters                */
 
 /* rr_dims.flags: RR_FLAG_ACCUMULATE makes rr_solve ADD its solution to sol (x += Δx, u += Δu,
  * y += Δy) instead of overwriting it -- the update step of iterative refinement with rr_residual.
@@ -293,6 +294,52 @@ int64_t ipm_workspace_bytes(const ipm_dims* dims);
 rr_err ipm_step(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it,
                 const ipm_params* params, const ipm_result* res, void* workspace, int64_t workspace_bytes,
                 int32_t* status, void* stream);
+
+/* ================================ batched IPM solve ================================
+ * ipm_solve: repeated ipm_step on every instance until its KKT residual meets the tolerance.  The
+ * paper fixes the step but not the outer loop; the loop is SPEC's ipm_solve /
+ * update_parameters (reading R21).  At iteration k, for every running instance:
+ *   evaluate the problem data at the iterate: costs quadratic with Hessian P and constraints linear
+ *     (exact from `data`, the evaluation at the INITIAL iterate, which serves as the model reference);
+ *     dynamics linear (IPM_MODEL_LQ) or the cart-pole model with its analytic Jacobians;
+ *   residuals r_stat = ||∇ₓL||∞ (∇ₓL = ∇f + Cᵀy + C_eᵀλ + Gᵀz), r_feas = max(||c||∞, ||c_e||∞, ||g+s||∞),
+ *     r_comp = ||Sz − μe||∞, r_comp0 = ||Sz||∞;
+ *   converged (status 0) if max(r_stat, r_feas, r_comp0) <= tol_kkt and μ <= 10 mu_min;
+ *   RR_ST_MAXITER if k == max_iters;
+ *   μ <- max(mu_min, min(kappa_mu μ, μ^theta_mu)) if max(r_stat, r_feas, r_comp) <= kappa μ;
+ *   η <- min(eta_max, kappa_eta η) if k >= 5, r_feas > tol_kkt and r_feas > 0.9 r_feas(k−5);
+ *   one ipm_step (rows a1-a8) with (μ, η, δ = 1/η); a failed step ends the instance with its status.
+ * Converged instances are masked out of later iterations (no host synchronisation: the step
+ * kernel runs over a device-built list of running instances).
+ * it: the iterate, updated in place (it->mu / it->eta are the initial values and are NOT written:
+ * the final μ, η are in the report).  report: any member may be NULL.
+ * workspace: >= ipm_solve_workspace_bytes(dims) device bytes, 256-byte aligned.
+ */
+typedef struct {
+  double mu_min;      /* 1e-9  */
+  double kappa;       /* 10    barrier-subproblem tolerance factor */
+  double kappa_mu;    /* 0.2   */
+  double theta_mu;    /* 1.5   */
+  double eta_max;     /* 1e8   */
+  double kappa_eta;   /* 10    */
+  double tol_kkt;     /* 1e-6  */
+  int32_t max_iters;  /* 100   */
+  int32_t pad;
+  ipm_params step;    /* line search of each step (tau, armijo_c, beta, max_backtracks) */
+} ipm_solve_settings;
+
+typedef struct {
+  int32_t* status;  /* [b] 0 converged, RR_ST_MAXITER, RR_ST_LS_FAILED, RR_ST_NONPOS_SLACK, pivot codes */
+  int32_t* iters;   /* [b] IPM steps taken                                                          */
+  double *mu, *eta; /* [b] final barrier / penalty parameters                                       */
+  double *r_stat, *r_feas, *r_comp; /* [b] residuals at the last evaluated iterate (r_comp = ||Sz||∞) */
+} ipm_solve_report;
+
+int64_t ipm_solve_workspace_bytes(const ipm_dims* dims);
+
+rr_err ipm_solve(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it,
+                 const ipm_solve_settings* settings, const ipm_solve_report* report, void* workspace,
+                 int64_t workspace_bytes, void* stream);
 
 /* Human-readable message of the last call-level error on this host thread. */
 const char* rr_last_error(void);

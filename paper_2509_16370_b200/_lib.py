@@ -66,6 +66,16 @@ class ipm_params(ctypes.Structure):
                 ("max_backtracks", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
+class ipm_solve_settings(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_double) for f in ("mu_min", "kappa", "kappa_mu", "theta_mu", "eta_max", "kappa_eta",
+                                               "tol_kkt")] + \
+               [("max_iters", ctypes.c_int32), ("pad", ctypes.c_int32), ("step", ipm_params)]
+
+
+class ipm_solve_report(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in ("status", "iters", "mu", "eta", "r_stat", "r_feas", "r_comp")]
+
+
 class ipm_result(ctypes.Structure):
     _fields_ = [(f, ctypes.c_void_p) for f in IPM_RES_FIELDS]
 
@@ -108,6 +118,12 @@ def lib():
                                       ctypes.POINTER(rr_residual_buf), ctypes.c_void_p, ctypes.c_void_p]
             L.ipm_workspace_bytes.restype = ctypes.c_int64
             L.ipm_workspace_bytes.argtypes = [ctypes.POINTER(ipm_dims)]
+            L.ipm_solve_workspace_bytes.restype = ctypes.c_int64
+            L.ipm_solve_workspace_bytes.argtypes = [ctypes.POINTER(ipm_dims)]
+            L.ipm_solve.restype = ctypes.c_int32
+            L.ipm_solve.argtypes = [ctypes.POINTER(ipm_dims), ctypes.POINTER(ipm_stage_data), ctypes.POINTER(ipm_iterate),
+                                    ctypes.POINTER(ipm_solve_settings), ctypes.POINTER(ipm_solve_report),
+                                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
             L.ipm_step.restype = ctypes.c_int32
             L.ipm_step.argtypes = [ctypes.POINTER(ipm_dims), ctypes.POINTER(ipm_stage_data),
                                    ctypes.POINTER(ipm_iterate), ctypes.POINTER(ipm_params),

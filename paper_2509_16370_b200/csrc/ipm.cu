@@ -121,8 +121,16 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   double* xs = rbuf + 2 * RC::PAD;
 
   int64_t inst = ((int64_t)blockIdx.x * WARPS + warp) * IPW + grp;
-  const bool valid = inst < a.d.batch;
-  if (!valid) inst = a.d.batch - 1;
+  bool valid;
+  if (a.list != nullptr) {  // ipm_solve: only the instances on the device-built active list
+    const int64_t cnt = *a.count;
+    if ((int64_t)blockIdx.x * WARPS * IPW >= cnt) return;  // whole CTA past the list (uniform exit)
+    valid = inst < cnt;
+    inst = a.list[valid ? inst : 0];
+  } else {
+    valid = inst < a.d.batch;
+    if (!valid) inst = a.d.batch - 1;
+  }
   const int64_t sN = N;
   const double mu = a.it.mu[inst], eta = a.it.eta[inst];
   const double delta = 1.0 / eta;  // P:387-394 (reading R15)
@@ -754,6 +762,10 @@ int64_t ipm_ws_bytes(const ipm_dims& d) {
     return true;
   });
   return out;
+}
+
+bool ipm_supported(const ipm_dims& d) {
+  return dispatch_ipm(d, [](auto) { return true; });
 }
 
 cudaError_t ipm_launch(const IpmArgs& a, cudaStream_t s, bool* supported) {

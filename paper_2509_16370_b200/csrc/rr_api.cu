@@ -5,6 +5,7 @@
 
 #include "rr.h"
 #include "ipm.cuh"
+#include "ipm_solve.cuh"
 #include "rr_fused.cuh"
 #include "rr_split.cuh"
 
@@ -279,6 +280,40 @@ rr_err ipm_step(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iter
   cudaError_t e = rrk::ipm_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "ipm_step: unsupported dims%s");
   if (e != cudaSuccess) return set_err(RR_E_CUDA, "ipm_step: CUDA error %s", cudaGetErrorString(e));
+  return RR_OK;
+}
+
+int64_t ipm_solve_workspace_bytes(const ipm_dims* dims) {
+  if (!ipm_dims_ok(dims)) return -1;
+  return rrk::ipm_solve_ws_bytes(*dims);
+}
+
+rr_err ipm_solve(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it,
+                 const ipm_solve_settings* S, const ipm_solve_report* rep, void* workspace, int64_t workspace_bytes,
+                 void* stream) {
+  if (!ipm_dims_ok(dims)) return set_err(RR_E_INVALID, "ipm_solve: invalid dims%s");
+  if (!data || !it || !S || !rep) return set_err(RR_E_INVALID, "ipm_solve: null %s", "argument");
+  if (dims->batch == 0) return RR_OK;
+  const ipm_params& p = S->step;
+  if (!(p.tau > 0.0 && p.tau < 1.0) || !(p.armijo_c > 0.0 && p.armijo_c < 0.5) || !(p.beta > 0.0 && p.beta < 1.0) ||
+      p.max_backtracks < 0 || S->max_iters < 0 || !(S->mu_min > 0.0) || !(S->kappa_mu > 0.0 && S->kappa_mu < 1.0) ||
+      !(S->theta_mu > 1.0) || !(S->tol_kkt > 0.0) || !(S->kappa > 0.0) || !(S->kappa_eta >= 1.0) || !(S->eta_max > 0.0))
+    return set_err(RR_E_INVALID, "ipm_solve: invalid %s", "settings");
+  if (dims->batch > 0x7fffffffLL) return set_err(RR_E_INVALID, "ipm_solve: batch above %s", "2^31-1");
+  const int64_t need = ipm_solve_workspace_bytes(dims);
+  if (need < 0) return set_err(RR_E_UNSUPPORTED, "ipm_solve: no kernel compiled for these dims/model%s");
+  if (workspace == nullptr || workspace_bytes < need)
+    return set_err(RR_E_INVALID, "ipm_solve: workspace missing or smaller than %s", "ipm_solve_workspace_bytes()");
+  if (!data->s0 || !data->fval || !data->gradfN || !data->QN || !it->x || !it->y || !it->mu || !it->eta ||
+      (dims->N > 0 && (!data->gradf || !data->Q || !data->M || !data->R || !data->A || !data->B || !data->dres || !it->u)))
+    return set_err(RR_E_INVALID, "ipm_solve: null %s", "required pointer");
+  if (dims->model == IPM_MODEL_CARTPOLE && data->model_params == nullptr)
+    return set_err(RR_E_INVALID, "ipm_solve: cart-pole model needs %s", "model_params");
+  bool supported = false;
+  cudaError_t e = rrk::ipm_solve_launch(*dims, *data, *it, *S, *rep, workspace, static_cast<cudaStream_t>(stream),
+                                        &supported);
+  if (!supported) return set_err(RR_E_UNSUPPORTED, "ipm_solve: unsupported dims%s");
+  if (e != cudaSuccess) return set_err(RR_E_CUDA, "ipm_solve: CUDA error %s", cudaGetErrorString(e));
   return RR_OK;
 }
 

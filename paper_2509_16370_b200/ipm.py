@@ -7,7 +7,7 @@ import ctypes
 import torch
 
 from ._lib import (IPM_DATA_FIELDS, IPM_ITER_FIELDS, IPM_RES_FIELDS, RRError, check, ipm_dims, ipm_iterate,
-                   ipm_params, ipm_result, ipm_stage_data, lib)
+                   ipm_params, ipm_result, ipm_solve_report, ipm_solve_settings, ipm_stage_data, lib)
 
 RES_SHAPE_OF = dict(dx="x", du="u", ds="s", dsN="sN", dy="y", dlam="lam", dlamN="lamN", dz="z", dzN="zN")
 
@@ -72,3 +72,47 @@ def ipm_step(b, tau=0.995, armijo_c=1e-4, beta=0.5, max_backtracks=50, stream=No
     """One regularized-IPM step for every instance of the IPMBatch `b` (CUDA tensors); the iterate
     b.it is updated in place.  Returns the result dict (direction, α_p, α_d, D, 𝒜(0), 𝒜(α), k, status)."""
     return IpmCall(b, tau=tau, armijo_c=armijo_c, beta=beta, max_backtracks=max_backtracks).launch(stream)
+
+
+SOLVE_DEFAULTS = dict(mu_min=1e-9, kappa=10.0, kappa_mu=0.2, theta_mu=1.5, eta_max=1e8, kappa_eta=10.0,
+                      tol_kkt=1e-6, max_iters=100, tau=0.995, armijo_c=1e-4, beta=0.5, max_backtracks=50)
+REPORT_FIELDS = ("status", "iters", "mu", "eta", "r_stat", "r_feas", "r_comp")
+
+
+class IpmSolveCall:
+    """Pre-marshalled ipm_solve launch (the batched IPM loop) on fixed buffers.
+    b.data is the evaluation at the initial iterate (the model reference); b.it is updated in place."""
+
+    def __init__(self, b, ws=None, **settings):
+        S = dict(SOLVE_DEFAULTS)
+        S.update(settings)
+        self.b = b
+        dev = b.it["mu"].device
+        self.d = dims_of(b)
+        nb = lib().ipm_solve_workspace_bytes(ctypes.byref(self.d))
+        if nb < 0:
+            raise RRError("no ipm_solve kernel compiled for these dims/model")
+        self.ws = ws if ws is not None else torch.empty((nb + 7) // 8, dtype=torch.float64, device=dev)
+        self.data = ipm_stage_data(*[_p(b.data[f]) for f in IPM_DATA_FIELDS])
+        self.it = ipm_iterate(*[_p(b.it[f]) for f in IPM_ITER_FIELDS])
+        self.S = ipm_solve_settings(S["mu_min"], S["kappa"], S["kappa_mu"], S["theta_mu"], S["eta_max"],
+                                    S["kappa_eta"], S["tol_kkt"], int(S["max_iters"]), 0,
+                                    ipm_params(S["tau"], S["armijo_c"], S["beta"], int(S["max_backtracks"]), 0))
+        self.rep = {k: torch.empty(b.batch, dtype=torch.int32 if k in ("status", "iters") else torch.float64, device=dev)
+                    for k in REPORT_FIELDS}
+        self.r = ipm_solve_report(*[_p(self.rep[k]) for k in REPORT_FIELDS])
+        self.wsp, self.wsb = _p(self.ws), self.ws.numel() * 8
+
+    def launch(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.b.it["mu"].device)
+        rc = lib().ipm_solve(ctypes.byref(self.d), ctypes.byref(self.data), ctypes.byref(self.it), ctypes.byref(self.S),
+                             ctypes.byref(self.r), self.wsp, self.wsb, ctypes.c_void_p(s.cuda_stream))
+        check(rc, "ipm_solve")
+        return self.rep
+
+
+def ipm_solve(b, stream=None, **settings):
+    """Solve every instance of the IPMBatch `b` (CUDA tensors; data evaluated at the initial
+    iterate) with the batched regularized IPM; b.it is updated in place.  Returns the report
+    (status, iters, mu, eta, r_stat, r_feas, r_comp)."""
+    return IpmSolveCall(b, **settings).launch(stream)

@@ -212,3 +212,37 @@ def cartpole_c4(batch, seed=2511, N=100, variant="C4", mu=0.1, eta=1e4, first=0,
     data = {k2: v.contiguous() for k2, v in data.items()}
     it = {k2: v.contiguous() for k2, v in it.items()}
     return IPMBatch(n, m, N, 4, 2, 0, 0, MODEL_CARTPOLE, data, it)
+
+
+# ----------------------------------------------------------------------------- double integrator OCP
+def double_integrator_ocp(batch=1, N=20, h=0.1, x0=(5.0, 0.0), umax=1.0, q=1.0, r=0.1, qN=10.0, mu=0.1, eta=1e4,
+                          device="cpu") -> IPMBatch:
+    """SPEC's end-to-end OCP example (acceptance 6): double integrator A = [[1,h],[0,1]],
+    B = [h²/2, h] (S:324), N = 20, h = 0.1, x₀ = (5, 0), |u| <= umax as u − umax <= 0, −u − umax <= 0,
+    cost ½ Σ (q|x_i|² + r u_i²) + ½ qN |x_N|² (model LQ).  Iterate x̄ = 0, ū = 0, s = max(−g, 1e-2),
+    z = μ/s, y = 0, μ₀ = 0.1 (SPEC Design Decisions); η₀ = 1e4 as in C1/C4 (SPEC's 1e2 needs ~100
+    iterations under its own η rule: DESIGN.md reading R21).  All instances identical."""
+    dev = torch.device(device)
+    n, m, k = 2, 1, 3
+    A = torch.tensor([[1.0, h], [0.0, 1.0]], dtype=torch.float64, device=dev)
+    B = torch.tensor([[h * h / 2], [h]], dtype=torch.float64, device=dev)
+    P = torch.diag(torch.tensor([q, q, r], dtype=torch.float64, device=dev))
+    G = torch.tensor([[0.0, 0.0, 1.0], [0.0, 0.0, -1.0]], dtype=torch.float64, device=dev)
+    rep = lambda t, *s: t.reshape(-1).expand(*s, t.numel()).contiguous()
+    gv = torch.full((batch, N, 2), -umax, dtype=torch.float64, device=dev)
+    s = torch.clamp(-gv, min=1e-2)
+    data = dict(s0=torch.tensor(x0, dtype=torch.float64, device=dev).expand(batch, n).contiguous(),
+                fval=_zeros(batch, device=dev), gradf=_zeros(batch, N, k, device=dev), gradfN=_zeros(batch, n, device=dev),
+                Q=rep(pack_lower(P[:n, :n]), batch, N), M=_zeros(batch, N, n * m, device=dev),
+                R=rep(pack_lower(P[n:, n:]), batch, N), QN=rep(pack_lower(qN * torch.eye(n, dtype=torch.float64, device=dev)), batch),
+                A=rep(colmajor(A), batch, N), B=rep(colmajor(B), batch, N), dres=_zeros(batch, N, n, device=dev),
+                ce=_zeros(batch, N, 0, device=dev), Ce=_zeros(batch, N, 0, device=dev),
+                ceN=_zeros(batch, 0, device=dev), CeN=_zeros(batch, 0, device=dev),
+                gv=gv, Gj=rep(colmajor(G), batch, N), gvN=_zeros(batch, 0, device=dev), GjN=_zeros(batch, 0, device=dev),
+                model_params=_zeros(N_MODEL_PARAMS, device=dev))
+    it = dict(x=_zeros(batch, N + 1, n, device=dev), u=_zeros(batch, N, m, device=dev), s=s, z=mu / s,
+              sN=_zeros(batch, 0, device=dev), zN=_zeros(batch, 0, device=dev), y=_zeros(batch, N + 1, n, device=dev),
+              lam=_zeros(batch, N, 0, device=dev), lamN=_zeros(batch, 0, device=dev),
+              mu=torch.full((batch,), float(mu), dtype=torch.float64, device=dev),
+              eta=torch.full((batch,), float(eta), dtype=torch.float64, device=dev))
+    return IPMBatch(n, m, N, 2, 0, 0, 0, MODEL_LQ, data, it)
