@@ -42,11 +42,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample wall time")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5", "split"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5", "split", "c4solve"],
                     help="c2 (default, BASELINE configs[1]); c3 = 4,096 dense n64 m32 N50 (configs[2]); "
                          "c4 = ipm_step on 16,384 cart-pole instances (configs[3]); c5 = 1,048,576 "
                          "quadrotor n12 m4 N200 sharded over the ranks, chunks of 65,536 (configs[4]); split = "
-                         "rr_factor + rr_solve + rr_residual on the C2 workload, each kernel timed")
+                         "rr_factor + rr_solve + rr_residual on the C2 workload, each kernel timed; c4solve = ipm_solve "
+                         "(20 IPM iterations) on the C4 cart-pole batch")
     ap.add_argument("--c5-total", type=int, default=1048576, help=argparse.SUPPRESS)
     return ap.parse_args()
 
@@ -223,6 +224,8 @@ def main():
         return run_c5(a, ws, rank, local)
     if a.workload == "split":
         return run_split(a, ws, rank, local)
+    if a.workload == "c4solve":
+        return run_c4solve(a, ws, rank, local)
     global NX, NU, HORIZON, BATCH, SEED, ALG_BYTES_PER_STAGE, ALG_FLOPS_PER_STAGE
     if a.workload == "c3":
         # 206,208 B and 2.42M flop per stage (algorithmic)
@@ -570,6 +573,65 @@ def run_split(a, ws, rank, local):
                      "traffic": None, "kernel": "rr_factor_kernel<12,4> + rr_solve_kernel<12,4>",
                      "peak_source": src, "kernels": kern},
         "clocks": clk, "e2e": None, "gpu_launches": 2 * a.steps}), flush=True)
+
+
+def run_c4solve(a, ws, rank, local):
+    """Extra line: ipm_solve (the batched IPM loop) on the C4 cart-pole batch, 16,384
+    instances per GPU, N = 100, a fixed budget of 20 IPM iterations (the nonconvex swing-up does not
+    converge within it, so every instance runs all 20: a fixed amount of work per step).  Each
+    timed step solves a fresh device copy of the same initial iterate.  Per iteration and stage the
+    loop moves the ipm_step bytes (~1.9 KB) plus the evaluation / residual passes
+    (~0.9 KB); the roofline uses 2.8 KB per (instance, stage, iteration)."""
+    import copy
+    import torch
+    import paper_2509_16370_b200 as rr
+    from synth.ipm_workloads import cartpole_c4
+    dev = torch.device("cuda", local)
+    B, Nh, IT = 16384, 100, 20
+    b = cartpole_c4(B, seed=2511, N=Nh, first=rank * B, device=dev)
+    call0 = rr.IpmSolveCall(b, max_iters=IT)
+
+    def fresh():
+        bk = copy.copy(b)
+        bk.it = {k: v.clone() for k, v in b.it.items()}
+        return rr.IpmSolveCall(bk, ws=call0.ws, max_iters=IT)
+    nw = max(3, a.warmup)
+    calls = [fresh() for _ in range(nw + a.steps)]
+    stream = torch.cuda.current_stream(dev)
+    for k in range(nw):
+        calls[k].launch(stream)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    clocks = ClockSampler(local)
+    barrier(ws)
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    for k in range(a.steps):
+        ev[k][0].record(stream)
+        rep = calls[nw + k].launch(stream)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = clocks.stop()
+    ms = max_over_ranks(sum(s_.elapsed_time(e_) for s_, e_ in ev) / a.steps, ws)
+    iters = int(rep["iters"].sum())
+    if rank == 0:
+        alg = 2800 * Nh * iters
+        peak, src = measured_peaks()
+        print(json.dumps({
+            "metric": "regularized-IPM solve: instance-iterations/s (C4 cart-pole, ipm_solve, 20 iterations)",
+            "value": iters * ws / (ms / 1e3), "unit": "instance-iterations/s", "n_gpus": ws, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C4 ipm_solve: %d cart-pole instances per GPU, N=%d, max_iters=%d" % (B, Nh, IT),
+                       "l2": "stage data 3.1 GB/GPU > 126 MB L2 (no flush needed)"},
+            "solves_per_s": B * ws / (ms / 1e3), "iterations_total": iters,
+            "status_counts": {str(int(k)): int(v) for k, v in zip(*torch.unique(rep["status"], return_counts=True))},
+            "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": None,
+                         "alg_bytes_per_stage_iteration": 2800, "peak_source": src},
+            "clocks": clk, "gpu_launches": a.steps * (4 * IT + 3)}), flush=True)
 
 
 if __name__ == "__main__":
