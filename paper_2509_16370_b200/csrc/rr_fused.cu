@@ -483,6 +483,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
 #else
     auto P2 = [&](int q, int k) -> double {
       const int off = ptab[lane * LY::PTAB + k];
+      if constexpr ((NX + NU) % 8 == 0) return sbq[q][off];  // every fragment position inside P
       return off >= 0 ? sbq[q][off] : 0.0;
     };
     (void)Pat;
@@ -493,8 +494,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     };
     double* recq[2] = {rec0q[0] ? rec0q[0] + (int64_t)i * RC::PAD : nullptr,
                        rec0q[1] ? rec0q[1] + (int64_t)i * RC::PAD : nullptr};
-    double U[NZ], b[NZ];
-    SM::backward(wkq, Fq, cvq, P2, qjf, wait_inputs, prefetch, delta, grp, j, lane, Vc, U, b, recq, i, st);
+    double U[NZ], bj;
+    SM::backward(wkq, Fq, cvq, P2, qjf, wait_inputs, prefetch, delta, grp, j, lane, Vc, U, bj, recq, i, st);
     if (valid) {
       if (a.f.V != nullptr && j < n) {
         double* Vo = a.f.V + (inst * (sN + 1) + i) * sn;
@@ -507,16 +508,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
 #pragma unroll
         for (int u = 0; u < NU; ++u) Ko[j * m + u] = -U[NX + u];
       }
-      if (j == 0 && a.f.v != nullptr) {
-        double* vo = a.f.v + (inst * (sN + 1) + i) * n;
-#pragma unroll
-        for (int r = 0; r < NX; ++r) vo[r] = b[r];
-      }
-      if (j == 0 && a.f.k != nullptr) {
-        double* ko = a.f.k + (inst * sN + i) * m;
-#pragma unroll
-        for (int u = 0; u < NU; ++u) ko[u] = -b[NX + u];
-      }
+      if (j < NX && a.f.v != nullptr) a.f.v[(inst * (sN + 1) + i) * n + j] = bj;
+      if (j >= NX && j < NX + NU && a.f.k != nullptr) a.f.k[(inst * sN + i) * m + (j - NX)] = -bj;
     }
   }
 

@@ -67,7 +67,8 @@ struct WorkM {
   static constexpr int X2 = X1 + X1SZ;          // W (ld NX, NX+1 cols), then U (ld ULD)
   static constexpr int ULD = 18;                // U leading dimension: conflict-free C-fragment stores
   static constexpr int E = X2 + 16 * ULD;       // e = c_{i+1} − δ v_{i+1} (NX, even)
-  static constexpr int SIZE = E + ((NX + 1) & ~1);
+  static constexpr int BP = E + ((NX + 1) & ~1);  // 2 publish slots for b_p in the u-block elimination
+  static constexpr int SIZE = BP + 2;
   static constexpr int PAD = (SIZE + 1) & ~1;
 };
 
@@ -95,7 +96,7 @@ struct StageMMA {
                                                   const double* const (&cvq)[2], PFun&& Pat, QFun&& qjf,
                                                   WaitFn&& wait_inputs, PrefFn&& prefetch, double delta, int grp,
                                                   int j, int lane, double (&Vc)[NX], double (&U)[NZ],
-                                                  double (&b)[NZ], double* const (&recq)[2], int stage,
+                                                  double& bj, double* const (&recq)[2], int stage,
                                                   int32_t& st) {
     double* wk = grp ? wkq[1] : wkq[0];
     const double* F = grp ? Fq[1] : Fq[0];
@@ -172,7 +173,7 @@ struct StageMMA {
         b0 = fma(f2.x, gk[k], b0);
         b1 = fma(f2.y, gk[k + 1], b1);
       }
-      if (j < NZ) wk[WK::vb + j] = b0 + b1;
+      bj = b0 + b1;  // lane j owns entry j of b (distributed, not replicated)
     }
     // (4) T = W F (NX × NZ) -> X1 (ld NX)
 #pragma unroll
@@ -265,8 +266,10 @@ struct StageMMA {
       U[s] = (j < NZ) ? u2.x : 0.0;
       U[s + 1] = (j < NZ) ? u2.y : 0.0;
     }
-#pragma unroll
-    for (int s = 0; s < NZ; ++s) b[s] = wk[WK::vb + s];
+    // b is distributed: lane j updates its own entry b_j with the pivot-column entry of row j
+    // (own U[p] by symmetry, or lane p's published row for already processed pivots) and the
+    // published b_p
+    bool gbad = false;
 #pragma unroll
     for (int p = NX; p < NZ; ++p) {
       double* pb = wk + WK::pub + (p & 1) * WK::NZP;
@@ -274,33 +277,38 @@ struct StageMMA {
       if (j == p) {
 #pragma unroll
         for (int qq = NX; qq < p; ++qq) wk[WK::pq + (qq - NX)] = U[qq];
+        wk[WM::BP + (p & 1)] = bj;
       }
       __syncwarp();
       double col[NZ];
 #pragma unroll
       for (int s = 0; s < NZ; ++s) col[s] = (s >= NX && s < p) ? wk[WK::pq + (s - NX)] : pb[s];
+      const double cj = (j >= NX && j < p) ? wk[WK::pq + (j - NX)] : U[p];  // pivot-column entry of row j
       const double piv = col[p];
-      if (!(piv > 0.0) && st == 0) st = mk_status(RR_ST_G_NOT_PD, stage);
+      gbad |= !(piv > 0.0);
       const double ip = rcp_nr(piv);
       const double rp = U[p] * ip;
-      const double bp = b[p] * ip;
+      const double bp = wk[WM::BP + (p & 1)] * ip;
 #pragma unroll
       for (int s = 0; s < NZ; ++s) {
         if (s == p) continue;
         U[s] = fma(-col[s], rp, U[s]);
-        b[s] = fma(-col[s], bp, b[s]);
       }
       U[p] = rp;
-      b[p] = bp;
+      bj = (j == p) ? bp : fma(-cj, bp, bj);
       __syncwarp();
     }
+    if (gbad && st == 0) st = mk_status(RR_ST_G_NOT_PD, stage);
+    // lanes j < NX: U = [V_i; −K_i] column j, bj = (v_i)_j;  lanes NX + u: bj = −(k_i)_u
+    if (j < NZ) wk[WK::vb + j] = bj;
+    __syncwarp();
     // (7) M = [A + B K | B k + c − δ v] -> X1 (ld NX, NX+1 columns)
     if (j <= NX) {
       double tcol[NX];
       ST::bcast((j < NX) ? F + jc * NX : wk + WM::E, tcol);  // column j of A, or e for the φ column
 #pragma unroll
       for (int u = 0; u < NU; ++u) {
-        const double coef = (j < NX) ? -U[NX + u] : -b[NX + u];
+        const double coef = (j < NX) ? -U[NX + u] : -wk[WK::vb + NX + u];
         const double* Fu = F + (NX + u) * NX;
 #pragma unroll
         for (int r = 0; r < NX; r += 2) {
@@ -360,20 +368,15 @@ struct StageMMA {
 #pragma unroll
         for (int r = 0; r < NX; ++r)
           if (r >= j) Vp[r] = U[r];
-      } else if (j == NX) {
-#pragma unroll
-        for (int r = 0; r < NX; ++r) rec[RC::v + r] = b[r];
-#pragma unroll
-        for (int u = 0; u < NU; ++u) rec[RC::k + u] = -b[NX + u];
+        rec[RC::v + j] = bj;
+      } else if (j < NZ) {
+        rec[RC::k + (j - NX)] = -bj;
       }
     }
 #pragma unroll
     for (int r = 0; r < NX; ++r) Vc[r] = (j < NX) ? U[r] : 0.0;
     __syncwarp();
-    if (j == 0) {
-#pragma unroll
-      for (int r = 0; r < NX; ++r) wk[WK::vs + r] = b[r];
-    }
+    if (j < NX) wk[WK::vs + j] = bj;
     __syncwarp();
   }
 };
