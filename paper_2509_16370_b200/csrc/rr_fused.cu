@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
         else if (c < NX) off = oM + c + (s - NX) * n;
         else off = oR + (s >= c ? pidx(m, s - NX, c - NX) : pidx(m, c - NX, s - NX));
       }
-      ptab[lane * LY::PTAB + k] = off;
+      ptab[k * 32 + lane] = off;  // [position][lane]: consecutive lanes, conflict-free
     }
   }
   __syncthreads();
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     auto P2 = [&](int q, int s, int t) -> double { return Pat(sbq[q], s, t); };
 #else
     auto P2 = [&](int q, int k) -> double {
-      const int off = ptab[lane * LY::PTAB + k];
+      const int off = ptab[k * 32 + lane];
       if constexpr ((NX + NU) % 8 == 0) return sbq[q][off];  // every fragment position inside P
       return off >= 0 ? sbq[q][off] : 0.0;
     };
