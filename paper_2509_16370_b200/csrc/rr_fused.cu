@@ -332,7 +332,9 @@ struct MmaLayout {
                                RecM<NX, NU>::SIZE % 2 == 0;
 };
 
-template <int NX, int NU, int WARPS, int MINB>
+// FAC = true: rr_factor (the matrix half only): stage loads of A, B, Q, M, R, factor records
+// [V_i | S_i⁻¹ | K_i | G_i⁻¹] to a.frec (rr_split.cuh layout), no forward sweep.
+template <int NX, int NU, int WARPS, int MINB, bool FAC = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const FusedArgs a) {
   using LY = MmaLayout<NX, NU>;
   using SM = StageMMA<NX, NU>;
@@ -403,7 +405,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncwarp();
   uint32_t ph0 = 0, ph1 = 0;
-  constexpr uint32_t STG_BYTES = 8u * (n * n + 2 * n * m + sn + sm + 2 * n + m);
+  constexpr uint32_t STG_BYTES = 8u * (n * n + 2 * n * m + sn + sm + (FAC ? 0 : 2 * n + m));
+  constexpr int FREC = (NX * (NX + 1) + NX * NU + NU * (NU + 1) / 2 + 1) & ~1;  // factor record doubles
+  if constexpr (FAC) {  // no right-hand side: q, r, c slots of the stage buffers stay zero
+    for (int e = j; e < 2 * n + m; e += 16) slot[oq + e] = 0.0;
+  }
   auto issue_stage = [&](int i, double* dst) {
     const int64_t s = inst * sN + i;
     if constexpr (LY::BULK) {
@@ -420,9 +426,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
           bulk_g2s(d + oQ, a.p.Q + sq * sn, 8 * sn, bq);
           bulk_g2s(d + oM, a.p.M + sq * n * m, 8 * n * m, bq);
           bulk_g2s(d + oR, a.p.R + sq * sm, 8 * sm, bq);
-          bulk_g2s(d + oq, a.p.q + sq * n, 8 * n, bq);
-          bulk_g2s(d + orr, a.p.r + sq * m, 8 * m, bq);
-          bulk_g2s(d + oc, a.p.c + sq * n, 8 * n, bq);
+          if constexpr (!FAC) {
+            bulk_g2s(d + oq, a.p.q + sq * n, 8 * n, bq);
+            bulk_g2s(d + orr, a.p.r + sq * m, 8 * m, bq);
+            bulk_g2s(d + oc, a.p.c + sq * n, 8 * n, bq);
+          }
         }
       }
       (void)s;
@@ -462,13 +470,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     const double* QN = a.p.QN + inst * sn;
 #pragma unroll
     for (int r = 0; r < NX; ++r) Vc[r] = (j < n) ? (r >= j ? QN[pidx(n, r, j)] : QN[pidx(n, j, r)]) : 0.0;
-    if (j < NX) wk[WK::vs + j] = a.p.qN[inst * n + j];
+    if (j < NX) wk[WK::vs + j] = FAC ? 0.0 : a.p.qN[inst * n + j];
+    if (FAC && valid && j < n)  // record N: V_N = Q_N
+      for (int r = j; r < n; ++r) a.frec[inst * (sN + 1) * FREC + sN * FREC + pidx(n, r, j)] = QN[pidx(n, r, j)];
     if (valid && a.f.V != nullptr && j < n) {
       double* Vo = a.f.V + (inst * (sN + 1) + N) * sn;
       for (int r = j; r < n; ++r) Vo[pidx(n, r, j)] = QN[pidx(n, r, j)];
     }
-    if (valid && a.f.v != nullptr && j < n) a.f.v[(inst * (sN + 1) + N) * n + j] = a.p.qN[inst * n + j];
+    if (!FAC && valid && a.f.v != nullptr && j < n) a.f.v[(inst * (sN + 1) + N) * n + j] = a.p.qN[inst * n + j];
   }
+  __syncwarp();  // (FAC) zeroed rhs slots visible before the first stage
   if (N > 0) issue_stage(N - 1, slot);
   __syncwarp();
 
@@ -492,10 +503,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     auto prefetch = [&]() {
       if (i > 0) issue_stage(i - 1, slot);
     };
-    double* recq[2] = {rec0q[0] ? rec0q[0] + (int64_t)i * RC::PAD : nullptr,
-                       rec0q[1] ? rec0q[1] + (int64_t)i * RC::PAD : nullptr};
+    double* recq[2];
+    if constexpr (FAC) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) recq[q] = validq[q] ? a.frec + (instq[q] * (sN + 1) + i) * FREC : nullptr;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) recq[q] = rec0q[q] ? rec0q[q] + (int64_t)i * RC::PAD : nullptr;
+    }
     double U[NZ], bj;
-    SM::backward(wkq, Fq, cvq, P2, qjf, wait_inputs, prefetch, delta, grp, j, lane, Vc, U, bj, recq, i, st);
+    SM::template backward<FAC>(wkq, Fq, cvq, P2, qjf, wait_inputs, prefetch, delta, grp, j, lane, Vc, U, bj, recq,
+                               i, st);
     if (valid) {
       if (a.f.V != nullptr && j < n) {
         double* Vo = a.f.V + (inst * (sN + 1) + i) * sn;
@@ -508,9 +526,29 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
 #pragma unroll
         for (int u = 0; u < NU; ++u) Ko[j * m + u] = -U[NX + u];
       }
-      if (j < NX && a.f.v != nullptr) a.f.v[(inst * (sN + 1) + i) * n + j] = bj;
-      if (j >= NX && j < NX + NU && a.f.k != nullptr) a.f.k[(inst * sN + i) * m + (j - NX)] = -bj;
+      if (!FAC && j < NX && a.f.v != nullptr) a.f.v[(inst * (sN + 1) + i) * n + j] = bj;
+      if (!FAC && j >= NX && j < NX + NU && a.f.k != nullptr) a.f.k[(inst * sN + i) * m + (j - NX)] = -bj;
     }
+  }
+  if constexpr (FAC) {  // S_0⁻¹ -> record 0; status; NaN-fill a failed instance's records
+    ST::invS(Vc, delta, j, wk, 0, st);
+    double* rec = a.frec + inst * (sN + 1) * FREC;
+    if (valid && j < n)
+      for (int r = j; r < n; ++r) rec[sn + pidx(n, r, j)] = wk[WK::Si + r * NX + j];
+    int32_t status = st;
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) {
+      const int32_t o = __shfl_xor_sync(RR_FULL_MASK, status, off);
+      status = o > status ? o : status;
+    }
+    __syncwarp();
+    if (valid && status != 0) {
+      const double nan = __longlong_as_double(0x7ff8000000000000LL);
+      for (int64_t e = j; e < (sN + 1) * FREC; e += 16) rec[e] = nan;
+    }
+    if (valid && j == 0) a.status[inst] = status;
+    (void)gbase;
+    return;
   }
 
   // x_0 = (I + δV_0)⁻¹ (c_0 − δ v_0)
@@ -644,7 +682,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   if (valid && j == 0) a.status[inst] = status;
 }
 
-template <int NX, int NU, int WARPS, int MINB>
+template <int NX, int NU, int WARPS, int MINB, bool FAC = false>
 struct MmaCfg {
   static constexpr int IPB = WARPS * 2;
   static size_t smem_bytes() {
@@ -652,7 +690,7 @@ struct MmaCfg {
   }
   static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * RecM<NX, NU>::PAD; }
   static cudaError_t launch(const FusedArgs& a, cudaStream_t s) {
-    auto k = rr_fused_mma_kernel<NX, NU, WARPS, MINB>;
+    auto k = rr_fused_mma_kernel<NX, NU, WARPS, MINB, FAC>;
     const size_t sm = smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
@@ -710,4 +748,13 @@ cudaError_t fused_launch(const FusedArgs& a, cudaStream_t s, bool* supported) {
   return err;
 }
 
+}  // namespace rrk
+
+namespace rrk {
+// rr_factor for the 12x4 shape on the DMMA stage kernel (factor-only mode).
+cudaError_t factor_mma_launch(const FusedArgs& a, cudaStream_t s, bool* supported) {
+  *supported = (a.nx == 12 && a.nu == 4);
+  if (!*supported) return cudaSuccess;
+  return MmaCfg<12, 4, 4, 3, true>::launch(a, s);
+}
 }  // namespace rrk

@@ -15,11 +15,14 @@ struct FusedArgs {
   rr_solution s;
   double* ws;
   int32_t* status;
+  double* frec = nullptr;  // rr_factor on the DMMA kernel: factor records [batch][N+1][frec_doubles]
 };
 
 // Bytes of workspace for this shape (-1 if no kernel is compiled for it).
 int64_t fused_workspace_bytes(int nx, int nu, int N, int64_t batch);
 // Launch on stream s; *supported = false if no kernel covers (nx, nu).
 cudaError_t fused_launch(const FusedArgs& a, cudaStream_t s, bool* supported);
+// rr_factor on the DMMA stage kernel (factor-only mode); *supported = false outside its shapes.
+cudaError_t factor_mma_launch(const FusedArgs& a, cudaStream_t s, bool* supported);
 
 }  // namespace rrk

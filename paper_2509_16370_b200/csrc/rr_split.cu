@@ -25,9 +25,12 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "rr_common.cuh"
 #include "rr_split.cuh"
+#include "rr_fused.cuh"
 #include "rr_stage.cuh"
 
 namespace rrk {
@@ -735,6 +738,22 @@ bool split_supported(int nx, int nu) {
 
 cudaError_t factor_launch(const SplitArgs& a, cudaStream_t s, bool* supported) {
   cudaError_t err = cudaSuccess;
+  // 12x4: the DMMA stage kernel in factor-only mode (RR_B200_FACTOR=simt selects the SIMT kernel)
+  const char* fv = getenv("RR_B200_FACTOR");
+  if (a.nx == 12 && a.nu == 4 && !(fv && strcmp(fv, "simt") == 0)) {
+    FusedArgs f{};
+    f.nx = a.nx;
+    f.nu = a.nu;
+    f.N = a.N;
+    f.batch = a.batch;
+    f.p = a.p;
+    f.f = a.f;
+    f.ws = nullptr;
+    f.status = a.status;
+    f.frec = a.fr;
+    err = factor_mma_launch(f, s, supported);
+    if (*supported) return err;
+  }
   *supported = dispatch_split(a.nx, a.nu, [&](auto cfg) {
     err = decltype(cfg)::factor(a, s);
     return true;

@@ -91,7 +91,10 @@ struct StageMMA {
   //   Pat(q, s, t): P_i[s][t] of instance q;  qjf(): this lane's entry of (q_i; r_i)
   //   wait_inputs(): waits for this stage's input copies (called after the S⁻¹ sweep, which needs
   //   none);  prefetch(): issues the next stage's input copies (called once the inputs are dead)
-  template <typename PFun, typename QFun, typename WaitFn, typename PrefFn>
+  // FAC = true: the factorization only (rr_factor): no Φ / φ, the u-block is eliminated with the
+  // symmetric sweep operator (−G⁻¹ lands in the u-columns) and recq[q] points at factor record i
+  // [V_i | S_i⁻¹ | K_i | G_i⁻¹] (record i+1 receives S_{i+1}⁻¹).
+  template <bool FAC = false, typename PFun, typename QFun, typename WaitFn, typename PrefFn>
   __device__ static __forceinline__ void backward(double* const (&wkq)[2], const double* const (&Fq)[2],
                                                   const double* const (&cvq)[2], PFun&& Pat, QFun&& qjf,
                                                   WaitFn&& wait_inputs, PrefFn&& prefetch, double delta, int grp,
@@ -282,19 +285,24 @@ struct StageMMA {
       __syncwarp();
       double col[NZ];
 #pragma unroll
-      for (int s = 0; s < NZ; ++s) col[s] = (s >= NX && s < p) ? wk[WK::pq + (s - NX)] : pb[s];
-      const double cj = (j >= NX && j < p) ? wk[WK::pq + (j - NX)] : U[p];  // pivot-column entry of row j
+      for (int s = 0; s < NZ; ++s) col[s] = (!FAC && s >= NX && s < p) ? wk[WK::pq + (s - NX)] : pb[s];
+      const double cj = (!FAC && j >= NX && j < p) ? wk[WK::pq + (j - NX)] : U[p];  // pivot-column entry of row j
       const double piv = col[p];
       gbad |= !(piv > 0.0);
       const double ip = rcp_nr(piv);
       const double rp = U[p] * ip;
       const double bp = wk[WM::BP + (p & 1)] * ip;
+      if (FAC && j == p) {  // symmetric sweep: pivot column scaled, pivot -> −1/piv
 #pragma unroll
-      for (int s = 0; s < NZ; ++s) {
-        if (s == p) continue;
-        U[s] = fma(-col[s], rp, U[s]);
+        for (int s = 0; s < NZ; ++s) U[s] = (s == p) ? -ip : U[s] * ip;
+      } else {
+#pragma unroll
+        for (int s = 0; s < NZ; ++s) {
+          if (s == p) continue;
+          U[s] = fma(-col[s], rp, U[s]);
+        }
+        U[p] = rp;
       }
-      U[p] = rp;
       bj = (j == p) ? bp : fma(-cj, bp, bj);
       __syncwarp();
     }
@@ -302,6 +310,37 @@ struct StageMMA {
     // lanes j < NX: U = [V_i; −K_i] column j, bj = (v_i)_j;  lanes NX + u: bj = −(k_i)_u
     if (j < NZ) wk[WK::vb + j] = bj;
     __syncwarp();
+    if constexpr (FAC) {  // factor record i (and S_{i+1}⁻¹ into record i+1); no closed loop
+      __syncwarp();
+      prefetch();
+      double* rec = grp ? recq[1] : recq[0];
+      constexpr int SN = NX * (NX + 1) / 2;
+      constexpr int REC = (NX * (NX + 1) + NX * NU + NU * (NU + 1) / 2 + 1) & ~1;
+      if (rec != nullptr) {
+        if (j < NX) {
+          double* Vp = rec + j * (2 * NX - j - 1) / 2;
+          double* Sp = rec + REC + SN + j * (2 * NX - j - 1) / 2;  // record i+1: S_{i+1}⁻¹
+#pragma unroll
+          for (int r = 0; r < NX; ++r)
+            if (r >= j) {
+              Vp[r] = U[r];
+              Sp[r] = wk[WK::Si + r * NX + j];
+            }
+#pragma unroll
+          for (int u = 0; u < NU; ++u) rec[2 * SN + j * NU + u] = -U[NX + u];
+        } else if (j < NZ) {
+          const int w = j - NX;
+          double* Gp = rec + 2 * SN + NX * NU + w * (2 * NU - w - 1) / 2;
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+            if (u >= w) Gp[u] = -U[NX + u];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < NX; ++r) Vc[r] = (j < NX) ? U[r] : 0.0;
+      __syncwarp();
+      return;
+    }
     // (7) M = [A + B K | B k + c − δ v] -> X1 (ld NX, NX+1 columns)
     if (j <= NX) {
       double tcol[NX];
