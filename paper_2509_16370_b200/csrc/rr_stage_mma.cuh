@@ -285,7 +285,15 @@ struct StageMMA {
       __syncwarp();
       double col[NZ];
 #pragma unroll
-      for (int s = 0; s < NZ; ++s) col[s] = (!FAC && s >= NX && s < p) ? wk[WK::pq + (s - NX)] : pb[s];
+      for (int s = 0; s < NZ; s += 2) {  // published row p (= column p) as 128-bit broadcasts
+        const double2 v2 = *reinterpret_cast<const double2*>(pb + s);
+        col[s] = v2.x;
+        col[s + 1] = v2.y;
+      }
+      if (!FAC) {  // rows of already processed pivots: lane p's own column (GJ is not symmetric there)
+#pragma unroll
+        for (int s = NX; s < p; ++s) col[s] = wk[WK::pq + (s - NX)];
+      }
       const double cj = (!FAC && j >= NX && j < p) ? wk[WK::pq + (j - NX)] : U[p];  // pivot-column entry of row j
       const double piv = col[p];
       gbad |= !(piv > 0.0);
