@@ -48,14 +48,21 @@ typedef int32_t rr_err;
 
 /* rr_dims.flags: RR_FLAG_ACCUMULATE makes rr_solve ADD its solution to sol (x += Δx, u += Δu,
  * y += Δy) instead of overwriting it -- the update step of iterative refinement with rr_residual.
- * Every other entry point requires flags == 0. */
+ * (ipm_step / ipm_solve have their own dims.) */
 #define RR_FLAG_ACCUMULATE 1
+/* Batch-shared operands (LTI / fleet MPC): with RR_FLAG_SHARED_DYN, A and B are ONE
+ * [N][...] array used by every instance (no batch dimension); with RR_FLAG_SHARED_COST, Q, M, R
+ * ([N][...]) and Q_N ([sym n]) are shared the same way.  Everything else stays per instance.
+ * Accepted by rr_factor_solve (n, m <= 16 kernels), rr_factor, rr_solve, rr_residual and their size
+ * queries; rr_factor_solve on the CTA kernels (n or m > 16) returns RR_E_UNSUPPORTED. */
+#define RR_FLAG_SHARED_DYN 2
+#define RR_FLAG_SHARED_COST 4
 
 typedef struct {
   int32_t nx;    /* state dimension n   (1 <= nx)            */
   int32_t nu;    /* control dimension m (1 <= nu)            */
   int32_t N;     /* horizon (number of stages, N >= 0)       */
-  int32_t flags; /* 0, or RR_FLAG_ACCUMULATE for rr_solve     */
+  int32_t flags; /* RR_FLAG_* (0 = all operands per instance)  */
   int64_t batch; /* number of independent instances (>= 0)  */
 } rr_dims;
 

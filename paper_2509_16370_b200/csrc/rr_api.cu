@@ -17,7 +17,9 @@ rr_err set_err(rr_err code, const char* fmt, const char* what = "") {
   return code;
 }
 
-bool dims_ok(const rr_dims* d, int allowed_flags = 0) {
+constexpr int SHARED_FLAGS = RR_FLAG_SHARED_DYN | RR_FLAG_SHARED_COST;
+
+bool dims_ok(const rr_dims* d, int allowed_flags = SHARED_FLAGS) {
   return d != nullptr && d->nx >= 1 && d->nu >= 1 && d->N >= 0 && d->batch >= 0 && (d->flags & ~allowed_flags) == 0;
 }
 }  // namespace
@@ -30,6 +32,7 @@ const char* rr_version(void) { return "rr_b200 0.1 sm_100a"; }
 
 int64_t rr_workspace_bytes(const rr_dims* dims) {
   if (!dims_ok(dims)) return -1;
+  if ((dims->flags & SHARED_FLAGS) && (dims->nx > 16 || dims->nu > 16)) return -1;  // CTA kernels: per instance
   return rrk::fused_workspace_bytes(dims->nx, dims->nu, dims->N, dims->batch);
 }
 
@@ -68,6 +71,7 @@ rr_err rr_factor_solve(const rr_dims* dims, const rr_problem* prob, const rr_fac
   a.s = *sol;
   a.ws = static_cast<double*>(workspace);
   a.status = status;
+  a.shared = dims->flags & SHARED_FLAGS;
   bool supported = false;
   cudaError_t e = rrk::fused_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_factor_solve: unsupported shape%s");
@@ -85,10 +89,11 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* ph, const rr_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t b = dims->batch, N = dims->N, n = dims->nx, m = dims->nu;
   const int64_t sn = n * (n + 1) / 2, sm = m * (m + 1) / 2;
+  const int64_t bD = (dims->flags & RR_FLAG_SHARED_DYN) ? 1 : b, bP = (dims->flags & RR_FLAG_SHARED_COST) ? 1 : b;
   struct Op { const double* h; const double* d; int64_t cnt; } ops[] = {
-      {ph->A, pd->A, b * N * n * n}, {ph->B, pd->B, b * N * n * m}, {ph->Q, pd->Q, b * N * sn},
-      {ph->M, pd->M, b * N * n * m}, {ph->R, pd->R, b * N * sm},    {ph->q, pd->q, b * N * n},
-      {ph->r, pd->r, b * N * m},     {ph->c, pd->c, b * N * n},     {ph->QN, pd->QN, b * sn},
+      {ph->A, pd->A, bD * N * n * n}, {ph->B, pd->B, bD * N * n * m}, {ph->Q, pd->Q, bP * N * sn},
+      {ph->M, pd->M, bP * N * n * m}, {ph->R, pd->R, bP * N * sm},    {ph->q, pd->q, b * N * n},
+      {ph->r, pd->r, b * N * m},      {ph->c, pd->c, b * N * n},      {ph->QN, pd->QN, bP * sn},
       {ph->qN, pd->qN, b * n},       {ph->c0, pd->c0, b * n},       {ph->delta, pd->delta, b}};
   for (const Op& o : ops) {
     if (o.cnt == 0) continue;
@@ -115,12 +120,12 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* ph, const rr_
 int32_t rr_factor_record_doubles(int32_t n, int32_t m) { return rrk::frec_doubles(n, m); }
 
 int64_t rr_factor_bytes(const rr_dims* dims) {
-  if (!dims_ok(dims, RR_FLAG_ACCUMULATE) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
+  if (!dims_ok(dims, RR_FLAG_ACCUMULATE | SHARED_FLAGS) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
   return dims->batch * (int64_t)(dims->N + 1) * rrk::frec_doubles(dims->nx, dims->nu) * 8;
 }
 
 int64_t rr_solve_workspace_bytes(const rr_dims* dims) {
-  if (!dims_ok(dims, RR_FLAG_ACCUMULATE) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
+  if (!dims_ok(dims, RR_FLAG_ACCUMULATE | SHARED_FLAGS) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
   return dims->batch * (int64_t)dims->N * (dims->nx + dims->nu) * 8 + 256;
 }
 
@@ -155,6 +160,7 @@ rr_err rr_factor(const rr_dims* dims, const rr_problem* prob, void* factor, int6
   a.f.k = nullptr;
   a.fr = static_cast<double*>(factor);
   a.status = status;
+  a.shared = dims->flags & SHARED_FLAGS;
   bool supported = false;
   cudaError_t e = rrk::factor_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_factor: unsupported shape%s");
@@ -165,7 +171,7 @@ rr_err rr_factor(const rr_dims* dims, const rr_problem* prob, void* factor, int6
 rr_err rr_solve(const rr_dims* dims, const rr_problem* prob, const void* factor, int64_t factor_bytes,
                 const rr_factor_buf* fac, const rr_solution* sol, void* workspace, int64_t workspace_bytes,
                 int32_t* status, void* stream) {
-  if (!dims_ok(dims, RR_FLAG_ACCUMULATE)) return set_err(RR_E_INVALID, "rr_solve: invalid dims%s");
+  if (!dims_ok(dims, RR_FLAG_ACCUMULATE | SHARED_FLAGS)) return set_err(RR_E_INVALID, "rr_solve: invalid dims%s");
   if (prob == nullptr || sol == nullptr) return set_err(RR_E_INVALID, "rr_solve: null %s", "prob/sol");
   if (dims->batch == 0) return RR_OK;
   if (status == nullptr) return set_err(RR_E_INVALID, "rr_solve: null %s", "status");
@@ -201,6 +207,7 @@ rr_err rr_solve(const rr_dims* dims, const rr_problem* prob, const void* factor,
   a.ws = static_cast<double*>(workspace);
   a.status = status;
   a.accumulate = (dims->flags & RR_FLAG_ACCUMULATE) != 0;
+  a.shared = dims->flags & SHARED_FLAGS;
   bool supported = false;
   cudaError_t e = rrk::solve_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_solve: unsupported shape%s");
@@ -233,6 +240,7 @@ rr_err rr_residual(const rr_dims* dims, const rr_problem* prob, const rr_solutio
   rr_residual_buf none = {nullptr, nullptr, nullptr, nullptr, nullptr};
   a.r = res ? *res : none;
   a.norms = norms;
+  a.shared = dims->flags & SHARED_FLAGS;
   bool supported = false;
   cudaError_t e = rrk::residual_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_residual: unsupported shape%s");

@@ -78,13 +78,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_kernel(const FusedA
   double* rec0 = a.ws + inst * sN * RC::PAD;
   int32_t st = 0;
 
+  // batch-shared operands (include/rr.h RR_FLAG_SHARED_*): instance index 0 for them
+  const int64_t instD = (a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst;
+  const int64_t instP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;
   auto issue_stage = [&](int i, double* dst) {
-    const int64_t s = inst * sN + i;
-    copy_async(dst + oA, a.p.A + s * n * n, n * n, j, LG);
-    copy_async(dst + oB, a.p.B + s * n * m, n * m, j, LG);
-    copy_async(dst + oQ, a.p.Q + s * sn, sn, j, LG);
-    copy_async(dst + oM, a.p.M + s * n * m, n * m, j, LG);
-    copy_async(dst + oR, a.p.R + s * sm, sm, j, LG);
+    const int64_t s = inst * sN + i, sD = instD * sN + i, sP = instP * sN + i;
+    copy_async(dst + oA, a.p.A + sD * n * n, n * n, j, LG);
+    copy_async(dst + oB, a.p.B + sD * n * m, n * m, j, LG);
+    copy_async(dst + oQ, a.p.Q + sP * sn, sn, j, LG);
+    copy_async(dst + oM, a.p.M + sP * n * m, n * m, j, LG);
+    copy_async(dst + oR, a.p.R + sP * sm, sm, j, LG);
     copy_async(dst + oq, a.p.q + s * n, n, j, LG);
     copy_async(dst + orr, a.p.r + s * m, m, j, LG);
     copy_async(dst + oc, a.p.c + s * n, n, j, LG);
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_kernel(const FusedA
   // ---- carried state: Vc = column j of V_N = Q_N; v_N = q_N ----
   double Vc[NX];
   {
-    const double* QN = a.p.QN + inst * sn;
+    const double* QN = a.p.QN + instP * sn;
 #pragma unroll
     for (int r = 0; r < NX; ++r) {
       double val = 0.0;
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_kernel(const FusedA
   }
   // y_N = Q_N x_N + q_N
   {
-    const double* QN = a.p.QN + inst * sn;
+    const double* QN = a.p.QN + instP * sn;
     if (j < n) {
       double acc = a.p.qN[inst * n + j];
 #pragma unroll
@@ -386,6 +389,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     if (!validq[q]) instq[q] = a.batch - 1;
   const int64_t inst = grp ? instq[1] : instq[0];
   const bool valid = grp ? validq[1] : validq[0];
+  const int64_t instP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;  // batch-shared Q, M, R, Q_N
   const double delta = a.p.delta[inst];
   const int64_t sN = (int64_t)N;
   double* rec0 = a.ws + inst * sN * RC::PAD;
@@ -418,14 +422,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int64_t sq = instq[q] * sN + i;
+          const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : instq[q]) * sN + i;
+          const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : instq[q]) * sN + i;
           double* d = slotq[q];
           uint64_t* bq = barq[q];
           mbar_arrive_expect_tx(bq, STG_BYTES);
-          bulk_g2s(d + oA, a.p.A + sq * n * n, 8 * n * n, bq);
-          bulk_g2s(d + oB, a.p.B + sq * n * m, 8 * n * m, bq);
-          bulk_g2s(d + oQ, a.p.Q + sq * sn, 8 * sn, bq);
-          bulk_g2s(d + oM, a.p.M + sq * n * m, 8 * n * m, bq);
-          bulk_g2s(d + oR, a.p.R + sq * sm, 8 * sm, bq);
+          bulk_g2s(d + oA, a.p.A + sD * n * n, 8 * n * n, bq);
+          bulk_g2s(d + oB, a.p.B + sD * n * m, 8 * n * m, bq);
+          bulk_g2s(d + oQ, a.p.Q + sP * sn, 8 * sn, bq);
+          bulk_g2s(d + oM, a.p.M + sP * n * m, 8 * n * m, bq);
+          bulk_g2s(d + oR, a.p.R + sP * sm, 8 * sm, bq);
           if constexpr (!FAC) {
             bulk_g2s(d + oq, a.p.q + sq * n, 8 * n, bq);
             bulk_g2s(d + orr, a.p.r + sq * m, 8 * m, bq);
@@ -436,11 +442,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
       (void)s;
       (void)dst;
     } else {
-      copy_async(dst + oA, a.p.A + s * n * n, n * n, j, 16);
-      copy_async(dst + oB, a.p.B + s * n * m, n * m, j, 16);
-      copy_async(dst + oQ, a.p.Q + s * sn, sn, j, 16);
-      copy_async(dst + oM, a.p.M + s * n * m, n * m, j, 16);
-      copy_async(dst + oR, a.p.R + s * sm, sm, j, 16);
+      const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst) * sN + i;
+      const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : inst) * sN + i;
+      copy_async(dst + oA, a.p.A + sD * n * n, n * n, j, 16);
+      copy_async(dst + oB, a.p.B + sD * n * m, n * m, j, 16);
+      copy_async(dst + oQ, a.p.Q + sP * sn, sn, j, 16);
+      copy_async(dst + oM, a.p.M + sP * n * m, n * m, j, 16);
+      copy_async(dst + oR, a.p.R + sP * sm, sm, j, 16);
       copy_async(dst + oq, a.p.q + s * n, n, j, 16);
       copy_async(dst + orr, a.p.r + s * m, m, j, 16);
       copy_async(dst + oc, a.p.c + s * n, n, j, 16);
@@ -467,7 +475,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
 
   double Vc[NX];
   {
-    const double* QN = a.p.QN + inst * sn;
+    const double* QN = a.p.QN + instP * sn;
 #pragma unroll
     for (int r = 0; r < NX; ++r) Vc[r] = (j < n) ? (r >= j ? QN[pidx(n, r, j)] : QN[pidx(n, j, r)]) : 0.0;
     if (j < NX) wk[WK::vs + j] = FAC ? 0.0 : a.p.qN[inst * n + j];
@@ -659,7 +667,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     __syncwarp();
   }
   {
-    const double* QN = a.p.QN + inst * sn;
+    const double* QN = a.p.QN + instP * sn;
     if (j < n) {
       double acc = a.p.qN[inst * n + j];
 #pragma unroll

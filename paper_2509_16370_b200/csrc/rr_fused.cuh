@@ -16,6 +16,7 @@ struct FusedArgs {
   double* ws;
   int32_t* status;
   double* frec = nullptr;  // rr_factor on the DMMA kernel: factor records [batch][N+1][frec_doubles]
+  int shared = 0;          // RR_FLAG_SHARED_DYN | RR_FLAG_SHARED_COST (batch-shared operands)
 };
 
 // Bytes of workspace for this shape (-1 if no kernel is compiled for it).

@@ -84,13 +84,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_factor_kernel(const Split
   double* rec = a.fr + inst * (sN + 1) * REC;
   int32_t st = 0;
 
+  const int64_t instD = (a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst;  // batch-shared operands
+  const int64_t instP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;
   auto issue_stage = [&](int i, double* dst) {
-    const int64_t s = inst * sN + i;
-    copy_async(dst + oA, a.p.A + s * n * n, n * n, j, LG);
-    copy_async(dst + oB, a.p.B + s * n * m, n * m, j, LG);
-    copy_async(dst + oQ, a.p.Q + s * sn, sn, j, LG);
-    copy_async(dst + oM, a.p.M + s * n * m, n * m, j, LG);
-    copy_async(dst + oR, a.p.R + s * sm, sm, j, LG);
+    const int64_t sD = instD * sN + i, sP = instP * sN + i;
+    copy_async(dst + oA, a.p.A + sD * n * n, n * n, j, LG);
+    copy_async(dst + oB, a.p.B + sD * n * m, n * m, j, LG);
+    copy_async(dst + oQ, a.p.Q + sP * sn, sn, j, LG);
+    copy_async(dst + oM, a.p.M + sP * n * m, n * m, j, LG);
+    copy_async(dst + oR, a.p.R + sP * sm, sm, j, LG);
   };
   // P = [[Q M]; [Mᵀ R]] (padded u-diagonal = 1 keeps the padded G block = I)
   auto Pat = [&](const double* sb, int s, int t) -> double {
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_factor_kernel(const Split
   // V_N = Q_N (carried as column j in Vc; record N holds V_N and S_N⁻¹)
   double Vc[NX];
   {
-    const double* QN = a.p.QN + inst * sn;
+    const double* QN = a.p.QN + instP * sn;
 #pragma unroll
     for (int r = 0; r < NX; ++r) Vc[r] = (j < n && r < n) ? QN[sidx(n, r, j)] : 0.0;
     if (valid && j < n) {
@@ -326,11 +328,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
   const bool xl = j < n, ul = ui >= 0 && ui < m;
   const bool acc = a.accumulate;             // RR_FLAG_ACCUMULATE: sol += solution (refinement)
 
+  const int64_t instD = (a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst;  // batch-shared A, B
   auto issue_stage = [&](int i) {
-    const int64_t s = inst * sN + i;
+    const int64_t s = inst * sN + i, sD = instD * sN + i;
     double* dst = sbuf(i);
-    copy_async(dst + oA, a.p.A + s * n * n, n * n, j, LG);
-    copy_async(dst + oB, a.p.B + s * n * m, n * m, j, LG);
+    copy_async(dst + oA, a.p.A + sD * n * n, n * n, j, LG);
+    copy_async(dst + oB, a.p.B + sD * n * m, n * m, j, LG);
     copy_async(dst + oc, a.p.c + s * n, n, j, LG);
     copy_async(dst + oq, a.p.q + s * n, n, j, LG);
     copy_async(dst + orr, a.p.r + s * m, m, j, LG);
@@ -587,14 +590,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_residual_kernel(const Res
   const int ui = j - NX;
   const bool xl = j < n, ul = ui >= 0 && ui < m;
 
+  const int64_t instD = (a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst;  // batch-shared operands
+  const int64_t instP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;
   auto issue = [&](int i) {
-    const int64_t s = inst * sN + i;
+    const int64_t s = inst * sN + i, sD = instD * sN + i, sP = instP * sN + i;
     double* d = buf(i);
-    copy_async(d + oA, a.p.A + s * n * n, n * n, j, LG);
-    copy_async(d + oB, a.p.B + s * n * m, n * m, j, LG);
-    copy_async(d + oQ, a.p.Q + s * sn, sn, j, LG);
-    copy_async(d + oM, a.p.M + s * n * m, n * m, j, LG);
-    copy_async(d + oR, a.p.R + s * sm, sm, j, LG);
+    copy_async(d + oA, a.p.A + sD * n * n, n * n, j, LG);
+    copy_async(d + oB, a.p.B + sD * n * m, n * m, j, LG);
+    copy_async(d + oQ, a.p.Q + sP * sn, sn, j, LG);
+    copy_async(d + oM, a.p.M + sP * n * m, n * m, j, LG);
+    copy_async(d + oR, a.p.R + sP * sm, sm, j, LG);
     copy_async(d + oq, a.p.q + s * n, n, j, LG);
     copy_async(d + orr, a.p.r + s * m, m, j, LG);
     copy_async(d + oc, a.p.c + s * n, n, j, LG);
@@ -661,7 +666,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_residual_kernel(const Res
   }
   // terminal stationarity and the initial-state row
   if (xl) {
-    const double* QN = a.p.QN + inst * sn;
+    const double* QN = a.p.QN + instP * sn;
     const double* xN = xg + sN * n;
     double a0 = a.p.qN[inst * n + j] - yg[sN * n + j];
     for (int k = 0; k < n; ++k) a0 = fma(QN[sidx(n, j, k)], xN[k], a0);
@@ -751,6 +756,7 @@ cudaError_t factor_launch(const SplitArgs& a, cudaStream_t s, bool* supported) {
     f.ws = nullptr;
     f.status = a.status;
     f.frec = a.fr;
+    f.shared = a.shared;
     err = factor_mma_launch(f, s, supported);
     if (*supported) return err;
   }

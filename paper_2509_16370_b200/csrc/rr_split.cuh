@@ -18,6 +18,7 @@ struct SplitArgs {
   double* ws;        // rr_solve scratch: [batch][N][n+m] (v_i | k_i)
   int32_t* status;
   int accumulate;    // rr_solve: RR_FLAG_ACCUMULATE (sol += solution)
+  int shared;        // RR_FLAG_SHARED_DYN | RR_FLAG_SHARED_COST
 };
 
 struct ResArgs {
@@ -27,6 +28,7 @@ struct ResArgs {
   rr_solution s;     // candidate (read)
   rr_residual_buf r; // residual blocks (any member may be null)
   double* norms;     // [batch][2] or null
+  int shared;        // RR_FLAG_SHARED_DYN | RR_FLAG_SHARED_COST
 };
 
 // doubles per factor record: V (packed n) | S⁻¹ (packed n) | K (m×n) | G⁻¹ (packed m), even

@@ -25,12 +25,30 @@ def _p(t: Optional[torch.Tensor]):
     return ctypes.c_void_p(t.data_ptr())
 
 
+RR_FLAG_SHARED_DYN, RR_FLAG_SHARED_COST = 2, 4
+
+
+def shared_flags(prob) -> int:
+    """Batch-shared operands (include/rr.h RR_FLAG_SHARED_*) from the tensor ranks: A, B of shape
+    [N, elems] (no batch dimension) are shared dynamics; Q, M, R [N, elems] and Q_N [elems] shared costs."""
+    f = 0
+    if prob.A.dim() == 2:
+        if prob.B.dim() != 2:
+            raise RRError("A and B must both be shared ([N, elems]) or both per instance")
+        f |= RR_FLAG_SHARED_DYN
+    if prob.Q.dim() == 2:
+        if prob.M.dim() != 2 or prob.R.dim() != 2 or prob.QN.dim() != 1:
+            raise RRError("Q, M, R ([N, elems]) and QN ([elems]) must be shared together")
+        f |= RR_FLAG_SHARED_COST
+    return f
+
+
 def dims_of(prob) -> rr_dims:
-    return rr_dims(prob.nx, prob.nu, prob.N, 0, prob.batch)
+    return rr_dims(prob.nx, prob.nu, prob.N, shared_flags(prob), prob.batch)
 
 
-def workspace_bytes(nx: int, nu: int, N: int, batch: int) -> int:
-    d = rr_dims(nx, nu, N, 0, batch)
+def workspace_bytes(nx: int, nu: int, N: int, batch: int, flags: int = 0) -> int:
+    d = rr_dims(nx, nu, N, flags, batch)
     nb = lib().rr_workspace_bytes(ctypes.byref(d))
     if nb < 0:
         raise RRError("no kernel compiled for nx=%d nu=%d" % (nx, nu))
@@ -55,7 +73,7 @@ def alloc_factor(prob, device=None):
 
 def alloc_workspace(prob, device=None) -> torch.Tensor:
     device = device or prob.delta.device
-    nb = workspace_bytes(prob.nx, prob.nu, prob.N, prob.batch)
+    nb = workspace_bytes(prob.nx, prob.nu, prob.N, prob.batch, shared_flags(prob))
     return torch.empty((nb + 7) // 8, dtype=torch.float64, device=device)
 
 
@@ -159,7 +177,7 @@ def rr_solve(prob, factor, out=None, fac=None, workspace=None, stream=None, accu
     if accumulate:
         if out is None:
             raise RRError("rr_solve(accumulate=True) needs `out` (the solution to update)")
-        d.flags = RR_FLAG_ACCUMULATE
+        d.flags |= RR_FLAG_ACCUMULATE
     rc = lib().rr_solve(ctypes.byref(d), ctypes.byref(p), _p(factor), factor.numel() * 8,
                         ctypes.byref(f), ctypes.byref(s), _p(workspace), workspace.numel() * 8,
                         _p(sol["status"]), _stream(stream, dev))

@@ -143,6 +143,20 @@ class RRProblem:
     def nbytes(self) -> int:
         return sum(getattr(self, f).numel() * 8 for f in self.FIELDS)
 
+    def expanded(self) -> "RRProblem":
+        """Per-instance copy of a problem with batch-shared operands (RR_FLAG_SHARED_*): A, B, Q, M, R
+        of shape [N, elems] and Q_N [elems] are broadcast to the batch."""
+        b = self.batch
+        kw = {}
+        for f in self.FIELDS:
+            t = getattr(self, f)
+            if f in ("A", "B", "Q", "M", "R") and t.dim() == 2:
+                t = t.unsqueeze(0).expand(b, *t.shape)
+            elif f == "QN" and t.dim() == 1:
+                t = t.unsqueeze(0).expand(b, t.shape[0])
+            kw[f] = t.contiguous()
+        return RRProblem(self.nx, self.nu, self.N, **kw)
+
     def with_delta(self, delta: float) -> "RRProblem":
         kw = {f: getattr(self, f) for f in self.FIELDS}
         kw["delta"] = torch.full_like(self.delta, float(delta))
@@ -182,6 +196,22 @@ def random_stable_lqr(nx: int, nu: int, N: int, batch: int, seed: int, delta: fl
     return RRProblem(nx, nu, N, A.contiguous(), B.contiguous(), Q.contiguous(), M.contiguous(),
                      R.contiguous(), q.contiguous(), r.contiguous(), c.contiguous(), QN.contiguous(),
                      qN.contiguous(), c0.contiguous(), d)
+
+
+def lti_problem(nx: int, nu: int, N: int, batch: int, seed: int, delta: float = 1e-4, shared_dyn: bool = True,
+                shared_cost: bool = True, device="cpu") -> RRProblem:
+    """Fleet / LTI-MPC shaped batch: the matrices of one C2-recipe instance (global id
+    0) shared by every instance (A, B and/or Q, M, R, Q_N without a batch dimension), per-instance
+    right-hand sides q, r, c, q_N, c_0 and δ from instances 1..batch of the same generator."""
+    base = random_stable_lqr(nx, nu, N, 1, seed, delta, first=0, device=device)
+    rhs = random_stable_lqr(nx, nu, N, batch, seed, delta, first=1, device=device)
+    kw = {f: getattr(rhs, f) for f in RRProblem.FIELDS}
+    if shared_dyn:
+        kw["A"], kw["B"] = base.A[0].contiguous(), base.B[0].contiguous()
+    if shared_cost:
+        kw["Q"], kw["M"], kw["R"], kw["QN"] = (base.Q[0].contiguous(), base.M[0].contiguous(),
+                                               base.R[0].contiguous(), base.QN[0].contiguous())
+    return RRProblem(nx, nu, N, **kw)
 
 
 def random_stable_lqr_chunked(nx, nu, N, batch, seed, delta=1e-4, device="cpu", chunk=4096,

@@ -1,0 +1,74 @@
+"""Batch-shared operands (RR_FLAG_SHARED_DYN / RR_FLAG_SHARED_COST, LTI / fleet MPC):
+one [N][...] copy of A, B (and/or Q, M, R, Q_N) serves every instance.  The kernels read the same
+values as for the broadcast per-instance problem, so results must be bitwise identical to the
+expanded problem, and within 1e-9 of the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def rr():
+    import paper_2509_16370_b200 as m
+    return m
+
+
+def rel(g, o):
+    g = np.asarray(g).reshape(len(g), -1)
+    o = np.asarray(o).reshape(len(o), -1)
+    return float(np.max(np.max(np.abs(g - o), axis=1) / np.maximum(np.max(np.abs(o), axis=1), 1e-300)))
+
+
+@pytest.mark.parametrize("nx,nu,N,batch", [(12, 4, 20, 37), (4, 1, 15, 33), (3, 2, 7, 9), (16, 16, 4, 5)])
+@pytest.mark.parametrize("dyn,cost", [(True, True), (True, False), (False, True)])
+def test_shared_equals_expanded(nx, nu, N, batch, dyn, cost):
+    m = rr()
+    p = synth.lti_problem(nx, nu, N, batch, seed=nx + N, delta=1e-3, shared_dyn=dyn, shared_cost=cost)
+    e = p.expanded()
+    ps, pe = p.to("cuda"), e.to("cuda")
+    a = m.rr_factor_solve(ps)
+    b = m.rr_factor_solve(pe)
+    Fs, _ = m.rr_factor(ps)
+    Fe, _ = m.rr_factor(pe)
+    ss = m.rr_solve(ps, Fs)
+    se = m.rr_solve(pe, Fe)
+    rs, ns = m.rr_residual(ps, ss)
+    re_, ne = m.rr_residual(pe, se)
+    torch.cuda.synchronize()
+    for k in ("x", "u", "y", "status"):
+        assert torch.equal(a[k], b[k]), k
+        assert torch.equal(ss[k], se[k]), k
+    sn = nx * (nx + 1) // 2
+    used = 2 * sn + nx * nu + nu * (nu + 1) // 2   # record padding and record N's K / G⁻¹ are unused
+    assert torch.equal(Fs[:, :N, :used], Fe[:, :N, :used]) and torch.equal(Fs[:, N, :2 * sn], Fe[:, N, :2 * sn])
+    assert torch.equal(ns, ne)
+    o = oracle.rr_solve_t2(e)
+    for k in ("x", "u", "y"):
+        assert rel(a[k].cpu().numpy(), o[k]) <= 1e-9
+
+
+def test_shared_host_path():
+    m = rr()
+    p = synth.lti_problem(12, 4, 10, 16, seed=3)
+    hp = synth.RRProblem(p.nx, p.nu, p.N, **{f: getattr(p, f).pin_memory() for f in p.FIELDS})
+    dp = p.to("cuda")
+    hs = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in m.alloc_solution(dp).items()}
+    ds = m.alloc_solution(dp)
+    call = m.HostMarshalled(hp, hs, dp, ds)
+    call.launch()
+    torch.cuda.synchronize()
+    o = oracle.rr_solve_t2(p.expanded())
+    for k in ("x", "u", "y"):
+        assert rel(hs[k].numpy(), o[k]) <= 1e-9
+    assert call.h2d_bytes < p.expanded().nbytes() / 2
+
+
+def test_shared_large_shape_unsupported():
+    m = rr()
+    p = synth.lti_problem(40, 20, 3, 2, seed=1).to("cuda")
+    with pytest.raises(m.RRError):
+        m.rr_factor_solve(p)
