@@ -57,9 +57,11 @@ def dist_init():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
+        import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local)  # one GPU per rank before the communicator exists
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return ws, rank, local
 
 
@@ -207,11 +209,12 @@ def run_reference(a, ws, rank):
 
 def main():
     a = parse()
-    ws, rank, local = dist_init()
-    if a.impl == "reference":
+    if a.impl == "reference":  # the oracle on host cores: rank 0 alone, no process group needed
+        ws, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+        a.gpus = max(a.gpus, ws)
         run_reference(a, ws, rank)
-        barrier(ws)
         return
+    ws, rank, local = dist_init()
     import torch
     import synth
     import paper_2509_16370_b200 as rr
