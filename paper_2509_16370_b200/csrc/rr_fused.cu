@@ -321,7 +321,11 @@ struct MmaLayout {
   static constexpr int STG = NX * NX + 2 * NX * NU + NX * (NX + 1) / 2 + NU * (NU + 1) / 2 + 2 * NX + NU;
   static constexpr int STG_PAD = (STG + 1) & ~1;
   static constexpr int SLOT_B = STG_PAD + WorkM<NX, NU>::PAD;  // single stage buffer (prefetched mid-stage)
+#ifndef RR_FWD_PHI
+  static constexpr int SLOT_F = 2 * RecM<NX, NU>::PAD + 2 * (((NX * NX + NX * NU) + 1) & ~1) + ((NU + 1) & ~1) + 2 * NX;
+#else
   static constexpr int SLOT_F = 2 * RecM<NX, NU>::PAD + NX;
+#endif
   static constexpr int BAR = ((SLOT_B > SLOT_F ? SLOT_B : SLOT_F) + 1) & ~1;  // 2 mbarriers (TMA completion)
   static constexpr int SLOT = BAR + 2;
   static constexpr int SLOT_PAD = (SLOT + 1) & ~1;
@@ -572,6 +576,123 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     status = o > status ? o : status;
   }
 
+#ifndef RR_FWD_PHI
+  // forward sweep: u = K x + k, y = V x + v, x⁺ = S_{i+1}⁻¹ (A x + B u + e),
+  // record i and A_i, B_i streamed by TMA into double buffers (one stage ahead)
+  bool bad = false;
+  double* xo = a.s.x + inst * (sN + 1) * n;
+  double* uo = a.s.u + inst * sN * m;
+  double* yo = a.s.y + inst * (sN + 1) * n;
+  const int ui = j - NX;
+  constexpr int ABP = ((n * n + n * m) + 1) & ~1;
+  __syncwarp();
+  auto rbuf = [&](double* sl, int b) { return sl + b * RC::PAD; };
+  auto abuf = [&](double* sl, int b) { return sl + 2 * RC::PAD + b * ABP; };
+  double* xch = slot + 2 * RC::PAD + 2 * ABP;  // exchange: u (NU, padded to even) | z (NX) | x (NX)
+  double* uch = xch;
+  double* zch = xch + ((NU + 1) & ~1);
+  double* xsh = zch + NX;
+  asm volatile("fence.proxy.async;\n" ::: "memory");
+  __syncwarp();
+  auto issue_fwd = [&](int i, int b) {
+    if (lane == 0) {
+      fence_proxy_async();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : instq[q]) * sN + i;
+        mbar_arrive_expect_tx(&barq[q][b], 8u * (RC::SIZE + n * n + n * m));
+        bulk_g2s(rbuf(slotq[q], b), a.ws + (instq[q] * sN + i) * RC::PAD, 8u * RC::SIZE, &barq[q][b]);
+        bulk_g2s(abuf(slotq[q], b), a.p.A + sD * n * n, 8u * n * n, &barq[q][b]);
+        bulk_g2s(abuf(slotq[q], b) + n * n, a.p.B + sD * n * m, 8u * n * m, &barq[q][b]);
+      }
+    }
+  };
+  auto wait_fwd = [&](int b) {
+    if (b == 0) {
+      mbar_wait_parity(&bar[0], ph0);
+      ph0 ^= 1u;
+    } else {
+      mbar_wait_parity(&bar[1], ph1);
+      ph1 ^= 1u;
+    }
+    __syncwarp();
+  };
+  if (N > 0) issue_fwd(0, 0);
+  {
+    double xj = 0.0;
+#pragma unroll
+    for (int r = 0; r < NX; ++r) xj = (r == j) ? xr[r] : xj;
+    if (valid && j < n) xo[j] = xj;
+    bad |= (j < n) && !isfinite(xj);
+  }
+  for (int i = 0; i < N; ++i) {
+    const int b = i & 1;
+    const double* rc = rbuf(slot, b);
+    const double* ab = abuf(slot, b);
+    if (i + 1 < N) issue_fwd(i + 1, b ^ 1);
+    wait_fwd(b);
+    // y_i = V_i x_i + v_i (lanes < NX);  u_i = K_i x_i + k_i (lanes NX..)
+    double a0 = 0.0, a1 = 0.0;
+    if (j < NX) {
+      a0 = rc[RC::v + j];
+#pragma unroll
+      for (int k = 0; k < NX; k += 2) {
+        const int i0 = k >= j ? pidx(NX, k, j) : pidx(NX, j, k);
+        const int i1 = k + 1 >= j ? pidx(NX, k + 1, j) : pidx(NX, j, k + 1);
+        a0 = fma(rc[RC::V + i0], xr[k], a0);
+        a1 = fma(rc[RC::V + i1], xr[k + 1], a1);
+      }
+    } else if (ui < NU) {
+      a0 = rc[RC::k + ui];
+#pragma unroll
+      for (int k = 0; k < NX; k += 2) {
+        a0 = fma(rc[RC::K + k * NU + ui], xr[k], a0);
+        a1 = fma(rc[RC::K + (k + 1) * NU + ui], xr[k + 1], a1);
+      }
+    }
+    const double yu = a0 + a1;
+    if (valid) {
+      if (j < n) yo[(int64_t)i * n + j] = yu;
+      if (ui >= 0 && ui < m) uo[(int64_t)i * m + ui] = yu;
+    }
+    bad |= (j < NZ) && !isfinite(yu);
+    if (ui >= 0 && ui < NU) uch[ui] = yu;
+    __syncwarp();
+    // z = A x + B u + e  (A, B column-major: row j)
+    if (j < NX) {
+      double z0 = rc[RC::e + j], z1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < NX; k += 2) {
+        z0 = fma(ab[j + k * n], xr[k], z0);
+        z1 = fma(ab[j + (k + 1) * n], xr[k + 1], z1);
+      }
+#pragma unroll
+      for (int u = 0; u < NU; ++u) z0 = fma(ab[n * n + j + u * n], uch[u], z0);
+      zch[j] = z0 + z1;
+    }
+    __syncwarp();
+    // x_{i+1} = S_{i+1}⁻¹ z
+    double zr[NX];
+    ST::bcast(zch, zr);
+    if (j < NX) {
+      double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < NX; k += 2) {
+        const int i0 = k >= j ? pidx(NX, k, j) : pidx(NX, j, k);
+        const int i1 = k + 1 >= j ? pidx(NX, k + 1, j) : pidx(NX, j, k + 1);
+        x0 = fma(rc[RC::S + i0], zr[k], x0);
+        x1 = fma(rc[RC::S + i1], zr[k + 1], x1);
+      }
+      const double xv = x0 + x1;
+      if (valid && j < n) xo[(int64_t)(i + 1) * n + j] = xv;
+      bad |= !isfinite(xv);
+      xsh[j] = xv;
+    }
+    __syncwarp();
+    ST::bcast(xsh, xr);
+    __syncwarp();
+  }
+#else
   // forward sweep from the records (row-major [Φ | φ], packed V)
   bool bad = false;
   double* xo = a.s.x + inst * (sN + 1) * n;
@@ -666,6 +787,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     ST::bcast(xs, xr);
     __syncwarp();
   }
+#endif
   {
     const double* QN = a.p.QN + instP * sn;
     if (j < n) {
