@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def main(rep, so, warp_stages=32768 * 100):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sass_lines.py"), rep, so,
-                          "rr_fused_mma_kernelILi12ELi4ELi4ELi3"], capture_output=True, text=True,
+                          "rr_fused_mma_kernelILi12ELi4ELi4ELi3ELb0"], capture_output=True, text=True,
                          env=dict(os.environ, TOP="5000")).stdout.splitlines()
     mma = open(os.path.join(ROOT, "paper_2509_16370_b200/csrc/rr_stage_mma.cuh")).read().splitlines()
     marks = [(i, "mma" + re.match(r"\s*// (\(\d\))", l).group(1)) for i, l in enumerate(mma, 1)
