@@ -18,7 +18,7 @@ def main(rep, so, warp_stages=32768 * 100):
     marks = [(i, "mma" + re.match(r"\s*// (\(\d\))", l).group(1)) for i, l in enumerate(mma, 1)
              if re.match(r"\s*// \(\d\)", l)]
     fused = open(os.path.join(ROOT, "paper_2509_16370_b200/csrc/rr_fused.cu")).read().splitlines()
-    fwd = max(i for i, l in enumerate(fused, 1) if "forward sweep from the records" in l)
+    fwd = min(i for i, l in enumerate(fused, 1) if "forward sweep from the records" in l or "// forward sweep: u = K x + k" in l)
     stage = open(os.path.join(ROOT, "paper_2509_16370_b200/csrc/rr_stage.cuh")).read().splitlines()
     inv0 = min(i for i, l in enumerate(stage, 1) if "static __forceinline__ void invS" in l)
     inv1 = min(i for i, l in enumerate(stage, 1) if "X <- S⁻¹ X" in l)
