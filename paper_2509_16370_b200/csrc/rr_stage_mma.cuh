@@ -79,14 +79,24 @@ struct WorkM {
   static_assert(W::Wb + NX * NX == W::SIZE, "Work<> must end with Wb");
   static constexpr int MLD = ((NX + 1 + 15) / 16) * 16 + 4;  // row-major ld of M (≡ 4 mod 16: B fragments)
   static constexpr int X1SZ = (NX * MLD > NX * 16 ? NX * MLD : NX * 16);
+
   static constexpr int X1 = W::Wb;              // [V | Ve] (ld NX), then T (ld NX), then M (row-major, ld MLD)
   static constexpr int X2 = X1 + X1SZ;          // W (ld NX, NX+1 cols), then U (ld ULD)
   static constexpr int ULD = 18;                // U leading dimension: conflict-free C-fragment stores
+  static_assert(16 * ULD >= NX * 16 && X2 - X1 >= NX * 16, "X1 / X2 must hold the swizzled T / W (NX rows x 16)");
   static constexpr int E = X2 + 16 * ULD;       // e = c_{i+1} − δ v_{i+1} (NX, even)
   static constexpr int BP = E + ((NX + 1) & ~1);  // 2 publish slots for b_p in the u-block elimination
   static constexpr int SIZE = BP + 2;
   static constexpr int PAD = (SIZE + 1) & ~1;
 };
+
+// W and T live in shared memory row-major with a row stride of 16 doubles and the 16-byte column
+// pairs XOR-swizzled by σ(r) = 4(r&1) + 2((r>>1)&1): C-fragment pair stores (c0, c1 adjacent), A-fragment
+// loads (row r, column k) and B-fragment loads (row k, column n) are then all free of bank conflicts
+// (each quarter-warp of 128-bit stores and each half-warp of 64-bit loads hits distinct banks).
+__device__ __forceinline__ int swz16(int r, int c) {
+  return 16 * r + 2 * ((c >> 1) ^ (4 * (r & 1) + 2 * ((r >> 1) & 1))) + (c & 1);
+}
 
 template <int NX, int NU>
 struct StageMMA {
@@ -166,20 +176,18 @@ struct StageMMA {
           for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aS[mt], bv);
         }
       }
-      double* Wb = wkq[q] + WM::X2;
+      double* Wb = wkq[q] + WM::X2;  // [W | We | 0 pad] row-major, swizzled (swz16)
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < CT; ++nt)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int r = 8 * mt + g, col = 8 * nt + 2 * t + e;
-            if (r < NX && col <= NX) Wb[col * NX + r] = c[mt][nt][e];
-          }
+        for (int nt = 0; nt < CT; ++nt) {
+          const int r = 8 * mt + g, col = 8 * nt + 2 * t;
+          if (r < NX) *reinterpret_cast<double2*>(Wb + swz16(r, col)) = make_double2(c[mt][nt][0], c[mt][nt][1]);
+        }
     }
     __syncwarp();
     // (3) g = v + W e;  b_j = [q + Aᵀg; r + Bᵀg]_j
-    if (j < NX) wk[WK::gb + j] = wk[WK::vs + j] + wk[WM::X2 + NX * NX + j];
+    if (j < NX) wk[WK::gb + j] = wk[WK::vs + j] + wk[WM::X2 + swz16(j, NX)];
     __syncwarp();
     const int jc = (j < NZ) ? j : 0;
     {
@@ -210,7 +218,7 @@ struct StageMMA {
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int r = 8 * mt + g;
-          aW[mt] = (r < NX) ? Wb[(4 * kt + t) * NX + r] : 0.0;
+          aW[mt] = (r < NX) ? Wb[swz16(r, 4 * kt + t)] : 0.0;
         }
 #pragma unroll
         for (int nt = 0; nt < ZT; ++nt) {
@@ -220,16 +228,14 @@ struct StageMMA {
           for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aW[mt], bF);
         }
       }
-      double* Tb = wkq[q] + WM::X1;
+      double* Tb = wkq[q] + WM::X1;  // T row-major, swizzled (swz16)
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < ZT; ++nt)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int r = 8 * mt + g, col = 8 * nt + 2 * t + e;
-            if (r < NX && col < NZ) Tb[col * NX + r] = c[mt][nt][e];
-          }
+        for (int nt = 0; nt < ZT; ++nt) {
+          const int r = 8 * mt + g, col = 8 * nt + 2 * t;
+          if (r < NX) *reinterpret_cast<double2*>(Tb + swz16(r, col)) = make_double2(c[mt][nt][0], c[mt][nt][1]);
+        }
     }
     __syncwarp();
     // (5) U = Fᵀ T + P (NZ × NZ) -> X2 (ld 16); A-fragment of Fᵀ = B-fragment layout of F
@@ -262,7 +268,7 @@ struct StageMMA {
 #pragma unroll
         for (int nt = 0; nt < ZT; ++nt) {
           const int col = 8 * nt + g;
-          const double bT = (col < NZ) ? Tb[col * NX + 4 * kt + t] : 0.0;
+          const double bT = (col < NZ) ? Tb[swz16(4 * kt + t, col)] : 0.0;
 #pragma unroll
           for (int mt = 0; mt < ZT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aF[mt], bT);
         }
