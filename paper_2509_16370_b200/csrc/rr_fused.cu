@@ -501,8 +501,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     const double* cvq[2] = {sbq[0] + oc, sbq[1] + oc};
     const double* sb = grp ? sbq[1] : sbq[0];
     auto qjf = [&]() -> double { return (j < NX) ? sb[oq + j] : sb[orr + j - NX]; };
-#ifdef RR_NO_PTAB
+#if defined(RR_NO_PTAB)
     auto P2 = [&](int q, int s, int t) -> double { return Pat(sbq[q], s, t); };
+#elif defined(RR_P_SIMT)
+    auto P2 = [&](int s) -> double { return Pat(sb, s, j); };  // column j of this lane's P
+    (void)ptab;
 #else
     auto P2 = [&](int q, int k) -> double {
       const int off = ptab[k * 32 + lane];

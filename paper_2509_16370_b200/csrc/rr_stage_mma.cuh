@@ -250,11 +250,13 @@ struct StageMMA {
         for (int nt = 0; nt < ZT; ++nt)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-#ifdef RR_NO_PTAB
+#if defined(RR_NO_PTAB)
             const int r = 8 * mt + g, col = 8 * nt + 2 * t + e;
             c[mt][nt][e] = (r < NZ && col < NZ) ? Pat(q, r, col) : 0.0;
-#else
+#elif !defined(RR_P_SIMT)
             c[mt][nt][e] = Pat(q, (mt * ZT + nt) * 2 + e);  // P-gather table (kernel)
+#else
+            c[mt][nt][e] = 0.0;  // RR_P_SIMT: P added in (6) column by column (measured 3% slower)
 #endif
           }
 #pragma unroll
@@ -291,6 +293,11 @@ struct StageMMA {
       U[s] = (j < NZ) ? u2.x : 0.0;
       U[s + 1] = (j < NZ) ? u2.y : 0.0;
     }
+#if !defined(RR_NO_PTAB) && defined(RR_P_SIMT)
+    // U = FᵀWF + P: lane j adds column j of P (packed Q / M / R of its own instance's stage)
+#pragma unroll
+    for (int s = 0; s < NZ; ++s) U[s] += Pat(s);
+#endif
     // b is distributed: lane j updates its own entry b_j with the pivot-column entry of row j
     // (own U[p] by symmetry, or lane p's published row for already processed pivots) and the
     // published b_p
