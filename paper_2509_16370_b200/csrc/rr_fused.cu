@@ -328,7 +328,9 @@ struct MmaLayout {
 #endif
   static constexpr int BAR = ((SLOT_B > SLOT_F ? SLOT_B : SLOT_F) + 1) & ~1;  // 2 mbarriers (TMA completion)
   static constexpr int SLOT = BAR + 2;
-  static constexpr int SLOT_PAD = (SLOT + 1) & ~1;
+  // slot stride ≡ 8 (mod 16) doubles: the two instances of a warp (half-warps) reading the same
+  // offset of their own slots (SIMT broadcasts, per-lane columns) fall in different banks
+  static constexpr int SLOT_PAD = ((SLOT + 1) & ~1) + ((8 - (((SLOT + 1) & ~1) % 16) + 16) % 16);
   // TMA bulk copies need 16-byte sizes/offsets for every operand block of a stage
   // P-gather table: per lane, the stage-buffer offset of each P_i element of its U C-fragments
   // (ZT × ZT tiles × 2 values), -1 outside NZ; stage independent, built once per CTA
