@@ -98,8 +98,10 @@ __device__ __forceinline__ void cartpole_step(const double* prm, const double* x
   xn[3] = x[3] + dt * thdd;
 }
 
-template <int NX, int NU, int NG, int NC, int LG, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
+// EXACT: the dimensions are the template's (n = NX, m = NU, n_g = NG, n_c = NC; terminal counts stay
+// runtime), so the compiler folds the padding guards and loop bounds.
+template <int NX, int NU, int NG, int NC, int LG, int WARPS, bool EXACT = false>
+__global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(const IpmArgs a) {
   using ST = Stage<NX, NU, LG>;
   using WK = Work<NX, NU>;
   using RC = Rec<NX, NU>;
@@ -109,7 +111,8 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   constexpr int SLOT = group_stride(2 * IB::PAD + WK::PAD + 2 * RC::PAD + NX, LG);
   static_assert(NG <= LG && NC <= LG, "constraint count per stage exceeds the lane group");
 
-  const int n = a.d.nx, m = a.d.nu, N = a.d.N, w = n + m;
+  const int n = EXACT ? NX : a.d.nx, m = EXACT ? NU : a.d.nu, N = a.d.N, w = n + m;
+  const int ngd = EXACT ? NG : a.d.ng, ncd = EXACT ? NC : a.d.nc;
   const int sn = n * (n + 1) / 2, sm = m * (m + 1) / 2;
 
   extern __shared__ __align__(16) double smem[];
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   // Real elements travel by cp.async (8-byte LDGSTS, asynchronous); padding is stored directly.
   // finish_stage() completes Σ, r_z and the positivity check once the copies have landed.
   // the padded layout equals the global one when the dims are the template dims: contiguous copies
-  const bool exact = (n == NX && m == NU && a.d.ng == NG && a.d.nc == NC);
+  const bool exact = (n == NX && m == NU && ngd == NG && ncd == NC);
   // per-lane gather table of the unpacked P (exact path): entry e = j + t·LG of the NZ × NZ
   // col-major P comes from Q (sel 0, packed 'L'), M (sel 1) or R (sel 2, packed); code = off·4 + sel
   constexpr int PT = (NZ * NZ + LG - 1) / LG;
@@ -165,8 +168,8 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   auto issue_stage_data = [&](int i, double* dst) {
     const bool term = (i == N);
     const int ww = term ? n : w;
-    const int ng = term ? a.d.ngN : a.d.ng;
-    const int nc = term ? a.d.ncN : a.d.nc;
+    const int ng = term ? a.d.ngN : ngd;
+    const int nc = term ? a.d.ncN : ncd;
     const int64_t si = inst * sN + i;
     auto put = [&](int off, const double* src, bool ok, double pad) {
       if (ok) cp_async8(dst + off, src);
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   };
   // after the copies of stage i landed in sb: Σ = (s/z + 1/η)⁻¹, r_z = g + μ/z
   auto finish_stage = [&](int i) {
-    const int ng = (i == N) ? a.d.ngN : a.d.ng;
+    const int ng = (i == N) ? a.d.ngN : ngd;
     for (int e = j; e < NG; e += LG) {
       const double sv = sb[IB::s + e], zv = sb[IB::z + e], gvv = sb[IB::gv + e];
       if (e < ng && (!(sv > 0.0) || !(zv > 0.0))) nonpos_stage = min(nonpos_stage, i);
@@ -405,8 +408,8 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
   auto expand_stage = [&](int i, const double (&dz_full)[NZ]) {
     // inequality e on lane e; equality e on lane e
     const bool term = (i == N);
-    const int ng = term ? a.d.ngN : a.d.ng;
-    const int nc = term ? a.d.ncN : a.d.nc;
+    const int ng = term ? a.d.ngN : ngd;
+    const int nc = term ? a.d.ncN : ncd;
     const int64_t si = inst * sN + i;
     if (j < ng) {
       double gd = 0.0;
@@ -617,7 +620,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
       bool pos = true;
       for (int i = j; i <= N; i += LG) {  // stages distributed over the lanes
         const bool term = (i == N);
-        const int ng = term ? a.d.ngN : a.d.ng;
+        const int ng = term ? a.d.ngN : ngd;
         const double* sp = term ? a.it.sN + inst * ng : a.it.s + (inst * sN + i) * ng;
         const double* dsp = term ? a.r.dsN + inst * ng : a.r.ds + (inst * sN + i) * ng;
         if (ng == NG) {  // all loads of the stage issued before the first use
@@ -681,7 +684,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
     axpy_group(a.it.x + inst * nx1, a.r.dx + inst * nx1, alpha, nx1, j);
     axpy_group(a.it.y + inst * nx1, a.r.dy + inst * nx1, alpha, nx1, j);
     axpy_group(a.it.u + inst * sN * m, a.r.du + inst * sN * m, alpha, sN * m, j);
-    const int64_t ngt = sN * a.d.ng, nct = sN * a.d.nc;
+    const int64_t ngt = sN * ngd, nct = sN * ncd;
     axpy_group(a.it.s + inst * ngt, a.r.ds + inst * ngt, alpha, ngt, j);
     axpy_group(a.it.z + inst * ngt, a.r.dz + inst * ngt, admax, ngt, j);
     axpy_group(a.it.sN + inst * a.d.ngN, a.r.dsN + inst * a.d.ngN, alpha, a.d.ngN, j);
@@ -709,7 +712,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
       a.r.dy[inst * nx1 + e] = nan;
     }
     for (int64_t e = j; e < sN * m; e += LG) a.r.du[inst * sN * m + e] = nan;
-    const int64_t ngt = sN * a.d.ng, nct = sN * a.d.nc;
+    const int64_t ngt = sN * ngd, nct = sN * ncd;
     for (int64_t e = j; e < ngt; e += LG) {
       a.r.ds[inst * ngt + e] = nan;
       a.r.dz[inst * ngt + e] = nan;
@@ -724,7 +727,7 @@ __global__ void __launch_bounds__(WARPS * 32) ipm_step_kernel(const IpmArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
-template <int NX, int NU, int NG, int NC, int LG>
+template <int NX, int NU, int NG, int NC, int LG, bool EXACT = false>
 struct IpmCfg {
   static constexpr int WARPS = 4;
   static constexpr int IPB = WARPS * (32 / LG);
@@ -733,7 +736,7 @@ struct IpmCfg {
   static size_t smem_bytes() { return sizeof(double) * (size_t)IPB * SLOT; }
   static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * Rec<NX, NU>::PAD; }
   static cudaError_t launch(const IpmArgs& a, cudaStream_t s) {
-    auto k = ipm_step_kernel<NX, NU, NG, NC, LG, WARPS>;
+    auto k = ipm_step_kernel<NX, NU, NG, NC, LG, WARPS, EXACT>;
     const size_t sm = smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
@@ -748,6 +751,8 @@ static bool dispatch_ipm(const ipm_dims& d, F&& f) {
   const int ngm = d.ng > d.ngN ? d.ng : d.ngN;
   const int ncm = d.nc > d.ncN ? d.nc : d.ncN;
   if (d.model == IPM_MODEL_CARTPOLE && (d.nx != 4 || d.nu != 1)) return false;
+  if (d.nx == 4 && d.nu == 1 && d.ng == 4 && d.nc == 0 && d.ngN <= 4 && d.ncN == 0)
+    return f(IpmCfg<4, 1, 4, 0, 8, true>{});  // C4 (cart-pole) shape
   if (d.nx <= 4 && d.nu <= 1 && ngm <= 4 && ncm == 0) return f(IpmCfg<4, 1, 4, 0, 8>{});
   if (d.nx <= 4 && d.nu <= 4 && ngm <= 8 && ncm <= 4) return f(IpmCfg<4, 4, 8, 4, 8>{});
   if (d.nx <= 8 && d.nu <= 8 && ngm <= 16 && ncm <= 8) return f(IpmCfg<8, 8, 16, 8, 16>{});
