@@ -27,3 +27,24 @@ b = random_lq_ocp(3, 2, 4, 5, seed=4, ng=2, ngN=1, nc=1, ncN=1, device="cuda")
 res = rr.ipm_step(b)
 torch.cuda.synchronize()
 print("ipm lq", res["status"].tolist())
+# split API, residual, refinement, shared operands, IPM solve
+for (n, m, N, b) in [(12, 4, 5, 5), (4, 1, 4, 9), (5, 3, 3, 3)]:
+    p = synth.random_stable_lqr(n, m, N, b, seed=5).to("cuda")
+    F, st = rr.rr_factor(p)
+    sol = rr.rr_solve(p, F)
+    rr.rr_refine(p, F, sol, iters=1)
+    torch.cuda.synchronize()
+    print("split", n, m, N, b, int(st.abs().sum()), int(sol["status"].abs().sum()))
+p = synth.lti_problem(12, 4, 6, 5, seed=6).to("cuda")
+rr.rr_factor_solve(p)
+F, _ = rr.rr_factor(p)
+rr.rr_residual(p, rr.rr_solve(p, F))
+torch.cuda.synchronize()
+print("shared ok")
+from synth.ipm_workloads import double_integrator_ocp  # noqa: E402
+b = double_integrator_ocp(batch=3, device="cuda")
+rep = rr.ipm_solve(b, max_iters=30)
+b = cartpole_c4(4, seed=3, N=8, device="cuda")
+rep2 = rr.ipm_solve(b, max_iters=3)
+torch.cuda.synchronize()
+print("ipm_solve", rep["status"].tolist(), rep2["status"].tolist())
