@@ -42,12 +42,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample wall time")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5", "split", "c4solve"],
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "split", "c4solve"],
                     help="c2 (default, BASELINE configs[1]); c3 = 4,096 dense n64 m32 N50 (configs[2]); "
                          "c4 = ipm_step on 16,384 cart-pole instances (configs[3]); c5 = 1,048,576 "
                          "quadrotor n12 m4 N200 sharded over the ranks, chunks of 65,536 (configs[4]); split = "
                          "rr_factor + rr_solve + rr_residual on the C2 workload, each kernel timed; c4solve = ipm_solve "
-                         "(20 IPM iterations) on the C4 cart-pole batch")
+                         "(20 IPM iterations) on the C4 cart-pole batch; c1 = single double-integrator instance latency")
     ap.add_argument("--c5-total", type=int, default=1048576, help=argparse.SUPPRESS)
     return ap.parse_args()
 
@@ -229,6 +229,8 @@ def main():
         return run_split(a, ws, rank, local)
     if a.workload == "c4solve":
         return run_c4solve(a, ws, rank, local)
+    if a.workload == "c1":
+        return run_c1(a, ws, rank, local)
     global NX, NU, HORIZON, BATCH, SEED, ALG_BYTES_PER_STAGE, ALG_FLOPS_PER_STAGE
     if a.workload == "c3":
         # 206,208 B and 2.42M flop per stage (algorithmic)
@@ -635,6 +637,68 @@ def run_c4solve(a, ws, rank, local):
                          "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": None,
                          "alg_bytes_per_stage_iteration": 2800, "peak_source": src},
             "clocks": clk, "gpu_launches": a.steps * (4 * IT + 3)}), flush=True)
+
+
+def run_c1(a, ws, rank, local):
+    """BASELINE configs[0]: ONE double-integrator instance (n=2, m=1, N=10, terminal equality folded
+    with η = 1e4, δ = 1e-4; latency, no roofline claim).  Latency of one
+    rr_factor_solve launch (CUDA events around each launch, median of K), the same through the
+    host-buffer C-ABI path (H2D + solve + D2H), and the T2 oracle on one host thread (median)."""
+    import torch
+    import synth
+    import oracle
+    import paper_2509_16370_b200 as rr
+    if rank != 0:
+        return
+    dev = torch.device("cuda", local)
+    p = synth.double_integrator_c1()
+    pd = p.to(dev)
+    sol = rr.alloc_solution(pd)
+    call = rr.Marshalled(pd, sol)
+    stream = torch.cuda.current_stream(dev)
+    K = max(a.steps, 50)
+    for _ in range(max(3, a.warmup)):
+        call.launch(stream)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for s_, e_ in ev:
+        s_.record(stream)
+        call.launch(stream)
+        e_.record(stream)
+    torch.cuda.synchronize()
+    us = statistics.median(s_.elapsed_time(e_) * 1e3 for s_, e_ in ev)
+    hp = synth.RRProblem(p.nx, p.nu, p.N, **{f: getattr(p, f).pin_memory() for f in p.FIELDS})
+    hs = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in sol.items()}
+    hcall = rr.HostMarshalled(hp, hs, pd, rr.alloc_solution(pd), ws=call.ws)
+    for _ in range(3):
+        hcall.launch(stream)
+    torch.cuda.synchronize()
+    evh = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for s_, e_ in evh:
+        s_.record(stream)
+        hcall.launch(stream)
+        e_.record(stream)
+    torch.cuda.synchronize()
+    us_h = statistics.median(s_.elapsed_time(e_) * 1e3 for s_, e_ in evh)
+    o = oracle.rr_solve_t2(p)
+    err = max(float(abs(hs[k].numpy() - o[k]).max() / abs(o[k]).max()) for k in ("x", "u", "y"))
+    t_or = []
+    for _ in range(21):
+        t0 = time.perf_counter()
+        oracle.rr_solve_t2(p, nthreads=1)
+        t_or.append(time.perf_counter() - t0)
+    print(json.dumps({
+        "metric": "regularized-LQR single-instance latency (C1 double integrator)", "value": us, "unit": "us",
+        "n_gpus": 1, "steps": K, "warmup": a.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
+        "scaling": "none", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C1: 1 double integrator n_x=2 n_u=1 N=10, terminal equality folded (eta=1e4), delta=1e-4"},
+        "kernel": "rr_fused_kernel<2,1> (lane group of 4)",
+        "e2e": {"value": us_h, "unit": "us", "h2d_bytes_per_step": hcall.h2d_bytes, "d2h_bytes_per_step": hcall.d2h_bytes,
+                "path": "rr_factor_solve_host (C-ABI, pinned host buffers)"},
+        "max_rel_err_vs_oracle": err, "roofline": None,
+        "cpu_baseline": {"value": statistics.median(t_or) * 1e6, "unit": "us", "cores": 1, "kind": "oracle",
+                         "sample": "the C1 instance, T2 plain-C oracle through ctypes, median of 21"},
+        "gpu_launches": K}), flush=True)
 
 
 if __name__ == "__main__":
