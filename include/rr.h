@@ -189,6 +189,22 @@ rr_err rr_solve(const rr_dims* dims, const rr_problem* prob, const void* factor,
                 const rr_factor_buf* fac, const rr_solution* sol, void* workspace, int64_t workspace_bytes,
                 int32_t* status, void* stream);
 
+/* ======================== parallel-in-time solve (the paper's future work) ========================
+ * rr_factor_solve_pit: the same solution (x, u, y) as rr_factor_solve, computed with O(log N) depth
+ * instead of N sequential stages -- for few instances with long horizons (latency).  For δ > 0 the
+ * regularized system is equivalent to (δP + CᵀC) z = −(δs + Cᵀc), y = (Cz + c)/δ: the
+ * controls are eliminated stage by stage (Schur complement on δR_i + B_iᵀB_i), the remaining
+ * block-tridiagonal SPD system in x_0..x_N is solved by block cyclic reduction (⌈log2(N+1)⌉ levels),
+ * then u_i follows per stage and y from the dual identity y = (Cz + c)/δ.
+ * Requires δ > 0 for every instance (y carries a cancellation error of order ε|x|/δ: intended for
+ * δ >= 1e-6); nx, nu <= 16; RR_FLAG_SHARED_* accepted.  status: 0, RR_ST_G_NOT_PD | stage << 8,
+ * RR_ST_S_NOT_PD | index << 8 (a non-positive pivot of the reduced system), RR_ST_NONFINITE.
+ * workspace: >= rr_pit_workspace_bytes(dims) device bytes.
+ */
+int64_t rr_pit_workspace_bytes(const rr_dims* dims);
+rr_err rr_factor_solve_pit(const rr_dims* dims, const rr_problem* prob, const rr_solution* sol, void* workspace,
+                           int64_t workspace_bytes, int32_t* status, void* stream);
+
 /* ================================ KKT residual (the paper's third callback) ================================
  * rr_residual: r = K [x; y] + [s; c] for the §1.4 system K [x; y] = −[s; c], i.e. the
  * paper's "KKT system residual computation callback", block by block:

@@ -113,6 +113,11 @@ def lib():
             L.rr_solve.argtypes = [ctypes.POINTER(rr_dims), ctypes.POINTER(rr_problem), ctypes.c_void_p,
                                    ctypes.c_int64, ctypes.POINTER(rr_factor_buf), ctypes.POINTER(rr_solution),
                                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+            L.rr_pit_workspace_bytes.restype = ctypes.c_int64
+            L.rr_pit_workspace_bytes.argtypes = [ctypes.POINTER(rr_dims)]
+            L.rr_factor_solve_pit.restype = ctypes.c_int32
+            L.rr_factor_solve_pit.argtypes = [ctypes.POINTER(rr_dims), ctypes.POINTER(rr_problem), ctypes.POINTER(rr_solution),
+                                              ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
             L.rr_residual.restype = ctypes.c_int32
             L.rr_residual.argtypes = [ctypes.POINTER(rr_dims), ctypes.POINTER(rr_problem), ctypes.POINTER(rr_solution),
                                       ctypes.POINTER(rr_residual_buf), ctypes.c_void_p, ctypes.c_void_p]

@@ -8,6 +8,7 @@
 #include "ipm_solve.cuh"
 #include "rr_fused.cuh"
 #include "rr_split.cuh"
+#include "rr_pit.cuh"
 
 namespace {
 thread_local char g_err[512] = "";
@@ -245,6 +246,47 @@ rr_err rr_residual(const rr_dims* dims, const rr_problem* prob, const rr_solutio
   cudaError_t e = rrk::residual_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_residual: unsupported shape%s");
   if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_residual: CUDA error %s", cudaGetErrorString(e));
+  return RR_OK;
+}
+
+int64_t rr_pit_workspace_bytes(const rr_dims* dims) {
+  if (!dims_ok(dims)) return -1;
+  return rrk::pit_ws_bytes(dims->nx, dims->nu, dims->N, dims->batch);
+}
+
+rr_err rr_factor_solve_pit(const rr_dims* dims, const rr_problem* prob, const rr_solution* sol, void* workspace,
+                           int64_t workspace_bytes, int32_t* status, void* stream) {
+  if (!dims_ok(dims)) return set_err(RR_E_INVALID, "rr_factor_solve_pit: invalid dims%s");
+  if (prob == nullptr || sol == nullptr) return set_err(RR_E_INVALID, "rr_factor_solve_pit: null %s", "prob/sol");
+  if (dims->batch == 0) return RR_OK;
+  if (status == nullptr) return set_err(RR_E_INVALID, "rr_factor_solve_pit: null %s", "status");
+  const double* req[] = {prob->QN, prob->qN, prob->c0, prob->delta, sol->x, sol->y};
+  for (const double* p : req)
+    if (p == nullptr) return set_err(RR_E_INVALID, "rr_factor_solve_pit: null %s", "terminal operand / solution");
+  if (dims->N > 0) {
+    const double* req2[] = {prob->A, prob->B, prob->Q, prob->M, prob->R, prob->q, prob->r, prob->c, sol->u};
+    for (const double* p : req2)
+      if (p == nullptr) return set_err(RR_E_INVALID, "rr_factor_solve_pit: null %s", "stage operand / u");
+  }
+  const int64_t need = rr_pit_workspace_bytes(dims);
+  if (need < 0) return set_err(RR_E_UNSUPPORTED, "rr_factor_solve_pit: nx, nu must be <= 16%s");
+  if (workspace == nullptr || workspace_bytes < need)
+    return set_err(RR_E_INVALID, "rr_factor_solve_pit: workspace missing or smaller than %s", "rr_pit_workspace_bytes()");
+  rrk::PitArgs a{};
+  a.nx = dims->nx;
+  a.nu = dims->nu;
+  a.N = dims->N;
+  a.batch = dims->batch;
+  a.p = *prob;
+  a.s = *sol;
+  a.ws = static_cast<double*>(workspace);
+  a.status = status;
+  a.shared = dims->flags & SHARED_FLAGS;
+  a.refine = 1;
+  if (!rrk::split_supported(dims->nx, dims->nu))
+    return set_err(RR_E_UNSUPPORTED, "rr_factor_solve_pit: no residual kernel for this (nx, nu)%s");
+  cudaError_t e = rrk::pit_launch(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_factor_solve_pit: CUDA error %s", cudaGetErrorString(e));
   return RR_OK;
 }
 

@@ -185,6 +185,27 @@ def rr_solve(prob, factor, out=None, fac=None, workspace=None, stream=None, accu
     return sol
 
 
+def rr_factor_solve_pit(prob, out=None, workspace=None, stream=None):
+    """Parallel-in-time solve: the same x, u, y, status as rr_factor_solve, with
+    O(log N) depth (block cyclic reduction on the δ-reduced state system); needs δ > 0."""
+    if not prob.delta.is_cuda:
+        raise RRError("rr_factor_solve_pit needs CUDA tensors (no CPU fallback)")
+    dev = prob.delta.device
+    sol = out if out is not None else alloc_solution(prob)
+    d = dims_of(prob)
+    if workspace is None:
+        nb = lib().rr_pit_workspace_bytes(ctypes.byref(d))
+        if nb < 0:
+            raise RRError("rr_factor_solve_pit: nx, nu must be <= 16")
+        workspace = torch.empty((nb + 7) // 8, dtype=torch.float64, device=dev)
+    p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
+    s = rr_solution(_p(sol["x"]), _p(sol["u"]), _p(sol["y"]))
+    rc = lib().rr_factor_solve_pit(ctypes.byref(d), ctypes.byref(p), ctypes.byref(s), _p(workspace),
+                                   workspace.numel() * 8, _p(sol["status"]), _stream(stream, dev))
+    check(rc, "rr_factor_solve_pit")
+    return sol
+
+
 RESIDUAL_FIELDS = ("q", "r", "c", "qN", "c0")
 
 

@@ -1,0 +1,66 @@
+"""GPU parity of the parallel-in-time solve (rr_factor_solve_pit, the paper's future
+work P:688-691) against the oracle T2: the same unique solution of the regularized system, computed
+by block cyclic reduction on the δ-reduced state system.  FP64 bar 1e-9 (y is recovered through
+y = (Cz + c)/δ, so δ >= 1e-6 is required for that bar)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def rr():
+    import paper_2509_16370_b200 as m
+    return m
+
+
+def rel(g, o):
+    g = np.asarray(g).reshape(len(g), -1)
+    o = np.asarray(o).reshape(len(o), -1)
+    if g.size == 0:
+        return 0.0
+    return float(np.max(np.max(np.abs(g - o), axis=1) / np.maximum(np.max(np.abs(o), axis=1), 1e-300)))
+
+
+@pytest.mark.parametrize("nx,nu,N,batch", [(12, 4, 100, 3), (12, 4, 1, 4), (12, 4, 2, 2), (4, 1, 37, 5),
+                                           (2, 1, 10, 1), (3, 2, 64, 2), (16, 16, 9, 2), (5, 3, 0, 2),
+                                           (7, 6, 129, 2)])
+@pytest.mark.parametrize("delta", [1e-4, 1e-2, 1.0])
+def test_pit_parity(nx, nu, N, batch, delta):
+    p = synth.random_stable_lqr(nx, nu, N, batch, seed=nx * 13 + N, delta=delta)
+    out = rr().rr_factor_solve_pit(p.to("cuda"))
+    torch.cuda.synchronize()
+    o = oracle.rr_solve_t2(p)
+    assert np.all(out["status"].cpu().numpy() == 0)
+    for k in ("x", "u", "y"):
+        assert rel(out[k].cpu().numpy(), o[k]) <= 1e-9, (k, rel(out[k].cpu().numpy(), o[k]))
+
+
+def test_pit_c1_golden_and_long_horizon():
+    m = rr()
+    p = synth.double_integrator_c1()
+    out = m.rr_factor_solve_pit(p.to("cuda"))
+    o = oracle.rr_solve_t2(p)
+    for k in ("x", "u", "y"):
+        assert rel(out[k].cpu().numpy(), o[k]) <= 1e-9
+    q = synth.random_stable_lqr(12, 4, 2048, 1, seed=5, delta=1e-4)
+    a = m.rr_factor_solve_pit(q.to("cuda"))
+    b = m.rr_factor_solve(q.to("cuda"))
+    torch.cuda.synchronize()
+    for k in ("x", "u", "y"):
+        assert rel(a[k].cpu().numpy(), b[k].cpu().numpy()) <= 1e-9
+
+
+def test_pit_shared_and_failure():
+    m = rr()
+    p = synth.lti_problem(12, 4, 33, 3, seed=2, delta=1e-3)
+    out = m.rr_factor_solve_pit(p.to("cuda"))
+    o = oracle.rr_solve_t2(p.expanded())
+    for k in ("x", "u", "y"):
+        assert rel(out[k].cpu().numpy(), o[k]) <= 1e-9
+    z = synth.random_stable_lqr(4, 1, 6, 3, seed=4).with_delta(0.0)   # δ = 0: outside the method
+    bad = m.rr_factor_solve_pit(z.to("cuda"))
+    assert np.all(bad["status"].cpu().numpy() != 0)
