@@ -42,12 +42,13 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample wall time")
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "split", "c4solve"],
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "split", "c4solve", "pit"],
                     help="c2 (default, BASELINE configs[1]); c3 = 4,096 dense n64 m32 N50 (configs[2]); "
                          "c4 = ipm_step on 16,384 cart-pole instances (configs[3]); c5 = 1,048,576 "
                          "quadrotor n12 m4 N200 sharded over the ranks, chunks of 65,536 (configs[4]); split = "
                          "rr_factor + rr_solve + rr_residual on the C2 workload, each kernel timed; c4solve = ipm_solve "
-                         "(20 IPM iterations) on the C4 cart-pole batch; c1 = single double-integrator instance latency")
+                         "(20 IPM iterations) on the C4 cart-pole batch; c1 = single double-integrator instance latency; "
+                         "pit = single-instance latency, parallel-in-time vs sequential, long horizons")
     ap.add_argument("--c5-total", type=int, default=1048576, help=argparse.SUPPRESS)
     return ap.parse_args()
 
@@ -231,6 +232,8 @@ def main():
         return run_c4solve(a, ws, rank, local)
     if a.workload == "c1":
         return run_c1(a, ws, rank, local)
+    if a.workload == "pit":
+        return run_pit(a, ws, rank, local)
     global NX, NU, HORIZON, BATCH, SEED, ALG_BYTES_PER_STAGE, ALG_FLOPS_PER_STAGE
     if a.workload == "c3":
         # 206,208 B and 2.42M flop per stage (algorithmic)
@@ -699,6 +702,59 @@ def run_c1(a, ws, rank, local):
         "cpu_baseline": {"value": statistics.median(t_or) * 1e6, "unit": "us", "cores": 1, "kind": "oracle",
                          "sample": "the C1 instance, T2 plain-C oracle through ctypes, median of 21"},
         "gpu_launches": K}), flush=True)
+
+
+def run_pit(a, ws, rank, local):
+    """Extra line: single-instance latency of the parallel-in-time solve
+    (rr_factor_solve_pit: O(log N) levels + one refinement) against the sequential fused recursion
+    (rr_factor_solve: N dependent stages) on C2-recipe instances (n=12, m=4, δ=1e-4) with long
+    horizons.  CUDA events around each call, median of K."""
+    import torch
+    import synth
+    import paper_2509_16370_b200 as rr
+    if rank != 0:
+        return
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    K = max(a.steps, 10)
+
+    def lat(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for s_, e_ in ev:
+            s_.record(stream)
+            fn()
+            e_.record(stream)
+        torch.cuda.synchronize()
+        return statistics.median(s_.elapsed_time(e_) for s_, e_ in ev)
+    rows = []
+    for N in (64, 512, 4096):
+        p = synth.random_stable_lqr(12, 4, N, 1, SEED, DELTA, device=dev)
+        sol = rr.alloc_solution(p)
+        call = rr.Marshalled(p, sol)
+        t_seq = lat(lambda: call.launch(stream))
+        ws_ = torch.empty((rr._lib.lib().rr_pit_workspace_bytes(ctypes_dims(rr, p)) + 7) // 8, dtype=torch.float64,
+                          device=dev)
+        sol2 = rr.alloc_solution(p)
+        t_pit = lat(lambda: rr.rr_factor_solve_pit(p, out=sol2, workspace=ws_, stream=stream))
+        err = max(float(((sol2[k] - sol[k]).abs().max() / sol[k].abs().max()).item()) for k in ("x", "u", "y"))
+        rows.append({"N": N, "sequential_ms": t_seq, "pit_ms": t_pit, "speedup": t_seq / t_pit, "max_rel_diff": err})
+    best = rows[-1]
+    print(json.dumps({
+        "metric": "regularized-LQR single-instance latency, parallel-in-time vs sequential (n=12 m=4, N=4096)",
+        "value": best["pit_ms"] * 1e3, "unit": "us", "n_gpus": 1, "steps": K, "warmup": 3,
+        "ms_per_step": best["pit_ms"], "higher_is_better": False, "scaling": "none", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "1 random stable regularized LQR (C2 recipe) n_x=12 n_u=4 delta=1e-4, N in {64, 512, 4096}"},
+        "horizons": rows, "roofline": None, "gpu_launches": None}), flush=True)
+
+
+def ctypes_dims(rr, p):
+    import ctypes
+    from paper_2509_16370_b200.rr import dims_of
+    return ctypes.byref(dims_of(p))
 
 
 if __name__ == "__main__":

@@ -283,8 +283,6 @@ rr_err rr_factor_solve_pit(const rr_dims* dims, const rr_problem* prob, const rr
   a.status = status;
   a.shared = dims->flags & SHARED_FLAGS;
   a.refine = 1;
-  if (!rrk::split_supported(dims->nx, dims->nu))
-    return set_err(RR_E_UNSUPPORTED, "rr_factor_solve_pit: no residual kernel for this (nx, nu)%s");
   cudaError_t e = rrk::pit_launch(a, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_factor_solve_pit: CUDA error %s", cudaGetErrorString(e));
   return RR_OK;

@@ -26,7 +26,6 @@
 
 #include "rr_common.cuh"
 #include "rr_pit.cuh"
-#include "rr_split.cuh"
 
 namespace rrk {
 
@@ -626,6 +625,65 @@ __global__ void __launch_bounds__(WPB * 32) pit_rhs_root_kernel(PitArgs a) {
   }
 }
 
+// KKT residual r = K[x; y] + [s; c] (as rr_residual), one warp per (instance, stage i):
+// rows x_i, u_i, primal row i+1 (item i < N); rows x_N and primal row 0 (item N) -- stage-parallel,
+// unlike rr_residual's lane group walking the horizon, so a single long instance is not serialised
+__global__ void __launch_bounds__(WPB * 32) pit_residual_kernel(PitArgs a, rr_residual_buf rb) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
+  const int n = a.nx, m = a.nu, N = a.N;
+  if (item >= a.batch * (int64_t)(N + 1)) return;
+  const int64_t inst = item / (N + 1);
+  const int i = (int)(item % (N + 1));
+  const double d = a.p.delta[inst];
+  const double* x = a.s.x + inst * (int64_t)(N + 1) * n;
+  const double* y = a.s.y + inst * (int64_t)(N + 1) * n;
+  const int sn = n * (n + 1) / 2, smm = m * (m + 1) / 2;
+  if (i == N) {
+    const int64_t iP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;
+    if (lane < n) {
+      double g = a.p.qN[inst * n + lane] - y[(int64_t)N * n + lane];
+      for (int k = 0; k < n; ++k) g = fma(a.p.QN[iP * sn + pk(n, lane, k)], x[(int64_t)N * n + k], g);
+      rb.qN[inst * n + lane] = g;
+      rb.c0[inst * n + lane] = a.p.c0[inst * n + lane] - x[lane] - d * y[lane];
+    }
+    return;
+  }
+  const int64_t s = inst * N + i;
+  const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst) * N + i;
+  const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : inst) * N + i;
+  const double *A = a.p.A + sD * n * n, *B = a.p.B + sD * n * m;
+  const double *Q = a.p.Q + sP * sn, *M = a.p.M + sP * n * m, *R = a.p.R + sP * smm;
+  const double* xi = x + (int64_t)i * n;
+  const double* x1 = xi + n;
+  const double* yi = y + (int64_t)i * n;
+  const double* y1 = yi + n;
+  const double* u = a.s.u + s * m;
+  if (lane < n) {  // stationarity x_i and primal row i+1, entry `lane`
+    double g = a.p.q[s * n + lane] - yi[lane], pr = a.p.c[s * n + lane] - x1[lane] - d * y1[lane];
+    for (int k = 0; k < n; ++k) {
+      g = fma(Q[pk(n, lane, k)], xi[k], g);
+      g = fma(A[k + lane * n], y1[k], g);
+      pr = fma(A[lane + k * n], xi[k], pr);
+    }
+    for (int k = 0; k < m; ++k) {
+      g = fma(M[lane + k * n], u[k], g);
+      pr = fma(B[lane + k * n], u[k], pr);
+    }
+    rb.q[s * n + lane] = g;
+    rb.c[s * n + lane] = pr;
+  } else if (lane - 16 >= 0 && lane - 16 < m) {  // stationarity u_i
+    const int w = lane - 16;
+    double g = a.p.r[s * m + w];
+    for (int k = 0; k < n; ++k) {
+      g = fma(M[k + w * n], xi[k], g);
+      g = fma(B[k + w * n], y1[k], g);
+    }
+    for (int k = 0; k < m; ++k) g = fma(R[pk(m, w, k)], u[k], g);
+    rb.r[s * m + w] = g;
+  }
+}
+
 __global__ void pit_axpy_kernel(double* __restrict__ y, const double* __restrict__ x, int64_t cnt) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < cnt) y[t] += x[t];
@@ -694,19 +752,7 @@ cudaError_t pit_launch(const PitArgs& a, cudaStream_t s) {
   double* cu = cx + b * (N + 1) * n;
   double* cy = cu + b * N * m;
   for (int it = 0; it < a.refine; ++it) {
-    ResArgs ra{};
-    ra.nx = n;
-    ra.nu = m;
-    ra.N = N;
-    ra.batch = b;
-    ra.p = a.p;
-    ra.s = a.s;
-    ra.r = rb;
-    ra.norms = nullptr;
-    ra.shared = a.shared;
-    bool sup = false;
-    cudaError_t e = residual_launch(ra, s, &sup);
-    if (e != cudaSuccess || !sup) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    pit_residual_kernel<<<blocks_for(b * (N + 1)), WPB * 32, 0, s>>>(a, rb);
     PitArgs c = a;  // the correction system: right-hand side = the residual
     c.p.q = rb.q;
     c.p.r = rb.r;
