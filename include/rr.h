@@ -318,6 +318,33 @@ rr_err ipm_step(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iter
                 const ipm_params* params, const ipm_result* res, void* workspace, int64_t workspace_bytes,
                 int32_t* status, void* stream);
 
+/* ======================= caller-evaluated line search (user models) =======================
+ * For models other than the built-in ones, the step is split in three calls:
+ *   ipm_direction: rows a1-a7 of ipm_step (same arguments): the direction (res->dx..dzN), D, 𝒜(0)
+ *     (merit0), the fraction-to-boundary caps α_max (alpha_p) and α_d (alpha_d); no line search, the
+ *     iterate is not modified.
+ *   ipm_merit: 𝒜(α) = f − μΣlog(s+αΔs) + yᵀc + λᵀc_e + zᵀ(g+s+αΔs) + η/2(‖c‖² + ‖c_e‖² + ‖g+s+αΔs‖²)
+ *     (reading R14) at the trial point, from the caller's model values there (ipm_trial_values,
+ *     layouts of ipm_stage_data: f, d_i(trial) − x_{i+1}(trial), c_e, g); c_0 = s_0 − (x_0 + αΔx_0) and the
+ *     trial slacks are formed inside.  alpha, merit: [b] device arrays; NaN if a trial slack is <= 0.
+ *   ipm_update: x, u, s, y, λ += α_p Δ; z += α_d Δz (reading R12) for the caller's accepted α_p, α_d
+ *     ([b] device arrays; 0 leaves an instance untouched).
+ */
+typedef struct {
+  const double* fval;             /* [b]            f at the trial point               */
+  const double* dres;             /* [b][N][n]      d_i(x_i, u_i) − x_{i+1} at the trial */
+  const double *ce, *ceN;         /* [b][N][nc], [b][ncN]                              */
+  const double *gv, *gvN;         /* [b][N][ng], [b][ngN]                              */
+} ipm_trial_values;
+
+rr_err ipm_direction(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it,
+                     const ipm_params* params, const ipm_result* res, void* workspace, int64_t workspace_bytes,
+                     int32_t* status, void* stream);
+rr_err ipm_merit(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it, const ipm_result* res,
+                 const double* alpha, const ipm_trial_values* trial, double* merit, void* stream);
+rr_err ipm_update(const ipm_dims* dims, const ipm_iterate* it, const ipm_result* res, const double* alpha_p,
+                  const double* alpha_d, void* stream);
+
 /* ================================ batched IPM solve ================================
  * ipm_solve: repeated ipm_step on every instance until its KKT residual meets the tolerance.  The
  * paper fixes the step but not the outer loop; the loop is SPEC's ipm_solve /

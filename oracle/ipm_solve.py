@@ -199,3 +199,40 @@ def ipm_solve_oracle(batch, settings: SolveSettings = SolveSettings(), nthreads=
     if record:
         rep["trace"] = trace
     return it, rep
+
+
+def merit_at_values(batch, res, alpha, trial):
+    """𝒜(x̄ + αΔx, s + αΔs; y, λ, z, μ, η) from caller-evaluated values at the trial point (P:61-66,
+    reading R14): f − μΣlog(s+αΔs) + yᵀc + λᵀc_e + zᵀ(g+s+αΔs) + η/2(‖c‖² + ‖c_e‖² + ‖g+s+αΔs‖²),
+    c = (s_0 − x_0 − αΔx_0, d_i(trial) − x_{i+1}(trial)).  Every argument numpy; returns [b]."""
+    it = {k: np.asarray(v.detach().cpu().numpy() if hasattr(v, "detach") else v, dtype=np.float64)
+          for k, v in batch.it.items()}
+    s0 = np.asarray(batch.data["s0"].cpu().numpy() if hasattr(batch.data["s0"], "cpu") else batch.data["s0"])
+    b = it["mu"].shape[0]
+    al = np.asarray(alpha, dtype=np.float64)
+    out = np.zeros(b)
+    for k in range(b):
+        a = al[k]
+        terms_lin, terms_pen, bar = 0.0, 0.0, 0.0
+        ok = True
+        for sk, dk, zk, gk in (("s", "ds", "z", "gv"), ("sN", "dsN", "zN", "gvN")):
+            if it[sk].size == 0:
+                continue
+            sa = it[sk][k] + a * res[dk][k]
+            if np.any(sa <= 0):
+                ok = False
+            ga = trial[gk][k] + sa
+            bar += np.sum(np.log(np.where(sa > 0, sa, 1.0)))
+            terms_lin += np.sum(it[zk][k] * ga)
+            terms_pen += np.sum(ga * ga)
+        for lk, ck in (("lam", "ce"), ("lamN", "ceN")):
+            if it[lk].size == 0:
+                continue
+            terms_lin += np.sum(it[lk][k] * trial[ck][k])
+            terms_pen += np.sum(trial[ck][k] ** 2)
+        c0 = s0[k] - (it["x"][k, 0] + a * res["dx"][k, 0])
+        cd = trial["dres"][k]
+        terms_lin += np.sum(it["y"][k, 0] * c0) + np.sum(it["y"][k, 1:] * cd)
+        terms_pen += np.sum(c0 * c0) + np.sum(cd * cd)
+        out[k] = (trial["fval"][k] - it["mu"][k] * bar + terms_lin + 0.5 * it["eta"][k] * terms_pen) if ok else np.nan
+    return out

@@ -7,6 +7,6 @@ from .rr import (rr_factor_solve, alloc_solution, alloc_factor, alloc_workspace,
                  rr_factor, rr_solve, factor_bytes, factor_record_doubles, solve_workspace_bytes,
                  rr_residual, rr_refine, rr_factor_solve_pit)
 
-from .ipm import ipm_step, IpmCall, ipm_solve, IpmSolveCall  # noqa: F401,E402
+from .ipm import ipm_step, IpmCall, ipm_solve, IpmSolveCall, ipm_direction, ipm_merit, ipm_update  # noqa: F401,E402
 
 __version__ = "0.1"

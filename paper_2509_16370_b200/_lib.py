@@ -76,6 +76,10 @@ class ipm_solve_report(ctypes.Structure):
     _fields_ = [(f, ctypes.c_void_p) for f in ("status", "iters", "mu", "eta", "r_stat", "r_feas", "r_comp")]
 
 
+class ipm_trial_values(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in ("fval", "dres", "ce", "ceN", "gv", "gvN")]
+
+
 class ipm_result(ctypes.Structure):
     _fields_ = [(f, ctypes.c_void_p) for f in IPM_RES_FIELDS]
 
@@ -129,6 +133,18 @@ def lib():
             L.ipm_solve.argtypes = [ctypes.POINTER(ipm_dims), ctypes.POINTER(ipm_stage_data), ctypes.POINTER(ipm_iterate),
                                     ctypes.POINTER(ipm_solve_settings), ctypes.POINTER(ipm_solve_report),
                                     ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+            L.ipm_direction.restype = ctypes.c_int32
+            L.ipm_direction.argtypes = [ctypes.POINTER(ipm_dims), ctypes.POINTER(ipm_stage_data),
+                                        ctypes.POINTER(ipm_iterate), ctypes.POINTER(ipm_params),
+                                        ctypes.POINTER(ipm_result), ctypes.c_void_p, ctypes.c_int64,
+                                        ctypes.c_void_p, ctypes.c_void_p]
+            L.ipm_merit.restype = ctypes.c_int32
+            L.ipm_merit.argtypes = [ctypes.POINTER(ipm_dims), ctypes.POINTER(ipm_stage_data), ctypes.POINTER(ipm_iterate),
+                                    ctypes.POINTER(ipm_result), ctypes.c_void_p, ctypes.POINTER(ipm_trial_values),
+                                    ctypes.c_void_p, ctypes.c_void_p]
+            L.ipm_update.restype = ctypes.c_int32
+            L.ipm_update.argtypes = [ctypes.POINTER(ipm_dims), ctypes.POINTER(ipm_iterate), ctypes.POINTER(ipm_result),
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
             L.ipm_step.restype = ctypes.c_int32
             L.ipm_step.argtypes = [ctypes.POINTER(ipm_dims), ctypes.POINTER(ipm_stage_data),
                                    ctypes.POINTER(ipm_iterate), ctypes.POINTER(ipm_params),

@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
   double alpha = amax, Aacc = __longlong_as_double(0x7ff8000000000000LL);
   int nb = 0;
   bool accepted = false;
-  if (status == 0) {
+  if (status == 0 && !a.direction_only) {
     for (nb = 0; nb <= a.prm.max_backtracks; ++nb) {
       LogAcc sl;
       double sdyn = 0.0;

@@ -17,10 +17,16 @@ struct IpmArgs {
   int32_t* status;
   const int32_t* list = nullptr;   // ipm_solve: active instance ids (nullptr: all instances)
   const int32_t* count = nullptr;  // device count of `list`
+  int direction_only = 0;          // ipm_direction: rows a1-a7 only (no line search, no update)
 };
 
 int64_t ipm_ws_bytes(const ipm_dims& d);
 cudaError_t ipm_launch(const IpmArgs& a, cudaStream_t s, bool* supported);
 bool ipm_supported(const ipm_dims& d);
+// caller-evaluated line search (ipm_user.cu)
+cudaError_t ipm_merit_launch(const ipm_dims& d, const ipm_stage_data& data, const ipm_iterate& it, const ipm_result& r,
+                             const double* alpha, const ipm_trial_values& tv, double* merit, cudaStream_t s);
+cudaError_t ipm_update_launch(const ipm_dims& d, const ipm_iterate& it, const ipm_result& r, const double* alpha_p,
+                              const double* alpha_d, cudaStream_t s);
 
 }  // namespace rrk

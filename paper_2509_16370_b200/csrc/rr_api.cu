@@ -298,8 +298,50 @@ int64_t ipm_workspace_bytes(const ipm_dims* dims) {
   return rrk::ipm_ws_bytes(*dims);
 }
 
+static rr_err ipm_step_impl(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it,
+                            const ipm_params* params, const ipm_result* res, void* workspace, int64_t workspace_bytes,
+                            int32_t* status, void* stream, int direction_only);
+
 rr_err ipm_step(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it, const ipm_params* params,
                 const ipm_result* res, void* workspace, int64_t workspace_bytes, int32_t* status, void* stream) {
+  return ipm_step_impl(dims, data, it, params, res, workspace, workspace_bytes, status, stream, 0);
+}
+
+rr_err ipm_direction(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it, const ipm_params* params,
+                     const ipm_result* res, void* workspace, int64_t workspace_bytes, int32_t* status, void* stream) {
+  return ipm_step_impl(dims, data, it, params, res, workspace, workspace_bytes, status, stream, 1);
+}
+
+rr_err ipm_merit(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it, const ipm_result* res,
+                 const double* alpha, const ipm_trial_values* trial, double* merit, void* stream) {
+  if (!ipm_dims_ok(dims)) return set_err(RR_E_INVALID, "ipm_merit: invalid dims%s");
+  if (!data || !it || !res || !trial) return set_err(RR_E_INVALID, "ipm_merit: null %s", "argument");
+  if (dims->batch == 0) return RR_OK;
+  if (!alpha || !merit || !trial->fval || !data->s0 || !it->x || !it->y || !it->mu || !it->eta || !res->dx ||
+      (dims->N > 0 && !trial->dres) || (dims->ng > 0 && (!trial->gv || !it->s || !it->z || !res->ds)) ||
+      (dims->ngN > 0 && (!trial->gvN || !it->sN || !it->zN || !res->dsN)) || (dims->nc > 0 && (!trial->ce || !it->lam)) ||
+      (dims->ncN > 0 && (!trial->ceN || !it->lamN)))
+    return set_err(RR_E_INVALID, "ipm_merit: null %s", "required pointer");
+  cudaError_t e = rrk::ipm_merit_launch(*dims, *data, *it, *res, alpha, *trial, merit, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return set_err(RR_E_CUDA, "ipm_merit: CUDA error %s", cudaGetErrorString(e));
+  return RR_OK;
+}
+
+rr_err ipm_update(const ipm_dims* dims, const ipm_iterate* it, const ipm_result* res, const double* alpha_p,
+                  const double* alpha_d, void* stream) {
+  if (!ipm_dims_ok(dims)) return set_err(RR_E_INVALID, "ipm_update: invalid dims%s");
+  if (!it || !res) return set_err(RR_E_INVALID, "ipm_update: null %s", "argument");
+  if (dims->batch == 0) return RR_OK;
+  if (!alpha_p || !alpha_d || !it->x || !it->y || !res->dx || !res->dy)
+    return set_err(RR_E_INVALID, "ipm_update: null %s", "required pointer");
+  cudaError_t e = rrk::ipm_update_launch(*dims, *it, *res, alpha_p, alpha_d, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return set_err(RR_E_CUDA, "ipm_update: CUDA error %s", cudaGetErrorString(e));
+  return RR_OK;
+}
+
+static rr_err ipm_step_impl(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it,
+                            const ipm_params* params, const ipm_result* res, void* workspace, int64_t workspace_bytes,
+                            int32_t* status, void* stream, int direction_only) {
   if (!ipm_dims_ok(dims)) return set_err(RR_E_INVALID, "ipm_step: invalid dims%s");
   if (!data || !it || !params || !res) return set_err(RR_E_INVALID, "ipm_step: null %s", "argument");
   if (dims->batch == 0) return RR_OK;  // nothing to do; status may be null for an empty batch
@@ -324,6 +366,7 @@ rr_err ipm_step(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iter
   a.r = *res;
   a.ws = static_cast<double*>(workspace);
   a.status = status;
+  a.direction_only = direction_only;
   bool supported = false;
   cudaError_t e = rrk::ipm_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "ipm_step: unsupported dims%s");

@@ -7,7 +7,7 @@ import ctypes
 import torch
 
 from ._lib import (IPM_DATA_FIELDS, IPM_ITER_FIELDS, IPM_RES_FIELDS, RRError, check, ipm_dims, ipm_iterate,
-                   ipm_params, ipm_result, ipm_solve_report, ipm_solve_settings, ipm_stage_data, lib)
+                   ipm_params, ipm_result, ipm_solve_report, ipm_solve_settings, ipm_stage_data, ipm_trial_values, lib)
 
 RES_SHAPE_OF = dict(dx="x", du="u", ds="s", dsN="sN", dy="y", dlam="lam", dlamN="lamN", dz="z", dzN="zN")
 
@@ -59,12 +59,13 @@ class IpmCall:
         self.st = _p(self.res["status"])
         self.wsp, self.wsb = _p(self.ws), self.ws.numel() * 8
 
-    def launch(self, stream=None):
+    def launch(self, stream=None, direction_only=False):
         s = stream if stream is not None else torch.cuda.current_stream(self.b.it["mu"].device)
-        rc = lib().ipm_step(ctypes.byref(self.d), ctypes.byref(self.data), ctypes.byref(self.it),
-                            ctypes.byref(self.prm), ctypes.byref(self.r), self.wsp, self.wsb, self.st,
-                            ctypes.c_void_p(s.cuda_stream))
-        check(rc, "ipm_step")
+        fn = lib().ipm_direction if direction_only else lib().ipm_step
+        rc = fn(ctypes.byref(self.d), ctypes.byref(self.data), ctypes.byref(self.it),
+                ctypes.byref(self.prm), ctypes.byref(self.r), self.wsp, self.wsb, self.st,
+                ctypes.c_void_p(s.cuda_stream))
+        check(rc, "ipm_direction" if direction_only else "ipm_step")
         return self.res
 
 
@@ -116,3 +117,37 @@ def ipm_solve(b, stream=None, **settings):
     iterate) with the batched regularized IPM; b.it is updated in place.  Returns the report
     (status, iters, mu, eta, r_stat, r_feas, r_comp)."""
     return IpmSolveCall(b, **settings).launch(stream)
+
+
+def ipm_direction(b, tau=0.995, armijo_c=1e-4, beta=0.5, max_backtracks=50, stream=None):
+    """Rows a1-a7 of the step for every instance of `b` (user models): the direction,
+    D, 𝒜(0) (merit0), α_max (alpha_p) and the dual cap α_d (alpha_d); the iterate is not modified."""
+    return IpmCall(b, tau=tau, armijo_c=armijo_c, beta=beta, max_backtracks=max_backtracks).launch(
+        stream, direction_only=True)
+
+
+TRIAL_FIELDS = ("fval", "dres", "ce", "ceN", "gv", "gvN")
+
+
+def ipm_merit(b, res, alpha, trial, out=None, stream=None):
+    """𝒜 at the trial points x̄ + αΔx, s + αΔs from the caller's model values there (`trial`: dict
+    fval, dres, ce, ceN, gv, gvN in the IPMBatch data layouts); alpha: [batch] CUDA tensor."""
+    dev = b.it["mu"].device
+    merit = out if out is not None else torch.empty(b.batch, dtype=torch.float64, device=dev)
+    tv = ipm_trial_values(*[_p(trial.get(f)) for f in TRIAL_FIELDS])
+    rc = lib().ipm_merit(ctypes.byref(dims_of(b)), ctypes.byref(ipm_stage_data(*[_p(b.data[f]) for f in IPM_DATA_FIELDS])),
+                         ctypes.byref(ipm_iterate(*[_p(b.it[f]) for f in IPM_ITER_FIELDS])),
+                         ctypes.byref(ipm_result(*[_p(res.get(f)) for f in IPM_RES_FIELDS])), _p(alpha),
+                         ctypes.byref(tv), _p(merit),
+                         ctypes.c_void_p((stream or torch.cuda.current_stream(dev)).cuda_stream))
+    check(rc, "ipm_merit")
+    return merit
+
+
+def ipm_update(b, res, alpha_p, alpha_d, stream=None):
+    """x, u, s, y, λ += α_p Δ and z += α_d Δz in place (per-instance [batch] CUDA tensors)."""
+    dev = b.it["mu"].device
+    rc = lib().ipm_update(ctypes.byref(dims_of(b)), ctypes.byref(ipm_iterate(*[_p(b.it[f]) for f in IPM_ITER_FIELDS])),
+                          ctypes.byref(ipm_result(*[_p(res.get(f)) for f in IPM_RES_FIELDS])), _p(alpha_p), _p(alpha_d),
+                          ctypes.c_void_p((stream or torch.cuda.current_stream(dev)).cuda_stream))
+    check(rc, "ipm_update")

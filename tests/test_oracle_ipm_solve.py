@@ -82,3 +82,24 @@ def test_random_lq_all_converge():
     it, rep = ipm_solve_oracle(b, SolveSettings())
     assert np.all(rep["status"] == 0)
     assert np.all(np.maximum(np.maximum(rep["r_stat"], rep["r_feas"]), rep["r_comp0"]) <= 1e-6)
+
+
+def test_merit_at_values_matches_c_oracle_on_lq():
+    """The caller-evaluated merit (numpy, the definition) equals the C oracle's merit for the LQ model,
+    whose trial values are exact from the linearisation (evaluate() at the trial point)."""
+    from oracle.ipm import ipm_merit_oracle, ipm_step_oracle
+    from oracle.ipm_solve import merit_at_values
+    b = random_lq_ocp(4, 2, 6, 3, seed=7, ng=2, ngN=1, nc=1, ncN=1)
+    res, _ = ipm_step_oracle(b)
+    for alpha in (0.0, 0.05, 0.3, 0.9):
+        x = b.it["x"].numpy() + alpha * res["dx"]
+        u = b.it["u"].numpy() + alpha * res["du"]
+        d = evaluate(b, x, u)
+        trial = {k: d[k] for k in ("fval", "dres", "ce", "ceN", "gv", "gvN")}
+        got = merit_at_values(b, res, np.full(3, alpha), trial)
+        for k in range(3):
+            ref = ipm_merit_oracle(b, res, k, alpha)
+            if np.isnan(ref):  # a trial slack left the positive orthant: both sides NaN
+                assert np.isnan(got[k])
+            else:
+                assert abs(got[k] - ref) <= 1e-10 * max(1.0, abs(ref)), (alpha, k, got[k], ref)
