@@ -168,3 +168,21 @@ def test_split_unsupported_and_empty():
     F, st = m.rr_factor(e)
     sol = m.rr_solve(e, F)
     assert sol["x"].numel() == 0
+
+
+def test_split_c2_full_size_sampled_parity():
+    """rr_factor + rr_solve (+ rr_residual) in the configuration `bench.py --workload split` times:
+    65,536 C2 instances; sampled instances against the oracle, all residual norms small."""
+    m = rr()
+    p = synth.random_stable_lqr_chunked(12, 4, 100, 65536, seed=2509, delta=1e-4, device="cuda")
+    F, st = m.rr_factor(p)
+    sol = m.rr_solve(p, F)
+    _, norms = m.rr_residual(p, sol)
+    torch.cuda.synchronize()
+    assert int(st.abs().sum()) == 0 and int(sol["status"].abs().sum()) == 0
+    assert float(norms.max()) < 1e-9
+    idx = torch.tensor(sorted(set(np.random.default_rng(5).integers(0, 65536, 128).tolist()) | {0, 65535}), device="cuda")
+    sub = p.select(idx)
+    o = oracle.rr_solve_t2(sub.to("cpu"), nthreads=8)
+    for k in ("x", "u", "y"):
+        assert blockwise_rel(sol[k][idx].cpu().numpy(), o[k]) <= TOL, k
