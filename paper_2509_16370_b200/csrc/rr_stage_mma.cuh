@@ -117,6 +117,59 @@ struct StageMMA {
   //   Pat(q, s, t): P_i[s][t] of instance q;  qjf(): this lane's entry of (q_i; r_i)
   //   wait_inputs(): waits for this stage's input copies (called after the S⁻¹ sweep, which needs
   //   none);  prefetch(): issues the next stage's input copies (called once the inputs are dead)
+  // S⁻¹ = (I + δV)⁻¹ by the symmetric sweep operator on a 4 × 4 lane grid of 3 × 3 blocks (NX = 12):
+  // lane (R, C) = (j / 4, j % 4) holds A[3R..3R+2][3C..3C+2].  Per pivot p the four lanes of block
+  // column p / 3 publish their rows of column p (= row p by symmetry); every lane reads the 3 entries
+  // of its rows and the 3 of its columns (8 distinct addresses per warp-wide load instead of the 12
+  // broadcasts of the column-per-lane sweep), then updates its 9 entries.  V is read from Vs = X1
+  // (column-major, written by the caller), S⁻¹ = −A is stored to wk[Si] (column-major, symmetric).
+  __device__ static __forceinline__ void invS_grid(double* wk, double delta, int j, int stage, int32_t& st) {
+    static_assert(NX == 12, "grid sweep is laid out for NX = 12 (4 x 4 lanes of 3 x 3 blocks)");
+    const int R = j >> 2, C = j & 3;
+    double a[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        a[i][k] = delta * wk[WM::X1 + (3 * C + k) * NX + 3 * R + i] + ((3 * R + i == 3 * C + k) ? 1.0 : 0.0);
+    bool notpd = false;
+#pragma unroll
+    for (int p = 0; p < NX; ++p) {
+      double* pb = wk + WK::pub + (p & 1) * WK::NZP;
+      const int pc = p / 3, pk = p % 3;
+      if (C == pc) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) pb[3 * R + i] = a[i][pk];
+      }
+      __syncwarp();
+      double cr[3], cc[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        cr[i] = pb[3 * R + i];  // A[3R+i][p]
+        cc[i] = pb[3 * C + i];  // A[p][3C+i] = A[3C+i][p]
+      }
+      const double d = pb[p];
+      notpd |= !(d > 0.0);
+      const double id = rcp_nr(d);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const bool rp = (3 * R + i == p);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const bool cp = (3 * C + k == p);
+          const double upd = fma(-cr[i] * id, cc[k], a[i][k]);
+          a[i][k] = rp ? (cp ? -id : cc[k] * id) : (cp ? cr[i] * id : upd);
+        }
+      }
+    }
+    if (notpd && st == 0) st = mk_status(RR_ST_S_NOT_PD, stage);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) wk[WK::Si + (3 * C + k) * NX + 3 * R + i] = -a[i][k];
+    __syncwarp();
+  }
+
   // FAC = true: the factorization only (rr_factor): no Φ / φ, the u-block is eliminated with the
   // symmetric sweep operator (−G⁻¹ lands in the u-columns) and recq[q] points at factor record i
   // [V_i | S_i⁻¹ | K_i | G_i⁻¹] (record i+1 receives S_{i+1}⁻¹).
@@ -132,13 +185,24 @@ struct StageMMA {
     const double* cv = grp ? cvq[1] : cvq[0];
     const int g = lane >> 2, t = lane & 3;
     // (1) S⁻¹ (no stage input needed), then Vs = [V | V e] (V symmetric: (V e)_j = column j · e)
+#ifndef RR_INVS_GRID
     ST::invS(Vc, delta, j, wk, stage, st);
+    if (j < NX) {
+#pragma unroll
+      for (int r = 0; r < NX; ++r) wk[WM::X1 + r * NX + j] = Vc[r];  // V symmetric: column j as row j
+    }
+#else  // 4 × 4 grid sweep: measured 6% slower on C2 (more scalar loads and selects per pivot)
+    if (j < NX) {
+#pragma unroll
+      for (int r = 0; r < NX; ++r) wk[WM::X1 + r * NX + j] = Vc[r];
+    }
+    __syncwarp();
+    invS_grid(wk, delta, j, stage, st);
+#endif
     wait_inputs();
     if (j < NX) wk[WM::E + j] = cv[j] - delta * wk[WK::vs + j];  // e = c_{i+1} − δ v_{i+1}
     __syncwarp();
     if (j < NX) {
-#pragma unroll
-      for (int r = 0; r < NX; ++r) wk[WM::X1 + r * NX + j] = Vc[r];  // V symmetric: column j as row j
       double ek[NX];
       ST::bcast(wk + WM::E, ek);
       double ve0 = 0.0, ve1 = 0.0;
