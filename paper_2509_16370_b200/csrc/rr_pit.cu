@@ -723,11 +723,9 @@ cudaError_t pit_launch(const PitArgs& a, cudaStream_t s) {
   const int N = a.N;
   pit_status_init<<<(unsigned)((b + 255) / 256), 256, 0, s>>>(a);
   const size_t sm8 = sizeof(double) * WPB * 8 * TILE, sm4 = sizeof(double) * WPB * 4 * TILE;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(pit_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm8);
-    attr = true;
-  }
+  // per call (the attribute is per device; no global state in the library)
+  cudaError_t ea = cudaFuncSetAttribute(pit_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm8);
+  if (ea != cudaSuccess) return ea;
   if (N > 0) pit_assemble_kernel<<<blocks_for(b * N), WPB * 32, sm8, s>>>(a);
   pit_diag_kernel<<<blocks_for(b * (N + 1)), WPB * 32, 0, s>>>(a);
   int levels = 0;
