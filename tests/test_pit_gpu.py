@@ -64,3 +64,35 @@ def test_pit_shared_and_failure():
     z = synth.random_stable_lqr(4, 1, 6, 3, seed=4).with_delta(0.0)   # δ = 0: outside the method
     bad = m.rr_factor_solve_pit(z.to("cuda"))
     assert np.all(bad["status"].cpu().numpy() != 0)
+
+
+def test_cuda_graph_capture_replay():
+    """The C-ABI calls are stream-ordered with no host synchronisation, so they can be captured in a
+    CUDA graph and replayed (the latency path for the multi-launch parallel-in-time solve)."""
+    m = rr()
+    p = synth.random_stable_lqr(12, 4, 200, 2, seed=8, delta=1e-3).to("cuda")
+    ref_pit = m.rr_factor_solve_pit(p)
+    ref_seq = m.rr_factor_solve(p)
+    torch.cuda.synchronize()
+    out_pit = m.alloc_solution(p)
+    nb = m._lib.lib().rr_pit_workspace_bytes(__import__("ctypes").byref(m.rr.dims_of(p)))
+    ws = torch.empty((nb + 7) // 8, dtype=torch.float64, device="cuda")
+    call = m.Marshalled(p, m.alloc_solution(p))
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):   # warm-up outside the capture
+        m.rr_factor_solve_pit(p, out=out_pit, workspace=ws, stream=s)
+        call.launch(s)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        m.rr_factor_solve_pit(p, out=out_pit, workspace=ws, stream=torch.cuda.current_stream())
+        call.launch(torch.cuda.current_stream())
+    for k in ("x", "u", "y"):
+        out_pit[k].zero_()
+        call.sol[k].zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for k in ("x", "u", "y"):
+        assert torch.equal(out_pit[k], ref_pit[k]) and torch.equal(call.sol[k], ref_seq[k]), k
