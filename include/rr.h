@@ -244,12 +244,16 @@ rr_err rr_residual(const rr_dims* dims, const rr_problem* prob, const rr_solutio
  *      𝒜(x̄+αΔx, s+αΔs) ≤ 𝒜(x̄, s) + c₁ α D (reading R12); α_d = min(1, min τz/(−Δz));
  *      update x, u, s, y, λ with α, z with α_d (in place).
  * Trial merit values use the built-in model `model` (reading R19): IPM_MODEL_LQ (dynamics,
- * constraints linear: trial values exact from the linearisation) or IPM_MODEL_CARTPOLE (dynamics
- * x⁺ = cartpole(x, u; model_params = [dt, m_c, m_p, l, g]) evaluated at trial points).  Costs are
- * quadratic with Hessian P for both, so f(x̄ + αΔ) = f̄ + α∇fᵀΔ + ½α²ΔᵀPΔ exactly.
+ * constraints linear: trial values exact from the linearisation), IPM_MODEL_CARTPOLE (n = 4, m = 1;
+ * dynamics x⁺ = cartpole(x, u; model_params = [dt, m_c, m_p, l, g]) evaluated at trial points) or
+ * IPM_MODEL_QUADROTOR (n = 12, m = 4; x⁺ = x + dt f(x, u) with f the SURVEY §8(d) C5 quadrotor:
+ * x = (p, ZYX Euler angles φ θ ψ, world velocity, body rates), u = (thrust, 3 torques),
+ * model_params = [dt, mass, J_x, J_y, J_z, g]).  Costs are quadratic with Hessian P for all three,
+ * so f(x̄ + αΔ) = f̄ + α∇fᵀΔ + ½α²ΔᵀPΔ exactly.  ipm_solve supports LQ and the cart-pole only.
  */
 #define IPM_MODEL_LQ 0
 #define IPM_MODEL_CARTPOLE 1
+#define IPM_MODEL_QUADROTOR 2
 
 typedef struct {
   int32_t nx, nu, N;
@@ -276,7 +280,8 @@ typedef struct {
   const double *ceN, *CeN;    /* [b][ncN], [b][ncN*n]                                             */
   const double *gv, *Gj;      /* [b][N][ng], [b][N][ng*w]   stage inequalities g_i ≤ 0, Jacobian  */
   const double *gvN, *GjN;    /* [b][ngN], [b][ngN*n]                                             */
-  const double* model_params; /* [8] shared by the batch (cart-pole: dt, m_c, m_p, l, g)         */
+  const double* model_params; /* [8] shared by the batch (cart-pole: dt, m_c, m_p, l, g;           */
+                              /*     quadrotor: dt, mass, J_x, J_y, J_z, g)                       */
 } ipm_stage_data;
 
 /* Iterate (updated in place on success). */

@@ -85,3 +85,16 @@ def cartpole_step_oracle(prm, x, u):
     out = np.zeros(4)
     f(p.ctypes.data, xx.ctypes.data, uu.ctypes.data, out.ctypes.data)
     return out
+
+
+def quadrotor_step_oracle(prm, x, u):
+    """x⁺ = x + dt f(x, u) of the C oracle's quadrotor (SURVEY §8(d) C5 model)."""
+    lib = load_oracle()
+    f = lib.orc_quadrotor_step
+    f.argtypes = [ctypes.c_void_p] * 4
+    p = np.ascontiguousarray(prm, dtype=np.float64)
+    xx = np.ascontiguousarray(x, dtype=np.float64)
+    uu = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.zeros(12)
+    f(p.ctypes.data, xx.ctypes.data, uu.ctypes.data, out.ctypes.data)
+    return out

@@ -16,7 +16,8 @@
  *   τ, Armijo c₁, backtracking β, ≤ max_backtracks; z uses α_d, y and λ use α_p)
  * Built-in models for the trial points (reading R19): 0 = LQ (linear d, g, c_e; cost quadratic
  * with Hessian P, so every trial value is exact), 1 = cart-pole (explicit-Euler cart-pole
- * dynamics evaluated at the trial point; costs quadratic; constraints linear).
+ * dynamics evaluated at the trial point; costs quadratic; constraints linear), 2 = quadrotor
+ * (explicit-Euler C5 quadrotor dynamics at the trial point; costs quadratic; constraints linear).
  */
 #define _USE_MATH_DEFINES
 #include <math.h>
@@ -81,6 +82,51 @@ static void cartpole_step(const double* prm, const double* x, const double* u, d
 /* exported for tests (model pin against finite differences / the generator) */
 void orc_cartpole_step(const double* prm, const double* x, const double* u, double* xn) {
   cartpole_step(prm, x, u, xn);
+}
+
+/* quadrotor, explicit Euler x+ = x + dt f(x, u) (SURVEY §8(d), C5 model).
+ * state (p[3], ZYX Euler angles phi theta psi, world velocity v[3], body rates w[3]);
+ * input (thrust T, torques tau[3]); params: [dt, mass, Jx, Jy, Jz, g].
+ * f: p' = v;  (phi, theta, psi)' = W(phi, theta) w;  v' = R(phi, theta, psi) (0, 0, T/mass) - (0, 0, g)
+ * with R = Rz(psi) Ry(theta) Rx(phi);  J w' = tau - w x (J w), J = diag(Jx, Jy, Jz). */
+static void quadrotor_step(const double* prm, const double* x, const double* u, double* xn) {
+  const double dt = prm[0], mass = prm[1], J[3] = {prm[2], prm[3], prm[4]}, g = prm[5];
+  const double ph = x[3], th = x[4], ps = x[5];
+  const double* v = x + 6;
+  const double* w = x + 9;
+  /* R = Rz(psi) Ry(theta) Rx(phi), written out as the product of the three elementary rotations */
+  const double Rz[3][3] = {{cos(ps), -sin(ps), 0}, {sin(ps), cos(ps), 0}, {0, 0, 1}};
+  const double Ry[3][3] = {{cos(th), 0, sin(th)}, {0, 1, 0}, {-sin(th), 0, cos(th)}};
+  const double Rx[3][3] = {{1, 0, 0}, {0, cos(ph), -sin(ph)}, {0, sin(ph), cos(ph)}};
+  double Ryx[3][3], R[3][3];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      Ryx[a][b] = 0.0;
+      for (int k = 0; k < 3; ++k) Ryx[a][b] += Ry[a][k] * Rx[k][b];
+    }
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      R[a][b] = 0.0;
+      for (int k = 0; k < 3; ++k) R[a][b] += Rz[a][k] * Ryx[k][b];
+    }
+  /* Euler-angle rates: W = [[1, s_ph t_th, c_ph t_th], [0, c_ph, -s_ph], [0, s_ph / c_th, c_ph / c_th]] */
+  const double W[3][3] = {{1.0, sin(ph) * tan(th), cos(ph) * tan(th)},
+                          {0.0, cos(ph), -sin(ph)},
+                          {0.0, sin(ph) / cos(th), cos(ph) / cos(th)}};
+  double f[12];
+  for (int a = 0; a < 3; ++a) f[a] = v[a];
+  for (int a = 0; a < 3; ++a) f[3 + a] = W[a][0] * w[0] + W[a][1] * w[1] + W[a][2] * w[2];
+  const double Tm = u[0] / mass;
+  for (int a = 0; a < 3; ++a) f[6 + a] = R[a][2] * Tm - (a == 2 ? g : 0.0);
+  /* w x (J w) */
+  const double Jw[3] = {J[0] * w[0], J[1] * w[1], J[2] * w[2]};
+  const double cr[3] = {w[1] * Jw[2] - w[2] * Jw[1], w[2] * Jw[0] - w[0] * Jw[2], w[0] * Jw[1] - w[1] * Jw[0]};
+  for (int a = 0; a < 3; ++a) f[9 + a] = (u[1 + a] - cr[a]) / J[a];
+  for (int a = 0; a < 12; ++a) xn[a] = x[a] + dt * f[a];
+}
+
+void orc_quadrotor_step(const double* prm, const double* x, const double* u, double* xn) {
+  quadrotor_step(prm, x, u, xn);
 }
 
 /* y = Mat v, Mat rows×cols column-major */
@@ -255,10 +301,11 @@ static double merit(const inst_t* I, const double* prm, int model, double alpha)
   for (int i = 0; i < N; ++i) {
     const double* Ai = I->A + (int64_t)i * n * n;
     const double* Bi = I->B + (int64_t)i * n * m;
-    if (model == 1) {
+    if (model == 1 || model == 2) {
       for (int r = 0; r < n; ++r) xa[r] = I->x[(int64_t)i * n + r] + alpha * I->dx[(int64_t)i * n + r];
       for (int r = 0; r < m; ++r) ua[r] = I->u[(int64_t)i * m + r] + alpha * I->du[(int64_t)i * m + r];
-      cartpole_step(prm, xa, ua, xn);
+      if (model == 1) cartpole_step(prm, xa, ua, xn);
+      else quadrotor_step(prm, xa, ua, xn);
     } else {
       /* linear model: d(x̄+αΔx, ū+αΔu) − x̄_{i+1} = dres_i + α(AΔx + BΔu) */
       matvec(n, n, Ai, I->dx + (int64_t)i * n, xa);

@@ -98,6 +98,54 @@ __device__ __forceinline__ void cartpole_step(const double* prm, const double* x
   xn[3] = x[3] + dt * thdd;
 }
 
+// quadrotor, explicit Euler x⁺ = x + dt f(x, u) (SURVEY §8(d) C5 model): x = (p, ZYX Euler angles
+// (φ, θ, ψ), world velocity v, body rates ω), u = (thrust T, torques τ); params [dt, mass, Jx, Jy, Jz, g].
+// Euler-angle rates W(φ, θ)ω; acceleration R(φ, θ, ψ)[0, 0, T/m] − [0, 0, g] with R = Rz(ψ)Ry(θ)Rx(φ);
+// Euler's equations J ω̇ = τ − ω × Jω for the diagonal inertia J.
+__device__ __forceinline__ void quadrotor_step(const double* prm, const double* x, const double* u, double* xn) {
+  const double dt = prm[0], mass = prm[1], Jx = prm[2], Jy = prm[3], Jz = prm[4], g = prm[5];
+  double sph, cph, sth, cth, sps, cps;
+  sincos(x[3], &sph, &cph);
+  sincos(x[4], &sth, &cth);
+  sincos(x[5], &sps, &cps);
+  const double wx = x[9], wy = x[10], wz = x[11];
+  const double tth = sth / cth;
+  const double dphi = wx + sph * tth * wy + cph * tth * wz;
+  const double dth = cph * wy - sph * wz;
+  const double dpsi = (sph * wy + cph * wz) / cth;
+  const double Tm = u[0] / mass;
+  const double ax = (cps * sth * cph + sps * sph) * Tm;
+  const double ay = (sps * sth * cph - cps * sph) * Tm;
+  const double az = cth * cph * Tm - g;
+  const double dwx = (u[1] - (Jz - Jy) * wy * wz) / Jx;
+  const double dwy = (u[2] - (Jx - Jz) * wz * wx) / Jy;
+  const double dwz = (u[3] - (Jy - Jx) * wx * wy) / Jz;
+  xn[0] = x[0] + dt * x[6];
+  xn[1] = x[1] + dt * x[7];
+  xn[2] = x[2] + dt * x[8];
+  xn[3] = x[3] + dt * dphi;
+  xn[4] = x[4] + dt * dth;
+  xn[5] = x[5] + dt * dpsi;
+  xn[6] = x[6] + dt * ax;
+  xn[7] = x[7] + dt * ay;
+  xn[8] = x[8] + dt * az;
+  xn[9] = wx + dt * dwx;
+  xn[10] = wy + dt * dwy;
+  xn[11] = wz + dt * dwz;
+}
+
+// x⁺ = d(x, u) of the built-in nonlinear models (their n, m are fixed; checked by ipm_supported)
+template <int NX, int NU>
+__device__ __forceinline__ void model_step(int model, const double* prm, const double* x, const double* u, double* xn) {
+  if (model == IPM_MODEL_CARTPOLE) {
+    cartpole_step(prm, x, u[0], xn);
+    return;
+  }
+  if constexpr (NX >= 12 && NU >= 4) {
+    if (model == IPM_MODEL_QUADROTOR) quadrotor_step(prm, x, u, xn);
+  }
+}
+
 // EXACT: the dimensions are the template's (n = NX, m = NU, n_g = NG, n_c = NC; terminal counts stay
 // runtime), so the compiler folds the padding guards and loop bounds.
 template <int NX, int NU, int NG, int NC, int LG, int WARPS, bool EXACT = false>
@@ -544,16 +592,17 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
         sK2 += 0.5 * eta * cd * cd;
       }
     }
-    if (model == IPM_MODEL_CARTPOLE && j == 0) {
+    if (model != IPM_MODEL_LQ && j == 0) {
       // dynamics terms at α = 0 through the model (as the oracle's merit does)
-      double xnm[4];
-      const double* prm = a.d_.model_params;
-      cartpole_step(prm, sb + IB::xb, sb[IB::ub], xnm);
+      double xnm[NX];
+      model_step<NX, NU>(model, a.d_.model_params, sb + IB::xb, sb + IB::ub, xnm);
       const double* xb1 = a.it.x + (inst * (sN + 1) + i + 1) * n;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const double cr = xnm[r] - xb1[r];
-        sDyn0 += sb[IB::yn + r] * cr + 0.5 * eta * cr * cr;
+      for (int r = 0; r < NX; ++r) {
+        if (r < n) {
+          const double cr = xnm[r] - xb1[r];
+          sDyn0 += sb[IB::yn + r] * cr + 0.5 * eta * cr * cr;
+        }
       }
     }
 #pragma unroll
@@ -643,19 +692,24 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
             sl.add(sa);
           }
         }
-        if (model == IPM_MODEL_CARTPOLE && !term) {
-          double xa[4], xnm[4];
+        if (model != IPM_MODEL_LQ && !term) {
+          double xa[NX], ua[NU], xnm[NX];
           const double* xb = a.it.x + (inst * (sN + 1) + i) * n;
           const double* dxb = a.r.dx + (inst * (sN + 1) + i) * n;
+          const double* ub = a.it.u + (inst * sN + i) * m;
+          const double* dub = a.r.du + (inst * sN + i) * m;
 #pragma unroll
-          for (int r = 0; r < 4; ++r) xa[r] = xb[r] + alpha * dxb[r];
-          const double ua = a.it.u[inst * sN + i] + alpha * a.r.du[inst * sN + i];
-          cartpole_step(a.d_.model_params, xa, ua, xnm);
+          for (int r = 0; r < NX; ++r) xa[r] = (r < n) ? xb[r] + alpha * dxb[r] : 0.0;
+#pragma unroll
+          for (int r = 0; r < NU; ++r) ua[r] = (r < m) ? ub[r] + alpha * dub[r] : 0.0;
+          model_step<NX, NU>(model, a.d_.model_params, xa, ua, xnm);
           const double* yb = a.it.y + (inst * (sN + 1) + i + 1) * n;
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const double cr = xnm[r] - (xb[n + r] + alpha * dxb[n + r]);
-            sdyn += yb[r] * cr + 0.5 * eta * cr * cr;
+          for (int r = 0; r < NX; ++r) {
+            if (r < n) {
+              const double cr = xnm[r] - (xb[n + r] + alpha * dxb[n + r]);
+              sdyn += yb[r] * cr + 0.5 * eta * cr * cr;
+            }
           }
         }
       }
@@ -751,6 +805,7 @@ static bool dispatch_ipm(const ipm_dims& d, F&& f) {
   const int ngm = d.ng > d.ngN ? d.ng : d.ngN;
   const int ncm = d.nc > d.ncN ? d.nc : d.ncN;
   if (d.model == IPM_MODEL_CARTPOLE && (d.nx != 4 || d.nu != 1)) return false;
+  if (d.model == IPM_MODEL_QUADROTOR && (d.nx != 12 || d.nu != 4)) return false;
   if (d.nx == 4 && d.nu == 1 && d.ng == 4 && d.nc == 0 && d.ngN <= 4 && d.ncN == 0)
     return f(IpmCfg<4, 1, 4, 0, 8, true>{});  // C4 (cart-pole) shape
   if (d.nx <= 4 && d.nu <= 1 && ngm <= 4 && ncm == 0) return f(IpmCfg<4, 1, 4, 0, 8>{});

@@ -290,7 +290,7 @@ rr_err rr_factor_solve_pit(const rr_dims* dims, const rr_problem* prob, const rr
 
 static bool ipm_dims_ok(const ipm_dims* d) {
   return d != nullptr && d->nx >= 1 && d->nu >= 1 && d->N >= 0 && d->batch >= 0 && d->ng >= 0 && d->ngN >= 0 &&
-         d->nc >= 0 && d->ncN >= 0 && (d->model == IPM_MODEL_LQ || d->model == IPM_MODEL_CARTPOLE);
+         d->nc >= 0 && d->ncN >= 0 && (d->model == IPM_MODEL_LQ || d->model == IPM_MODEL_CARTPOLE || d->model == IPM_MODEL_QUADROTOR);
 }
 
 int64_t ipm_workspace_bytes(const ipm_dims* dims) {
@@ -356,8 +356,8 @@ static rr_err ipm_step_impl(const ipm_dims* dims, const ipm_stage_data* data, co
   if (!data->s0 || !data->fval || !data->gradfN || !data->QN || !it->x || !it->y || !it->mu || !it->eta ||
       !res->dx || !res->dy)
     return set_err(RR_E_INVALID, "ipm_step: null %s", "required pointer");
-  if (dims->model == IPM_MODEL_CARTPOLE && data->model_params == nullptr)
-    return set_err(RR_E_INVALID, "ipm_step: cart-pole model needs %s", "model_params");
+  if (dims->model != IPM_MODEL_LQ && data->model_params == nullptr)
+    return set_err(RR_E_INVALID, "ipm_step: the built-in nonlinear models need %s", "model_params");
   rrk::IpmArgs a;
   a.d = *dims;
   a.d_ = *data;
@@ -375,7 +375,8 @@ static rr_err ipm_step_impl(const ipm_dims* dims, const ipm_stage_data* data, co
 }
 
 int64_t ipm_solve_workspace_bytes(const ipm_dims* dims) {
-  if (!ipm_dims_ok(dims)) return -1;
+  // the solve loop re-evaluates the model's Jacobians: LQ and the cart-pole only (no quadrotor Jacobians)
+  if (!ipm_dims_ok(dims) || dims->model == IPM_MODEL_QUADROTOR) return -1;
   return rrk::ipm_solve_ws_bytes(*dims);
 }
 

@@ -4,7 +4,7 @@ An IPMBatch holds, per instance, the stagewise OCP data of §1.1 evaluated at th
 (cost gradient, a positive-definite Hessian approximation P, dynamics Jacobians and
 residuals, equality/inequality values and Jacobians) plus the iterate (x, s, y, z, μ, η) of
 §1.2, in the C-ABI layout of include/rr.h (ipm_* structs).  Model ids: 0 = LQ (linear dynamics
-and constraints, quadratic cost), 1 = cart-pole (C4).
+and constraints, quadratic cost), 1 = cart-pole (C4), 2 = quadrotor (the C5 model of §8(d)).
 
 The cart-pole dynamics below are the workload DEFINITION used to produce iterates and their
 Jacobians (torch autograd); the oracle and the CUDA library each carry their own copy of the
@@ -18,9 +18,9 @@ from typing import Dict
 
 import torch
 
-from .workloads import OP_A, OP_B, OP_L, colmajor, from_colmajor, pack_lower, sym_size, uniform
+from .workloads import OP_A, OP_B, OP_L, colmajor, from_colmajor, pack_lower, quadrotor_f, sym_size, uniform
 
-MODEL_LQ, MODEL_CARTPOLE = 0, 1
+MODEL_LQ, MODEL_CARTPOLE, MODEL_QUADROTOR = 0, 1, 2
 N_MODEL_PARAMS = 8
 
 DATA_FIELDS = ("s0", "fval", "gradf", "gradfN", "Q", "M", "R", "QN", "A", "B", "dres",
@@ -246,3 +246,76 @@ def double_integrator_ocp(batch=1, N=20, h=0.1, x0=(5.0, 0.0), umax=1.0, q=1.0, 
               mu=torch.full((batch,), float(mu), dtype=torch.float64, device=dev),
               eta=torch.full((batch,), float(eta), dtype=torch.float64, device=dev))
     return IPMBatch(n, m, N, 2, 0, 0, 0, MODEL_LQ, data, it)
+
+
+def quadrotor_params(dt=0.02, mass=0.5, J=(2.32e-3, 2.32e-3, 4e-3), g=9.81, device="cpu"):
+    p = _zeros(N_MODEL_PARAMS, device=device)
+    p[:6] = torch.tensor([dt, mass, J[0], J[1], J[2], g], dtype=torch.float64)
+    return p
+
+
+def quadrotor_step_torch(prm, x, u):
+    """Explicit Euler x + dt f(x, u) of the C5 quadrotor (workload definition, synth.workloads.quadrotor_f)."""
+    dt, mass = prm[0], prm[1]
+    return x + dt * quadrotor_f(x, u, mass=mass, J=(prm[2], prm[3], prm[4]), g=prm[5])
+
+
+def quadrotor_ipm(batch, seed=2513, N=50, mu=0.1, eta=1e4, first=0, device="cpu") -> IPMBatch:
+    """Quadrotor IPM iterates (model 2; a test workload, not a BASELINE config): n = 12, m = 4, the C5
+    model and weights (§8(d): Q = diag(10,10,10,1,…,.1), R = diag(.1,1,1,1), Q_N = 10Q, dt = 0.02),
+    cost ½xᵀQx + ½(u − u_h)ᵀR(u − u_h) with hover thrust u_h = (mg, 0, 0, 0); inequalities
+    T ≤ 2mg, −T ≤ −0.2mg, τ_x ≤ 0.05, −τ_x ≤ 0.05 (n_g = 4, none terminal).
+    Iterate: s_0 = (U, 0.3U, U, 0.5U) by block; ū = (mg(1 + 0.1U), 0.01U); x̄ = rollout of ū with
+    defects 1e-3U; s = max(−g, 1e-2), z = μ/s, y = 0.1U."""
+    dev = torch.device(device)
+    n, m, k = 12, 4, 16
+    prm = quadrotor_params(device=dev)
+    mass, grav = 0.5, 9.81
+    inst = torch.arange(first, first + batch, dtype=torch.int64, device=dev)
+    st = torch.arange(N, dtype=torch.int64, device=dev)
+    scale = torch.tensor([1, 1, 1, .3, .3, .3, 1, 1, 1, .5, .5, .5], dtype=torch.float64, device=dev)
+    s0 = uniform(seed, inst, 0, OP_S0, n) * scale
+    Uu = uniform(seed, inst, st, OP_U, m)
+    ubar = torch.cat([mass * grav * (1 + 0.1 * Uu[..., :1]), 0.01 * Uu[..., 1:]], dim=-1)
+    defect = 1e-3 * uniform(seed, inst, torch.arange(N + 1, device=dev), OP_DRES, n)
+    xs = [s0 + defect[:, 0]]
+    for i in range(N):
+        xs.append(quadrotor_step_torch(prm, xs[-1], ubar[:, i]) + defect[:, i + 1])
+    xbar = torch.stack(xs, dim=1)
+    xi = xbar[:, :N].reshape(-1, n)
+    ui = ubar.reshape(-1, m)
+    dres = quadrotor_step_torch(prm, xi, ui).reshape(batch, N, n) - xbar[:, 1:]
+    jac = torch.func.vmap(torch.func.jacrev(lambda xx, uu: quadrotor_step_torch(prm, xx, uu), argnums=(0, 1)))
+    Jx, Ju = jac(xi, ui)
+    A = colmajor(Jx).reshape(batch, N, n * n)
+    B = colmajor(Ju).reshape(batch, N, n * m)
+    qd = torch.tensor([10, 10, 10, 1, 1, 1, 1, 1, 1, .1, .1, .1], dtype=torch.float64, device=dev)
+    rd = torch.tensor([0.1, 1, 1, 1], dtype=torch.float64, device=dev)
+    uh = torch.tensor([mass * grav, 0, 0, 0], dtype=torch.float64, device=dev)
+    du_ = ubar - uh
+    gradf = torch.cat([qd * xbar[:, :N], rd * du_], dim=-1)
+    gradfN = 10.0 * qd * xbar[:, N]
+    fval = 0.5 * (qd * xbar[:, :N] ** 2).sum((-1, -2)) + 0.5 * (rd * du_ ** 2).sum((-1, -2)) \
+        + 5.0 * (qd * xbar[:, N] ** 2).sum(-1)
+    Q = pack_lower(torch.diag(qd)).expand(batch, N, sym_size(n)).contiguous()
+    M = _zeros(batch, N, n * m, device=dev)
+    R = pack_lower(torch.diag(rd)).expand(batch, N, sym_size(m)).contiguous()
+    QN = pack_lower(torch.diag(10.0 * qd)).expand(batch, sym_size(n)).contiguous()
+    G = _zeros(4, k, device=dev)
+    G[0, 12], G[1, 12], G[2, 13], G[3, 13] = 1.0, -1.0, 1.0, -1.0
+    Gj = colmajor(G).expand(batch, N, 4 * k).contiguous()
+    T, tx = ubar[..., 0], ubar[..., 1]
+    gv = torch.stack([T - 2 * mass * grav, -T + 0.2 * mass * grav, tx - 0.05, -tx - 0.05], dim=-1)
+    s = torch.clamp(-gv, min=1e-2)
+    yv = 0.1 * uniform(seed, inst, torch.arange(N + 1, device=dev), OP_Y, n)
+    data = dict(s0=s0, fval=fval, gradf=gradf, gradfN=gradfN, Q=Q, M=M, R=R, QN=QN, A=A, B=B, dres=dres,
+                ce=_zeros(batch, N, 0, device=dev), Ce=_zeros(batch, N, 0, device=dev),
+                ceN=_zeros(batch, 0, device=dev), CeN=_zeros(batch, 0, device=dev),
+                gv=gv, Gj=Gj, gvN=_zeros(batch, 0, device=dev), GjN=_zeros(batch, 0, device=dev), model_params=prm)
+    it = dict(x=xbar, u=ubar, s=s, z=mu / s, sN=_zeros(batch, 0, device=dev), zN=_zeros(batch, 0, device=dev), y=yv,
+              lam=_zeros(batch, N, 0, device=dev), lamN=_zeros(batch, 0, device=dev),
+              mu=torch.full((batch,), float(mu), dtype=torch.float64, device=dev),
+              eta=torch.full((batch,), float(eta), dtype=torch.float64, device=dev))
+    data = {k2: v.contiguous() for k2, v in data.items()}
+    it = {k2: v.contiguous() for k2, v in it.items()}
+    return IPMBatch(n, m, N, 4, 0, 0, 0, MODEL_QUADROTOR, data, it)

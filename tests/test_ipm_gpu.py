@@ -7,7 +7,7 @@ import pytest
 import torch
 
 from oracle.ipm import ipm_step_oracle
-from synth.ipm_workloads import cartpole_c4, random_lq_ocp
+from synth.ipm_workloads import cartpole_c4, quadrotor_ipm, random_lq_ocp
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-9
@@ -131,3 +131,24 @@ def test_ipm_invalid_parameters_rejected():
         rr.ipm_step(p, tau=1.5)
     with pytest.raises(rr.RRError):
         rr.ipm_step(p, beta=0.0)
+
+
+@pytest.mark.parametrize("batch,N,seed", [(37, 20, 2513), (300, 50, 11)])
+def test_ipm_parity_quadrotor_model(batch, N, seed):
+    """IPM_MODEL_QUADROTOR: trial merits through the C5 quadrotor dynamics (n = 12, m = 4)."""
+    p = quadrotor_ipm(batch, seed=seed, N=N)
+    g, git, o, oit = run(p)
+    assert np.all(o["status"] == 0) and np.any(o["alpha_p"] < 1.0)
+    assert_ipm_parity(g, git, o, oit)
+
+
+def test_quadrotor_model_rules():
+    """The quadrotor model needs n = 12, m = 4 and model_params; ipm_solve does not take it."""
+    import paper_2509_16370_b200 as rr
+    p = quadrotor_ipm(4, N=5).to("cuda")
+    with pytest.raises(rr.RRError):
+        rr.ipm_solve(p, max_iters=2)
+    bad = random_lq_ocp(4, 1, 5, 3, seed=1, ng=2)
+    bad.model = 2
+    with pytest.raises(rr.RRError):
+        rr.ipm_step(bad.to("cuda"))
