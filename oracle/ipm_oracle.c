@@ -29,31 +29,9 @@
 #include <stdlib.h>
 #include <string.h>
 
-int orc_rr_solve(int nx, int nu, int N, int64_t batch, int nthreads, const double* A, const double* B,
-                 const double* Q, const double* M, const double* R, const double* q, const double* r,
-                 const double* c, const double* QN, const double* qN, const double* c0, const double* delta,
-                 double* x, double* u, double* y, double* V, double* v, double* K, double* k, int32_t* status);
+#include "orc.h"
 
-#define OIPM_NONPOS_SLACK 4
-#define OIPM_LS_FAILED 5
-
-typedef struct {
-  int nx, nu, N, ng, ngN, nc, ncN, model;
-  int64_t batch;
-  /* stage data at the iterate */
-  const double *s0, *fval, *gradf, *gradfN, *Q, *M, *R, *QN, *A, *B, *dres;
-  const double *ce, *Ce, *ceN, *CeN, *gv, *Gj, *gvN, *GjN, *model_params;
-  /* iterate (updated in place) */
-  double *x, *u, *s, *z, *sN, *zN, *y, *lam, *lamN;
-  const double *mu, *eta;
-  /* params */
-  double tau, armijo_c, beta;
-  int max_backtracks;
-  /* results */
-  double *dx, *du, *ds, *dsN, *dy, *dlam, *dlamN, *dz, *dzN;
-  double *alpha_p, *alpha_d, *D, *D_closed, *merit0, *merit_acc;
-  int32_t *n_backtracks, *status;
-} orc_ipm_args;
+/* status codes and orc_ipm_args: orc.h */
 
 static int64_t symn(int n) { return (int64_t)n * (n + 1) / 2; }
 static int64_t pk(int n, int r, int c) {

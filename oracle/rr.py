@@ -10,6 +10,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = [os.path.join(_HERE, "rr_oracle.c"), os.path.join(_HERE, "ipm_oracle.c")]
+_HDR = [os.path.join(_HERE, "orc.h")]
 _LIB = os.path.join(_HERE, "liborc.so")
 _lock = threading.Lock()
 _lib = None
@@ -18,7 +19,7 @@ _lib = None
 def build_oracle(force: bool = False) -> str:
     """Compile the C oracle with plain -O2 (no BLAS, no intrinsics, no fast-math)."""
     srcs = [s for s in _SRC if os.path.exists(s)]
-    newest = max(os.path.getmtime(s) for s in srcs)
+    newest = max(os.path.getmtime(s) for s in srcs + [h for h in _HDR if os.path.exists(h)])
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
         tmp = _LIB + ".tmp%d" % os.getpid()
         subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-std=c11", "-ffp-contract=off",

@@ -31,10 +31,7 @@
 #include <stdlib.h>
 #include <string.h>
 
-#define ORC_OK 0
-#define ORC_G_NOT_PD 1
-#define ORC_S_NOT_PD 2
-#define ORC_NONFINITE 3
+#include "orc.h"
 
 static int64_t sym_size(int n) { return (int64_t)n * (n + 1) / 2; }
 
