@@ -249,7 +249,7 @@ rr_err rr_residual(const rr_dims* dims, const rr_problem* prob, const rr_solutio
  * IPM_MODEL_QUADROTOR (n = 12, m = 4; x⁺ = x + dt f(x, u) with f the SURVEY §8(d) C5 quadrotor:
  * x = (p, ZYX Euler angles φ θ ψ, world velocity, body rates), u = (thrust, 3 torques),
  * model_params = [dt, mass, J_x, J_y, J_z, g]).  Costs are quadratic with Hessian P for all three,
- * so f(x̄ + αΔ) = f̄ + α∇fᵀΔ + ½α²ΔᵀPΔ exactly.  ipm_solve supports LQ and the cart-pole only.
+ * so f(x̄ + αΔ) = f̄ + α∇fᵀΔ + ½α²ΔᵀPΔ exactly.
  */
 #define IPM_MODEL_LQ 0
 #define IPM_MODEL_CARTPOLE 1
@@ -356,7 +356,7 @@ rr_err ipm_update(const ipm_dims* dims, const ipm_iterate* it, const ipm_result*
  * update_parameters (reading R21).  At iteration k, for every running instance:
  *   evaluate the problem data at the iterate: costs quadratic with Hessian P and constraints linear
  *     (exact from `data`, the evaluation at the INITIAL iterate, which serves as the model reference);
- *     dynamics linear (IPM_MODEL_LQ) or the cart-pole model with its analytic Jacobians;
+ *     dynamics linear (IPM_MODEL_LQ) or the cart-pole / quadrotor model with analytic Jacobians;
  *   residuals r_stat = ||∇ₓL||∞ (∇ₓL = ∇f + Cᵀy + C_eᵀλ + Gᵀz), r_feas = max(||c||∞, ||c_e||∞, ||g+s||∞),
  *     r_comp = ||Sz − μe||∞, r_comp0 = ||Sz||∞;
  *   converged (status 0) if max(r_stat, r_feas, r_comp0) <= tol_kkt and μ <= 10 mu_min;

@@ -99,14 +99,15 @@ def evaluate(ref, x, u):
         A, B = _cm(d["A"], n, n), _cm(d["B"], n, m)
         out["dres"] = (d["dres"] + np.einsum("bisr,bir->bis", A, dx[:, :N]) + np.einsum("bisr,bir->bis", B, du)
                        - dx[:, 1:])
-    else:                # cart-pole (the workload definition, synth/ipm_workloads.py)
-        from synth.ipm_workloads import cartpole_step_torch
+    else:                # cart-pole / quadrotor (the workload definitions, synth/ipm_workloads.py)
+        from synth.ipm_workloads import cartpole_step_torch, quadrotor_step_torch
+        step = cartpole_step_torch if ref.model == 1 else quadrotor_step_torch
         prm = torch.as_tensor(d["model_params"])
         xi = torch.as_tensor(x[:, :N].reshape(-1, n))
         ui = torch.as_tensor(u.reshape(-1, m))
-        fx = cartpole_step_torch(prm, xi, ui).numpy().reshape(b, N, n)
+        fx = step(prm, xi, ui).numpy().reshape(b, N, n)
         out["dres"] = fx - x[:, 1:]
-        jac = torch.func.vmap(torch.func.jacrev(lambda xx, uu: cartpole_step_torch(prm, xx, uu), argnums=(0, 1)))
+        jac = torch.func.vmap(torch.func.jacrev(lambda xx, uu: step(prm, xx, uu), argnums=(0, 1)))
         Jx, Ju = jac(xi, ui)
         out["A"] = np.swapaxes(Jx.numpy(), -1, -2).reshape(b, N, n * n)   # column-major
         out["B"] = np.swapaxes(Ju.numpy(), -1, -2).reshape(b, N, n * m)

@@ -7,7 +7,7 @@
 //   iteration k, every running instance:
 //     eval      problem data at the iterate: cost quadratic with Hessian P and constraints linear
 //               (exact from the reference data at the initial iterate, reading R19); dynamics
-//               linear (LQ) or the cart-pole model with analytic Jacobians
+//               linear (LQ), the cart-pole or the quadrotor model with analytic Jacobians
 //     residuals r_stat = ||∇ₓL||∞, r_feas = max(||c||∞, ||c_e||∞, ||g+s||∞), r_comp = ||Sz − μ||∞,
 //               r_comp0 = ||Sz||∞
 //     stop      converged if max(r_stat, r_feas, r_comp0) <= tol and μ <= 10 μ_min; MAXITER at k = max
@@ -80,9 +80,9 @@ int64_t carve(const ipm_dims& d, char* base, SolveWs* w) {
   D(&v->gvN, b * d.ngN);
   D(&v->ce, b * N * d.nc);
   D(&v->ceN, b * d.ncN);
-  const bool cp = d.model == IPM_MODEL_CARTPOLE;
-  D(&v->A, cp ? b * N * n * n : 0);
-  D(&v->B, cp ? b * N * n * m : 0);
+  const bool nl = d.model != IPM_MODEL_LQ;  // nonlinear model: Jacobians re-evaluated at every iterate
+  D(&v->A, nl ? b * N * n * n : 0);
+  D(&v->B, nl ? b * N * n * m : 0);
   D(&v->mu, b);
   D(&v->eta, b);
   D(&v->hist, b * 5);
@@ -173,6 +173,78 @@ __device__ void cartpole_eval(const double* prm, const double* x, double F, doub
   Bv[3] = dt * thdd_F;
 }
 
+// ---- quadrotor explicit-Euler step x⁺ = x + dt f(x, u) and its Jacobians (SURVEY §8(d) C5 model) ----
+// x = (p, φ θ ψ ZYX Euler angles, world velocity v, body rates ω), u = (T, τ); prm [dt, mass, Jx, Jy, Jz, g].
+// A = I + dt ∂f/∂x (column-major 12×12), B = dt ∂f/∂u (column-major 12×4), derivatives written out.
+__device__ void quadrotor_eval(const double* prm, const double* x, const double* u, double* xn, double* A,
+                               double* B) {
+  const double dt = prm[0], mass = prm[1], Jx = prm[2], Jy = prm[3], Jz = prm[4], g = prm[5];
+  double sph, cph, sth, cth, sps, cps;
+  sincos(x[3], &sph, &cph);
+  sincos(x[4], &sth, &cth);
+  sincos(x[5], &sps, &cps);
+  const double wx = x[9], wy = x[10], wz = x[11], T = u[0], Tm = T / mass;
+  const double tth = sth / cth, ic = 1.0 / cth;
+  const double a1 = sph * wy + cph * wz;  // W row terms
+  const double a2 = cph * wy - sph * wz;
+  const double r0 = cps * sth * cph + sps * sph, r1 = sps * sth * cph - cps * sph, r2 = cth * cph;  // R e₃
+  double f[12];
+  f[0] = x[6];
+  f[1] = x[7];
+  f[2] = x[8];
+  f[3] = wx + tth * a1;
+  f[4] = a2;
+  f[5] = ic * a1;
+  f[6] = r0 * Tm;
+  f[7] = r1 * Tm;
+  f[8] = r2 * Tm - g;
+  f[9] = (u[1] - (Jz - Jy) * wy * wz) / Jx;
+  f[10] = (u[2] - (Jx - Jz) * wz * wx) / Jy;
+  f[11] = (u[3] - (Jy - Jx) * wx * wy) / Jz;
+  for (int r = 0; r < 12; ++r) xn[r] = x[r] + dt * f[r];
+  for (int e = 0; e < 144; ++e) A[e] = (e % 13 == 0) ? 1.0 : 0.0;
+  for (int e = 0; e < 48; ++e) B[e] = 0.0;
+  auto a = [&](int r, int c, double v) { A[r + 12 * c] += dt * v; };
+  for (int k = 0; k < 3; ++k) a(k, 6 + k, 1.0);  // ṗ = v
+  // φ̇ = ωx + tanθ (sφ ωy + cφ ωz)
+  a(3, 3, tth * a2);
+  a(3, 4, ic * ic * a1);
+  a(3, 9, 1.0);
+  a(3, 10, tth * sph);
+  a(3, 11, tth * cph);
+  // θ̇ = cφ ωy − sφ ωz
+  a(4, 3, -a1);
+  a(4, 10, cph);
+  a(4, 11, -sph);
+  // ψ̇ = (sφ ωy + cφ ωz) / cθ
+  a(5, 3, ic * a2);
+  a(5, 4, ic * tth * a1);
+  a(5, 10, ic * sph);
+  a(5, 11, ic * cph);
+  // v̇ = R(φ, θ, ψ) e₃ T/m − g e₃
+  a(6, 3, (-cps * sth * sph + sps * cph) * Tm);
+  a(6, 4, cps * cth * cph * Tm);
+  a(6, 5, (-sps * sth * cph + cps * sph) * Tm);
+  a(7, 3, (-sps * sth * sph - cps * cph) * Tm);
+  a(7, 4, sps * cth * cph * Tm);
+  a(7, 5, r0 * Tm);
+  a(8, 3, -cth * sph * Tm);
+  a(8, 4, -sth * cph * Tm);
+  // ω̇ = J⁻¹(τ − ω × Jω)
+  a(9, 10, -(Jz - Jy) * wz / Jx);
+  a(9, 11, -(Jz - Jy) * wy / Jx);
+  a(10, 9, -(Jx - Jz) * wz / Jy);
+  a(10, 11, -(Jx - Jz) * wx / Jy);
+  a(11, 9, -(Jy - Jx) * wy / Jz);
+  a(11, 10, -(Jy - Jx) * wx / Jz);
+  B[6 + 12 * 0] = dt * r0 / mass;
+  B[7 + 12 * 0] = dt * r1 / mass;
+  B[8 + 12 * 0] = dt * r2 / mass;
+  B[9 + 12 * 1] = dt / Jx;
+  B[10 + 12 * 2] = dt / Jy;
+  B[11 + 12 * 3] = dt / Jz;
+}
+
 // ---- evaluation: one thread per (instance, stage 0..N) of the running instances ----
 __global__ void solve_eval_kernel(ipm_dims d, ipm_stage_data ref, ipm_iterate it, SolveWs w) {
   const int N = d.N, n = d.nx, m = d.nu, wd = n + m, ng = d.ng, nc = d.nc;
@@ -236,6 +308,12 @@ __global__ void solve_eval_kernel(ipm_dims d, ipm_stage_data ref, ipm_iterate it
     for (int r = 0; r < 4; ++r) dr[r] = xn[r] - x1[r];
     for (int e = 0; e < 16; ++e) w.A[(b * sN + i) * 16 + e] = A[e];
     for (int e = 0; e < 4; ++e) w.B[(b * sN + i) * 4 + e] = Bv[e];
+  } else if (d.model == IPM_MODEL_QUADROTOR) {
+    double xn[12], A[144], Bq[48];
+    quadrotor_eval(ref.model_params, xi, it.u + (b * sN + i) * 4, xn, A, Bq);
+    for (int r = 0; r < 12; ++r) dr[r] = xn[r] - x1[r];
+    for (int e = 0; e < 144; ++e) w.A[(b * sN + i) * 144 + e] = A[e];
+    for (int e = 0; e < 48; ++e) w.B[(b * sN + i) * 48 + e] = Bq[e];
   } else {
     const double* A = ref.A + (b * sN + i) * n * n;
     const double* B = ref.B + (b * sN + i) * n * m;
@@ -263,8 +341,8 @@ __global__ void solve_kkt_kernel(ipm_dims d, ipm_stage_data ref, ipm_iterate it,
   const int N = d.N, n = d.nx, m = d.nu, wd = n + m, ng = d.ng, nc = d.nc;
   const int64_t sN = N;
   const double mu = w.mu[b];
-  const double* A = (d.model == IPM_MODEL_CARTPOLE) ? w.A : ref.A;
-  const double* B = (d.model == IPM_MODEL_CARTPOLE) ? w.B : ref.B;
+  const double* A = (d.model != IPM_MODEL_LQ) ? w.A : ref.A;
+  const double* B = (d.model != IPM_MODEL_LQ) ? w.B : ref.B;
   double rs = 0.0, rf = 0.0, rc = 0.0, rc0 = 0.0, fsum = 0.0;
   bool bad = false;
   auto mx = [&](double& acc, double v) {
@@ -378,7 +456,7 @@ cudaError_t ipm_solve_launch(const ipm_dims& d, const ipm_stage_data& data, cons
   cur.gvN = d.ngN ? w.gvN : nullptr;
   cur.ce = d.nc ? w.ce : nullptr;
   cur.ceN = d.ncN ? w.ceN : nullptr;
-  if (d.model == IPM_MODEL_CARTPOLE) {
+  if (d.model != IPM_MODEL_LQ) {
     cur.A = w.A;
     cur.B = w.B;
   }

@@ -375,8 +375,7 @@ static rr_err ipm_step_impl(const ipm_dims* dims, const ipm_stage_data* data, co
 }
 
 int64_t ipm_solve_workspace_bytes(const ipm_dims* dims) {
-  // the solve loop re-evaluates the model's Jacobians: LQ and the cart-pole only (no quadrotor Jacobians)
-  if (!ipm_dims_ok(dims) || dims->model == IPM_MODEL_QUADROTOR) return -1;
+  if (!ipm_dims_ok(dims)) return -1;
   return rrk::ipm_solve_ws_bytes(*dims);
 }
 
@@ -399,8 +398,8 @@ rr_err ipm_solve(const ipm_dims* dims, const ipm_stage_data* data, const ipm_ite
   if (!data->s0 || !data->fval || !data->gradfN || !data->QN || !it->x || !it->y || !it->mu || !it->eta ||
       (dims->N > 0 && (!data->gradf || !data->Q || !data->M || !data->R || !data->A || !data->B || !data->dres || !it->u)))
     return set_err(RR_E_INVALID, "ipm_solve: null %s", "required pointer");
-  if (dims->model == IPM_MODEL_CARTPOLE && data->model_params == nullptr)
-    return set_err(RR_E_INVALID, "ipm_solve: cart-pole model needs %s", "model_params");
+  if (dims->model != IPM_MODEL_LQ && data->model_params == nullptr)
+    return set_err(RR_E_INVALID, "ipm_solve: the built-in nonlinear models need %s", "model_params");
   bool supported = false;
   cudaError_t e = rrk::ipm_solve_launch(*dims, *data, *it, *S, *rep, workspace, static_cast<cudaStream_t>(stream),
                                         &supported);

@@ -143,11 +143,8 @@ def test_ipm_parity_quadrotor_model(batch, N, seed):
 
 
 def test_quadrotor_model_rules():
-    """The quadrotor model needs n = 12, m = 4 and model_params; ipm_solve does not take it."""
+    """The quadrotor model needs n = 12, m = 4."""
     import paper_2509_16370_b200 as rr
-    p = quadrotor_ipm(4, N=5).to("cuda")
-    with pytest.raises(rr.RRError):
-        rr.ipm_solve(p, max_iters=2)
     bad = random_lq_ocp(4, 1, 5, 3, seed=1, ng=2)
     bad.model = 2
     with pytest.raises(rr.RRError):

@@ -8,7 +8,7 @@ import pytest
 import torch
 
 from oracle.ipm_solve import SolveSettings, ipm_solve_oracle
-from synth.ipm_workloads import cartpole_c4, double_integrator_ocp, random_lq_ocp
+from synth.ipm_workloads import cartpole_c4, double_integrator_ocp, quadrotor_ipm, random_lq_ocp
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-9
@@ -78,3 +78,23 @@ def test_converged_instances_are_frozen_and_empty_batch():
     assert torch.all(rep["status"] == 0)
     e = double_integrator_ocp(batch=0).to("cuda")
     m.ipm_solve(e)
+
+
+@pytest.mark.parametrize("iters", [1, 4])
+def test_quadrotor_first_iterations(iters):
+    """Quadrotor model (analytic Jacobians re-evaluated at every iterate) over the first iterations."""
+    b = quadrotor_ipm(24, N=20)
+    it_g, rep_g, it_o, rep_o = run_both(b, max_iters=iters)
+    check(it_g, rep_g, it_o, rep_o, tol=1e-8)
+
+
+def test_quadrotor_solve_converges():
+    """The quadrotor hover problems converge (oracle: 18-34 iterations); GPU report against the oracle."""
+    b = quadrotor_ipm(6, N=20)
+    it_g, rep_g, it_o, rep_o = run_both(b)
+    assert np.all(rep_o["status"] == 0)
+    assert np.all(rep_g["status"] == 0)
+    assert np.max(np.abs(rep_g["iters"] - rep_o["iters"])) <= 1
+    assert np.all(np.maximum(np.maximum(rep_g["r_stat"], rep_g["r_feas"]), rep_g["r_comp"]) <= 1e-6)
+    for k in ("x", "u"):
+        assert rel(it_g[k], it_o[k]) <= 1e-5, k

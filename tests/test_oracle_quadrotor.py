@@ -114,3 +114,11 @@ def test_descent_theorem_quadrotor():
         fd = (ipm_merit_oracle(p, res, b, h) - ipm_merit_oracle(p, res, b, -h)) / (2 * h)
         assert abs(fd - D) <= max(1e-6, 1e-4 * abs(D)), (fd, D)
         assert res["merit_acc"][b] <= res["merit0"][b] + 1e-4 * res["alpha_p"][b] * D
+
+
+def test_solve_loop_converges_on_quadrotor():
+    """The oracle IPM loop (reading R21) with the quadrotor model converges on the hover problems."""
+    from oracle.ipm_solve import ipm_solve_oracle
+    _, rep = ipm_solve_oracle(quadrotor_ipm(4, N=20))
+    assert np.all(rep["status"] == 0) and np.all(rep["iters"] <= 60)
+    assert np.all(np.maximum(np.maximum(rep["r_stat"], rep["r_feas"]), rep["r_comp0"]) <= 1e-6)
