@@ -125,15 +125,10 @@ __device__ void store_tile(double* g, const double* T, int rows, int cols, int l
 }
 
 // ---- 1. stage assembly: warp per (instance, stage) ----
-__global__ void __launch_bounds__(WPB * 32) pit_assemble_kernel(PitArgs a) {
-  extern __shared__ __align__(16) double sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
+__device__ void pit_assemble_item(const PitArgs& a, int64_t item, double* T, int lane) {  // T: 8 tiles
   const int n = a.nx, m = a.nu, N = a.N;
-  if (item >= a.batch * (int64_t)N) return;
   const int64_t inst = item / N;
   const int i = (int)(item % N);
-  double* T = sm + warp * 8 * TILE;
   double *tA = T, *tB = T + TILE, *tG = T + 2 * TILE, *tHxu = T + 3 * TILE, *tW1 = T + 4 * TILE, *tW2 = T + 5 * TILE,
          *tE = T + 6 * TILE, *tv = T + 7 * TILE;
   const double d = a.p.delta[inst];
@@ -255,11 +250,8 @@ __global__ void __launch_bounds__(WPB * 32) pit_assemble_kernel(PitArgs a) {
 }
 
 // ---- 2. block-tridiagonal system: D_k, b_k (warp per (instance, k)) ----
-__global__ void __launch_bounds__(WPB * 32) pit_diag_kernel(PitArgs a) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
+__device__ void pit_diag_item(const PitArgs& a, int64_t item, int lane) {
   const int n = a.nx, m = a.nu, N = a.N;
-  if (item >= a.batch * (int64_t)(N + 1)) return;
   const int64_t inst = item / (N + 1);
   const int k = (int)(item % (N + 1));
   PitWs v = views(a.ws, inst, N, n, m);
@@ -290,17 +282,12 @@ __global__ void __launch_bounds__(WPB * 32) pit_diag_kernel(PitArgs a) {
 //  index k are overwritten later only by the elimination of index k itself)
 
 // ---- 3a. cyclic reduction, elimination of the indices k ≡ s (mod 2s) ----
-__global__ void __launch_bounds__(WPB * 32) pit_elim_kernel(PitArgs a, int s) {
-  extern __shared__ __align__(16) double sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ void pit_elim_item(const PitArgs& a, int s, int64_t item, double* T, int lane) {  // T: 4 tiles
   const int n = a.nx, m = a.nu, N = a.N;
   const int64_t per = (int64_t)((N - s) / (2 * s) + 1);  // eliminated indices per instance
-  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
-  if (item >= a.batch * per) return;
   const int64_t inst = item / per;
   const int k = s + 2 * s * (int)(item % per);
   PitWs v = views(a.ws, inst, N, n, m);
-  double* T = sm + warp * 4 * TILE;
   double *tD = T, *tC = T + TILE, *tY = T + 2 * TILE, *tb = T + 3 * TILE;
   load_tile(tD, v.D + (int64_t)k * n * n, n, n, lane);
   bool bad = false;
@@ -344,17 +331,12 @@ __global__ void __launch_bounds__(WPB * 32) pit_elim_kernel(PitArgs a, int s) {
 }
 
 // ---- 3b. cyclic reduction, Schur updates of the remaining indices j ≡ 0 (mod 2s) ----
-__global__ void __launch_bounds__(WPB * 32) pit_update_kernel(PitArgs a, int s) {
-  extern __shared__ __align__(16) double sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ void pit_update_item(const PitArgs& a, int s, int64_t item, double* T, int lane) {  // T: 4 tiles
   const int n = a.nx, m = a.nu, N = a.N;
   const int64_t per = (int64_t)(N / (2 * s) + 1);
-  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
-  if (item >= a.batch * per) return;
   const int64_t inst = item / per;
   const int j = 2 * s * (int)(item % per);
   PitWs v = views(a.ws, inst, N, n, m);
-  double* T = sm + warp * 4 * TILE;
   double *tD = T, *tC = T + TILE, *tY = T + 2 * TILE, *tb = T + 3 * TILE;
   load_tile(tD, v.D + (int64_t)j * n * n, n, n, lane);
   if (lane < n) tb[lane] = v.b[(int64_t)j * n + lane];
@@ -406,14 +388,9 @@ __global__ void __launch_bounds__(WPB * 32) pit_update_kernel(PitArgs a, int s) 
 }
 
 // ---- 3c. root x_0 = D_0⁻¹ b_0, then back-substitution per level ----
-__global__ void __launch_bounds__(WPB * 32) pit_root_kernel(PitArgs a) {
-  extern __shared__ __align__(16) double sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ void pit_root_item(const PitArgs& a, int64_t inst, double* T, int lane) {  // T: 1 tile
   const int n = a.nx, m = a.nu, N = a.N;
-  const int64_t inst = (int64_t)blockIdx.x * WPB + warp;
-  if (inst >= a.batch) return;
   PitWs v = views(a.ws, inst, N, n, m);
-  double* T = sm + warp * 4 * TILE;
   load_tile(T, v.D, n, n, lane);
   bool bad = false;
   warp_inv_spd(T, n, lane, bad);
@@ -426,12 +403,9 @@ __global__ void __launch_bounds__(WPB * 32) pit_root_kernel(PitArgs a) {
   if (bad && lane == 0) atomicMax(a.status + inst, (int32_t)mk_status(RR_ST_S_NOT_PD, 0));
 }
 
-__global__ void __launch_bounds__(WPB * 32) pit_backsub_kernel(PitArgs a, int s) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ void pit_backsub_item(const PitArgs& a, int s, int64_t item, int lane) {
   const int n = a.nx, m = a.nu, N = a.N;
   const int64_t per = (int64_t)((N - s) / (2 * s) + 1);
-  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
-  if (item >= a.batch * per) return;
   const int64_t inst = item / per;
   const int k = s + 2 * s * (int)(item % per);
   PitWs v = views(a.ws, inst, N, n, m);
@@ -449,11 +423,8 @@ __global__ void __launch_bounds__(WPB * 32) pit_backsub_kernel(PitArgs a, int s)
 }
 
 // ---- 4. controls and duals: warp per (instance, stage) ----
-__global__ void __launch_bounds__(WPB * 32) pit_recover_kernel(PitArgs a) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ void pit_recover_item(const PitArgs& a, int64_t item, int lane) {
   const int n = a.nx, m = a.nu, N = a.N;
-  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
-  if (item >= a.batch * (int64_t)(N + 1)) return;
   const int64_t inst = item / (N + 1);
   const int i = (int)(item % (N + 1));
   const double d = a.p.delta[inst];
@@ -507,11 +478,8 @@ __global__ void __launch_bounds__(WPB * 32) pit_recover_kernel(PitArgs a) {
 // ---- refinement (re-solve with the stored reduction for a new right-hand side) ----
 // rhs assembly: l_u = δr + Bᵀc, l_x = δq + Aᵀc, t1 = G'⁻¹l_u, e_x = l_x − Hxu t1 (-> yb_i),
 // e_x' = −c + B t1 (-> b_{i+1}), l_u kept for the recovery of u
-__global__ void __launch_bounds__(WPB * 32) pit_rhs_assemble_kernel(PitArgs a) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
+__device__ void pit_rhs_assemble_item(const PitArgs& a, int64_t item, int lane) {
   const int n = a.nx, m = a.nu, N = a.N;
-  if (item >= a.batch * (int64_t)N) return;
   const int64_t inst = item / N;
   const int i = (int)(item % N);
   PitWs v = views(a.ws, inst, N, n, m);
@@ -553,11 +521,8 @@ __global__ void __launch_bounds__(WPB * 32) pit_rhs_assemble_kernel(PitArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(WPB * 32) pit_rhs_diag_kernel(PitArgs a) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
+__device__ void pit_rhs_diag_item(const PitArgs& a, int64_t item, int lane) {
   const int n = a.nx, m = a.nu, N = a.N;
-  if (item >= a.batch * (int64_t)(N + 1)) return;
   const int64_t inst = item / (N + 1);
   const int k = (int)(item % (N + 1));
   PitWs v = views(a.ws, inst, N, n, m);
@@ -571,12 +536,9 @@ __global__ void __launch_bounds__(WPB * 32) pit_rhs_diag_kernel(PitArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(WPB * 32) pit_rhs_elim_kernel(PitArgs a, int s) {  // yb_k = D_k⁻¹ b_k
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ void pit_rhs_elim_item(const PitArgs& a, int s, int64_t item, int lane) {  // yb_k = D_k⁻¹ b_k
   const int n = a.nx, m = a.nu, N = a.N;
   const int64_t per = (int64_t)((N - s) / (2 * s) + 1);
-  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
-  if (item >= a.batch * per) return;
   const int64_t inst = item / per;
   const int k = s + 2 * s * (int)(item % per);
   PitWs v = views(a.ws, inst, N, n, m);
@@ -588,13 +550,10 @@ __global__ void __launch_bounds__(WPB * 32) pit_rhs_elim_kernel(PitArgs a, int s
   }
 }
 
-__global__ void __launch_bounds__(WPB * 32) pit_rhs_update_kernel(PitArgs a, int s) {
+__device__ void pit_rhs_update_item(const PitArgs& a, int s, int64_t item, int lane) {
   // b_j −= C_jᵀ yb_{j+s} + C_{j−s} yb_{j−s} = Y1_{j+s}ᵀ b_{j+s} + Y2_{j−s}ᵀ b_{j−s}
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = a.nx, m = a.nu, N = a.N;
   const int64_t per = (int64_t)(N / (2 * s) + 1);
-  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
-  if (item >= a.batch * per) return;
   const int64_t inst = item / per;
   const int j = 2 * s * (int)(item % per);
   PitWs v = views(a.ws, inst, N, n, m);
@@ -612,11 +571,8 @@ __global__ void __launch_bounds__(WPB * 32) pit_rhs_update_kernel(PitArgs a, int
   }
 }
 
-__global__ void __launch_bounds__(WPB * 32) pit_rhs_root_kernel(PitArgs a) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ void pit_rhs_root_item(const PitArgs& a, int64_t inst, int lane) {
   const int n = a.nx, m = a.nu, N = a.N;
-  const int64_t inst = (int64_t)blockIdx.x * WPB + warp;
-  if (inst >= a.batch) return;
   PitWs v = views(a.ws, inst, N, n, m);
   if (lane < n) {
     double acc = 0.0;
@@ -628,11 +584,8 @@ __global__ void __launch_bounds__(WPB * 32) pit_rhs_root_kernel(PitArgs a) {
 // KKT residual r = K[x; y] + [s; c] (as rr_residual), one warp per (instance, stage i):
 // rows x_i, u_i, primal row i+1 (item i < N); rows x_N and primal row 0 (item N) -- stage-parallel,
 // unlike rr_residual's lane group walking the horizon, so a single long instance is not serialised
-__global__ void __launch_bounds__(WPB * 32) pit_residual_kernel(PitArgs a, rr_residual_buf rb) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t item = (int64_t)blockIdx.x * WPB + warp;
+__device__ void pit_residual_item(const PitArgs& a, const rr_residual_buf& rb, int64_t item, int lane) {
   const int n = a.nx, m = a.nu, N = a.N;
-  if (item >= a.batch * (int64_t)(N + 1)) return;
   const int64_t inst = item / (N + 1);
   const int i = (int)(item % (N + 1));
   const double d = a.p.delta[inst];
@@ -707,6 +660,69 @@ __global__ void pit_nanfill(PitArgs a) {  // NaN-fill the outputs of failed inst
   else a.s.u[b * N * m + e - 2 * (N + 1) * n] = nan;
 }
 
+// ---- one launch per step (any batch): warp per item ----
+#define PIT_ITEM_PROLOGUE(count)                                   \
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;     \
+  const int64_t item = (int64_t)blockIdx.x * WPB + warp;          \
+  if (item >= (count)) return;
+__global__ void __launch_bounds__(WPB * 32) pit_assemble_kernel(PitArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  PIT_ITEM_PROLOGUE(a.batch * (int64_t)a.N)
+  pit_assemble_item(a, item, sm + warp * 8 * TILE, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_diag_kernel(PitArgs a) {
+  PIT_ITEM_PROLOGUE(a.batch * (int64_t)(a.N + 1))
+  pit_diag_item(a, item, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_elim_kernel(PitArgs a, int s) {
+  extern __shared__ __align__(16) double sm[];
+  PIT_ITEM_PROLOGUE(a.batch * (int64_t)((a.N - s) / (2 * s) + 1))
+  pit_elim_item(a, s, item, sm + warp * 4 * TILE, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_update_kernel(PitArgs a, int s) {
+  extern __shared__ __align__(16) double sm[];
+  PIT_ITEM_PROLOGUE(a.batch * (int64_t)(a.N / (2 * s) + 1))
+  pit_update_item(a, s, item, sm + warp * 4 * TILE, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_root_kernel(PitArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  PIT_ITEM_PROLOGUE(a.batch)
+  pit_root_item(a, item, sm + warp * 4 * TILE, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_backsub_kernel(PitArgs a, int s) {
+  PIT_ITEM_PROLOGUE(a.batch * (int64_t)((a.N - s) / (2 * s) + 1))
+  pit_backsub_item(a, s, item, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_recover_kernel(PitArgs a) {
+  PIT_ITEM_PROLOGUE(a.batch * (int64_t)(a.N + 1))
+  pit_recover_item(a, item, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_rhs_assemble_kernel(PitArgs a) {
+  PIT_ITEM_PROLOGUE(a.batch * (int64_t)a.N)
+  pit_rhs_assemble_item(a, item, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_rhs_diag_kernel(PitArgs a) {
+  PIT_ITEM_PROLOGUE(a.batch * (int64_t)(a.N + 1))
+  pit_rhs_diag_item(a, item, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_rhs_elim_kernel(PitArgs a, int s) {
+  PIT_ITEM_PROLOGUE(a.batch * (int64_t)((a.N - s) / (2 * s) + 1))
+  pit_rhs_elim_item(a, s, item, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_rhs_update_kernel(PitArgs a, int s) {
+  PIT_ITEM_PROLOGUE(a.batch * (int64_t)(a.N / (2 * s) + 1))
+  pit_rhs_update_item(a, s, item, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_rhs_root_kernel(PitArgs a) {
+  PIT_ITEM_PROLOGUE(a.batch)
+  pit_rhs_root_item(a, item, lane);
+}
+__global__ void __launch_bounds__(WPB * 32) pit_residual_kernel(PitArgs a, rr_residual_buf rb) {
+  PIT_ITEM_PROLOGUE(a.batch * (int64_t)(a.N + 1))
+  pit_residual_item(a, rb, item, lane);
+}
+#undef PIT_ITEM_PROLOGUE
+
 unsigned blocks_for(int64_t items) { return (unsigned)((items + WPB - 1) / WPB); }
 
 }  // namespace
@@ -716,6 +732,25 @@ int64_t pit_ws_bytes(int nx, int nu, int N, int64_t batch) {
   // per-instance reduction + batch-wide residual (q, r, c, qN, c0) and correction (x, u, y) buffers
   const int64_t glob = (int64_t)N * (2 * nx + nu) + 2 * nx + (int64_t)(N + 1) * 2 * nx + (int64_t)N * nu;
   return batch * (pit_per(N, nx, nu) + glob) * 8 + 256;
+}
+
+// the correction system of the refinement step: right-hand side = the residual, solution → (cx, cu, cy)
+static void pit_buffers(const PitArgs& a, rr_residual_buf& rb, PitArgs& c) {
+  const int64_t b = a.batch;
+  const int N = a.N, n = a.nx, m = a.nu;
+  double* glob = a.ws + b * pit_per(N, n, m);
+  rb = rr_residual_buf{glob, glob + b * N * n, glob + b * N * (n + m), glob + b * N * (2 * n + m),
+                       glob + b * (N * (2 * n + m) + n)};
+  double* cx = glob + b * (N * (2 * n + m) + 2 * n);
+  double* cu = cx + b * (N + 1) * n;
+  double* cy = cu + b * N * m;
+  c = a;
+  c.p.q = rb.q;
+  c.p.r = rb.r;
+  c.p.c = rb.c;
+  c.p.qN = rb.qN;
+  c.p.c0 = rb.c0;
+  c.s = rr_solution{cx, cu, cy};
 }
 
 cudaError_t pit_launch(const PitArgs& a, cudaStream_t s) {
@@ -743,21 +778,12 @@ cudaError_t pit_launch(const PitArgs& a, cudaStream_t s) {
   // one step of iterative refinement in FP64 (residual kernel of rr_split.cu, re-solve with the
   // stored reduction): the δ-scaled state system is conditioned like 1/δ, the recursion is not
   const int n = a.nx, m = a.nu;
-  double* glob = a.ws + b * pit_per(N, n, m);
-  rr_residual_buf rb{glob, glob + b * N * n, glob + b * N * (n + m), glob + b * N * (2 * n + m),
-                     glob + b * (N * (2 * n + m) + n)};
-  double* cx = glob + b * (N * (2 * n + m) + 2 * n);
-  double* cu = cx + b * (N + 1) * n;
-  double* cy = cu + b * N * m;
+  rr_residual_buf rb;
+  PitArgs c;
+  pit_buffers(a, rb, c);
+  double *cx = c.s.x, *cu = c.s.u, *cy = c.s.y;
   for (int it = 0; it < a.refine; ++it) {
     pit_residual_kernel<<<blocks_for(b * (N + 1)), WPB * 32, 0, s>>>(a, rb);
-    PitArgs c = a;  // the correction system: right-hand side = the residual
-    c.p.q = rb.q;
-    c.p.r = rb.r;
-    c.p.c = rb.c;
-    c.p.qN = rb.qN;
-    c.p.c0 = rb.c0;
-    c.s = rr_solution{cx, cu, cy};
     if (N > 0) pit_rhs_assemble_kernel<<<blocks_for(b * N), WPB * 32, 0, s>>>(c);
     pit_rhs_diag_kernel<<<blocks_for(b * (N + 1)), WPB * 32, 0, s>>>(c);
     for (int st = 1; st <= N; st *= 2) {
