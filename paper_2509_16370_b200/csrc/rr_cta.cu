@@ -9,8 +9,9 @@
 //   [U | b] = Fᵀ [T | g] + [P | (q; r)]          U = [[AᵀWA+Q, Hᵀ]; [H, G]], b = [q+Aᵀg; r+Bᵀg]
 //   G⁻¹ by a symmetric sweep; K̃ = G⁻¹ [H | h]                    (−K_i, −k_i)
 //   [V_i | v_i] = [AᵀWA+Q | q+Aᵀg] − Hᵀ K̃                        (P:623-624 with P:606-611)
-//   [Φ_i | φ_i] = S⁻¹ ([A | c_{i+1} − δ v_{i+1}] − B K̃)  -> record for the forward sweep
-// forward: x_{i+1} = Φ_i x_i + φ_i, u_i = K_i x_i + k_i, y_i = V_i x_i + v_i.
+//   record for the forward sweep: K_i, k_i, V_i, v_i, S_{i+1}⁻¹ (packed), e_i
+// forward: u_i = K_i x_i + k_i, y_i = V_i x_i + v_i,
+//   x_{i+1} = S_{i+1}⁻¹ (A_i x_i + B_i u_i + e_i) with A_i, B_i re-read by TMA (no Φ products).
 // Shared-memory plan (doubles) for one instance: stage input (cp.async) | S⁻¹ | V/W/U | T/K̃/M |
 // vectors -- about 230 KB, one CTA per SM; the next stage's input streams in during the last
 // contraction of the current stage.
