@@ -48,3 +48,15 @@ b = cartpole_c4(4, seed=3, N=8, device="cuda")
 rep2 = rr.ipm_solve(b, max_iters=3)
 torch.cuda.synchronize()
 print("ipm_solve", rep["status"].tolist(), rep2["status"].tolist())
+# parallel in time, quadrotor model (ipm_step, ipm_solve), user-model line search
+p = synth.random_stable_lqr(12, 4, 37, 2, seed=7, delta=1e-3).to("cuda")
+rr.rr_factor_solve_pit(p)
+from synth.ipm_workloads import quadrotor_ipm  # noqa: E402
+q = quadrotor_ipm(3, N=6, device="cuda")
+resq = rr.ipm_step(q)
+q = quadrotor_ipm(3, N=6, device="cuda")
+repq = rr.ipm_solve(q, max_iters=3)
+b = random_lq_ocp(3, 2, 4, 5, seed=8, ng=2, ngN=1, nc=1, ncN=1, device="cuda")
+d = rr.ipm_direction(b)
+torch.cuda.synchronize()
+print("pit / quadrotor / direction", resq["status"].tolist(), repq["status"].tolist(), d["status"].tolist())
