@@ -9,8 +9,10 @@ with P = blkdiag(P_0..P_{N-1}, Q_N), P_i = [[Q_i, M_i], [M_i^T, R_i]] (P:321-333
 C banded with block rows  -x_0  and  A_i x_i + B_i u_i - x_{i+1},
 s = (q_0, r_0, ..., q_{N-1}, r_{N-1}, q_N), c = (c_0, ..., c_N) (reading R1:
 N+1 blocks), x = (x_0, u_0, ..., x_N), y = (y_0, ..., y_N).
-It is assembled densely and solved with LAPACK (numpy.linalg.solve), a library
-primitive; no structure is exploited.
+It is assembled densely and solved with LAPACK, a library primitive; no structure is exploited:
+numpy.linalg.solve (LU), or `ldl_solve` -- the symmetric-indefinite Bunch-Kaufman LDLᵀ
+factorisation (LAPACK sytrf via scipy.linalg.ldl) followed by the two triangular solves and the
+1×1 / 2×2 block-diagonal solve; both are pinned against each other in tests/test_oracle_rr.py.
 """
 from __future__ import annotations
 
@@ -98,10 +100,32 @@ def unpack_solution(sol, n, m, N):
     return x, u, y
 
 
-def rr_solve_dense(prob, b=0):
-    """T1 solve of instance b.  Returns dict(x [N+1,n], u [N,m], y [N+1,n], K, rhs, C)."""
+def ldl_solve(K, rhs):
+    """Solve K z = rhs for symmetric (indefinite) K by Bunch-Kaufman LDLᵀ: P K Pᵀ = L D Lᵀ with D
+    block diagonal (1×1 and 2×2 pivots).  scipy returns K = lu·D·luᵀ with lu[perm] lower triangular."""
+    import scipy.linalg as sl
+    lu, D, perm = sl.ldl(K, lower=True)
+    L = lu[perm]                                                        # unit lower triangular
+    w = sl.solve_triangular(L, np.asarray(rhs, dtype=np.float64)[perm], lower=True, unit_diagonal=True)
+    v = np.zeros_like(w)
+    i, nn = 0, K.shape[0]
+    while i < nn:                                                       # D w' = w, block by block
+        if i + 1 < nn and D[i + 1, i] != 0.0:
+            v[i:i + 2] = np.linalg.solve(D[i:i + 2, i:i + 2], w[i:i + 2])
+            i += 2
+        else:
+            v[i] = w[i] / D[i, i]
+            i += 1
+    z = np.empty_like(v)
+    z[perm] = sl.solve_triangular(L.T, v, lower=False, unit_diagonal=True)
+    return z
+
+
+def rr_solve_dense(prob, b=0, method="lu"):
+    """T1 solve of instance b (method "lu" or "ldl").  Returns dict(x [N+1,n], u [N,m], y [N+1,n],
+    K, rhs, C)."""
     blk = instance_blocks(prob, b)
     K, rhs, C = assemble_reglqr(blk)
-    sol = np.linalg.solve(K, rhs)
+    sol = ldl_solve(K, rhs) if method == "ldl" else np.linalg.solve(K, rhs)
     x, u, y = unpack_solution(sol, blk["n"], blk["m"], blk["N"])
     return dict(x=x, u=u, y=y, K=K, rhs=rhs, C=C, blk=blk, sol=sol)

@@ -90,10 +90,14 @@ def kkt4x4(nlp):
     return K, (gL_x, gL_s, gL_y, gL_z), (ox, os_, oy, oz)
 
 
-def solve4x4(prob, b=0):
+def solve4x4(prob, b=0, method="lu"):
     nlp = assemble_nlp(prob, b)
     K, gL, off = kkt4x4(nlp)
-    sol = np.linalg.solve(K, -np.concatenate(gL))
+    if method == "ldl":
+        from .dense import ldl_solve
+        sol = ldl_solve(K, -np.concatenate(gL))
+    else:
+        sol = np.linalg.solve(K, -np.concatenate(gL))
     ox, os_, oy, oz = off
     return dict(dX=sol[ox:os_], ds=sol[os_:oy], dy=sol[oy:oz], dz=sol[oz:], nlp=nlp, K=K, gL=gL)
 

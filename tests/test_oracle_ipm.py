@@ -208,3 +208,21 @@ def test_kkt_point_gives_zero_direction():
     res, _ = ipm_step_oracle(p.select(slice(0, 1)))
     for k in ("dx", "du", "dy", "ds", "dz"):
         assert np.max(np.abs(res[k][0])) < 1e-10, k
+
+
+def test_dense_4x4_ldlt_equals_lu():
+    """North star (a): the full 4×4-block KKT system (Eq.(4×4)) solved by the dense
+    Bunch-Kaufman LDLᵀ equals the LU solution and the structured chain condense → T2 → expand."""
+    for seed, kw in ((4, dict(ng=2, ngN=1, nc=1, ncN=1)), (5, dict(ng=3, ngN=2, nc=0, ncN=0))):
+        p = random_lq_ocp(3, 2, 5, 2, seed=seed, **kw)
+        res, _ = ipm_step_oracle(p)
+        for b in range(2):
+            lu = solve4x4(p, b)
+            ld = solve4x4(p, b, method="ldl")
+            for k in ("dX", "ds", "dy", "dz"):
+                if lu[k].size:
+                    assert rel(ld[k], lu[k]) <= 1e-10, k
+            N = p.N  # the chain's (Δx, Δu) in the dense ordering (x_0, u_0, ..., x_N)
+            dx = np.concatenate([np.concatenate([res["dx"][b][i], res["du"][b][i]]) for i in range(N)]
+                                + [res["dx"][b][N]])
+            assert rel(dx, ld["dX"]) <= 1e-8

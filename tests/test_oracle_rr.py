@@ -322,3 +322,26 @@ def test_threads_identical():
     b = oracle.rr_solve_t2(p, nthreads=5)
     for k in ("x", "u", "y"):
         assert np.array_equal(a[k], b[k])
+
+
+def test_t1_bunch_kaufman_ldlt_equals_lu_and_t2():
+    """North star (a): the dense symmetric-indefinite LDLᵀ (Bunch-Kaufman, 1×1 / 2×2 pivots) of the
+    full KKT matrix gives the LU solution, and the recursion T2 matches it, δ ∈ {0, 1e-8, 1e-4, 1}."""
+    from oracle.dense import ldl_solve
+    saw_2x2 = False
+    for t, d in enumerate((0.0, 1e-8, 1e-4, 1.0)):
+        p = synth.random_stable_lqr(3, 2, 7, 2, seed=40 + t, delta=d)
+        for b in range(2):
+            lu = oracle.rr_solve_dense(p, b)
+            ld = oracle.rr_solve_dense(p, b, method="ldl")
+            assert rel(ld["sol"], lu["sol"]) <= 1e-11
+            t2 = oracle.rr_solve_t2(p)
+            for k in ("x", "u", "y"):
+                assert rel(t2[k][b], ld[k]) <= 1e-8, (d, k)
+            _, D, _ = scipy.linalg.ldl(ld["K"], lower=True)
+            saw_2x2 |= bool(np.any(np.diag(D, -1) != 0.0))
+    assert saw_2x2  # the KKT matrix is indefinite: Bunch-Kaufman takes 2×2 pivots
+    # a plain symmetric indefinite matrix with a zero diagonal (only 2×2 pivots work)
+    K = np.array([[0.0, 2.0, 1.0], [2.0, 0.0, 3.0], [1.0, 3.0, 0.0]])
+    rhs = np.array([1.0, -2.0, 0.5])
+    assert np.max(np.abs(K @ ldl_solve(K, rhs) - rhs)) <= 1e-14
