@@ -32,6 +32,28 @@ ALG_FLOPS_PER_STAGE = 15769    # 13,077 factor + 864 vector backward + 1,828 for
 FP64_DMMA_TFLOPS = 37.1        # measured on this pool by tools/k0_probe.cu (profiles/r01_k0_fp64_probe.txt)
 
 
+def measure_dmma_peak():
+    """FP64 DMMA peak measured in this run (MEASURED_PEAKS.json has no FP64 entry):
+    build and run tools/k0_probe.cu (mma.sync m8n8k4 f64 throughput over every SM), best of its
+    repetitions.  Falls back to the recorded pool value if nvcc or the probe is unavailable."""
+    import re
+    import subprocess
+    import tempfile
+    src = os.path.join(ROOT, "tools", "k0_probe.cu")
+    try:
+        with tempfile.TemporaryDirectory() as d:
+            exe = os.path.join(d, "k0_probe")
+            subprocess.run(["nvcc", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-o", exe, src],
+                           check=True, capture_output=True, timeout=240)
+            out = subprocess.run([exe], check=True, capture_output=True, text=True, timeout=120).stdout
+        vals = [float(v) for v in re.findall(r"DMMA m8n8k4: ([0-9.]+) TFLOP/s", out)]
+        if vals:
+            return max(vals), "K0 probe (tools/k0_probe.cu, mma.sync m8n8k4 f64) measured in this run"
+    except Exception as e:  # noqa: BLE001
+        return FP64_DMMA_TFLOPS, "recorded K0 probe value 37.1 (profiles/r01_k0_fp64_probe.txt); in-run probe failed: %s" % str(e)[:80]
+    return FP64_DMMA_TFLOPS, "recorded K0 probe value 37.1 (profiles/r01_k0_fp64_probe.txt); in-run probe printed no DMMA line"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -323,11 +345,11 @@ def main():
     fp64_tflops = ALG_FLOPS_PER_STAGE * B * HORIZON / (kern_ms / 1e3) / 1e12
     c3 = a.workload == "c3"
     if c3:  # FP64 contraction-bound backward sweep: roofline against the DMMA peak
-        roof = {"bound": "tensor", "achieved": fp64_tflops, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
-                "frac": fp64_tflops / FP64_DMMA_TFLOPS, "traffic": ncu_traffic("rr_cta_c3"),
+        dmma_peak, dmma_src = measure_dmma_peak()
+        roof = {"bound": "tensor", "achieved": fp64_tflops, "peak": dmma_peak, "unit": "TFLOP/s",
+                "frac": fp64_tflops / dmma_peak, "traffic": ncu_traffic("rr_cta_c3"),
                 "kernel": "rr_cta_kernel<64,32>", "kernel_ms": kern_ms, "dtype_peak": "fp64 DMMA",
-                "alg_flops_per_stage": ALG_FLOPS_PER_STAGE,
-                "peak_source": "K0 probe mma.sync m8n8k4 f64 on this pool (profiles/r01_k0_fp64_probe.txt)",
+                "alg_flops_per_stage": ALG_FLOPS_PER_STAGE, "peak_source": dmma_src,
                 "hbm_gbs_alg": achieved}
     else:
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

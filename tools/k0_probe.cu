@@ -1,5 +1,6 @@
 // K0 probe (standalone): FP64 DFMA and DMMA (mma.sync m8n8k4 f64) throughput on this GPU.
-// Used once to pick the kernel design; the library's own peak_fp64 entry point re-measures in-run.
+// Used to pick the kernel design; `bench.py --workload c3` builds and runs it to measure the FP64
+// DMMA roofline peak in the same run.
 #include <cstdio>
 #include <cuda_runtime.h>
 
