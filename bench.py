@@ -178,10 +178,10 @@ def cpu_baseline(target_s, cores=None):
     import synth
     import oracle
     cores = cores or os.cpu_count() or 1
-    cal = synth.random_stable_lqr(NX, NU, HORIZON, 16, SEED, DELTA)
+    cal = synth.random_stable_lqr(NX, NU, HORIZON, 64, SEED, DELTA)
     t0 = time.perf_counter()
     oracle.rr_solve_t2(cal, nthreads=1)
-    per_inst = (time.perf_counter() - t0) / 16
+    per_inst = (time.perf_counter() - t0) / 64  # also the 1-thread rate
     S = max(cores, int(target_s * cores / max(per_inst, 1e-6)))
     S = min(S, 65536)
     prob = synth.random_stable_lqr(NX, NU, HORIZON, S, SEED, DELTA)
@@ -190,9 +190,20 @@ def cpu_baseline(target_s, cores=None):
     dt = time.perf_counter() - t0
     assert int((out["status"] != 0).sum()) == 0
     return {"value": S / dt, "unit": "solves/s", "cores": cores, "kind": "oracle",
-            "stage_updates_per_s": S * HORIZON / dt,
+            "stage_updates_per_s": S * HORIZON / dt, "one_thread_solves_per_s": 1.0 / per_inst,
+            "cpu_model": cpu_model(),
             "sample": "%d of the %d C2 instances (global ids 0..%d), T2 plain-C oracle, %d threads, %.1f s"
                       % (S, BATCH, S - 1, cores, dt)}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(a, ws, rank):
