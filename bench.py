@@ -196,6 +196,26 @@ def cpu_baseline(target_s, cores=None):
                       % (S, BATCH, S - 1, cores, dt)}
 
 
+def oracle_rate(make, solve, target_s, total, unit_desc, calib=8, cap=None):
+    """Time the oracle as it stands on all host cores on a bounded sample of a workload: `make(k)`
+    builds the first k instances (global ids 0..k-1), `solve(batch, threads)` runs the oracle.
+    The sample is sized from a 1-thread calibration run so it takes about `target_s` seconds."""
+    cores = os.cpu_count() or 1
+    cal = make(calib)
+    t0 = time.perf_counter()
+    solve(cal, 1)
+    per_inst = (time.perf_counter() - t0) / calib
+    S = max(cores, int(target_s * cores / max(per_inst, 1e-6)))
+    S = min(S, cap or total, total)
+    prob = make(S)
+    t0 = time.perf_counter()
+    solve(prob, cores)
+    dt = time.perf_counter() - t0
+    return {"value": S / dt, "unit": "solves/s", "cores": cores, "kind": "oracle",
+            "one_thread_solves_per_s": 1.0 / per_inst, "cpu_model": cpu_model(),
+            "sample": "%d of the %d %s (global ids 0..%d), %d threads, %.1f s" % (S, total, unit_desc, S - 1, cores, dt)}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -382,8 +402,15 @@ def main():
         "e2e": e2e,
         "gpu_launches": a.steps,
     }
-    if not a.no_cpu_baseline and not c3:
-        line["cpu_baseline"] = cpu_baseline(a.cpu_seconds)
+    if not a.no_cpu_baseline and ws == 1:
+        if c3:
+            import oracle
+            line["cpu_baseline"] = oracle_rate(
+                lambda k: synth.random_stable_lqr(NX, NU, HORIZON, k, SEED, DELTA),
+                lambda p, t: oracle.rr_solve_t2(p, nthreads=t), a.cpu_seconds, BATCH,
+                "C3 instances, T2 plain-C oracle", calib=2, cap=512)
+        else:
+            line["cpu_baseline"] = cpu_baseline(a.cpu_seconds)
     print(json.dumps(line), flush=True)
     barrier(ws)
 
@@ -442,7 +469,18 @@ def run_c4(a, ws, rank, local):
             "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": ncu_traffic("ipm_c4"),
                          "alg_bytes_per_stage": 1900, "peak_source": src},
+            "cpu_baseline": c4_cpu_baseline(a, B, Nh) if (ws == 1 and not a.no_cpu_baseline) else None,
             "gpu_launches": a.steps}), flush=True)
+
+
+def c4_cpu_baseline(a, B, Nh):
+    from synth.ipm_workloads import cartpole_c4
+    from oracle.ipm import ipm_step_oracle
+    r = oracle_rate(lambda k: cartpole_c4(k, seed=2511, N=Nh),
+                    lambda p, t: ipm_step_oracle(p, nthreads=t), a.cpu_seconds, B,
+                    "C4 cart-pole IPM iterates, C oracle ipm_step", calib=64)
+    r["unit"] = "instance-steps/s"
+    return r
 
 
 def run_c5(a, ws, rank, local):
@@ -532,7 +570,15 @@ def run_c5(a, ws, rank, local):
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": None, "kernel": "rr_fused_mma_kernel<12,4>", "kernel_ms_per_chunk": kern_ms_chunk,
                      "alg_bytes_per_stage": ALG_BYTES_PER_STAGE, "peak_source": src},
-        "clocks": clk, "e2e": None, "gpu_launches": a.steps * len(chunk_ms)}), flush=True)
+        "clocks": clk, "e2e": None, "gpu_launches": a.steps * len(chunk_ms),
+        "cpu_baseline": c5_cpu_baseline(a, total) if (ws == 1 and not a.no_cpu_baseline) else None}), flush=True)
+
+
+def c5_cpu_baseline(a, total):
+    import synth
+    import oracle
+    return oracle_rate(lambda k: synth.quadrotor_c5(k), lambda p, t: oracle.rr_solve_t2(p, nthreads=t),
+                       a.cpu_seconds, total, "C5 quadrotor instances, T2 plain-C oracle", calib=8, cap=8192)
 
 
 def run_split(a, ws, rank, local):
@@ -616,7 +662,8 @@ def run_split(a, ws, rank, local):
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": None, "kernel": "rr_factor_kernel<12,4> + rr_solve_kernel<12,4>",
                      "peak_source": src, "kernels": kern},
-        "clocks": clk, "e2e": None, "gpu_launches": 2 * a.steps}), flush=True)
+        "clocks": clk, "e2e": None, "gpu_launches": 2 * a.steps,
+        "cpu_baseline": cpu_baseline(a.cpu_seconds) if (ws == 1 and not a.no_cpu_baseline) else None}), flush=True)
 
 
 def run_c4solve(a, ws, rank, local):
