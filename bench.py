@@ -837,13 +837,27 @@ def run_pit(a, ws, rank, local):
         rows.append({"N": N, "sequential_ms": t_seq, "pit_ms": t_pit, "pit_graph_ms": t_graph,
                      "speedup": t_seq / t_pit, "speedup_graph": t_seq / t_graph, "max_rel_diff": err})
     best = rows[-1]
+    # the oracle (T2 plain C, one thread: a single instance) on the same N = 4096 instance
+    import oracle
+    pc = p.to("cpu")
+    t_or = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        oracle.rr_solve_t2(pc, nthreads=1)
+        t_or.append(time.perf_counter() - t0)
+    levels = max(1, (rows[-1]["N"]).bit_length())  # strides 1, 2, 4, ... <= N
+    per_call = (1 + 1 + 1 + 2 * levels + 1 + levels + 1) + (1 + 1 + 1 + 2 * levels + 1 + levels + 1 + 3) + 1
     print(json.dumps({
         "metric": "regularized-LQR single-instance latency, parallel-in-time vs sequential (n=12 m=4, N=4096)",
         "value": min(best["pit_ms"], best["pit_graph_ms"]) * 1e3, "unit": "us", "n_gpus": 1, "steps": K, "warmup": 3,
         "ms_per_step": min(best["pit_ms"], best["pit_graph_ms"]), "higher_is_better": False, "scaling": "none", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": "1 random stable regularized LQR (C2 recipe) n_x=12 n_u=4 delta=1e-4, N in {64, 512, 4096}"},
-        "horizons": rows, "roofline": None, "gpu_launches": None}), flush=True)
+        "horizons": rows, "roofline": None, "gpu_launches": per_call * K,
+        "cpu_baseline": {"value": statistics.median(t_or) * 1e6, "unit": "us", "cores": 1, "kind": "oracle",
+                         "cpu_model": cpu_model(),
+                         "sample": "the same N = %d instance, T2 plain-C oracle, 1 thread, median of 3" % rows[-1]["N"]}}),
+          flush=True)
 
 
 def ctypes_dims(rr, p):
