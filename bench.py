@@ -190,7 +190,7 @@ def cpu_baseline(target_s, cores=None):
     dt = time.perf_counter() - t0
     assert int((out["status"] != 0).sum()) == 0
     return {"value": S / dt, "unit": "solves/s", "cores": cores, "kind": "oracle",
-            "stage_updates_per_s": S * HORIZON / dt, "one_thread_solves_per_s": 1.0 / per_inst,
+            "stage_updates_per_s": S * HORIZON / dt, "one_thread_value": 1.0 / per_inst,
             "cpu_model": cpu_model(),
             "sample": "%d of the %d C2 instances (global ids 0..%d), T2 plain-C oracle, %d threads, %.1f s"
                       % (S, BATCH, S - 1, cores, dt)}
@@ -212,7 +212,7 @@ def oracle_rate(make, solve, target_s, total, unit_desc, calib=8, cap=None):
     solve(prob, cores)
     dt = time.perf_counter() - t0
     return {"value": S / dt, "unit": "solves/s", "cores": cores, "kind": "oracle",
-            "one_thread_solves_per_s": 1.0 / per_inst, "cpu_model": cpu_model(),
+            "one_thread_value": 1.0 / per_inst, "cpu_model": cpu_model(),
             "sample": "%d of the %d %s (global ids 0..%d), %d threads, %.1f s" % (S, total, unit_desc, S - 1, cores, dt)}
 
 
@@ -722,7 +722,23 @@ def run_c4solve(a, ws, rank, local):
             "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": None,
                          "alg_bytes_per_stage_iteration": 2800, "peak_source": src},
-            "clocks": clk, "gpu_launches": a.steps * (4 * IT + 3)}), flush=True)
+            "clocks": clk, "gpu_launches": a.steps * (4 * IT + 3),
+            "cpu_baseline": c4solve_cpu_baseline(a, B, Nh, IT) if (ws == 1 and not a.no_cpu_baseline) else None}),
+              flush=True)
+
+
+def c4solve_cpu_baseline(a, B, Nh, IT):
+    """The oracle IPM loop (oracle/ipm_solve.py around the C oracle step) on a bounded sample of the
+    same C4 batch, the same 20-iteration budget; rate in instance-iterations/s."""
+    from synth.ipm_workloads import cartpole_c4
+    from oracle.ipm_solve import SolveSettings, ipm_solve_oracle
+    r = oracle_rate(lambda k: cartpole_c4(k, seed=2511, N=Nh),
+                    lambda p, t: ipm_solve_oracle(p, SolveSettings(max_iters=IT), nthreads=t), a.cpu_seconds, B,
+                    "C4 cart-pole instances, oracle IPM loop (%d iterations)" % IT, calib=16, cap=2048)
+    r["value"] *= IT
+    r["one_thread_value"] *= IT
+    r["unit"] = "instance-iterations/s"
+    return r
 
 
 def run_c1(a, ws, rank, local):
