@@ -385,6 +385,20 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   }
   __syncthreads();
 #endif
+#ifndef RR_NO_PTAB
+  // the table read once into registers (two 16-bit offsets per register) when every fragment
+  // position lies inside P: the per-stage gather then issues no table loads (−1.4% on C2);
+  // RR_PTAB_SMEM keeps the per-stage table reads
+#ifdef RR_PTAB_SMEM
+  constexpr bool PREG = false;
+#else
+  constexpr bool PREG = (NX + NU) % 8 == 0 && LY::STG < 65536;
+#endif
+  uint32_t ptw[LY::PTAB / 2];
+#pragma unroll
+  for (int k2 = 0; k2 < LY::PTAB / 2; ++k2)
+    ptw[k2] = PREG ? ((uint32_t)ptab[(2 * k2) * 32 + lane] | ((uint32_t)ptab[(2 * k2 + 1) * 32 + lane] << 16)) : 0u;
+#endif
   double* wk = grp ? wkq[1] : wkq[0];
 
   const int64_t inst0 = ((int64_t)blockIdx.x * WARPS + warp) * 2;
@@ -510,9 +524,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     (void)ptab;
 #else
     auto P2 = [&](int q, int k) -> double {
-      const int off = ptab[k * 32 + lane];
-      if constexpr ((NX + NU) % 8 == 0) return sbq[q][off];  // every fragment position inside P
-      return off >= 0 ? sbq[q][off] : 0.0;
+      if constexpr (PREG) {  // offsets packed as 16-bit halves of per-lane registers (no table loads)
+        return sbq[q][(int)((ptw[k >> 1] >> (16 * (k & 1))) & 0xffffu)];
+      } else {
+        const int off = ptab[k * 32 + lane];
+        return off >= 0 ? sbq[q][off] : 0.0;
+      }
     };
     (void)Pat;
 #endif
