@@ -258,11 +258,16 @@ struct StageMMA {
       double gk[NX];
       ST::bcast(wk + WK::gb, gk);
       double b0 = qjf(), b1 = 0.0;
+      // column j of F read as 128-bit pairs; lanes with j & 4 walk the pairs rotated by one, so the
+      // 8 lanes of a quarter-warp (column stride NX = 12 doubles) hit 8 different 16-byte bank groups
+      // (unrotated: lanes j and j + 4 collide, 2 wavefronts per quarter)
+      const bool rot = (j & 4) != 0;
 #pragma unroll
       for (int k = 0; k < NX; k += 2) {
-        const double2 f2 = *reinterpret_cast<const double2*>(F + jc * NX + k);
-        b0 = fma(f2.x, gk[k], b0);
-        b1 = fma(f2.y, gk[k + 1], b1);
+        const int kr = (k + 2) % NX;
+        const double2 f2 = *reinterpret_cast<const double2*>(F + jc * NX + (rot ? kr : k));
+        b0 = fma(f2.x, rot ? gk[kr] : gk[k], b0);
+        b1 = fma(f2.y, rot ? gk[kr + 1] : gk[k + 1], b1);
       }
       bj = b0 + b1;  // lane j owns entry j of b (distributed, not replicated)
     }
