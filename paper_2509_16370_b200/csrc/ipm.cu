@@ -66,7 +66,10 @@ struct LogAcc {
 // per lane before the dependent stores (x and d may not alias, but the compiler cannot know that).
 template <int LG>
 __device__ __forceinline__ void axpy_lanes(double* x, const double* d, double alpha, int64_t cnt, int j) {
-  constexpr int U = 4;
+#ifndef RR_AXPY_U
+#define RR_AXPY_U 8
+#endif
+  constexpr int U = RR_AXPY_U;
   int64_t e = j;
   for (; e + (U - 1) * LG < cnt; e += U * LG) {
     double xv[U], dv[U];
