@@ -72,6 +72,7 @@ def parse():
                          "(20 IPM iterations) on the C4 cart-pole batch; c1 = single double-integrator instance latency; "
                          "pit = single-instance latency, parallel-in-time vs sequential, long horizons")
     ap.add_argument("--c5-total", type=int, default=1048576, help=argparse.SUPPRESS)
+    ap.add_argument("--ref-seconds", type=float, default=150.0, help=argparse.SUPPRESS)  # reference-arm budget
     return ap.parse_args()
 
 
@@ -238,7 +239,7 @@ def run_reference(a, ws, rank):
     oracle.rr_solve_t2(cal, nthreads=1)
     per_inst = (time.perf_counter() - t0) / 16
     # each step: a bounded sample sized so warmup+steps finish in ~2-3 minutes
-    budget = 150.0 / max(1, a.steps + a.warmup)
+    budget = a.ref_seconds / max(1, a.steps + a.warmup)
     S = max(cores, min(BATCH, int(budget * cores / max(per_inst, 1e-6))))
     prob = synth.random_stable_lqr(NX, NU, HORIZON, S, SEED, DELTA)
     for _ in range(a.warmup):
