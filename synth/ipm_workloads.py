@@ -319,3 +319,54 @@ def quadrotor_ipm(batch, seed=2513, N=50, mu=0.1, eta=1e4, first=0, device="cpu"
     data = {k2: v.contiguous() for k2, v in data.items()}
     it = {k2: v.contiguous() for k2, v in it.items()}
     return IPMBatch(n, m, N, 4, 0, 0, 0, MODEL_QUADROTOR, data, it)
+
+
+# ----------------------------------------------------------------------------- SPEC's scalar examples
+def _scalar_shell(batch, m, ng, nc, mu, eta, device):
+    """n = 1, N = 1 shell whose state is pinned at 0 (x̄_0 = x̄_1 = s_0 = 0, A = 1, B = 0, Q = Q_N = 1):
+    the decision variable of a static NLP becomes the stage-0 control u_0 (P:27-37 with N = 1)."""
+    dev = torch.device(device)
+    n, k = 1, 1 + m
+    z0 = lambda *s: _zeros(batch, *s, device=dev)
+    data = dict(s0=z0(1), fval=z0(), gradf=z0(1, k), gradfN=z0(1),
+                Q=torch.ones(batch, 1, 1, dtype=torch.float64, device=dev), M=z0(1, m),
+                R=z0(1, sym_size(m)), QN=torch.ones(batch, 1, dtype=torch.float64, device=dev),
+                A=torch.ones(batch, 1, 1, dtype=torch.float64, device=dev), B=z0(1, m), dres=z0(1, 1),
+                ce=z0(1, nc), Ce=z0(1, nc * k), ceN=z0(0), CeN=z0(0),
+                gv=z0(1, ng), Gj=z0(1, ng * k), gvN=z0(0), GjN=z0(0),
+                model_params=_zeros(N_MODEL_PARAMS, device=dev))
+    it = dict(x=z0(2, 1), u=z0(1, m), s=z0(1, ng), z=z0(1, ng), sN=z0(0), zN=z0(0), y=z0(2, 1),
+              lam=z0(1, nc), lamN=z0(0),
+              mu=torch.full((batch,), float(mu), dtype=torch.float64, device=dev),
+              eta=torch.full((batch,), float(eta), dtype=torch.float64, device=dev))
+    return data, it
+
+
+def spec_scalar_ocp(batch=1, xbar=2.0, s=1.0, z=1.0, mu=1.0, eta=10.0, device="cpu") -> IPMBatch:
+    """SPEC's scalar NLP min x² s.t. g(x) = 1 − x ≤ 0 as an OCP with
+    N = 1, n = m = 1 (model LQ): x = u_0, f = u_0² (R = 2, ∇f_u = 2ū, f̄ = ū²), g = 1 − u_0
+    (G = [0, −1] over (x_0, u_0)), slack s, multiplier z.  The defaults are S:234's iterate
+    (x = 2, s = 1, z = 1, μ = 1, η = 10)."""
+    data, it = _scalar_shell(batch, 1, 1, 0, mu, eta, device)
+    data["R"].fill_(2.0)
+    data["fval"].fill_(xbar * xbar)
+    data["gradf"][..., 1] = 2.0 * xbar
+    data["gv"].fill_(1.0 - xbar)
+    data["Gj"][..., 1] = -1.0
+    it["u"].fill_(xbar)
+    it["s"].fill_(s)
+    it["z"].fill_(z)
+    return IPMBatch(1, 1, 1, 1, 0, 0, 0, MODEL_LQ, {k: v.contiguous() for k, v in data.items()},
+                    {k: v.contiguous() for k, v in it.items()})
+
+
+def spec_equality_qp_ocp(batch=1, m=3, mu=0.1, eta=1e4, device="cpu") -> IPMBatch:
+    """min ½‖x‖² s.t. x₁ = 1, start x = 0, as an OCP with N = 1, n = 1: x = u_0 ∈ R^m,
+    f = ½‖u_0‖² (R = I), one stage equality c_e = u_0[0] − 1 (C_e = [0, 1, 0, …]) with
+    multiplier λ; no inequalities."""
+    data, it = _scalar_shell(batch, m, 0, 1, mu, eta, device)
+    data["R"][...] = pack_lower(torch.eye(m, dtype=torch.float64, device=data["R"].device))
+    data["ce"].fill_(-1.0)
+    data["Ce"][..., 1] = 1.0
+    return IPMBatch(1, m, 1, 0, 0, 1, 0, MODEL_LQ, {k: v.contiguous() for k, v in data.items()},
+                    {k: v.contiguous() for k, v in it.items()})

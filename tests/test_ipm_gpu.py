@@ -149,3 +149,18 @@ def test_quadrotor_model_rules():
     bad.model = 2
     with pytest.raises(rr.RRError):
         rr.ipm_step(bad.to("cuda"))
+
+
+def test_spec_scalar_step_exact_on_gpu():
+    """S:234 through the CUDA ipm_step (padded 4×1 kernel): (Δu, Δs, Δz) = (−33/32, −15/16, 15/16),
+    D = −99/32, α = 1, 𝒜(0) = 4, 𝒜(1) = 3.848760597239781, for a batch of identical instances."""
+    from synth.ipm_workloads import spec_scalar_ocp
+    p = spec_scalar_ocp(batch=37)
+    g, git, o, oit = run(p)
+    assert_ipm_parity(g, git, o, oit)
+    assert np.all(g["status"] == 0) and np.all(g["n_backtracks"] == 0)
+    for k, v in (("du", -33 / 32), ("ds", -15 / 16), ("dz", 15 / 16)):
+        assert np.all(np.abs(g[k] - v) <= 2e-16), k
+    assert np.all(np.abs(g["D"] + 99 / 32) <= 1e-15) and np.all(g["alpha_p"] == 1.0)
+    assert np.all(np.abs(g["merit0"] - 4.0) <= 1e-15)
+    assert np.all(np.abs(g["merit_acc"] - 3.848760597239781) <= 2e-15)

@@ -68,16 +68,75 @@ def test_cartpole_first_iterations(iters):
 
 
 def test_converged_instances_are_frozen_and_empty_batch():
+    """A converged instance is frozen: re-solving a converged batch (μ ≤ 10 μ_min already, KKT ≤ tol)
+    takes zero steps and leaves every iterate array bitwise unchanged; an empty batch is a no-op.
+    (Instances converging at different iterations inside one batch: the next test.)"""
     import paper_2509_16370_b200 as m
     b = double_integrator_ocp(batch=2).to("cuda")
     rep = m.ipm_solve(b, max_iters=200)
-    x1 = b.it["x"].clone()
-    n1 = rep["iters"].clone()
-    rep2 = m.ipm_solve(b, max_iters=200)    # restart from the solution: converges at once (μ restarts)
     torch.cuda.synchronize()
-    assert torch.all(rep["status"] == 0)
+    assert torch.all(rep["status"] == 0) and torch.all(rep["iters"] > 0)
+    snap = {k: v.clone() for k, v in b.it.items()}
+    rep2 = m.ipm_solve(b, max_iters=200)
+    torch.cuda.synchronize()
+    assert torch.all(rep2["status"] == 0) and torch.all(rep2["iters"] == 0)
+    for k, v in snap.items():
+        assert torch.equal(b.it[k], v), k
     e = double_integrator_ocp(batch=0).to("cuda")
     m.ipm_solve(e)
+
+
+def test_mixed_batch_each_instance_as_if_alone():
+    """Per-instance convergence masks: a batch interleaving two scalar problems that converge after
+    different numbers of iterations gives every instance the status, iteration count and iterate
+    bits of its own single-instance solve (the early finisher is frozen while the other keeps
+    stepping)."""
+    import paper_2509_16370_b200 as m
+    from synth.ipm_workloads import spec_equality_qp_ocp, spec_scalar_ocp
+    mk = [lambda bb: spec_scalar_ocp(batch=bb, xbar=3.0, s=2.0, z=0.05, mu=0.1, eta=1e4),
+          lambda bb: spec_scalar_ocp(batch=bb, xbar=5.0, s=4.0, z=0.025, mu=0.1, eta=1e2)]
+    singles = []
+    for f in mk:
+        b = f(1).to("cuda")
+        r = m.ipm_solve(b)
+        singles.append((b, r))
+    torch.cuda.synchronize()
+    # interleave the two problems in one batch of 6
+    parts = [mk[i % 2](1) for i in range(6)]
+    from synth.ipm_workloads import IPMBatch
+    cat = IPMBatch(1, 1, 1, 1, 0, 0, 0, 0,
+                   {k: (parts[0].data[k] if k == "model_params" else torch.cat([p.data[k] for p in parts]))
+                    for k in parts[0].data},
+                   {k: torch.cat([p.it[k] for p in parts]) for k in parts[0].it}).to("cuda")
+    rc = m.ipm_solve(cat)
+    torch.cuda.synchronize()
+    assert int(singles[0][1]["iters"][0]) != int(singles[1][1]["iters"][0])
+    for i in range(6):
+        b, r = singles[i % 2]
+        assert int(rc["iters"][i]) == int(r["iters"][0]) and int(rc["status"][i]) == int(r["status"][0])
+        for k in ("u", "s", "z", "x", "y"):
+            assert torch.equal(cat.it[k][i], b.it[k][0]), (i, k)
+
+
+@pytest.mark.parametrize("case", ["ineq_eta1e4", "ineq_eta1e2", "eq_m1", "eq_m3"])
+def test_spec_end_to_end_examples(case):
+    """min x² s.t. x ≥ 1 from x = 3 → (x, z) = (1, 2); min ½‖x‖² s.t. x₁ = 1 from 0 →
+    x = e₁, y = −1; within 1e-6 on the GPU, with the oracle loop's status and iteration count."""
+    from synth.ipm_workloads import spec_equality_qp_ocp, spec_scalar_ocp
+    b = {"ineq_eta1e4": lambda: spec_scalar_ocp(batch=4, xbar=3.0, s=2.0, z=0.05, mu=0.1, eta=1e4),
+         "ineq_eta1e2": lambda: spec_scalar_ocp(batch=4, xbar=3.0, s=2.0, z=0.05, mu=0.1, eta=1e2),
+         "eq_m1": lambda: spec_equality_qp_ocp(batch=4, m=1),
+         "eq_m3": lambda: spec_equality_qp_ocp(batch=4, m=3)}[case]()
+    it_g, rep_g, it_o, rep_o = run_both(b)
+    check(it_g, rep_g, it_o, rep_o, keys=("x", "u", "s", "z", "y", "lam"))
+    assert np.all(rep_g["status"] == 0)
+    if case.startswith("ineq"):
+        assert np.all(np.abs(it_g["u"][:, 0, 0] - 1.0) <= 1e-6) and np.all(np.abs(it_g["z"][:, 0, 0] - 2.0) <= 1e-6)
+    else:
+        m = b.nu
+        e1 = np.zeros(m)
+        e1[0] = 1.0
+        assert np.all(np.abs(it_g["u"][:, 0] - e1) <= 1e-6) and np.all(np.abs(it_g["lam"][:, 0, 0] + 1.0) <= 1e-6)
 
 
 @pytest.mark.parametrize("iters", [1, 4])
