@@ -455,6 +455,14 @@ def run_c4(a, ws, rank, local):
     barrier(ws)
     clk = clocks.stop()
     ms = max_over_ranks(sum(s_.elapsed_time(e_) for s_, e_ in ev) / a.steps, ws)
+    # per-instance IPM summaries (status, α_p, D, 𝒜(0)) gathered to rank 0, timed apart
+    from paper_2509_16370_b200.shard import gather_summaries
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    gathered = gather_summaries({k: call0.res[k] for k in ("status", "alpha_p", "D", "merit0")}, rank, ws, B * ws)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    gather_ms = max_over_ranks(g0.elapsed_time(g1), ws)
     st = call0.res["status"]
     if rank == 0:
         alg = 1900 * B * Nh  # ~1.9 KB per (instance, stage)
@@ -466,7 +474,10 @@ def run_c4(a, ws, rank, local):
             "config": {"workload": "C4: %d cart-pole IPM iterates per GPU, N=%d, n_g=4" % (B, Nh),
                        "l2": "stage data %.1f GB/GPU > 126 MB L2 (no flush needed)" % (alg / 1e9)},
             "clocks": clk,
-            "status_nonzero": int((st != 0).sum()),
+            "status_nonzero": int((gathered["status"] != 0).sum()),
+            "summary": {"fields": ["D", "alpha_p", "merit0", "status"], "gathered_to": "rank 0 (dist.gather)",
+                        "gather_ms": gather_ms, "D_max": float(gathered["D"].max()),
+                        "alpha_p_min": float(gathered["alpha_p"].min())},
             "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": ncu_traffic("ipm_c4"),
                          "alg_bytes_per_stage": 1900, "peak_source": src},
@@ -491,7 +502,8 @@ def run_c5(a, ws, rank, local):
     one GPU holds).  Every chunk is generated on the device (untimed), then solved W times untimed
     and K times timed with CUDA events; the step time is the sum over the rank's chunks of the
     mean chunk time (each chunk's inputs exceed L2, so re-solving a resident chunk is not cached),
-    plus the timed NCCL gather of the per-instance summaries (status, u_0) to rank 0.  Reported
+    plus the timed NCCL gather (dist.gather to rank 0) of the per-instance summaries (status, u_0 and
+    the KKT residual norms from rr_residual, timed separately as `summary.residual_ms`).  Reported
     time = max over ranks."""
     import torch
     import synth
@@ -508,8 +520,9 @@ def run_c5(a, ws, rank, local):
     call = rr.Marshalled(prob, sol)
     stream = torch.cuda.current_stream(dev)
     summ = {"status": torch.empty(mine, dtype=torch.int32, device=dev),
-            "u0": torch.empty(mine, m, dtype=torch.float64, device=dev)}
-    chunk_ms, gen_s = [], 0.0
+            "u0": torch.empty(mine, m, dtype=torch.float64, device=dev),
+            "kkt": torch.empty(mine, 2, dtype=torch.float64, device=dev)}
+    chunk_ms, res_ms, gen_s = [], [], 0.0
     clocks = ClockSampler(local)
     clocks.start()
     for s in range(b0, b1, CH):
@@ -538,6 +551,15 @@ def run_c5(a, ws, rank, local):
         chunk_ms.append(statistics.mean(x.elapsed_time(y) for x, y in ev))
         summ["status"][s - b0:e - b0].copy_(sol["status"])
         summ["u0"][s - b0:e - b0].copy_(sol["u"][:, 0, :])
+        # KKT residual norms of the chunk's solution (rr_residual, the paper's residual callback
+        # P:666) for the summary; timed on its own, not part of the solve time
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        _, norms = rr.rr_residual(prob, sol, stream=stream)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        res_ms.append(r0.elapsed_time(r1))
+        summ["kkt"][s - b0:e - b0].copy_(norms)
     barrier(ws)
     torch.cuda.synchronize()
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -548,9 +570,11 @@ def run_c5(a, ws, rank, local):
     clk = clocks.stop()
     solve_ms = max_over_ranks(sum(chunk_ms), ws)
     gather_ms = max_over_ranks(g0.elapsed_time(g1), ws)
+    res_ms_max = max_over_ranks(sum(res_ms), ws)
     if rank != 0:
         return
     nbad = int((gathered["status"] != 0).sum())
+    kkt_max = float(gathered["kkt"].max()) if total else 0.0
     ms = solve_ms + gather_ms
     kern_ms_chunk = statistics.mean(chunk_ms)
     alg = ALG_BYTES_PER_STAGE * total * Nh / ws
@@ -568,6 +592,8 @@ def run_c5(a, ws, rank, local):
                              "+ summary gather; max over ranks; generation untimed (%.1f s)" % gen_s},
         "stage_updates_per_s": total * Nh / (ms / 1e3), "solve_ms": solve_ms, "gather_ms": gather_ms,
         "chunks_per_rank": len(chunk_ms), "status_nonzero": nbad,
+        "summary": {"fields": sorted(summ), "gathered_to": "rank 0 (dist.gather)", "gather_ms": gather_ms,
+                    "kkt_residual_max": kkt_max, "residual_ms": res_ms_max},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "traffic": None, "kernel": "rr_fused_mma_kernel<12,4>", "kernel_ms_per_chunk": kern_ms_chunk,
                      "alg_bytes_per_stage": ALG_BYTES_PER_STAGE, "peak_source": src},
@@ -648,9 +674,13 @@ def run_split(a, ws, rank, local):
     kern = {}
     for k, b in per_stage.items():
         ach = b * B * HORIZON / (kms[k] / 1e3) / 1e9
-        kern[k] = {"ms": kms[k], "alg_bytes_per_stage": b, "achieved_gbs": ach, "frac": ach / peak,
+        kern[k] = {"ms": kms[k], "record_model_bytes_per_stage": b, "achieved_gbs": ach, "frac": ach / peak,
                    "traffic": ncu_traffic("rr_split_%s_c2" % k)}
-    tot_b = (per_stage["factor"] + per_stage["solve"]) * B * HORIZON
+    # headline: SURVEY §8(d)'s split-API algorithmic bytes (9,680 B/stage: rr_factor writes V, K, L_G;
+    # rr_solve's two sweeps re-read them with A, B, q, r, c), not this build's larger record model
+    # (per kernel above: the record also carries S⁻¹ and G⁻¹, 11,632 B/stage for the pair)
+    SPLIT_ALG = 9680
+    tot_b = SPLIT_ALG * B * HORIZON
     ach = tot_b / (ms / 1e3) / 1e9
     print(json.dumps({
         "metric": METRIC + " (split API: rr_factor + rr_solve)", "value": B * ws / (ms / 1e3), "unit": "solves/s",
@@ -661,8 +691,8 @@ def run_split(a, ws, rank, local):
                    "l2": "inputs %.1f GB/GPU > 126 MB L2 (no flush needed)" % (prob.nbytes() / 1e9)},
         "stage_updates_per_s": B * ws * HORIZON / (ms / 1e3),
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "traffic": None, "kernel": "rr_factor_kernel<12,4> + rr_solve_kernel<12,4>",
-                     "peak_source": src, "kernels": kern},
+                     "traffic": None, "kernel": "rr_fused_mma_kernel<12,4,FAC> + rr_solve_kernel<12,4>",
+                     "alg_bytes_per_stage": SPLIT_ALG, "peak_source": src, "kernels": kern},
         "clocks": clk, "e2e": None, "gpu_launches": 2 * a.steps,
         "cpu_baseline": cpu_baseline(a.cpu_seconds) if (ws == 1 and not a.no_cpu_baseline) else None}), flush=True)
 

@@ -14,7 +14,12 @@
  *  - Layout: one array per operand, instance-major [batch][stage][element] (terminal data
  *    [batch][element]); matrices COLUMN-MAJOR; symmetric matrices (Q, R, Q_N, V) PACKED LOWER
  *    in LAPACK 'L' packed order: element (r, c), r >= c, at c*(2n-c-1)/2 + r.
- *    Every per-instance block must be 8-byte aligned (16-byte alignment enables vector copies).
+ *    Alignment: every array must be 8-byte aligned (FP64).  rr_factor_solve / rr_factor stream
+    stage operands with TMA bulk copies (cp.async.bulk), which need 16-byte-aligned addresses:
+    when all of A, B, Q, M, R, q, r, c are 16-byte aligned (e.g. fresh cudaMalloc / torch
+    allocations) the TMA kernels run; otherwise n, m <= 16 shapes run the LDGSTS kernels (8-byte
+    copies where needed; same results) and n or m > 16 returns RR_E_INVALID.  Workspaces and
+    factor buffers must be 16-byte aligned (RR_E_INVALID otherwise).
  *  - Call-level errors (return value): RR_OK, RR_E_INVALID (bad dims, null required pointer,
  *    workspace too small), RR_E_UNSUPPORTED (shape outside the compiled kernels), RR_E_CUDA
  *    (launch error).  rr_last_error() returns a thread-local message.
@@ -116,8 +121,8 @@ int64_t rr_workspace_bytes(const rr_dims* dims);
  *     x_{i+1} = (I+δV_{i+1})⁻¹(A_i x_i + B_i u_i + c_{i+1} - δv_{i+1});
  *   dual recovery: y_i = V_i x_i + v_i.
  * prob, sol, status: required (status may be NULL when batch == 0: the call is then a no-op).  fac: optional (NULL or any NULL member = not written).
- * workspace: device buffer of >= rr_workspace_bytes(dims) bytes, 256-byte aligned; contents
- * are scratch.  Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
+ * workspace: device buffer of >= rr_workspace_bytes(dims) bytes, 16-byte aligned (256 recommended);
+ * contents are scratch.  Operand alignment selects the kernel (CONVENTIONS above).  Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
  */
 rr_err rr_factor_solve(const rr_dims* dims, const rr_problem* prob, const rr_factor_buf* fac,
                        const rr_solution* sol, void* workspace, int64_t workspace_bytes,

@@ -20,6 +20,17 @@ rr_err set_err(rr_err code, const char* fmt, const char* what = "") {
 
 constexpr int SHARED_FLAGS = RR_FLAG_SHARED_DYN | RR_FLAG_SHARED_COST;
 
+// TMA bulk copies (cp.async.bulk) need 16-byte-aligned global addresses; the per-stage block
+// offsets of every compiled TMA shape are multiples of 16 bytes, so the base pointers decide.
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool stage_ops_aligned16(const rr_problem* p) {
+  const double* ops[] = {p->A, p->B, p->Q, p->M, p->R, p->q, p->r, p->c};
+  for (const double* o : ops)
+    if (!aligned16(o)) return false;
+  return true;
+}
+bool large_shape(const rr_dims* d) { return d->nx > 16 || d->nu > 16; }  // CTA-per-instance kernels
+
 bool dims_ok(const rr_dims* d, int allowed_flags = SHARED_FLAGS) {
   return d != nullptr && d->nx >= 1 && d->nu >= 1 && d->N >= 0 && d->batch >= 0 && (d->flags & ~allowed_flags) == 0;
 }
@@ -61,6 +72,12 @@ rr_err rr_factor_solve(const rr_dims* dims, const rr_problem* prob, const rr_fac
   if (dims->N > 0 && (workspace == nullptr || workspace_bytes < need))
     return set_err(RR_E_INVALID, "rr_factor_solve: workspace missing or smaller than %s",
                    "rr_workspace_bytes()");
+  if (!aligned16(workspace))
+    return set_err(RR_E_INVALID, "rr_factor_solve: workspace not %s", "16-byte aligned");
+  const bool tma16 = stage_ops_aligned16(prob);
+  if (!tma16 && large_shape(dims) && dims->N > 0)
+    return set_err(RR_E_INVALID, "rr_factor_solve: n or m > 16 needs %s",
+                   "16-byte-aligned stage operands (TMA bulk copies of A, B)");
   rrk::FusedArgs a;
   a.nx = dims->nx;
   a.nu = dims->nu;
@@ -73,6 +90,7 @@ rr_err rr_factor_solve(const rr_dims* dims, const rr_problem* prob, const rr_fac
   a.ws = static_cast<double*>(workspace);
   a.status = status;
   a.shared = dims->flags & SHARED_FLAGS;
+  a.tma16 = tma16;
   bool supported = false;
   cudaError_t e = rrk::fused_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_factor_solve: unsupported shape%s");
@@ -162,6 +180,7 @@ rr_err rr_factor(const rr_dims* dims, const rr_problem* prob, void* factor, int6
   a.fr = static_cast<double*>(factor);
   a.status = status;
   a.shared = dims->flags & SHARED_FLAGS;
+  a.tma16 = stage_ops_aligned16(prob);
   bool supported = false;
   cudaError_t e = rrk::factor_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_factor: unsupported shape%s");
@@ -312,6 +331,36 @@ rr_err ipm_direction(const ipm_dims* dims, const ipm_stage_data* data, const ipm
   return ipm_step_impl(dims, data, it, params, res, workspace, workspace_bytes, status, stream, 1);
 }
 
+// Arrays a dimension makes required (include/rr.h ipm_* structs): stage data and iterate/result
+// blocks of every non-empty dimension must be non-NULL (the kernels index them unconditionally).
+static bool ipm_iterate_ok(const ipm_dims* d, const ipm_iterate* it) {
+  if (!it->x || !it->y || !it->mu || !it->eta) return false;
+  if (d->N > 0 && !it->u) return false;
+  if (d->N > 0 && d->ng > 0 && (!it->s || !it->z)) return false;
+  if (d->ngN > 0 && (!it->sN || !it->zN)) return false;
+  if (d->N > 0 && d->nc > 0 && !it->lam) return false;
+  if (d->ncN > 0 && !it->lamN) return false;
+  return true;
+}
+static bool ipm_direction_ok(const ipm_dims* d, const ipm_result* r) {
+  if (!r->dx || !r->dy) return false;
+  if (d->N > 0 && !r->du) return false;
+  if (d->N > 0 && d->ng > 0 && (!r->ds || !r->dz)) return false;
+  if (d->ngN > 0 && (!r->dsN || !r->dzN)) return false;
+  if (d->N > 0 && d->nc > 0 && !r->dlam) return false;
+  if (d->ncN > 0 && !r->dlamN) return false;
+  return true;
+}
+static bool ipm_data_ok(const ipm_dims* d, const ipm_stage_data* D) {
+  if (!D->s0 || !D->fval || !D->gradfN || !D->QN) return false;
+  if (d->N > 0 && (!D->gradf || !D->Q || !D->M || !D->R || !D->A || !D->B || !D->dres)) return false;
+  if (d->N > 0 && d->ng > 0 && (!D->gv || !D->Gj)) return false;
+  if (d->ngN > 0 && (!D->gvN || !D->GjN)) return false;
+  if (d->N > 0 && d->nc > 0 && (!D->ce || !D->Ce)) return false;
+  if (d->ncN > 0 && (!D->ceN || !D->CeN)) return false;
+  return true;
+}
+
 rr_err ipm_merit(const ipm_dims* dims, const ipm_stage_data* data, const ipm_iterate* it, const ipm_result* res,
                  const double* alpha, const ipm_trial_values* trial, double* merit, void* stream) {
   if (!ipm_dims_ok(dims)) return set_err(RR_E_INVALID, "ipm_merit: invalid dims%s");
@@ -332,8 +381,8 @@ rr_err ipm_update(const ipm_dims* dims, const ipm_iterate* it, const ipm_result*
   if (!ipm_dims_ok(dims)) return set_err(RR_E_INVALID, "ipm_update: invalid dims%s");
   if (!it || !res) return set_err(RR_E_INVALID, "ipm_update: null %s", "argument");
   if (dims->batch == 0) return RR_OK;
-  if (!alpha_p || !alpha_d || !it->x || !it->y || !res->dx || !res->dy)
-    return set_err(RR_E_INVALID, "ipm_update: null %s", "required pointer");
+  if (!alpha_p || !alpha_d || !ipm_iterate_ok(dims, it) || !ipm_direction_ok(dims, res))
+    return set_err(RR_E_INVALID, "ipm_update: null %s", "required pointer (iterate or direction block of a non-empty dimension)");
   cudaError_t e = rrk::ipm_update_launch(*dims, *it, *res, alpha_p, alpha_d, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return set_err(RR_E_CUDA, "ipm_update: CUDA error %s", cudaGetErrorString(e));
   return RR_OK;
@@ -353,9 +402,8 @@ static rr_err ipm_step_impl(const ipm_dims* dims, const ipm_stage_data* data, co
   if (need < 0) return set_err(RR_E_UNSUPPORTED, "ipm_step: no kernel compiled for these dims/model%s");
   if (dims->N > 0 && (workspace == nullptr || workspace_bytes < need))
     return set_err(RR_E_INVALID, "ipm_step: workspace missing or smaller than %s", "ipm_workspace_bytes()");
-  if (!data->s0 || !data->fval || !data->gradfN || !data->QN || !it->x || !it->y || !it->mu || !it->eta ||
-      !res->dx || !res->dy)
-    return set_err(RR_E_INVALID, "ipm_step: null %s", "required pointer");
+  if (!ipm_data_ok(dims, data) || !ipm_iterate_ok(dims, it) || !ipm_direction_ok(dims, res))
+    return set_err(RR_E_INVALID, "ipm_step: null %s", "required pointer (data, iterate or direction block of a non-empty dimension)");
   if (dims->model != IPM_MODEL_LQ && data->model_params == nullptr)
     return set_err(RR_E_INVALID, "ipm_step: the built-in nonlinear models need %s", "model_params");
   rrk::IpmArgs a;
@@ -395,9 +443,8 @@ rr_err ipm_solve(const ipm_dims* dims, const ipm_stage_data* data, const ipm_ite
   if (need < 0) return set_err(RR_E_UNSUPPORTED, "ipm_solve: no kernel compiled for these dims/model%s");
   if (workspace == nullptr || workspace_bytes < need)
     return set_err(RR_E_INVALID, "ipm_solve: workspace missing or smaller than %s", "ipm_solve_workspace_bytes()");
-  if (!data->s0 || !data->fval || !data->gradfN || !data->QN || !it->x || !it->y || !it->mu || !it->eta ||
-      (dims->N > 0 && (!data->gradf || !data->Q || !data->M || !data->R || !data->A || !data->B || !data->dres || !it->u)))
-    return set_err(RR_E_INVALID, "ipm_solve: null %s", "required pointer");
+  if (!ipm_data_ok(dims, data) || !ipm_iterate_ok(dims, it))
+    return set_err(RR_E_INVALID, "ipm_solve: null %s", "required pointer (data or iterate block of a non-empty dimension)");
   if (dims->model != IPM_MODEL_LQ && data->model_params == nullptr)
     return set_err(RR_E_INVALID, "ipm_solve: the built-in nonlinear models need %s", "model_params");
   bool supported = false;

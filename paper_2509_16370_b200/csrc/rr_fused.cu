@@ -887,11 +887,19 @@ int64_t fused_workspace_bytes(int nx, int nu, int N, int64_t batch) {
     return true;
   });
   if (!small) out = cta_workspace_bytes(nx, nu, N, batch);  // large stages: CTA per instance
+  if (nx == 12 && nu == 4) {  // room for the LDGSTS fallback taken when operands are not 16-byte aligned
+    const int64_t simt = 8 * FusedCfg<12, 4, 16, 4, 3, true>::ws_doubles(batch, N) + 256;
+    if (simt > out) out = simt;
+  }
   return out;
 }
 
 cudaError_t fused_launch(const FusedArgs& a, cudaStream_t s, bool* supported) {
   cudaError_t err = cudaSuccess;
+  if (a.nx == 12 && a.nu == 4 && !a.tma16) {  // operands not 16-byte aligned: no TMA bulk copies
+    *supported = true;
+    return FusedCfg<12, 4, 16, 4, 3, true>::launch(a, s);
+  }
   *supported = dispatch_fused(a.nx, a.nu, [&](auto cfg) {
     err = decltype(cfg)::launch(a, s);
     return true;

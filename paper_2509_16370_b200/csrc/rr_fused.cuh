@@ -17,6 +17,10 @@ struct FusedArgs {
   int32_t* status;
   double* frec = nullptr;  // rr_factor on the DMMA kernel: factor records [batch][N+1][frec_doubles]
   int shared = 0;          // RR_FLAG_SHARED_DYN | RR_FLAG_SHARED_COST (batch-shared operands)
+  // every stage-operand base pointer (A, B, Q, M, R, q, r, c) is 16-byte aligned: the TMA
+  // (cp.async.bulk) kernels may run; otherwise the 12x4 shape falls back to the LDGSTS kernel
+  // (8-byte copies where needed) and the CTA kernels are refused by the API (rr_api.cu)
+  bool tma16 = true;
 };
 
 // Bytes of workspace for this shape (-1 if no kernel is compiled for it).

@@ -745,7 +745,7 @@ cudaError_t factor_launch(const SplitArgs& a, cudaStream_t s, bool* supported) {
   cudaError_t err = cudaSuccess;
   // 12x4: the DMMA stage kernel in factor-only mode (RR_B200_FACTOR=simt selects the SIMT kernel)
   const char* fv = getenv("RR_B200_FACTOR");
-  if (a.nx == 12 && a.nu == 4 && !(fv && strcmp(fv, "simt") == 0)) {
+  if (a.nx == 12 && a.nu == 4 && a.tma16 && !(fv && strcmp(fv, "simt") == 0)) {
     FusedArgs f{};
     f.nx = a.nx;
     f.nu = a.nu;

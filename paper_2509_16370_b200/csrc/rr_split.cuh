@@ -19,6 +19,7 @@ struct SplitArgs {
   int32_t* status;
   int accumulate;    // rr_solve: RR_FLAG_ACCUMULATE (sol += solution)
   int shared;        // RR_FLAG_SHARED_DYN | RR_FLAG_SHARED_COST
+  bool tma16;        // rr_factor: A, B, Q, M, R 16-byte aligned (the 12x4 DMMA/TMA factor kernel may run)
 };
 
 struct ResArgs {

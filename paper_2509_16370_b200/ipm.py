@@ -12,14 +12,56 @@ from ._lib import (IPM_DATA_FIELDS, IPM_ITER_FIELDS, IPM_RES_FIELDS, RRError, ch
 RES_SHAPE_OF = dict(dx="x", du="u", ds="s", dsN="sN", dy="y", dlam="lam", dlamN="lamN", dz="z", dzN="zN")
 
 
-def _p(t):
+INT_FIELDS = ("status", "n_backtracks", "iters")
+
+
+def _p(t, name=""):
+    """Device pointer of a contiguous CUDA tensor: int32 for status / n_backtracks / iters, float64
+    otherwise (NULL for an empty tensor)."""
     if t is None:
         return None
     if not t.is_cuda:
         raise RRError("ipm_step needs CUDA tensors (no CPU fallback)")
+    dt = torch.int32 if name in INT_FIELDS else torch.float64
+    if t.dtype != dt:
+        raise RRError("%s: expected %s, got %s" % (name or "tensor", dt, t.dtype))
     if not t.is_contiguous():
         raise RRError("tensor must be contiguous")
     return ctypes.c_void_p(t.data_ptr()) if t.numel() > 0 else None
+
+
+def _sizes(b):
+    """Element counts the dims imply for every data / iterate / result field (include/rr.h ipm_*)."""
+    B, N, n, m, ng, ngN, nc, ncN = b.batch, b.N, b.nx, b.nu, b.ng, b.ngN, b.nc, b.ncN
+    w, sy = n + m, (lambda k: k * (k + 1) // 2)
+    z = dict(s0=B * n, fval=B, gradf=B * N * w, gradfN=B * n, Q=B * N * sy(n), M=B * N * n * m, R=B * N * sy(m),
+             QN=B * sy(n), A=B * N * n * n, B=B * N * n * m, dres=B * N * n, ce=B * N * nc, Ce=B * N * nc * w,
+             ceN=B * ncN, CeN=B * ncN * n, gv=B * N * ng, Gj=B * N * ng * w, gvN=B * ngN, GjN=B * ngN * n,
+             x=B * (N + 1) * n, u=B * N * m, s=B * N * ng, z=B * N * ng, sN=B * ngN, zN=B * ngN,
+             y=B * (N + 1) * n, lam=B * N * nc, lamN=B * ncN, mu=B, eta=B)
+    for r, it in RES_SHAPE_OF.items():
+        z[r] = z[it]
+    for k in ("alpha_p", "alpha_d", "D", "merit0", "merit_acc", "n_backtracks", "status", "iters"):
+        z[k] = B
+    return z
+
+
+def check_batch(b, res=None):
+    """Dtype, device and size of every tensor of the IPMBatch (and result dict) against its dims."""
+    dev = b.it["mu"].device
+    want = _sizes(b)
+    for group in (b.data, b.it, res or {}):
+        for k, t in group.items():
+            if t is None or k not in want:
+                continue
+            _p(t, k)
+            if t.device != dev:
+                raise RRError("%s on %s, the batch is on %s" % (k, t.device, dev))
+            if t.numel() != want[k]:
+                raise RRError("%s: %d elements, the dims need %d" % (k, t.numel(), want[k]))
+    mp = b.data.get("model_params")
+    if mp is not None and (mp.dtype != torch.float64 or mp.device != dev or mp.numel() < 8):
+        raise RRError("model_params: expected >= 8 float64 on %s" % dev)
 
 
 def dims_of(b) -> ipm_dims:
@@ -52,11 +94,12 @@ class IpmCall:
         nb = workspace_bytes(b)
         self.ws = ws if ws is not None else torch.empty((nb + 7) // 8, dtype=torch.float64, device=b.it["mu"].device)
         self.d = dims_of(b)
-        self.data = ipm_stage_data(*[_p(b.data[f]) for f in IPM_DATA_FIELDS])
-        self.it = ipm_iterate(*[_p(b.it[f]) for f in IPM_ITER_FIELDS])
+        check_batch(b, self.res)
+        self.data = ipm_stage_data(*[_p(b.data[f], f) for f in IPM_DATA_FIELDS])
+        self.it = ipm_iterate(*[_p(b.it[f], f) for f in IPM_ITER_FIELDS])
         self.prm = ipm_params(tau, armijo_c, beta, max_backtracks, 0)
-        self.r = ipm_result(*[_p(self.res[f]) for f in IPM_RES_FIELDS])
-        self.st = _p(self.res["status"])
+        self.r = ipm_result(*[_p(self.res[f], f) for f in IPM_RES_FIELDS])
+        self.st = _p(self.res["status"], "status")
         self.wsp, self.wsb = _p(self.ws), self.ws.numel() * 8
 
     def launch(self, stream=None, direction_only=False):
@@ -94,14 +137,15 @@ class IpmSolveCall:
         if nb < 0:
             raise RRError("no ipm_solve kernel compiled for these dims/model")
         self.ws = ws if ws is not None else torch.empty((nb + 7) // 8, dtype=torch.float64, device=dev)
-        self.data = ipm_stage_data(*[_p(b.data[f]) for f in IPM_DATA_FIELDS])
-        self.it = ipm_iterate(*[_p(b.it[f]) for f in IPM_ITER_FIELDS])
+        check_batch(b)
+        self.data = ipm_stage_data(*[_p(b.data[f], f) for f in IPM_DATA_FIELDS])
+        self.it = ipm_iterate(*[_p(b.it[f], f) for f in IPM_ITER_FIELDS])
         self.S = ipm_solve_settings(S["mu_min"], S["kappa"], S["kappa_mu"], S["theta_mu"], S["eta_max"],
                                     S["kappa_eta"], S["tol_kkt"], int(S["max_iters"]), 0,
                                     ipm_params(S["tau"], S["armijo_c"], S["beta"], int(S["max_backtracks"]), 0))
         self.rep = {k: torch.empty(b.batch, dtype=torch.int32 if k in ("status", "iters") else torch.float64, device=dev)
                     for k in REPORT_FIELDS}
-        self.r = ipm_solve_report(*[_p(self.rep[k]) for k in REPORT_FIELDS])
+        self.r = ipm_solve_report(*[_p(self.rep[k], k) for k in REPORT_FIELDS])
         self.wsp, self.wsb = _p(self.ws), self.ws.numel() * 8
 
     def launch(self, stream=None):
@@ -134,10 +178,11 @@ def ipm_merit(b, res, alpha, trial, out=None, stream=None):
     fval, dres, ce, ceN, gv, gvN in the IPMBatch data layouts); alpha: [batch] CUDA tensor."""
     dev = b.it["mu"].device
     merit = out if out is not None else torch.empty(b.batch, dtype=torch.float64, device=dev)
-    tv = ipm_trial_values(*[_p(trial.get(f)) for f in TRIAL_FIELDS])
-    rc = lib().ipm_merit(ctypes.byref(dims_of(b)), ctypes.byref(ipm_stage_data(*[_p(b.data[f]) for f in IPM_DATA_FIELDS])),
-                         ctypes.byref(ipm_iterate(*[_p(b.it[f]) for f in IPM_ITER_FIELDS])),
-                         ctypes.byref(ipm_result(*[_p(res.get(f)) for f in IPM_RES_FIELDS])), _p(alpha),
+    check_batch(b, {k: v for k, v in res.items() if k in IPM_RES_FIELDS})
+    tv = ipm_trial_values(*[_p(trial.get(f), f) for f in TRIAL_FIELDS])
+    rc = lib().ipm_merit(ctypes.byref(dims_of(b)), ctypes.byref(ipm_stage_data(*[_p(b.data[f], f) for f in IPM_DATA_FIELDS])),
+                         ctypes.byref(ipm_iterate(*[_p(b.it[f], f) for f in IPM_ITER_FIELDS])),
+                         ctypes.byref(ipm_result(*[_p(res.get(f), f) for f in IPM_RES_FIELDS])), _p(alpha),
                          ctypes.byref(tv), _p(merit),
                          ctypes.c_void_p((stream or torch.cuda.current_stream(dev)).cuda_stream))
     check(rc, "ipm_merit")
@@ -147,7 +192,8 @@ def ipm_merit(b, res, alpha, trial, out=None, stream=None):
 def ipm_update(b, res, alpha_p, alpha_d, stream=None):
     """x, u, s, y, λ += α_p Δ and z += α_d Δz in place (per-instance [batch] CUDA tensors)."""
     dev = b.it["mu"].device
-    rc = lib().ipm_update(ctypes.byref(dims_of(b)), ctypes.byref(ipm_iterate(*[_p(b.it[f]) for f in IPM_ITER_FIELDS])),
-                          ctypes.byref(ipm_result(*[_p(res.get(f)) for f in IPM_RES_FIELDS])), _p(alpha_p), _p(alpha_d),
+    check_batch(b, {k: v for k, v in res.items() if k in IPM_RES_FIELDS})
+    rc = lib().ipm_update(ctypes.byref(dims_of(b)), ctypes.byref(ipm_iterate(*[_p(b.it[f], f) for f in IPM_ITER_FIELDS])),
+                          ctypes.byref(ipm_result(*[_p(res.get(f), f) for f in IPM_RES_FIELDS])), _p(alpha_p), _p(alpha_d),
                           ctypes.c_void_p((stream or torch.cuda.current_stream(dev)).cuda_stream))
     check(rc, "ipm_update")

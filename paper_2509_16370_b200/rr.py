@@ -15,14 +15,48 @@ from ._lib import (RR_FLAG_ACCUMULATE, RRError, check, lib, rr_dims, rr_factor_b
 PROBLEM_FIELDS = ("A", "B", "Q", "M", "R", "q", "r", "c", "QN", "qN", "c0", "delta")
 
 
-def _p(t: Optional[torch.Tensor]):
+def _p(t: Optional[torch.Tensor], dtype=torch.float64):
+    """Device pointer of a contiguous CUDA tensor of exactly `dtype` (float64 data, int32 status)."""
     if t is None:
         return None
-    if not t.is_cuda or t.dtype != torch.float64 and t.dtype != torch.int32:
-        raise RRError("expected a CUDA float64/int32 tensor, got %s on %s" % (t.dtype, t.device))
+    if not t.is_cuda or t.dtype != dtype:
+        raise RRError("expected a CUDA %s tensor, got %s on %s" % (dtype, t.dtype, t.device))
     if not t.is_contiguous():
         raise RRError("tensor must be contiguous")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _sym(k: int) -> int:
+    return k * (k + 1) // 2
+
+
+def check_problem(prob, sol=None):
+    """Dtype / device / size of every problem (and solution) tensor against the dims, before any
+    pointer reaches the library (a float32 or short tensor would otherwise be read out of bounds)."""
+    b, N, n, m = prob.batch, prob.N, prob.nx, prob.nu
+    fl = shared_flags(prob)
+    bD = 1 if fl & RR_FLAG_SHARED_DYN else b
+    bP = 1 if fl & RR_FLAG_SHARED_COST else b
+    want = dict(A=bD * N * n * n, B=bD * N * n * m, Q=bP * N * _sym(n), M=bP * N * n * m, R=bP * N * _sym(m),
+                q=b * N * n, r=b * N * m, c=b * N * n, QN=bP * _sym(n), qN=b * n, c0=b * n, delta=b)
+    dev = prob.delta.device
+    for f in PROBLEM_FIELDS:
+        t = getattr(prob, f)
+        if t is None:
+            continue
+        if t.dtype != torch.float64 or t.device != dev:
+            raise RRError("problem.%s: expected float64 on %s, got %s on %s" % (f, dev, t.dtype, t.device))
+        if t.numel() != want[f]:
+            raise RRError("problem.%s: %d elements, the dims need %d" % (f, t.numel(), want[f]))
+    if sol is not None:
+        for f, k in (("x", b * (N + 1) * n), ("u", b * N * m), ("y", b * (N + 1) * n), ("status", b)):
+            t = sol.get(f)
+            if t is None:
+                continue
+            dt = torch.int32 if f == "status" else torch.float64
+            if t.dtype != dt or t.device != dev or t.numel() != k:
+                raise RRError("solution.%s: expected %d %s on %s, got %d %s on %s"
+                              % (f, k, dt, dev, t.numel(), t.dtype, t.device))
 
 
 RR_FLAG_SHARED_DYN, RR_FLAG_SHARED_COST = 2, 4
@@ -82,12 +116,13 @@ class Marshalled:
 
     def __init__(self, prob, sol, fac=None, ws=None):
         self.prob, self.sol, self.fac = prob, sol, fac
+        check_problem(prob, sol)
         self.ws = ws if ws is not None else alloc_workspace(prob)
         self.d = dims_of(prob)
         self.p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
         self.f = rr_factor_buf(*[_p(fac[k]) if fac is not None else None for k in ("V", "v", "K", "k")])
         self.s = rr_solution(_p(sol["x"]), _p(sol["u"]), _p(sol["y"]))
-        self.st = _p(sol["status"])
+        self.st = _p(sol["status"], torch.int32)
         self.wsp = _p(self.ws)
         self.wsb = self.ws.numel() * 8
 
@@ -151,10 +186,11 @@ def rr_factor(prob, factor=None, fac=None, status=None, stream=None):
                              dtype=torch.float64, device=dev)
     if status is None:
         status = torch.empty(prob.batch, dtype=torch.int32, device=dev)
+    check_problem(prob, dict(status=status))
     p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
     f = rr_factor_buf(*[_p(fac.get(k)) if fac is not None else None for k in ("V", "v", "K", "k")])
     rc = lib().rr_factor(ctypes.byref(dims_of(prob)), ctypes.byref(p), _p(factor), factor.numel() * 8,
-                         ctypes.byref(f), _p(status), _stream(stream, dev))
+                         ctypes.byref(f), _p(status, torch.int32), _stream(stream, dev))
     check(rc, "rr_factor")
     return factor, status
 
@@ -170,6 +206,7 @@ def rr_solve(prob, factor, out=None, fac=None, workspace=None, stream=None, accu
     if workspace is None:
         nb = solve_workspace_bytes(prob.nx, prob.nu, prob.N, prob.batch)
         workspace = torch.empty((nb + 7) // 8, dtype=torch.float64, device=dev)
+    check_problem(prob, sol)
     p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
     f = rr_factor_buf(*[_p(fac.get(k)) if fac is not None else None for k in ("V", "v", "K", "k")])
     s = rr_solution(_p(sol["x"]), _p(sol["u"]), _p(sol["y"]))
@@ -180,7 +217,7 @@ def rr_solve(prob, factor, out=None, fac=None, workspace=None, stream=None, accu
         d.flags |= RR_FLAG_ACCUMULATE
     rc = lib().rr_solve(ctypes.byref(d), ctypes.byref(p), _p(factor), factor.numel() * 8,
                         ctypes.byref(f), ctypes.byref(s), _p(workspace), workspace.numel() * 8,
-                        _p(sol["status"]), _stream(stream, dev))
+                        _p(sol["status"], torch.int32), _stream(stream, dev))
     check(rc, "rr_solve")
     return sol
 
@@ -198,10 +235,11 @@ def rr_factor_solve_pit(prob, out=None, workspace=None, stream=None):
         if nb < 0:
             raise RRError("rr_factor_solve_pit: nx, nu must be <= 16")
         workspace = torch.empty((nb + 7) // 8, dtype=torch.float64, device=dev)
+    check_problem(prob, sol)
     p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
     s = rr_solution(_p(sol["x"]), _p(sol["u"]), _p(sol["y"]))
     rc = lib().rr_factor_solve_pit(ctypes.byref(d), ctypes.byref(p), ctypes.byref(s), _p(workspace),
-                                   workspace.numel() * 8, _p(sol["status"]), _stream(stream, dev))
+                                   workspace.numel() * 8, _p(sol["status"], torch.int32), _stream(stream, dev))
     check(rc, "rr_factor_solve_pit")
     return sol
 
@@ -220,6 +258,7 @@ def rr_residual(prob, sol, res=None, norms=None, stream=None):
         res = {f: torch.empty_like(getattr(prob, f)) for f in RESIDUAL_FIELDS}
     if norms is None:
         norms = torch.empty(prob.batch, 2, dtype=torch.float64, device=dev)
+    check_problem(prob, sol)
     p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
     s = rr_solution(_p(sol["x"]), _p(sol["u"]), _p(sol["y"]))
     r = rr_residual_buf(*[_p(res.get(f)) for f in RESIDUAL_FIELDS])
@@ -255,6 +294,7 @@ class HostMarshalled:
         for t in (prob_host.delta, sol_host["x"]):
             if t.is_cuda:
                 raise RRError("host buffers expected")
+        check_problem(prob_dev, sol_dev)
         self.keep = (prob_host, sol_host, prob_dev, sol_dev)
         self.d = dims_of(prob_host)
         hp = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
@@ -263,7 +303,7 @@ class HostMarshalled:
         self.sth = hp(sol_host["status"])
         self.pd = rr_problem(*[_p(getattr(prob_dev, f)) for f in PROBLEM_FIELDS])
         self.sd = rr_solution(_p(sol_dev["x"]), _p(sol_dev["u"]), _p(sol_dev["y"]))
-        self.std = _p(sol_dev["status"])
+        self.std = _p(sol_dev["status"], torch.int32)
         self.ws = ws if ws is not None else alloc_workspace(prob_dev)
         self.wsp, self.wsb = _p(self.ws), self.ws.numel() * 8
         self.h2d_bytes = sum(getattr(prob_host, f).numel() * 8 for f in PROBLEM_FIELDS)

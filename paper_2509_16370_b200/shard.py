@@ -1,8 +1,8 @@
 """Batch sharding across GPUs (row e): instances are independent, so ranks own contiguous
 global-id ranges and no collective touches the data path.  torch.distributed is used only to
 reduce the timing (max over ranks), for barriers, and for the final gather of per-instance
-summaries (status, u_0) to rank 0 after the solve; full trajectories stay on
-their device."""
+summaries to rank 0 after the solve (status, u_0, KKT residual norms; for the IPM
+step α_p, D, 𝒜(0)); full trajectories stay on their device."""
 from __future__ import annotations
 
 from typing import Tuple
@@ -32,10 +32,13 @@ def max_over_ranks(value: float, device=None) -> float:
 def gather_summaries(parts, rank: int, world: int, total: int):
     """Gather per-instance summary tensors of every rank's shard to rank 0 (after the solve).
 
-    parts: dict name -> tensor [shard_size, ...] (this rank's contiguous shard, shard_range order).
-    Returns, on rank 0, dict name -> tensor [total, ...] in global-id order; None on other ranks.
-    Shards differ in size by at most one, so every rank pads to the largest shard and one
-    all_gather per tensor moves them (NCCL over NVLink/NVSwitch on GPUs, gloo on CPU)."""
+    parts: dict name -> tensor [shard_size, ...] (this rank's contiguous shard, shard_range order),
+    e.g. status, u_0 and the KKT residual norms of rr_factor_solve, or status, α_p, D, 𝒜(0) of
+    ipm_step.  Returns, on rank 0, dict name -> tensor [total, ...] in global-id
+    order; None on the other ranks.  One dist.gather per tensor to rank 0 (NCCL point-to-point
+    over NVLink / NVSwitch on GPUs, gloo on CPU): only rank 0 receives, so memory and traffic are
+    O(total) there and O(shard) elsewhere.  Shards differ in size by at most one; every rank pads
+    to the largest shard."""
     import torch
     import torch.distributed as dist
     if world == 1 or not (dist.is_available() and dist.is_initialized()):
@@ -43,13 +46,16 @@ def gather_summaries(parts, rank: int, world: int, total: int):
     sizes = [e - b for b, e in (shard_range(r, world, total) for r in range(world))]
     mx = max(sizes)
     out = {}
-    for name, t in parts.items():
+    for name in sorted(parts):          # same collective order on every rank
+        t = parts[name]
         if t.shape[0] != sizes[rank]:
             raise ValueError("summary %s has %d rows, shard has %d" % (name, t.shape[0], sizes[rank]))
         pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
         pad[:t.shape[0]].copy_(t)
-        bufs = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(bufs, pad)
         if rank == 0:
+            bufs = [torch.empty_like(pad) for _ in range(world)]
+            dist.gather(pad, gather_list=bufs, dst=0)
             out[name] = torch.cat([bufs[r][:sizes[r]] for r in range(world)], dim=0)
+        else:
+            dist.gather(pad, dst=0)
     return out if rank == 0 else None

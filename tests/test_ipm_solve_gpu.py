@@ -1,8 +1,8 @@
 """GPU parity of ipm_solve (the batched regularized-IPM loop) against the oracle loop
 (oracle/ipm_solve.py) on identical inputs: per-instance status and iteration count bit-exact, final
-μ, η, iterate and residuals to 1e-9 relative (FP64).  The cart-pole swing-up is nonconvex and
-does not converge within the budget; it is compared over its first iterations, where rounding has
-not yet been amplified into different line-search decisions."""
+μ, η and iterate to 1e-9 relative (FP64), the north-star bar, in every case (measured worst case
+1.4e-10 on the random LQ with stage equalities, tools/f1_errors.py).  The cart-pole swing-up is
+nonconvex and does not converge within the budget; it is compared over its first 1-20 iterations."""
 import numpy as np
 import pytest
 import torch
@@ -44,7 +44,7 @@ def check(it_g, rep_g, it_o, rep_o, keys=("x", "u", "s", "z", "y"), tol=TOL):
 
 def test_double_integrator_converges_like_oracle():
     it_g, rep_g, it_o, rep_o = run_both(double_integrator_ocp(batch=3))
-    check(it_g, rep_g, it_o, rep_o, tol=1e-8)
+    check(it_g, rep_g, it_o, rep_o)
     assert np.all(rep_g["status"] == 0) and np.all(rep_g["iters"] <= 50)
     assert np.all(np.maximum(np.maximum(rep_g["r_stat"], rep_g["r_feas"]), rep_g["r_comp"]) <= 1e-6)
 
@@ -54,34 +54,40 @@ def test_double_integrator_converges_like_oracle():
 def test_random_lq_parity(nx, nu, ng, ngN, nc, ncN):
     b = random_lq_ocp(nx, nu, 12, 24, seed=nx * 7 + ng, ng=ng, ngN=ngN, nc=nc, ncN=ncN, eta=1e4)
     it_g, rep_g, it_o, rep_o = run_both(b)
-    check(it_g, rep_g, it_o, rep_o, tol=1e-7)
+    check(it_g, rep_g, it_o, rep_o, keys=("x", "u", "s", "z", "y", "lam"))
     conv = rep_g["status"] == 0
     assert conv.mean() >= 0.5 or nc > 0   # random stage equalities + inequalities may be infeasible
 
 
-@pytest.mark.parametrize("iters", [1, 3, 6])
+@pytest.mark.parametrize("iters", [1, 3, 6, 20])
 def test_cartpole_first_iterations(iters):
     b = cartpole_c4(16, N=40)
     it_g, rep_g, it_o, rep_o = run_both(b, max_iters=iters)
-    check(it_g, rep_g, it_o, rep_o, tol=1e-8)
+    check(it_g, rep_g, it_o, rep_o)
     assert np.all(rep_g["status"] == 6)
 
 
 def test_converged_instances_are_frozen_and_empty_batch():
-    """A converged instance is frozen: re-solving a converged batch (μ ≤ 10 μ_min already, KKT ≤ tol)
-    takes zero steps and leaves every iterate array bitwise unchanged; an empty batch is a no-op.
+    """A converged iterate is a fixed point of the loop: solving S:269's scalar problem, then
+    re-solving from the converged (x, s, z) with its final μ and η (the data re-generated at that
+    iterate: μ and the data are inputs of ipm_solve, include/rr.h) reports status 0 after zero
+    steps and leaves every iterate array bitwise unchanged.  An empty batch is a no-op.
     (Instances converging at different iterations inside one batch: the next test.)"""
     import paper_2509_16370_b200 as m
-    b = double_integrator_ocp(batch=2).to("cuda")
-    rep = m.ipm_solve(b, max_iters=200)
+    from synth.ipm_workloads import spec_scalar_ocp
+    b = spec_scalar_ocp(batch=3, xbar=3.0, s=2.0, z=0.05, mu=0.1, eta=1e4).to("cuda")
+    rep = m.ipm_solve(b)
     torch.cuda.synchronize()
     assert torch.all(rep["status"] == 0) and torch.all(rep["iters"] > 0)
-    snap = {k: v.clone() for k, v in b.it.items()}
-    rep2 = m.ipm_solve(b, max_iters=200)
+    u, sl, z = (float(b.it[k][0].reshape(-1)[0]) for k in ("u", "s", "z"))
+    mu, eta = float(rep["mu"][0]), float(rep["eta"][0])
+    b2 = spec_scalar_ocp(batch=3, xbar=u, s=sl, z=z, mu=mu, eta=eta).to("cuda")
+    snap = {k: v.clone() for k, v in b2.it.items()}
+    rep2 = m.ipm_solve(b2)
     torch.cuda.synchronize()
     assert torch.all(rep2["status"] == 0) and torch.all(rep2["iters"] == 0)
     for k, v in snap.items():
-        assert torch.equal(b.it[k], v), k
+        assert torch.equal(b2.it[k], v), k
     e = double_integrator_ocp(batch=0).to("cuda")
     m.ipm_solve(e)
 
@@ -144,16 +150,14 @@ def test_quadrotor_first_iterations(iters):
     """Quadrotor model (analytic Jacobians re-evaluated at every iterate) over the first iterations."""
     b = quadrotor_ipm(24, N=20)
     it_g, rep_g, it_o, rep_o = run_both(b, max_iters=iters)
-    check(it_g, rep_g, it_o, rep_o, tol=1e-8)
+    check(it_g, rep_g, it_o, rep_o)
 
 
 def test_quadrotor_solve_converges():
-    """The quadrotor hover problems converge (oracle: 18-34 iterations); GPU report against the oracle."""
+    """The quadrotor hover problems converge (oracle: 18-34 iterations): same status and iteration
+    count as the oracle loop, iterate within the 1e-9 bar."""
     b = quadrotor_ipm(6, N=20)
     it_g, rep_g, it_o, rep_o = run_both(b)
     assert np.all(rep_o["status"] == 0)
-    assert np.all(rep_g["status"] == 0)
-    assert np.max(np.abs(rep_g["iters"] - rep_o["iters"])) <= 1
+    check(it_g, rep_g, it_o, rep_o)
     assert np.all(np.maximum(np.maximum(rep_g["r_stat"], rep_g["r_feas"]), rep_g["r_comp"]) <= 1e-6)
-    for k in ("x", "u"):
-        assert rel(it_g[k], it_o[k]) <= 1e-5, k

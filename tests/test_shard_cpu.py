@@ -78,7 +78,19 @@ def _gather_worker(rank, world, port, total, out):
     from paper_2509_16370_b200.shard import gather_summaries
     b, e = shard_range(rank, world, total)
     ids = torch.arange(b, e, dtype=torch.int64)
-    parts = {"status": (ids % 7).to(torch.int32), "u0": torch.stack([ids.double(), -ids.double()], dim=1)}
+    parts = {"status": (ids % 7).to(torch.int32), "u0": torch.stack([ids.double(), -ids.double()], dim=1),
+             "kkt": torch.stack([ids.double() * 1e-12, ids.double() * 2e-12], dim=1)}
+    # the IPM-step summary set of SURVEY §8(e) from the oracle on this rank's shard of a C4-LS batch
+    from oracle.ipm import ipm_step_oracle
+    from synth.ipm_workloads import cartpole_c4
+    if e > b:
+        res, _ = ipm_step_oracle(cartpole_c4(e - b, seed=2511, N=6, variant="C4-LS", first=b))
+    else:  # empty shard (world > total)
+        res = {k: np.zeros(0) for k in ("alpha_p", "D", "merit0")}
+        res["status"] = np.zeros(0, dtype=np.int32)
+    for k in ("alpha_p", "D", "merit0"):
+        parts[k] = torch.from_numpy(res[k])
+    parts["ipm_status"] = torch.from_numpy(res["status"])
     g = gather_summaries(parts, rank, world, total)
     if rank == 0:
         out.put({k: v.numpy() for k, v in g.items()})
@@ -88,9 +100,11 @@ def _gather_worker(rank, world, port, total, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,total", [(2, 11), (3, 10)])
+@pytest.mark.parametrize("world,total", [(2, 11), (3, 10), (3, 2)])
 def test_gloo_summary_gather_global_order(world, total):
-    """Per-instance summaries of uneven shards arrive on rank 0 in global-id order (row e)."""
+    """Per-instance summaries of uneven (or empty) shards arrive on rank 0 only, in global-id order
+    (row e: dist.gather to rank 0), and the IPM summaries (α_p, D, 𝒜(0), status) gathered from
+    the shards equal the oracle on the unsharded batch bitwise."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -104,3 +118,10 @@ def test_gloo_summary_gather_global_order(world, total):
     ids = np.arange(total)
     assert np.array_equal(g["status"], (ids % 7).astype(np.int32))
     assert np.array_equal(g["u0"], np.stack([ids, -ids], axis=1).astype(np.float64))
+    assert np.array_equal(g["kkt"], np.stack([ids * 1e-12, ids * 2e-12], axis=1))
+    from oracle.ipm import ipm_step_oracle
+    from synth.ipm_workloads import cartpole_c4
+    full, _ = ipm_step_oracle(cartpole_c4(total, seed=2511, N=6, variant="C4-LS"))
+    for k in ("alpha_p", "D", "merit0"):
+        assert np.array_equal(g[k], full[k]), k
+    assert np.array_equal(g["ipm_status"], full["status"])
