@@ -400,22 +400,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     ptw[k2] = PREG ? ((uint32_t)ptab[(2 * k2) * 32 + lane] | ((uint32_t)ptab[(2 * k2 + 1) * 32 + lane] << 16)) : 0u;
 #endif
   double* wk = grp ? wkq[1] : wkq[0];
-
-  const int64_t inst0 = ((int64_t)blockIdx.x * WARPS + warp) * 2;
-  int64_t instq[2] = {inst0, inst0 + 1};
-  bool validq[2] = {instq[0] < a.batch, instq[1] < a.batch};
-#pragma unroll
-  for (int q = 0; q < 2; ++q)
-    if (!validq[q]) instq[q] = a.batch - 1;
-  const int64_t inst = grp ? instq[1] : instq[0];
-  const bool valid = grp ? validq[1] : validq[0];
-  const int64_t instP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;  // batch-shared Q, M, R, Q_N
-  const double delta = a.p.delta[inst];
   const int64_t sN = (int64_t)N;
-  double* rec0 = a.ws + inst * sN * RC::PAD;
-  double* rec0q[2] = {validq[0] ? a.ws + instq[0] * sN * RC::PAD : nullptr,
-                      validq[1] ? a.ws + instq[1] * sN * RC::PAD : nullptr};
-  int32_t st = 0;
 
   // stage inputs: TMA bulk copies for BOTH instances of the warp issued by lane 0, completion on
   // each instance's bar[0] (records in the forward sweep: bar[0] / bar[1] by buffer)
@@ -431,407 +416,374 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   uint32_t ph0 = 0, ph1 = 0;
   constexpr uint32_t STG_BYTES = 8u * (n * n + 2 * n * m + sn + sm + (FAC ? 0 : 2 * n + m));
   constexpr int FREC = (NX * (NX + 1) + NX * NU + NU * (NU + 1) / 2 + 1) & ~1;  // factor record doubles
-  if constexpr (FAC) {  // no right-hand side: q, r, c slots of the stage buffers stay zero
-    for (int e = j; e < 2 * n + m; e += 16) slot[oq + e] = 0.0;
-  }
-  auto issue_stage = [&](int i, double* dst) {
-    const int64_t s = inst * sN + i;
-    if constexpr (LY::BULK) {
-      if (lane == 0) {
-        fence_proxy_async();
+
+  // Persistent warps (DESIGN.md §5 "phase staggering"): warp w of CTA b solves the instance pairs
+  // p0 + k·stride, k = 0, 1, ...  The backward sweep is compute / shared-memory bound and the forward
+  // sweep is HBM bound; run in lockstep (every warp backward, then every warp forward) the two never
+  // overlap.  Each CTA therefore runs the forward sweep of pair k − d after the backward sweep of
+  // pair k, with a per-CTA delay d = (b / #SMs) mod a.defer_mod: the CTAs sharing an SM are then in
+  // their forward sweeps at different times and the forward's HBM traffic hides under the other
+  // CTAs' backward sweeps.  x_0 and the backward status go through the output arrays in between.
+  const int64_t npairs = (a.batch + 1) / 2;
+  const int64_t stride = (int64_t)gridDim.x * WARPS;
+  const int64_t p0 = (int64_t)blockIdx.x * WARPS + warp;
+  const int64_t K = p0 < npairs ? (npairs - 1 - p0) / stride + 1 : 0;
+  const int defer = (FAC || a.defer_mod <= 1) ? 0 : (int)((blockIdx.x / (a.nsm > 0 ? a.nsm : 1)) % a.defer_mod);
+
+  auto pair_insts = [&](int64_t pair, int64_t (&instq)[2], bool (&validq)[2]) {
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int64_t sq = instq[q] * sN + i;
-          const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : instq[q]) * sN + i;
-          const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : instq[q]) * sN + i;
-          double* d = slotq[q];
-          uint64_t* bq = barq[q];
-          mbar_arrive_expect_tx(bq, STG_BYTES);
-          bulk_g2s(d + oA, a.p.A + sD * n * n, 8 * n * n, bq);
-          bulk_g2s(d + oB, a.p.B + sD * n * m, 8 * n * m, bq);
-          bulk_g2s(d + oQ, a.p.Q + sP * sn, 8 * sn, bq);
-          bulk_g2s(d + oM, a.p.M + sP * n * m, 8 * n * m, bq);
-          bulk_g2s(d + oR, a.p.R + sP * sm, 8 * sm, bq);
-          if constexpr (!FAC) {
-            bulk_g2s(d + oq, a.p.q + sq * n, 8 * n, bq);
-            bulk_g2s(d + orr, a.p.r + sq * m, 8 * m, bq);
-            bulk_g2s(d + oc, a.p.c + sq * n, 8 * n, bq);
+    for (int q = 0; q < 2; ++q) {
+      instq[q] = 2 * pair + q;
+      validq[q] = instq[q] < a.batch;
+      if (!validq[q]) instq[q] = a.batch - 1;
+    }
+  };
+
+  // ---------------- backward sweep of one pair (+ x_0 and the backward status) ----------------
+  auto backward_pair = [&](int64_t pair) {
+    int64_t instq[2];
+    bool validq[2];
+    pair_insts(pair, instq, validq);
+    const int64_t inst = grp ? instq[1] : instq[0];
+    const bool valid = grp ? validq[1] : validq[0];
+    const int64_t instP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;  // batch-shared Q, M, R, Q_N
+    const double delta = a.p.delta[inst];
+    double* rec0q[2] = {validq[0] ? a.ws + instq[0] * sN * RC::PAD : nullptr,
+                        validq[1] ? a.ws + instq[1] * sN * RC::PAD : nullptr};
+    int32_t st = 0;
+    // generic-proxy writes of the previous pair's phase to this slot before the TMA refills it
+    fence_proxy_async();
+    __syncwarp();
+    if constexpr (FAC) {  // no right-hand side: q, r, c slots of the stage buffers stay zero
+      for (int e = j; e < 2 * n + m; e += 16) slot[oq + e] = 0.0;
+    }
+    auto issue_stage = [&](int i, double* dst) {
+      const int64_t s = inst * sN + i;
+      if constexpr (LY::BULK) {
+        if (lane == 0) {
+          fence_proxy_async();
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int64_t sq = instq[q] * sN + i;
+            const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : instq[q]) * sN + i;
+            const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : instq[q]) * sN + i;
+            double* d = slotq[q];
+            uint64_t* bq = barq[q];
+            mbar_arrive_expect_tx(bq, STG_BYTES);
+            bulk_g2s(d + oA, a.p.A + sD * n * n, 8 * n * n, bq);
+            bulk_g2s(d + oB, a.p.B + sD * n * m, 8 * n * m, bq);
+            bulk_g2s(d + oQ, a.p.Q + sP * sn, 8 * sn, bq);
+            bulk_g2s(d + oM, a.p.M + sP * n * m, 8 * n * m, bq);
+            bulk_g2s(d + oR, a.p.R + sP * sm, 8 * sm, bq);
+            if constexpr (!FAC) {
+              bulk_g2s(d + oq, a.p.q + sq * n, 8 * n, bq);
+              bulk_g2s(d + orr, a.p.r + sq * m, 8 * m, bq);
+              bulk_g2s(d + oc, a.p.c + sq * n, 8 * n, bq);
+            }
           }
         }
-      }
-      (void)s;
-      (void)dst;
-    } else {
-      const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst) * sN + i;
-      const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : inst) * sN + i;
-      copy_async(dst + oA, a.p.A + sD * n * n, n * n, j, 16);
-      copy_async(dst + oB, a.p.B + sD * n * m, n * m, j, 16);
-      copy_async(dst + oQ, a.p.Q + sP * sn, sn, j, 16);
-      copy_async(dst + oM, a.p.M + sP * n * m, n * m, j, 16);
-      copy_async(dst + oR, a.p.R + sP * sm, sm, j, 16);
-      copy_async(dst + oq, a.p.q + s * n, n, j, 16);
-      copy_async(dst + orr, a.p.r + s * m, m, j, 16);
-      copy_async(dst + oc, a.p.c + s * n, n, j, 16);
-      cp_async_commit();
-    }
-  };
-  auto wait_stage = [&]() {
-    if constexpr (LY::BULK) {
-      mbar_wait_parity(&bar[0], ph0);
-      ph0 ^= 1u;
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncwarp();
-  };
-  // P = [[Q M]; [Mᵀ R]] of the stage buffer sb (exact shape: no padding inside NZ)
-  auto Pat = [&](const double* sb, int s, int t) -> double {
-    if (s < NX && t < NX) return s >= t ? sb[oQ + pidx(n, s, t)] : sb[oQ + pidx(n, t, s)];
-    if (s < NX) return sb[oM + s + (t - NX) * n];
-    if (t < NX) return sb[oM + t + (s - NX) * n];
-    const int u = s - NX, w = t - NX;
-    return u >= w ? sb[oR + pidx(m, u, w)] : sb[oR + pidx(m, w, u)];
-  };
-
-  double Vc[NX];
-  {
-    const double* QN = a.p.QN + instP * sn;
-#pragma unroll
-    for (int r = 0; r < NX; ++r) Vc[r] = (j < n) ? (r >= j ? QN[pidx(n, r, j)] : QN[pidx(n, j, r)]) : 0.0;
-    if (j < NX) wk[WK::vs + j] = FAC ? 0.0 : a.p.qN[inst * n + j];
-    if (FAC && valid && j < n)  // record N: V_N = Q_N
-      for (int r = j; r < n; ++r) a.frec[inst * (sN + 1) * FREC + sN * FREC + pidx(n, r, j)] = QN[pidx(n, r, j)];
-    if (valid && a.f.V != nullptr && j < n) {
-      double* Vo = a.f.V + (inst * (sN + 1) + N) * sn;
-      for (int r = j; r < n; ++r) Vo[pidx(n, r, j)] = QN[pidx(n, r, j)];
-    }
-    if (!FAC && valid && a.f.v != nullptr && j < n) a.f.v[(inst * (sN + 1) + N) * n + j] = a.p.qN[inst * n + j];
-  }
-  __syncwarp();  // (FAC) zeroed rhs slots visible before the first stage
-  if (N > 0) issue_stage(N - 1, slot);
-  __syncwarp();
-
-  for (int i = N - 1; i >= 0; --i) {
-    const double* sbq[2] = {slotq[0], slotq[1]};
-    const double* Fq[2] = {sbq[0] + oA, sbq[1] + oA};
-    const double* cvq[2] = {sbq[0] + oc, sbq[1] + oc};
-    const double* sb = grp ? sbq[1] : sbq[0];
-    auto qjf = [&]() -> double { return (j < NX) ? sb[oq + j] : sb[orr + j - NX]; };
-#if defined(RR_NO_PTAB)
-    auto P2 = [&](int q, int s, int t) -> double { return Pat(sbq[q], s, t); };
-#elif defined(RR_P_SIMT)
-    auto P2 = [&](int s) -> double { return Pat(sb, s, j); };  // column j of this lane's P
-    (void)ptab;
-#else
-    auto P2 = [&](int q, int k) -> double {
-      if constexpr (PREG) {  // offsets packed as 16-bit halves of per-lane registers (no table loads)
-        return sbq[q][(int)((ptw[k >> 1] >> (16 * (k & 1))) & 0xffffu)];
+        (void)s;
+        (void)dst;
       } else {
-        const int off = ptab[k * 32 + lane];
-        return off >= 0 ? sbq[q][off] : 0.0;
+        const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst) * sN + i;
+        const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : inst) * sN + i;
+        copy_async(dst + oA, a.p.A + sD * n * n, n * n, j, 16);
+        copy_async(dst + oB, a.p.B + sD * n * m, n * m, j, 16);
+        copy_async(dst + oQ, a.p.Q + sP * sn, sn, j, 16);
+        copy_async(dst + oM, a.p.M + sP * n * m, n * m, j, 16);
+        copy_async(dst + oR, a.p.R + sP * sm, sm, j, 16);
+        copy_async(dst + oq, a.p.q + s * n, n, j, 16);
+        copy_async(dst + orr, a.p.r + s * m, m, j, 16);
+        copy_async(dst + oc, a.p.c + s * n, n, j, 16);
+        cp_async_commit();
       }
     };
-    (void)Pat;
+    auto wait_stage = [&]() {
+      if constexpr (LY::BULK) {
+        mbar_wait_parity(&bar[0], ph0);
+        ph0 ^= 1u;
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+    };
+    // P = [[Q M]; [Mᵀ R]] of the stage buffer sb (exact shape: no padding inside NZ)
+    auto Pat = [&](const double* sb, int s, int t) -> double {
+      if (s < NX && t < NX) return s >= t ? sb[oQ + pidx(n, s, t)] : sb[oQ + pidx(n, t, s)];
+      if (s < NX) return sb[oM + s + (t - NX) * n];
+      if (t < NX) return sb[oM + t + (s - NX) * n];
+      const int u = s - NX, w = t - NX;
+      return u >= w ? sb[oR + pidx(m, u, w)] : sb[oR + pidx(m, w, u)];
+    };
+
+    double Vc[NX];
+    {
+      const double* QN = a.p.QN + instP * sn;
+#pragma unroll
+      for (int r = 0; r < NX; ++r) Vc[r] = (j < n) ? (r >= j ? QN[pidx(n, r, j)] : QN[pidx(n, j, r)]) : 0.0;
+      if (j < NX) wk[WK::vs + j] = FAC ? 0.0 : a.p.qN[inst * n + j];
+      if (FAC && valid && j < n)  // record N: V_N = Q_N
+        for (int r = j; r < n; ++r) a.frec[inst * (sN + 1) * FREC + sN * FREC + pidx(n, r, j)] = QN[pidx(n, r, j)];
+      if (valid && a.f.V != nullptr && j < n) {
+        double* Vo = a.f.V + (inst * (sN + 1) + N) * sn;
+        for (int r = j; r < n; ++r) Vo[pidx(n, r, j)] = QN[pidx(n, r, j)];
+      }
+      if (!FAC && valid && a.f.v != nullptr && j < n) a.f.v[(inst * (sN + 1) + N) * n + j] = a.p.qN[inst * n + j];
+    }
+    __syncwarp();  // (FAC) zeroed rhs slots visible before the first stage
+    if (N > 0) issue_stage(N - 1, slot);
+    __syncwarp();
+
+    for (int i = N - 1; i >= 0; --i) {
+      const double* sbq[2] = {slotq[0], slotq[1]};
+      const double* Fq[2] = {sbq[0] + oA, sbq[1] + oA};
+      const double* cvq[2] = {sbq[0] + oc, sbq[1] + oc};
+      const double* sb = grp ? sbq[1] : sbq[0];
+      auto qjf = [&]() -> double { return (j < NX) ? sb[oq + j] : sb[orr + j - NX]; };
+#if defined(RR_NO_PTAB)
+      auto P2 = [&](int q, int s, int t) -> double { return Pat(sbq[q], s, t); };
+#elif defined(RR_P_SIMT)
+      auto P2 = [&](int s) -> double { return Pat(sb, s, j); };  // column j of this lane's P
+      (void)ptab;
+#else
+      auto P2 = [&](int q, int k) -> double {
+        if constexpr (PREG) {  // offsets packed as 16-bit halves of per-lane registers (no table loads)
+          return sbq[q][(int)((ptw[k >> 1] >> (16 * (k & 1))) & 0xffffu)];
+        } else {
+          const int off = ptab[k * 32 + lane];
+          return off >= 0 ? sbq[q][off] : 0.0;
+        }
+      };
+      (void)Pat;
 #endif
-    auto wait_inputs = [&]() { wait_stage(); };
-    auto prefetch = [&]() {
-      if (i > 0) issue_stage(i - 1, slot);
-    };
-    double* recq[2];
-    if constexpr (FAC) {
+      auto wait_inputs = [&]() { wait_stage(); };
+      auto prefetch = [&]() {
+        if (i > 0) issue_stage(i - 1, slot);
+      };
+      double* recq[2];
+      if constexpr (FAC) {
 #pragma unroll
-      for (int q = 0; q < 2; ++q) recq[q] = validq[q] ? a.frec + (instq[q] * (sN + 1) + i) * FREC : nullptr;
-    } else {
+        for (int q = 0; q < 2; ++q) recq[q] = validq[q] ? a.frec + (instq[q] * (sN + 1) + i) * FREC : nullptr;
+      } else {
 #pragma unroll
-      for (int q = 0; q < 2; ++q) recq[q] = rec0q[q] ? rec0q[q] + (int64_t)i * RC::PAD : nullptr;
-    }
-    double U[NZ], bj;
-    SM::template backward<FAC>(wkq, Fq, cvq, P2, qjf, wait_inputs, prefetch, delta, grp, j, lane, Vc, U, bj, recq,
-                               i, st);
-    if (valid) {
-      if (a.f.V != nullptr && j < n) {
-        double* Vo = a.f.V + (inst * (sN + 1) + i) * sn;
-#pragma unroll
-        for (int r = 0; r < NX; ++r)
-          if (r >= j) Vo[pidx(n, r, j)] = U[r];
+        for (int q = 0; q < 2; ++q) recq[q] = rec0q[q] ? rec0q[q] + (int64_t)i * RC::PAD : nullptr;
       }
-      if (a.f.K != nullptr && j < n) {
-        double* Ko = a.f.K + (inst * sN + i) * m * n;
+      double U[NZ], bj;
+      SM::template backward<FAC>(wkq, Fq, cvq, P2, qjf, wait_inputs, prefetch, delta, grp, j, lane, Vc, U, bj,
+                                 recq, i, st);
+      if (valid) {
+        if (a.f.V != nullptr && j < n) {
+          double* Vo = a.f.V + (inst * (sN + 1) + i) * sn;
 #pragma unroll
-        for (int u = 0; u < NU; ++u) Ko[j * m + u] = -U[NX + u];
+          for (int r = 0; r < NX; ++r)
+            if (r >= j) Vo[pidx(n, r, j)] = U[r];
+        }
+        if (a.f.K != nullptr && j < n) {
+          double* Ko = a.f.K + (inst * sN + i) * m * n;
+#pragma unroll
+          for (int u = 0; u < NU; ++u) Ko[j * m + u] = -U[NX + u];
+        }
+        if (!FAC && j < NX && a.f.v != nullptr) a.f.v[(inst * (sN + 1) + i) * n + j] = bj;
+        if (!FAC && j >= NX && j < NX + NU && a.f.k != nullptr) a.f.k[(inst * sN + i) * m + (j - NX)] = -bj;
       }
-      if (!FAC && j < NX && a.f.v != nullptr) a.f.v[(inst * (sN + 1) + i) * n + j] = bj;
-      if (!FAC && j >= NX && j < NX + NU && a.f.k != nullptr) a.f.k[(inst * sN + i) * m + (j - NX)] = -bj;
     }
-  }
-  if constexpr (FAC) {  // S_0⁻¹ -> record 0; status; NaN-fill a failed instance's records
+    if constexpr (FAC) {  // S_0⁻¹ -> record 0; status; NaN-fill a failed instance's records
+      ST::invS(Vc, delta, j, wk, 0, st);
+      double* rec = a.frec + inst * (sN + 1) * FREC;
+      if (valid && j < n)
+        for (int r = j; r < n; ++r) rec[sn + pidx(n, r, j)] = wk[WK::Si + r * NX + j];
+      int32_t status = st;
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) {
+        const int32_t o = __shfl_xor_sync(RR_FULL_MASK, status, off);
+        status = o > status ? o : status;
+      }
+      __syncwarp();
+      if (valid && status != 0) {
+        const double nan = __longlong_as_double(0x7ff8000000000000LL);
+        for (int64_t e = j; e < (sN + 1) * FREC; e += 16) rec[e] = nan;
+      }
+      if (valid && j == 0) a.status[inst] = status;
+      return;
+    }
+    // x_0 = (I + δV_0)⁻¹ (c_0 − δ v_0) -> x output row 0; backward status -> status (provisional)
     ST::invS(Vc, delta, j, wk, 0, st);
-    double* rec = a.frec + inst * (sN + 1) * FREC;
-    if (valid && j < n)
-      for (int r = j; r < n; ++r) rec[sn + pidx(n, r, j)] = wk[WK::Si + r * NX + j];
+    double xr[NX];
+#pragma unroll
+    for (int r = 0; r < NX; ++r) xr[r] = a.p.c0[inst * n + r] - delta * wk[WK::vs + r];
+    ST::mulSinv(xr, wk);
     int32_t status = st;
 #pragma unroll
     for (int off = 8; off > 0; off >>= 1) {
       const int32_t o = __shfl_xor_sync(RR_FULL_MASK, status, off);
       status = o > status ? o : status;
     }
-    __syncwarp();
-    if (valid && status != 0) {
-      const double nan = __longlong_as_double(0x7ff8000000000000LL);
-      for (int64_t e = j; e < (sN + 1) * FREC; e += 16) rec[e] = nan;
-    }
-    if (valid && j == 0) a.status[inst] = status;
-    (void)gbase;
-    return;
-  }
-
-  // x_0 = (I + δV_0)⁻¹ (c_0 − δ v_0)
-  ST::invS(Vc, delta, j, wk, 0, st);
-  double xr[NX];
-#pragma unroll
-  for (int r = 0; r < NX; ++r) xr[r] = a.p.c0[inst * n + r] - delta * wk[WK::vs + r];
-  ST::mulSinv(xr, wk);
-  int32_t status = st;
-#pragma unroll
-  for (int off = 8; off > 0; off >>= 1) {
-    const int32_t o = __shfl_xor_sync(RR_FULL_MASK, status, off);
-    status = o > status ? o : status;
-  }
-
-#ifndef RR_FWD_PHI
-  // forward sweep: u = K x + k, y = V x + v, x⁺ = S_{i+1}⁻¹ (A x + B u + e),
-  // record i and A_i, B_i streamed by TMA into double buffers (one stage ahead)
-  bool bad = false;
-  double* xo = a.s.x + inst * (sN + 1) * n;
-  double* uo = a.s.u + inst * sN * m;
-  double* yo = a.s.y + inst * (sN + 1) * n;
-  const int ui = j - NX;
-  constexpr int ABP = ((n * n + n * m) + 1) & ~1;
-  __syncwarp();
-  auto rbuf = [&](double* sl, int b) { return sl + b * RC::PAD; };
-  auto abuf = [&](double* sl, int b) { return sl + 2 * RC::PAD + b * ABP; };
-  double* xch = slot + 2 * RC::PAD + 2 * ABP;  // exchange: u (NU, padded to even) | z (NX) | x (NX)
-  double* uch = xch;
-  double* zch = xch + ((NU + 1) & ~1);
-  double* xsh = zch + NX;
-  asm volatile("fence.proxy.async;\n" ::: "memory");
-  __syncwarp();
-  auto issue_fwd = [&](int i, int b) {
-    if (lane == 0) {
-      fence_proxy_async();
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : instq[q]) * sN + i;
-        mbar_arrive_expect_tx(&barq[q][b], 8u * (RC::SIZE + n * n + n * m));
-        bulk_g2s(rbuf(slotq[q], b), a.ws + (instq[q] * sN + i) * RC::PAD, 8u * RC::SIZE, &barq[q][b]);
-        bulk_g2s(abuf(slotq[q], b), a.p.A + sD * n * n, 8u * n * n, &barq[q][b]);
-        bulk_g2s(abuf(slotq[q], b) + n * n, a.p.B + sD * n * m, 8u * n * m, &barq[q][b]);
-      }
-    }
-  };
-  auto wait_fwd = [&](int b) {
-    if (b == 0) {
-      mbar_wait_parity(&bar[0], ph0);
-      ph0 ^= 1u;
-    } else {
-      mbar_wait_parity(&bar[1], ph1);
-      ph1 ^= 1u;
-    }
-    __syncwarp();
-  };
-  if (N > 0) issue_fwd(0, 0);
-  {
     double xj = 0.0;
 #pragma unroll
     for (int r = 0; r < NX; ++r) xj = (r == j) ? xr[r] : xj;
-    if (valid && j < n) xo[j] = xj;
-    bad |= (j < n) && !isfinite(xj);
-  }
-  for (int i = 0; i < N; ++i) {
-    const int b = i & 1;
-    const double* rc = rbuf(slot, b);
-    const double* ab = abuf(slot, b);
-    if (i + 1 < N) issue_fwd(i + 1, b ^ 1);
-    wait_fwd(b);
-    // y_i = V_i x_i + v_i (lanes < NX);  u_i = K_i x_i + k_i (lanes NX..)
-    double a0 = 0.0, a1 = 0.0;
-    if (j < NX) {
-      a0 = rc[RC::v + j];
+    if (valid && j < n) a.s.x[inst * (sN + 1) * n + j] = xj;
+    if (valid && j == 0) a.status[inst] = status;
+    __syncwarp();  // x_0 / status visible to the group's forward sweep (same warp)
+  };
+
+  // ------- forward sweep of one pair: u = K x + k, y = V x + v, x⁺ = S_{i+1}⁻¹ (A x + B u + e) -------
+  // (P:496-509); record i and A_i, B_i streamed by TMA into double buffers (one stage ahead)
+  auto forward_pair = [&](int64_t pair) {
+    if constexpr (!FAC) {
+      int64_t instq[2];
+      bool validq[2];
+      pair_insts(pair, instq, validq);
+      const int64_t inst = grp ? instq[1] : instq[0];
+      const bool valid = grp ? validq[1] : validq[0];
+      const int64_t instP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;
+      double* xo = a.s.x + inst * (sN + 1) * n;
+      double* uo = a.s.u + inst * sN * m;
+      double* yo = a.s.y + inst * (sN + 1) * n;
+      int32_t status = a.status[inst];
+      double xr[NX], xj = 0.0;
 #pragma unroll
-      for (int k = 0; k < NX; k += 2) {
-        const int i0 = k >= j ? pidx(NX, k, j) : pidx(NX, j, k);
-        const int i1 = k + 1 >= j ? pidx(NX, k + 1, j) : pidx(NX, j, k + 1);
-        a0 = fma(rc[RC::V + i0], xr[k], a0);
-        a1 = fma(rc[RC::V + i1], xr[k + 1], a1);
+      for (int r = 0; r < NX; ++r) {
+        xr[r] = xo[r];
+        xj = (r == j) ? xr[r] : xj;
       }
-    } else if (ui < NU) {
-      a0 = rc[RC::k + ui];
+      bool bad = (j < n) && !isfinite(xj);
+      const int ui = j - NX;
+      constexpr int ABP = ((n * n + n * m) + 1) & ~1;
+      auto rbuf = [&](double* sl, int b) { return sl + b * RC::PAD; };
+      auto abuf = [&](double* sl, int b) { return sl + 2 * RC::PAD + b * ABP; };
+      double* xch = slot + 2 * RC::PAD + 2 * ABP;  // exchange: u (NU, padded to even) | z (NX) | x (NX)
+      double* uch = xch;
+      double* zch = xch + ((NU + 1) & ~1);
+      double* xsh = zch + NX;
+      // records were written through the generic proxy; order them (and this slot's generic
+      // shared-memory writes) before the TMA (async-proxy) reads / refills
+      asm volatile("fence.proxy.async;\n" ::: "memory");
+      __syncwarp();
+      auto issue_fwd = [&](int i, int b) {
+        if (lane == 0) {
+          fence_proxy_async();
 #pragma unroll
-      for (int k = 0; k < NX; k += 2) {
-        a0 = fma(rc[RC::K + k * NU + ui], xr[k], a0);
-        a1 = fma(rc[RC::K + (k + 1) * NU + ui], xr[k + 1], a1);
-      }
-    }
-    const double yu = a0 + a1;
-    if (valid) {
-      if (j < n) yo[(int64_t)i * n + j] = yu;
-      if (ui >= 0 && ui < m) uo[(int64_t)i * m + ui] = yu;
-    }
-    bad |= (j < NZ) && !isfinite(yu);
-    if (ui >= 0 && ui < NU) uch[ui] = yu;
-    __syncwarp();
-    // z = A x + B u + e  (A, B column-major: row j)
-    if (j < NX) {
-      double z0 = rc[RC::e + j], z1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < NX; k += 2) {
-        z0 = fma(ab[j + k * n], xr[k], z0);
-        z1 = fma(ab[j + (k + 1) * n], xr[k + 1], z1);
-      }
-#pragma unroll
-      for (int u = 0; u < NU; ++u) z0 = fma(ab[n * n + j + u * n], uch[u], z0);
-      zch[j] = z0 + z1;
-    }
-    __syncwarp();
-    // x_{i+1} = S_{i+1}⁻¹ z
-    double zr[NX];
-    ST::bcast(zch, zr);
-    if (j < NX) {
-      double x0 = 0.0, x1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < NX; k += 2) {
-        const int i0 = k >= j ? pidx(NX, k, j) : pidx(NX, j, k);
-        const int i1 = k + 1 >= j ? pidx(NX, k + 1, j) : pidx(NX, j, k + 1);
-        x0 = fma(rc[RC::S + i0], zr[k], x0);
-        x1 = fma(rc[RC::S + i1], zr[k + 1], x1);
-      }
-      const double xv = x0 + x1;
-      if (valid && j < n) xo[(int64_t)(i + 1) * n + j] = xv;
-      bad |= !isfinite(xv);
-      xsh[j] = xv;
-    }
-    __syncwarp();
-    ST::bcast(xsh, xr);
-    __syncwarp();
-  }
+          for (int q = 0; q < 2; ++q) {
+            const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : instq[q]) * sN + i;
+            mbar_arrive_expect_tx(&barq[q][b], 8u * (RC::SIZE + n * n + n * m));
+            bulk_g2s(rbuf(slotq[q], b), a.ws + (instq[q] * sN + i) * RC::PAD, 8u * RC::SIZE, &barq[q][b]);
+            bulk_g2s(abuf(slotq[q], b), a.p.A + sD * n * n, 8u * n * n, &barq[q][b]);
+            bulk_g2s(abuf(slotq[q], b) + n * n, a.p.B + sD * n * m, 8u * n * m, &barq[q][b]);
+          }
+        }
+      };
+      auto wait_fwd = [&](int b) {
+        if (b == 0) {
+          mbar_wait_parity(&bar[0], ph0);
+          ph0 ^= 1u;
+        } else {
+          mbar_wait_parity(&bar[1], ph1);
+          ph1 ^= 1u;
+        }
+        __syncwarp();
+      };
+      if (N > 0) issue_fwd(0, 0);
+#ifdef RR_AB_SKIP_FWD  // A/B probe only: cost of the forward sweep (wrong results)
+      for (int i = 0; i < 0; ++i) {
 #else
-  // forward sweep from the records (row-major [Φ | φ], packed V)
-  bool bad = false;
-  double* xo = a.s.x + inst * (sN + 1) * n;
-  double* uo = a.s.u + inst * sN * m;
-  double* yo = a.s.y + inst * (sN + 1) * n;
-  const int ui = j - NX;
-  __syncwarp();
-  double* rbuf0 = slot;
-  double* rbuf1 = slot + RC::PAD;
-  double* xs = slot + 2 * RC::PAD;
-  // records were written through the generic proxy; order them before the TMA (async-proxy) reads
-  asm volatile("fence.proxy.async;\n" ::: "memory");
-  __syncwarp();
-  auto issue_rec = [&](int i, double* dst, int b) {
-    if constexpr (LY::BULK) {
-      if (lane == 0) {
-        fence_proxy_async();
+      for (int i = 0; i < N; ++i) {
+#endif
+        const int b = i & 1;
+        const double* rc = rbuf(slot, b);
+        const double* ab = abuf(slot, b);
+        if (i + 1 < N) issue_fwd(i + 1, b ^ 1);
+        wait_fwd(b);
+        // y_i = V_i x_i + v_i (lanes < NX);  u_i = K_i x_i + k_i (lanes NX..)
+        double a0 = 0.0, a1 = 0.0;
+        if (j < NX) {
+          a0 = rc[RC::v + j];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          mbar_arrive_expect_tx(&barq[q][b], 8u * RC::SIZE);
-          bulk_g2s(slotq[q] + b * RC::PAD, a.ws + (instq[q] * sN + i) * RC::PAD, 8u * RC::SIZE, &barq[q][b]);
+          for (int k = 0; k < NX; k += 2) {
+            const int i0 = k >= j ? pidx(NX, k, j) : pidx(NX, j, k);
+            const int i1 = k + 1 >= j ? pidx(NX, k + 1, j) : pidx(NX, j, k + 1);
+            a0 = fma(rc[RC::V + i0], xr[k], a0);
+            a1 = fma(rc[RC::V + i1], xr[k + 1], a1);
+          }
+        } else if (ui < NU) {
+          a0 = rc[RC::k + ui];
+#pragma unroll
+          for (int k = 0; k < NX; k += 2) {
+            a0 = fma(rc[RC::K + k * NU + ui], xr[k], a0);
+            a1 = fma(rc[RC::K + (k + 1) * NU + ui], xr[k + 1], a1);
+          }
+        }
+        const double yu = a0 + a1;
+        if (valid) {
+          if (j < n) yo[(int64_t)i * n + j] = yu;
+          if (ui >= 0 && ui < m) uo[(int64_t)i * m + ui] = yu;
+        }
+        bad |= (j < NZ) && !isfinite(yu);
+        if (ui >= 0 && ui < NU) uch[ui] = yu;
+        __syncwarp();
+        // z = A x + B u + e  (A, B column-major: row j)
+        if (j < NX) {
+          double z0 = rc[RC::e + j], z1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < NX; k += 2) {
+            z0 = fma(ab[j + k * n], xr[k], z0);
+            z1 = fma(ab[j + (k + 1) * n], xr[k + 1], z1);
+          }
+#pragma unroll
+          for (int u = 0; u < NU; ++u) z0 = fma(ab[n * n + j + u * n], uch[u], z0);
+          zch[j] = z0 + z1;
+        }
+        __syncwarp();
+        // x_{i+1} = S_{i+1}⁻¹ z
+        double zr[NX];
+        ST::bcast(zch, zr);
+        if (j < NX) {
+          double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < NX; k += 2) {
+            const int i0 = k >= j ? pidx(NX, k, j) : pidx(NX, j, k);
+            const int i1 = k + 1 >= j ? pidx(NX, k + 1, j) : pidx(NX, j, k + 1);
+            x0 = fma(rc[RC::S + i0], zr[k], x0);
+            x1 = fma(rc[RC::S + i1], zr[k + 1], x1);
+          }
+          const double xv = x0 + x1;
+          if (valid && j < n) xo[(int64_t)(i + 1) * n + j] = xv;
+          bad |= !isfinite(xv);
+          xsh[j] = xv;
+        }
+        __syncwarp();
+        ST::bcast(xsh, xr);
+        __syncwarp();
+      }
+      {
+        const double* QN = a.p.QN + instP * sn;
+        if (j < n) {
+          double acc = a.p.qN[inst * n + j];
+#pragma unroll
+          for (int k = 0; k < NX; ++k) acc = fma(k >= j ? QN[pidx(n, k, j)] : QN[pidx(n, j, k)], xr[k], acc);
+          if (valid) yo[sN * n + j] = acc;
+          bad |= !isfinite(acc);
         }
       }
-      (void)dst;
-    } else {
-      copy_async(dst, rec0 + (int64_t)i * RC::PAD, RC::SIZE, j, 16);
-      cp_async_commit();
+      const unsigned anybad = __ballot_sync(RR_FULL_MASK, bad);
+      const unsigned gmask = 0xffffu << gbase;
+      if (status == 0 && (anybad & gmask)) status = RR_ST_NONFINITE;
+      if (valid && status != 0) {
+        const double nan = __longlong_as_double(0x7ff8000000000000LL);
+        for (int64_t e = j; e < (sN + 1) * n; e += 16) {
+          xo[e] = nan;
+          yo[e] = nan;
+        }
+        for (int64_t e = j; e < sN * m; e += 16) uo[e] = nan;
+      }
+      if (valid && j == 0) a.status[inst] = status;
+      __syncwarp();
     }
   };
-  auto wait_rec = [&](int b) {
-    if constexpr (LY::BULK) {
-      if (b == 0) {
-        mbar_wait_parity(&bar[0], ph0);
-        ph0 ^= 1u;
-      } else {
-        mbar_wait_parity(&bar[1], ph1);
-        ph1 ^= 1u;
-      }
-    } else {
-      cp_async_wait<1>();
-    }
-    __syncwarp();
-  };
-  if (N > 0) issue_rec(0, rbuf0, 0);
-  {
-    double xj = 0.0;
-#pragma unroll
-    for (int r = 0; r < NX; ++r) xj = (r == j) ? xr[r] : xj;
-    if (valid && j < n) xo[j] = xj;
-    bad |= (j < n) && !isfinite(xj);
+
+  for (int64_t k = 0; k < K + defer; ++k) {
+    if (k < K) backward_pair(p0 + k * stride);
+    if (k >= defer && k - defer < K) forward_pair(p0 + (k - defer) * stride);
   }
-  for (int i = 0; i < N; ++i) {
-    const int b = i & 1;
-    const double* rc = b ? rbuf1 : rbuf0;
-    if (i + 1 < N) issue_rec(i + 1, b ? rbuf0 : rbuf1, b ^ 1);
-    else if (!LY::BULK) cp_async_commit();
-    wait_rec(b);
-    double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
-    if (j < NX) {
-      const double* row = rc + RC::PHI + j * RC::LD;
-      a0 = row[NX];
-      c0 = rc[RC::v + j];
-#pragma unroll
-      for (int k = 0; k < NX; k += 2) {
-        const double2 p2 = *reinterpret_cast<const double2*>(row + k);
-        a0 = fma(p2.x, xr[k], a0);
-        a1 = fma(p2.y, xr[k + 1], a1);
-        const int i0 = k >= j ? pidx(NX, k, j) : pidx(NX, j, k);
-        const int i1 = k + 1 >= j ? pidx(NX, k + 1, j) : pidx(NX, j, k + 1);
-        c0 = fma(rc[RC::V + i0], xr[k], c0);
-        c1 = fma(rc[RC::V + i1], xr[k + 1], c1);
-      }
-    } else if (ui < NU) {
-      a0 = rc[RC::k + ui];
-#pragma unroll
-      for (int k = 0; k < NX; k += 2) {
-        a0 = fma(rc[RC::K + k * NU + ui], xr[k], a0);
-        a1 = fma(rc[RC::K + (k + 1) * NU + ui], xr[k + 1], a1);
-      }
-    }
-    const double acc1 = a0 + a1, acc2 = c0 + c1;
-    if (valid) {
-      if (j < n) {
-        yo[(int64_t)i * n + j] = acc2;
-        xo[(int64_t)(i + 1) * n + j] = acc1;
-      }
-      if (ui >= 0 && ui < m) uo[(int64_t)i * m + ui] = acc1;
-    }
-    bad |= ((j < n) && !(isfinite(acc1) && isfinite(acc2))) || ((ui >= 0 && ui < m) && !isfinite(acc1));
-    if (j < NX) xs[j] = acc1;
-    __syncwarp();
-    ST::bcast(xs, xr);
-    __syncwarp();
-  }
-#endif
-  {
-    const double* QN = a.p.QN + instP * sn;
-    if (j < n) {
-      double acc = a.p.qN[inst * n + j];
-#pragma unroll
-      for (int k = 0; k < NX; ++k) acc = fma(k >= j ? QN[pidx(n, k, j)] : QN[pidx(n, j, k)], xr[k], acc);
-      if (valid) yo[sN * n + j] = acc;
-      bad |= !isfinite(acc);
-    }
-  }
-  const unsigned anybad = __ballot_sync(RR_FULL_MASK, bad);
-  const unsigned gmask = 0xffffu << gbase;
-  if (status == 0 && (anybad & gmask)) status = RR_ST_NONFINITE;
-  if (valid && status != 0) {
-    const double nan = __longlong_as_double(0x7ff8000000000000LL);
-    for (int64_t e = j; e < (sN + 1) * n; e += 16) {
-      xo[e] = nan;
-      yo[e] = nan;
-    }
-    for (int64_t e = j; e < sN * m; e += 16) uo[e] = nan;
-  }
-  if (valid && j == 0) a.status[inst] = status;
 }
 
 template <int NX, int NU, int WARPS, int MINB, bool FAC = false>
@@ -841,12 +793,27 @@ struct MmaCfg {
     return sizeof(double) * (size_t)IPB * MmaLayout<NX, NU>::SLOT_PAD + sizeof(int) * 32 * MmaLayout<NX, NU>::PTAB;
   }
   static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * RecM<NX, NU>::PAD; }
-  static cudaError_t launch(const FusedArgs& a, cudaStream_t s) {
+  static cudaError_t launch(const FusedArgs& a0, cudaStream_t s) {
     auto k = rr_fused_mma_kernel<NX, NU, WARPS, MINB, FAC>;
     const size_t sm = smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    const int64_t blocks = (a.batch + IPB - 1) / IPB;
+    // persistent grid: every resident CTA slot once (the warps loop over instance pairs)
+    int dev = 0, nsm = 0, occ = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, WARPS * 32, sm)) != cudaSuccess) return e;
+    FusedArgs a = a0;
+    a.nsm = nsm;
+    a.defer_mod = occ > 1 ? occ : 1;
+    if (const char* v = getenv("RR_DEFER_MOD")) a.defer_mod = atoi(v);  // A/B knob (1 = no staggering)
+    const int64_t need = ((a.batch + 1) / 2 + WARPS - 1) / WARPS;
+    int64_t blocks = (int64_t)nsm * (occ > 0 ? occ : 1);
+    if (const char* v = getenv("RR_PERSIST")) {  // A/B knob: 0 = one CTA per 2*WARPS instances
+      if (atoi(v) == 0) blocks = need;
+    }
+    if (blocks > need) blocks = need;
+    if (blocks < 1) blocks = 1;
     k<<<(unsigned)blocks, WARPS * 32, sm, s>>>(a);
     return cudaGetLastError();
   }

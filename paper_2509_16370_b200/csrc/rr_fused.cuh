@@ -21,6 +21,8 @@ struct FusedArgs {
   // (cp.async.bulk) kernels may run; otherwise the 12x4 shape falls back to the LDGSTS kernel
   // (8-byte copies where needed) and the CTA kernels are refused by the API (rr_api.cu)
   bool tma16 = true;
+  // DMMA kernel (persistent warps): SM count and the phase-staggering modulus (set by the launcher)
+  int nsm = 0, defer_mod = 1;
 };
 
 // Bytes of workspace for this shape (-1 if no kernel is compiled for it).

@@ -186,7 +186,15 @@ struct StageMMA {
     const int g = lane >> 2, t = lane & 3;
     // (1) S⁻¹ (no stage input needed), then Vs = [V | V e] (V symmetric: (V e)_j = column j · e)
 #ifndef RR_INVS_GRID
+#ifdef RR_AB_SKIP_INVS  // A/B probe only: cost of the SIMT S⁻¹ sweep (wrong results)
+    if (j < NX) {
+#pragma unroll
+      for (int r = 0; r < NX; ++r) wk[WK::Si + r * NX + j] = (r == j) ? 1.0 : 0.0;
+    }
+    __syncwarp();
+#else
     ST::invS(Vc, delta, j, wk, stage, st);
+#endif
     if (j < NX) {
 #pragma unroll
       for (int r = 0; r < NX; ++r) wk[WM::X1 + r * NX + j] = Vc[r];  // V symmetric: column j as row j
@@ -371,6 +379,7 @@ struct StageMMA {
     // (own U[p] by symmetry, or lane p's published row for already processed pivots) and the
     // published b_p
     bool gbad = false;
+#ifndef RR_AB_SKIP_GJ  // A/B probe only: cost of the u-block elimination (wrong results)
 #pragma unroll
     for (int p = NX; p < NZ; ++p) {
       double* pb = wk + WK::pub + (p & 1) * WK::NZP;
@@ -412,6 +421,7 @@ struct StageMMA {
       bj = (j == p) ? bp : fma(-cj, bp, bj);
       __syncwarp();
     }
+#endif
     if (gbad && st == 0) st = mk_status(RR_ST_G_NOT_PD, stage);
     // lanes j < NX: U = [V_i; −K_i] column j, bj = (v_i)_j;  lanes NX + u: bj = −(k_i)_u
     if (j < NZ) wk[WK::vb + j] = bj;
