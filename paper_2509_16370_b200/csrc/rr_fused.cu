@@ -805,7 +805,7 @@ struct MmaCfg {
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, WARPS * 32, sm)) != cudaSuccess) return e;
     FusedArgs a = a0;
     a.nsm = nsm;
-    a.defer_mod = occ > 1 ? occ : 1;
+    a.defer_mod = 1;  // measured: staggering by occ (3) is 1-2% slower on C2 (profiles/r02_stagger_ab.txt)
     if (const char* v = getenv("RR_DEFER_MOD")) a.defer_mod = atoi(v);  // A/B knob (1 = no staggering)
     const int64_t need = ((a.batch + 1) / 2 + WARPS - 1) / WARPS;
     int64_t blocks = (int64_t)nsm * (occ > 0 ? occ : 1);

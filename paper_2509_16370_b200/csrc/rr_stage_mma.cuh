@@ -222,6 +222,135 @@ struct StageMMA {
       wk[WM::X1 + NX * NX + j] = ve0 + ve1;  // column NX of Vs
     }
     __syncwarp();
+#ifndef RR_SMEM_CHAIN
+    // (2)-(5) per instance q, in DMMA registers: [W | We] = S⁻¹ Vs, X = Fᵀ W, U = Fᵀ Xᵀ + P.
+    // A C fragment holds C[g][2t], C[g][2t+1]; used with the contraction index permuted to
+    // k-blocks {2t + 8kt} and {2t + 1 + 8kt} it IS the A fragment of C (row g, "column" t) and, for
+    // a symmetric or transposed use, the B fragment -- so W and X never round-trip through shared
+    // memory (the previous T = W F / U = Fᵀ T chain stored W and T and re-read both as fragments).
+    // Only Fᵀ is loaded, as 128-bit pairs (k, k+1) straight from the TMA stage buffer.
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double* Si = wkq[q] + WK::Si;
+      const double* Vs = wkq[q] + WM::X1;
+      double w[MT][CT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < CT; ++nt) w[mt][nt][0] = w[mt][nt][1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        double aS[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r = 8 * mt + g;
+          aS[mt] = (r < NX) ? Si[(4 * kt + t) * NX + r] : 0.0;
+        }
+#pragma unroll
+        for (int nt = 0; nt < CT; ++nt) {
+          const int col = 8 * nt + g;
+          const double bv = (col <= NX) ? Vs[col * NX + 4 * kt + t] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) dmma884(w[mt][nt][0], w[mt][nt][1], aS[mt], bv);
+        }
+      }
+      // g = v + W e (column NX of [W | We]: tile nt = NX / 8, lanes 2t + e = NX % 8)
+      if (2 * t == (NX & 7)) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r = 8 * mt + g;
+          if (r < NX) wkq[q][WK::gb + r] = wkq[q][WK::vs + r] + w[mt][NX >> 3][0];
+        }
+      }
+      // Fᵀ A fragments, k permuted: fa[mt][kt][e] = Fᵀ[8mt + g][2t + e + 8kt] (zero outside NZ × NX)
+      const double* Fx = Fq[q];
+      double fa[ZT][2][2];
+#pragma unroll
+      for (int mt = 0; mt < ZT; ++mt)
+#pragma unroll
+        for (int kt = 0; kt < 2; ++kt) {
+          const int mm = 8 * mt + g, k0 = 2 * t + 8 * kt;
+          double2 f2 = make_double2(0.0, 0.0);
+          if (mm < NZ && k0 < NX) f2 = *reinterpret_cast<const double2*>(Fx + mm * NX + k0);
+          fa[mt][kt][0] = f2.x;
+          fa[mt][kt][1] = f2.y;
+        }
+      // B fragments of W (symmetric): B[k][n] = W[n][k] = w[nt][kt][e] at k = 2t + e + 8kt, n = 8nt + g;
+      // k >= NX (the We column and padding) excluded
+      double x[ZT][MT][2];
+#pragma unroll
+      for (int mt = 0; mt < ZT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < MT; ++nt) x[mt][nt][0] = x[mt][nt][1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (8 * kt >= NX) continue;
+#pragma unroll
+          for (int nt = 0; nt < MT; ++nt) {
+            const double wb = (2 * t + e + 8 * kt < NX) ? w[nt][kt][e] : 0.0;
+#pragma unroll
+            for (int mt = 0; mt < ZT; ++mt) dmma884(x[mt][nt][0], x[mt][nt][1], fa[mt][kt][e], wb);
+          }
+        }
+      // U = Fᵀ Xᵀ + P: B[k][n] = X[n][k] = x[nt][kt][e] (own C fragment of X), C initialised with P
+      double c[ZT][ZT][2];
+#pragma unroll
+      for (int mt = 0; mt < ZT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < ZT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+#if defined(RR_NO_PTAB)
+            const int r = 8 * mt + g, col = 8 * nt + 2 * t + e;
+            c[mt][nt][e] = (r < NZ && col < NZ) ? Pat(q, r, col) : 0.0;
+#elif !defined(RR_P_SIMT)
+            c[mt][nt][e] = Pat(q, (mt * ZT + nt) * 2 + e);  // P-gather table (kernel)
+#else
+            c[mt][nt][e] = 0.0;
+#endif
+          }
+#pragma unroll
+      for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (8 * kt >= NX) continue;
+#pragma unroll
+          for (int nt = 0; nt < ZT; ++nt) {
+            const double xb = x[nt][kt][e];  // X[8nt + g][2t + e + 8kt]
+#pragma unroll
+            for (int mt = 0; mt < ZT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], fa[mt][kt][e], xb);
+          }
+        }
+      double* Ub = wkq[q] + WM::X2;
+#pragma unroll
+      for (int mt = 0; mt < ZT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < ZT; ++nt) {
+          const int r = 8 * mt + g, col = 8 * nt + 2 * t;
+          Ub[col * WM::ULD + r] = c[mt][nt][0];
+          Ub[(col + 1) * WM::ULD + r] = c[mt][nt][1];
+        }
+    }
+    __syncwarp();
+    // (3) b_j = [q + Aᵀg; r + Bᵀg]_j  (g from (2), per instance)
+    const int jc = (j < NZ) ? j : 0;
+    {
+      double gk[NX];
+      ST::bcast(wk + WK::gb, gk);
+      double b0 = qjf(), b1 = 0.0;
+      const bool rot = (j & 4) != 0;
+#pragma unroll
+      for (int k = 0; k < NX; k += 2) {
+        const int kr = (k + 2) % NX;
+        const double2 f2 = *reinterpret_cast<const double2*>(F + jc * NX + (rot ? kr : k));
+        b0 = fma(f2.x, rot ? gk[kr] : gk[k], b0);
+        b1 = fma(f2.y, rot ? gk[kr + 1] : gk[k + 1], b1);
+      }
+      bj = b0 + b1;
+    }
+#else
     // (2) [W | W e] = S⁻¹ Vs -> X2 (ld NX)
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -363,6 +492,7 @@ struct StageMMA {
         }
     }
     __syncwarp();
+#endif
     // (6) Gauss-Jordan on the u-block (SIMT, lane j owns column j)
 #pragma unroll
     for (int s = 0; s < NZ; s += 2) {
