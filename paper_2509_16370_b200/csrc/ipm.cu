@@ -595,19 +595,6 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
         sK2 += 0.5 * eta * cd * cd;
       }
     }
-    if (model != IPM_MODEL_LQ && j == 0) {
-      // dynamics terms at α = 0 through the model (as the oracle's merit does)
-      double xnm[NX];
-      model_step<NX, NU>(model, a.d_.model_params, sb + IB::xb, sb + IB::ub, xnm);
-      const double* xb1 = a.it.x + (inst * (sN + 1) + i + 1) * n;
-#pragma unroll
-      for (int r = 0; r < NX; ++r) {
-        if (r < n) {
-          const double cr = xnm[r] - xb1[r];
-          sDyn0 += sb[IB::yn + r] * cr + 0.5 * eta * cr * cr;
-        }
-      }
-    }
 #pragma unroll
     for (int r = 0; r < NX; ++r) xr[r] = xn[r];
     __syncwarp();
@@ -645,6 +632,28 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
     for (int off = LG / 2; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(gmask, v, off));
     return v;
   };
+  // dynamics terms of 𝒜 at α = 0 through the built-in model (as the oracle's merit evaluates them),
+  // stages distributed over the lanes of the group (one model evaluation per lane per LG stages)
+  if (model != IPM_MODEL_LQ) {
+    for (int i = j; i < N; i += LG) {
+      const double* xb = a.it.x + (inst * (sN + 1) + i) * n;
+      const double* ub = a.it.u + (inst * sN + i) * m;
+      const double* yb = a.it.y + (inst * (sN + 1) + i + 1) * n;
+      double xa[NX], ua[NU], xnm[NX];
+#pragma unroll
+      for (int r = 0; r < NX; ++r) xa[r] = (r < n) ? xb[r] : 0.0;
+#pragma unroll
+      for (int r = 0; r < NU; ++r) ua[r] = (r < m) ? ub[r] : 0.0;
+      model_step<NX, NU>(model, a.d_.model_params, xa, ua, xnm);
+#pragma unroll
+      for (int r = 0; r < NX; ++r) {
+        if (r < n) {
+          const double cr = xnm[r] - xb[n + r];
+          sDyn0 += yb[r] * cr + 0.5 * eta * cr * cr;
+        }
+      }
+    }
+  }
   const double D = gsum(sD);
   const double K0 = gsum(sK0) + a.d_.fval[inst];
   const double K1 = gsum(sK1), K2 = gsum(sK2);
