@@ -368,7 +368,8 @@ rr_err ipm_update(const ipm_dims* dims, const ipm_iterate* it, const ipm_result*
  *   RR_ST_MAXITER if k == max_iters;
  *   μ <- max(mu_min, min(kappa_mu μ, μ^theta_mu)) if max(r_stat, r_feas, r_comp) <= kappa μ;
  *   η <- min(eta_max, kappa_eta η) if k >= 5, r_feas > tol_kkt and r_feas > 0.9 r_feas(k−5);
- *   one ipm_step (rows a1-a8) with (μ, η, δ = 1/η); a failed step ends the instance with its status.
+ *   one ipm_step (rows a1-a8) with (μ, η, δ = 1/η); a failed step ends the instance with its status
+ *     (settings->linear_merit: the step's trial merits use the linearised dynamics, reading R22).
  * Converged instances are masked out of later iterations (no host synchronisation: the step
  * kernel runs over a device-built list of running instances).
  * it: the iterate, updated in place (it->mu / it->eta are the initial values and are NOT written:
@@ -384,7 +385,10 @@ typedef struct {
   double kappa_eta;   /* 10    */
   double tol_kkt;     /* 1e-6  */
   int32_t max_iters;  /* 100   */
-  int32_t pad;
+  int32_t linear_merit; /* 0: each step's trial merits through the model (ipm_step as is); 1: through
+                           the linearisation at the iterate, i.e. the step's line search runs with
+                           IPM_MODEL_LQ on the re-evaluated Jacobians (SQP-style globalisation of the
+                           outer loop; reading R22 -- converges the C4 swing-up)        */
   ipm_params step;    /* line search of each step (tau, armijo_c, beta, max_backtracks) */
 } ipm_solve_settings;
 

@@ -15,7 +15,8 @@ SPEC's ipm_solve / update_parameters and DESIGN.md reading R21:
     3. converged  if max(r_stat, r_feas, r_comp0) <= tol_kkt and μ <= 10 mu_min
     4. μ update   if max(r_stat, r_feas, r_comp) <= kappa μ:  μ <- max(mu_min, min(kappa_mu μ, μ^theta_mu))
     5. η update   if k >= 5 and r_feas > tol_kkt and r_feas > 0.9 r_feas(k-5):  η <- min(eta_max, kappa_eta η)
-    6. one IPM step at (data(x_k), μ, η); a line-search failure ends the instance (status 5)
+    6. one IPM step at (data(x_k), μ, η); a line-search failure ends the instance (status 5);
+     with settings.linear_merit the step's trial merits use the linearised dynamics (reading R22)
   instances still running after max_iters end with status MAXITER (6).
 """
 from __future__ import annotations
@@ -45,6 +46,7 @@ class SolveSettings:
     armijo_c: float = 1e-4
     beta: float = 0.5
     max_backtracks: int = 50
+    linear_merit: bool = False   # reading R22: the step's trial merits on the linearised dynamics
 
 
 def _unpack(P, n):
@@ -152,7 +154,7 @@ def residuals(ref, d, it, mu):
 def ipm_solve_oracle(batch, settings: SolveSettings = SolveSettings(), nthreads=8, record=False):
     """Solve every instance of `batch` (an IPMBatch, CPU) from its iterate.  Returns
     (final iterate dict, report dict: status, iters, mu, eta, r_stat, r_feas, r_comp0 [+ history])."""
-    from synth.ipm_workloads import IPMBatch
+    from synth.ipm_workloads import IPMBatch, MODEL_LQ
     ref = batch
     it = {k: v.detach().cpu().numpy().astype(np.float64).copy() for k, v in batch.it.items()}
     b = batch.batch
@@ -183,7 +185,10 @@ def ipm_solve_oracle(batch, settings: SolveSettings = SolveSettings(), nthreads=
         it["eta"] = np.where(stag, np.minimum(S.eta_max, S.kappa_eta * it["eta"]), it["eta"])
         hist[:, k % 5] = np.where(act, rf, hist[:, k % 5])
         idx = np.nonzero(act)[0]
-        cur = IPMBatch(ref.nx, ref.nu, ref.N, ref.ng, ref.ngN, ref.nc, ref.ncN, ref.model,
+        # reading R22: with linear_merit the step's line search evaluates 𝒜 at the trial
+        # points through the linearisation at the iterate (the LQ merit on the re-evaluated data)
+        cur = IPMBatch(ref.nx, ref.nu, ref.N, ref.ng, ref.ngN, ref.nc, ref.ncN,
+                       MODEL_LQ if S.linear_merit else ref.model,
                        {kk: torch.as_tensor(v[idx] if kk != "model_params" else v) for kk, v in d.items()},
                        {kk: torch.as_tensor(v[idx]) for kk, v in it.items()})
         res, it2 = ipm_step_oracle(cur, tau=S.tau, armijo_c=S.armijo_c, beta=S.beta,

@@ -69,7 +69,7 @@ class ipm_params(ctypes.Structure):
 class ipm_solve_settings(ctypes.Structure):
     _fields_ = [(f, ctypes.c_double) for f in ("mu_min", "kappa", "kappa_mu", "theta_mu", "eta_max", "kappa_eta",
                                                "tol_kkt")] + \
-               [("max_iters", ctypes.c_int32), ("pad", ctypes.c_int32), ("step", ipm_params)]
+               [("max_iters", ctypes.c_int32), ("linear_merit", ctypes.c_int32), ("step", ipm_params)]
 
 
 class ipm_solve_report(ctypes.Structure):

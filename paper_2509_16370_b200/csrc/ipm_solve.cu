@@ -465,6 +465,7 @@ cudaError_t ipm_solve_launch(const ipm_dims& d, const ipm_stage_data& data, cons
   cit.eta = w.eta;
   IpmArgs a;
   a.d = d;
+  if (S.linear_merit) a.d.model = IPM_MODEL_LQ;  // trial merits on the linearisation (reading R22)
   a.d_ = cur;
   a.it = cit;
   a.prm = S.step;

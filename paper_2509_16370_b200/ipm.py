@@ -119,7 +119,8 @@ def ipm_step(b, tau=0.995, armijo_c=1e-4, beta=0.5, max_backtracks=50, stream=No
 
 
 SOLVE_DEFAULTS = dict(mu_min=1e-9, kappa=10.0, kappa_mu=0.2, theta_mu=1.5, eta_max=1e8, kappa_eta=10.0,
-                      tol_kkt=1e-6, max_iters=100, tau=0.995, armijo_c=1e-4, beta=0.5, max_backtracks=50)
+                      tol_kkt=1e-6, max_iters=100, tau=0.995, armijo_c=1e-4, beta=0.5, max_backtracks=50,
+                      linear_merit=False)
 REPORT_FIELDS = ("status", "iters", "mu", "eta", "r_stat", "r_feas", "r_comp")
 
 
@@ -141,7 +142,7 @@ class IpmSolveCall:
         self.data = ipm_stage_data(*[_p(b.data[f], f) for f in IPM_DATA_FIELDS])
         self.it = ipm_iterate(*[_p(b.it[f], f) for f in IPM_ITER_FIELDS])
         self.S = ipm_solve_settings(S["mu_min"], S["kappa"], S["kappa_mu"], S["theta_mu"], S["eta_max"],
-                                    S["kappa_eta"], S["tol_kkt"], int(S["max_iters"]), 0,
+                                    S["kappa_eta"], S["tol_kkt"], int(S["max_iters"]), int(bool(S["linear_merit"])),
                                     ipm_params(S["tau"], S["armijo_c"], S["beta"], int(S["max_backtracks"]), 0))
         self.rep = {k: torch.empty(b.batch, dtype=torch.int32 if k in ("status", "iters") else torch.float64, device=dev)
                     for k in REPORT_FIELDS}

@@ -103,3 +103,18 @@ def test_merit_at_values_matches_c_oracle_on_lq():
                 assert np.isnan(got[k])
             else:
                 assert abs(got[k] - ref) <= 1e-10 * max(1.0, abs(ref)), (alpha, k, got[k], ref)
+
+
+def test_cartpole_swing_up_converges_with_linearised_merit():
+    """Reading R22: the C4 swing-up from the C4 iterate converges (status 0, KKT
+    residuals <= tol) to the upright goal when the step's trial merits use the linearised
+    dynamics; with the nonlinear trial merits the same loop stalls (tiny accepted steps)."""
+    from synth.ipm_workloads import cartpole_c4
+    b = cartpole_c4(3, N=100)
+    it, rep = ipm_solve_oracle(b, SolveSettings(max_iters=300, linear_merit=True), nthreads=3)
+    assert np.all(rep["status"] == 0), rep["status"]
+    assert np.all(np.maximum(np.maximum(rep["r_stat"], rep["r_feas"]), rep["r_comp0"]) <= 1e-6)
+    assert np.all(np.abs(it["x"][:, -1, 1] - np.pi) < 0.05)
+    assert np.all(np.abs(it["u"]) <= 3.0 + 1e-6) and np.all(np.abs(it["x"][..., 0]) <= 0.5 + 1e-6)
+    it2, rep2 = ipm_solve_oracle(b, SolveSettings(max_iters=40), nthreads=3)
+    assert np.all(rep2["status"] == 6)   # MAXITER: the nonlinear-merit loop has not converged
