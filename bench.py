@@ -64,7 +64,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample wall time")
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "split", "c4solve", "pit"],
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "split", "c4solve", "c4swing", "pit"],
                     help="c2 (default, BASELINE configs[1]); c3 = 4,096 dense n64 m32 N50 (configs[2]); "
                          "c4 = ipm_step on 16,384 cart-pole instances (configs[3]); c5 = 1,048,576 "
                          "quadrotor n12 m4 N200 sharded over the ranks, chunks of 65,536 (configs[4]); split = "
@@ -284,6 +284,8 @@ def main():
         return run_split(a, ws, rank, local)
     if a.workload == "c4solve":
         return run_c4solve(a, ws, rank, local)
+    if a.workload == "c4swing":
+        return run_c4solve(a, ws, rank, local, swing=True)
     if a.workload == "c1":
         return run_c1(a, ws, rank, local)
     if a.workload == "pit":
@@ -698,26 +700,31 @@ def run_split(a, ws, rank, local):
         "cpu_baseline": cpu_baseline(a.cpu_seconds) if (ws == 1 and not a.no_cpu_baseline) else None}), flush=True)
 
 
-def run_c4solve(a, ws, rank, local):
+def run_c4solve(a, ws, rank, local, swing=False):
     """Extra line: ipm_solve (the batched IPM loop) on the C4 cart-pole batch, 16,384
-    instances per GPU, N = 100, a fixed budget of 20 IPM iterations (the nonconvex swing-up does not
-    converge within it, so every instance runs all 20: a fixed amount of work per step).  Each
-    timed step solves a fresh device copy of the same initial iterate.  Per iteration and stage the
-    loop moves the ipm_step bytes (~1.9 KB) plus the evaluation / residual passes
-    (~0.9 KB); the roofline uses 2.8 KB per (instance, stage, iteration)."""
+    instances per GPU, N = 100.
+      c4solve: a fixed budget of 20 IPM iterations with the model's trial merits (the swing-up does
+        not converge within it, so every instance runs all 20: a fixed amount of work per step);
+      c4swing: the whole swing-up to convergence (settings.linear_merit, reading R22; at most 300
+        iterations) -- converged instances drop out of the loop's active list.
+    Each timed step solves a fresh device copy of the same initial iterate.  Per iteration and
+    stage the loop moves the ipm_step bytes (~1.9 KB) plus the evaluation /
+    residual passes (~0.9 KB); the roofline uses 2.8 KB per (instance, stage, iteration)."""
     import copy
+    import numpy as np
     import torch
     import paper_2509_16370_b200 as rr
     from synth.ipm_workloads import cartpole_c4
     dev = torch.device("cuda", local)
-    B, Nh, IT = 16384, 100, 20
+    B, Nh, IT = 16384, 100, (300 if swing else 20)
+    S = dict(max_iters=IT, linear_merit=swing)
     b = cartpole_c4(B, seed=2511, N=Nh, first=rank * B, device=dev)
-    call0 = rr.IpmSolveCall(b, max_iters=IT)
+    call0 = rr.IpmSolveCall(b, **S)
 
     def fresh():
         bk = copy.copy(b)
         bk.it = {k: v.clone() for k, v in b.it.items()}
-        return rr.IpmSolveCall(bk, ws=call0.ws, max_iters=IT)
+        return rr.IpmSolveCall(bk, ws=call0.ws, **S)
     nw = max(3, a.warmup)
     calls = [fresh() for _ in range(nw + a.steps)]
     stream = torch.cuda.current_stream(dev)
@@ -739,37 +746,54 @@ def run_c4solve(a, ws, rank, local):
     clk = clocks.stop()
     ms = max_over_ranks(sum(s_.elapsed_time(e_) for s_, e_ in ev) / a.steps, ws)
     iters = int(rep["iters"].sum())
+    nconv = int((rep["status"] == 0).sum())
     if rank == 0:
         alg = 2800 * Nh * iters
         peak, src = measured_peaks()
+        if swing:
+            metric = "regularized-IPM solve: converged C4 cart-pole swing-ups/s (ipm_solve to tol 1e-6)"
+            value, unit = nconv * ws / (ms / 1e3), "solves/s"
+        else:
+            metric = "regularized-IPM solve: instance-iterations/s (C4 cart-pole, ipm_solve, 20 iterations)"
+            value, unit = iters * ws / (ms / 1e3), "instance-iterations/s"
+        it_np = rep["iters"].cpu().numpy()
         print(json.dumps({
-            "metric": "regularized-IPM solve: instance-iterations/s (C4 cart-pole, ipm_solve, 20 iterations)",
-            "value": iters * ws / (ms / 1e3), "unit": "instance-iterations/s", "n_gpus": ws, "steps": a.steps,
+            "metric": metric, "value": value, "unit": unit, "n_gpus": ws, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C4 ipm_solve: %d cart-pole instances per GPU, N=%d, max_iters=%d" % (B, Nh, IT),
+            "config": {"workload": "C4 ipm_solve: %d cart-pole instances per GPU, N=%d, max_iters=%d%s" % (
+                B, Nh, IT, ", linear_merit (reading R22)" if swing else ""),
                        "l2": "stage data 3.1 GB/GPU > 126 MB L2 (no flush needed)"},
             "solves_per_s": B * ws / (ms / 1e3), "iterations_total": iters,
+            "instance_iterations_per_s": iters * ws / (ms / 1e3),
+            "iterations": {"min": int(it_np.min()), "median": float(np.median(it_np)), "max": int(it_np.max())},
             "status_counts": {str(int(k)): int(v) for k, v in zip(*torch.unique(rep["status"], return_counts=True))},
             "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / (ms / 1e3) / 1e9 / peak, "traffic": None,
                          "alg_bytes_per_stage_iteration": 2800, "peak_source": src},
             "clocks": clk, "gpu_launches": a.steps * (4 * IT + 3),
-            "cpu_baseline": c4solve_cpu_baseline(a, B, Nh, IT) if (ws == 1 and not a.no_cpu_baseline) else None}),
+            "cpu_baseline": c4solve_cpu_baseline(a, B, Nh, IT, swing) if (ws == 1 and not a.no_cpu_baseline) else None}),
               flush=True)
 
 
-def c4solve_cpu_baseline(a, B, Nh, IT):
+def c4solve_cpu_baseline(a, B, Nh, IT, swing=False):
     """The oracle IPM loop (oracle/ipm_solve.py around the C oracle step) on a bounded sample of the
-    same C4 batch, the same 20-iteration budget; rate in instance-iterations/s."""
+    same C4 batch and settings; rate in the line's unit (instance-iterations/s, or converged
+    solves/s for the swing-up)."""
     from synth.ipm_workloads import cartpole_c4
     from oracle.ipm_solve import SolveSettings, ipm_solve_oracle
     r = oracle_rate(lambda k: cartpole_c4(k, seed=2511, N=Nh),
-                    lambda p, t: ipm_solve_oracle(p, SolveSettings(max_iters=IT), nthreads=t), a.cpu_seconds, B,
-                    "C4 cart-pole instances, oracle IPM loop (%d iterations)" % IT, calib=16, cap=2048)
-    r["value"] *= IT
-    r["one_thread_value"] *= IT
-    r["unit"] = "instance-iterations/s"
+                    lambda p, t: ipm_solve_oracle(p, SolveSettings(max_iters=IT, linear_merit=swing), nthreads=t),
+                    a.cpu_seconds, B,
+                    "C4 cart-pole instances, oracle IPM loop (%s)" % ("swing-up to convergence, linear_merit" if swing
+                                                                      else "%d iterations" % IT),
+                    calib=(2 if swing else 16), cap=(256 if swing else 2048))
+    if not swing:
+        r["value"] *= IT
+        r["one_thread_value"] *= IT
+        r["unit"] = "instance-iterations/s"
+    else:
+        r["unit"] = "solves/s"
     return r
 
 
