@@ -62,6 +62,15 @@ typedef int32_t rr_err;
  * queries; rr_factor_solve on the CTA kernels (n or m > 16) returns RR_E_UNSUPPORTED. */
 #define RR_FLAG_SHARED_DYN 2
 #define RR_FLAG_SHARED_COST 4
+/* FP32 factor record (the paper's low-precision factorization + residual callback,
+ * P:664-666): rr_factor stores its records in FP32 (same layout and element offsets, record stride
+ * rr_factor_bytes()/(batch*(N+1)*4) = the double count rounded up to a multiple of 4 floats) and
+ * rr_solve reads them (arithmetic stays FP64).  The solution then carries the FP32 rounding of the
+ * factor (~1e-7 relative times the conditioning); one or two rr_residual + rr_solve(ACCUMULATE)
+ * refinement steps restore the FP64 result.  rr_factor_bytes, rr_factor, rr_solve and
+ * rr_solve_workspace_bytes accept it; compiled for nx = 12, nu = 4 only (else RR_E_UNSUPPORTED /
+ * -1) and the stage operands must be 16-byte aligned. */
+#define RR_FLAG_FACTOR_FP32 8
 
 typedef struct {
   int32_t nx;    /* state dimension n   (1 <= nx)            */
@@ -157,8 +166,9 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* prob_host, co
  */
 int32_t rr_factor_record_doubles(int32_t n, int32_t m);
 
-/* Bytes of the factor record array for `dims` (batch * (N+1) * R * 8), or -1 if no kernel covers
- * (nx, nu) (rr_factor / rr_solve are compiled for nx, nu <= 16). */
+/* Bytes of the factor record array for `dims` (batch * (N+1) * R * 8; with RR_FLAG_FACTOR_FP32
+ * batch * (N+1) * R32 * 4, R32 = R rounded up to a multiple of 4), or -1 if no kernel covers
+ * (nx, nu) (rr_factor / rr_solve are compiled for nx, nu <= 16; FP32 records for 12 x 4). */
 int64_t rr_factor_bytes(const rr_dims* dims);
 
 /*

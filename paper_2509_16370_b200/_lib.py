@@ -39,6 +39,7 @@ class rr_residual_buf(ctypes.Structure):
 
 
 RR_FLAG_ACCUMULATE = 1
+RR_FLAG_FACTOR_FP32 = 8
 
 
 class ipm_dims(ctypes.Structure):

@@ -139,18 +139,24 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* ph, const rr_
 int32_t rr_factor_record_doubles(int32_t n, int32_t m) { return rrk::frec_doubles(n, m); }
 
 int64_t rr_factor_bytes(const rr_dims* dims) {
-  if (!dims_ok(dims, RR_FLAG_ACCUMULATE | SHARED_FLAGS) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
+  if (!dims_ok(dims, RR_FLAG_ACCUMULATE | SHARED_FLAGS | RR_FLAG_FACTOR_FP32) || !rrk::split_supported(dims->nx, dims->nu))
+    return -1;
+  if (dims->flags & RR_FLAG_FACTOR_FP32) {  // FP32 records: the 12x4 DMMA factor kernel and rr_solve<12,4>
+    if (dims->nx != 12 || dims->nu != 4) return -1;
+    return dims->batch * (int64_t)(dims->N + 1) * rrk::frec_floats(dims->nx, dims->nu) * 4;
+  }
   return dims->batch * (int64_t)(dims->N + 1) * rrk::frec_doubles(dims->nx, dims->nu) * 8;
 }
 
 int64_t rr_solve_workspace_bytes(const rr_dims* dims) {
-  if (!dims_ok(dims, RR_FLAG_ACCUMULATE | SHARED_FLAGS) || !rrk::split_supported(dims->nx, dims->nu)) return -1;
+  if (!dims_ok(dims, RR_FLAG_ACCUMULATE | SHARED_FLAGS | RR_FLAG_FACTOR_FP32) || !rrk::split_supported(dims->nx, dims->nu))
+    return -1;
   return dims->batch * (int64_t)dims->N * (dims->nx + dims->nu) * 8 + 256;
 }
 
 rr_err rr_factor(const rr_dims* dims, const rr_problem* prob, void* factor, int64_t factor_bytes,
                  const rr_factor_buf* fac, int32_t* status, void* stream) {
-  if (!dims_ok(dims)) return set_err(RR_E_INVALID, "rr_factor: invalid dims%s");
+  if (!dims_ok(dims, SHARED_FLAGS | RR_FLAG_FACTOR_FP32)) return set_err(RR_E_INVALID, "rr_factor: invalid dims%s");
   if (prob == nullptr) return set_err(RR_E_INVALID, "rr_factor: null %s", "prob");
   if (dims->batch == 0) return RR_OK;
   if (status == nullptr) return set_err(RR_E_INVALID, "rr_factor: null %s", "status");
@@ -181,6 +187,9 @@ rr_err rr_factor(const rr_dims* dims, const rr_problem* prob, void* factor, int6
   a.status = status;
   a.shared = dims->flags & SHARED_FLAGS;
   a.tma16 = stage_ops_aligned16(prob);
+  a.f32 = (dims->flags & RR_FLAG_FACTOR_FP32) != 0;
+  if (a.f32 && !a.tma16)
+    return set_err(RR_E_UNSUPPORTED, "rr_factor: FP32 records need 16-byte aligned stage operands%s");
   bool supported = false;
   cudaError_t e = rrk::factor_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_factor: unsupported shape%s");
@@ -191,7 +200,8 @@ rr_err rr_factor(const rr_dims* dims, const rr_problem* prob, void* factor, int6
 rr_err rr_solve(const rr_dims* dims, const rr_problem* prob, const void* factor, int64_t factor_bytes,
                 const rr_factor_buf* fac, const rr_solution* sol, void* workspace, int64_t workspace_bytes,
                 int32_t* status, void* stream) {
-  if (!dims_ok(dims, RR_FLAG_ACCUMULATE | SHARED_FLAGS)) return set_err(RR_E_INVALID, "rr_solve: invalid dims%s");
+  if (!dims_ok(dims, RR_FLAG_ACCUMULATE | SHARED_FLAGS | RR_FLAG_FACTOR_FP32))
+    return set_err(RR_E_INVALID, "rr_solve: invalid dims%s");
   if (prob == nullptr || sol == nullptr) return set_err(RR_E_INVALID, "rr_solve: null %s", "prob/sol");
   if (dims->batch == 0) return RR_OK;
   if (status == nullptr) return set_err(RR_E_INVALID, "rr_solve: null %s", "status");
@@ -228,6 +238,7 @@ rr_err rr_solve(const rr_dims* dims, const rr_problem* prob, const void* factor,
   a.status = status;
   a.accumulate = (dims->flags & RR_FLAG_ACCUMULATE) != 0;
   a.shared = dims->flags & SHARED_FLAGS;
+  a.f32 = (dims->flags & RR_FLAG_FACTOR_FP32) != 0;
   bool supported = false;
   cudaError_t e = rrk::solve_launch(a, static_cast<cudaStream_t>(stream), &supported);
   if (!supported) return set_err(RR_E_UNSUPPORTED, "rr_solve: unsupported shape%s");

@@ -21,6 +21,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "rr_common.cuh"
 #include "rr_fused.cuh"
 #include "rr_stage.cuh"
@@ -343,7 +345,8 @@ struct MmaLayout {
 
 // FAC = true: rr_factor (the matrix half only): stage loads of A, B, Q, M, R, factor records
 // [V_i | S_i⁻¹ | K_i | G_i⁻¹] to a.frec (rr_split.cuh layout), no forward sweep.
-template <int NX, int NU, int WARPS, int MINB, bool FAC = false>
+// F32 (with FAC): the factor records are written in FP32 (RR_FLAG_FACTOR_FP32, a.frec32).
+template <int NX, int NU, int WARPS, int MINB, bool FAC = false, bool F32 = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const FusedArgs a) {
   using LY = MmaLayout<NX, NU>;
   using SM = StageMMA<NX, NU>;
@@ -415,7 +418,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   __syncwarp();
   uint32_t ph0 = 0, ph1 = 0;
   constexpr uint32_t STG_BYTES = 8u * (n * n + 2 * n * m + sn + sm + (FAC ? 0 : 2 * n + m));
-  constexpr int FREC = (NX * (NX + 1) + NX * NU + NU * (NU + 1) / 2 + 1) & ~1;  // factor record doubles
+  using RT = typename std::conditional<F32, float, double>::type;  // factor record element type
+  constexpr int FRECD = (NX * (NX + 1) + NX * NU + NU * (NU + 1) / 2 + 1) & ~1;  // factor record doubles
+  constexpr int FREC = F32 ? ((FRECD + 3) & ~3) : FRECD;  // record stride in elements (16-byte multiple)
+  RT* const frecb = F32 ? reinterpret_cast<RT*>(a.frec32) : reinterpret_cast<RT*>(a.frec);
 
   // Persistent warps (DESIGN.md §5 "phase staggering"): warp w of CTA b solves the instance pairs
   // p0 + k·stride, k = 0, 1, ...  The backward sweep is compute / shared-memory bound and the forward
@@ -523,7 +529,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
       for (int r = 0; r < NX; ++r) Vc[r] = (j < n) ? (r >= j ? QN[pidx(n, r, j)] : QN[pidx(n, j, r)]) : 0.0;
       if (j < NX) wk[WK::vs + j] = FAC ? 0.0 : a.p.qN[inst * n + j];
       if (FAC && valid && j < n)  // record N: V_N = Q_N
-        for (int r = j; r < n; ++r) a.frec[inst * (sN + 1) * FREC + sN * FREC + pidx(n, r, j)] = QN[pidx(n, r, j)];
+        for (int r = j; r < n; ++r) frecb[inst * (sN + 1) * FREC + sN * FREC + pidx(n, r, j)] = (RT)QN[pidx(n, r, j)];
       if (valid && a.f.V != nullptr && j < n) {
         double* Vo = a.f.V + (inst * (sN + 1) + N) * sn;
         for (int r = j; r < n; ++r) Vo[pidx(n, r, j)] = QN[pidx(n, r, j)];
@@ -560,16 +566,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
       auto prefetch = [&]() {
         if (i > 0) issue_stage(i - 1, slot);
       };
-      double* recq[2];
+      RT* recq[2];
       if constexpr (FAC) {
 #pragma unroll
-        for (int q = 0; q < 2; ++q) recq[q] = validq[q] ? a.frec + (instq[q] * (sN + 1) + i) * FREC : nullptr;
+        for (int q = 0; q < 2; ++q) recq[q] = validq[q] ? frecb + (instq[q] * (sN + 1) + i) * FREC : nullptr;
       } else {
 #pragma unroll
-        for (int q = 0; q < 2; ++q) recq[q] = rec0q[q] ? rec0q[q] + (int64_t)i * RC::PAD : nullptr;
+        for (int q = 0; q < 2; ++q) recq[q] = rec0q[q] ? reinterpret_cast<RT*>(rec0q[q] + (int64_t)i * RC::PAD) : nullptr;
       }
       double U[NZ], bj;
-      SM::template backward<FAC>(wkq, Fq, cvq, P2, qjf, wait_inputs, prefetch, delta, grp, j, lane, Vc, U, bj,
+      SM::template backward<FAC, RT>(wkq, Fq, cvq, P2, qjf, wait_inputs, prefetch, delta, grp, j, lane, Vc, U, bj,
                                  recq, i, st);
       if (valid) {
         if (a.f.V != nullptr && j < n) {
@@ -589,9 +595,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
     }
     if constexpr (FAC) {  // S_0⁻¹ -> record 0; status; NaN-fill a failed instance's records
       ST::invS(Vc, delta, j, wk, 0, st);
-      double* rec = a.frec + inst * (sN + 1) * FREC;
+      RT* rec = frecb + inst * (sN + 1) * FREC;
       if (valid && j < n)
-        for (int r = j; r < n; ++r) rec[sn + pidx(n, r, j)] = wk[WK::Si + r * NX + j];
+        for (int r = j; r < n; ++r) rec[sn + pidx(n, r, j)] = (RT)wk[WK::Si + r * NX + j];
       int32_t status = st;
 #pragma unroll
       for (int off = 8; off > 0; off >>= 1) {
@@ -601,7 +607,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
       __syncwarp();
       if (valid && status != 0) {
         const double nan = __longlong_as_double(0x7ff8000000000000LL);
-        for (int64_t e = j; e < (sN + 1) * FREC; e += 16) rec[e] = nan;
+        for (int64_t e = j; e < (sN + 1) * FREC; e += 16) rec[e] = (RT)nan;
       }
       if (valid && j == 0) a.status[inst] = status;
       return;
@@ -786,7 +792,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   }
 }
 
-template <int NX, int NU, int WARPS, int MINB, bool FAC = false>
+template <int NX, int NU, int WARPS, int MINB, bool FAC = false, bool F32 = false>
 struct MmaCfg {
   static constexpr int IPB = WARPS * 2;
   static size_t smem_bytes() {
@@ -794,7 +800,7 @@ struct MmaCfg {
   }
   static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * RecM<NX, NU>::PAD; }
   static cudaError_t launch(const FusedArgs& a0, cudaStream_t s) {
-    auto k = rr_fused_mma_kernel<NX, NU, WARPS, MINB, FAC>;
+    auto k = rr_fused_mma_kernel<NX, NU, WARPS, MINB, FAC, F32>;
     const size_t sm = smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
@@ -882,6 +888,7 @@ namespace rrk {
 cudaError_t factor_mma_launch(const FusedArgs& a, cudaStream_t s, bool* supported) {
   *supported = (a.nx == 12 && a.nu == 4);
   if (!*supported) return cudaSuccess;
+  if (a.frec32 != nullptr) return MmaCfg<12, 4, 4, 3, true, true>::launch(a, s);  // FP32 records
   return MmaCfg<12, 4, 4, 3, true>::launch(a, s);
 }
 }  // namespace rrk

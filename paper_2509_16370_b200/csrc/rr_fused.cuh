@@ -16,6 +16,7 @@ struct FusedArgs {
   double* ws;
   int32_t* status;
   double* frec = nullptr;  // rr_factor on the DMMA kernel: factor records [batch][N+1][frec_doubles]
+  float* frec32 = nullptr; // ... or FP32 records [batch][N+1][frec_floats] (RR_FLAG_FACTOR_FP32)
   int shared = 0;          // RR_FLAG_SHARED_DYN | RR_FLAG_SHARED_COST (batch-shared operands)
   // every stage-operand base pointer (A, B, Q, M, R, q, r, c) is 16-byte aligned: the TMA
   // (cp.async.bulk) kernels may run; otherwise the 12x4 shape falls back to the LDGSTS kernel

@@ -30,6 +30,8 @@
 
 #include "rr_common.cuh"
 #include "rr_split.cuh"
+
+#include <type_traits>
 #include "rr_fused.cuh"
 #include "rr_stage.cuh"
 
@@ -291,9 +293,11 @@ struct SolLayout {
   static constexpr int SLOT_PAD = (SLOT + 1) & ~1;
 };
 
-template <int NX, int NU, int LG, int WARPS, int MINB, bool EXACT>
+// F32: the factor records are FP32 (RR_FLAG_FACTOR_FP32): loaded as floats, used in FP64 arithmetic.
+template <int NX, int NU, int LG, int WARPS, int MINB, bool EXACT, bool F32 = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitArgs a) {
   using LY = SolLayout<NX, NU>;
+  using RT = typename std::conditional<F32, float, double>::type;
   constexpr int IPW = 32 / LG;
   static_assert(NX + NU <= LG, "lane group narrower than n+m");
   const int n = EXACT ? NX : a.nx;
@@ -301,7 +305,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
   const int N = a.N;
   const int sn = symn(n), sm = symn(m);
   const int oA = 0, oB = n * n, oc = oB + n * m, oq = oc + n, orr = oq + n;
-  const int REC = frec_doubles(n, m);
+  const int REC = F32 ? frec_floats(n, m) : frec_doubles(n, m);  // record stride in elements
   const int rS = sn, rK = 2 * sn, rG = 2 * sn + n * m;
   (void)sm;
 
@@ -310,7 +314,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
   const int grp = lane / LG, j = lane % LG, gbase = grp * LG;
   double* slot = smem + (warp * IPW + grp) * group_stride(LY::SLOT_PAD, LG);
   auto sbuf = [&](int i) { return slot + LY::oS + (i & 1) * LY::VSTG_PAD; };
-  auto rbuf = [&](int i) { return slot + LY::oR + (i % 3) * LY::REC_PAD; };
+  auto rbuf = [&](int i) { return reinterpret_cast<RT*>(slot + LY::oR + (i % 3) * LY::REC_PAD); };
   double* vs = slot + LY::ovs;
   double* wb = slot + LY::ow;
   double* gb = slot + LY::og;
@@ -322,7 +326,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
   if (!valid) inst = a.batch - 1;
   const double delta = a.p.delta[inst];
   const int64_t sN = (int64_t)N;
-  const double* rec = a.frc + inst * (sN + 1) * REC;
+  const RT* rec = reinterpret_cast<const RT*>(a.frc) + inst * (sN + 1) * REC;
   double* kv = a.ws + inst * sN * (n + m);  // per stage: v_i (n) | k_i (m)
   const int ui = j - NX;                     // control row of this lane (0 <= ui < m)
   const bool xl = j < n, ul = ui >= 0 && ui < m;
@@ -338,7 +342,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
     copy_async(dst + oq, a.p.q + s * n, n, j, LG);
     copy_async(dst + orr, a.p.r + s * m, m, j, LG);
   };
-  auto issue_rec = [&](int i) { copy_async(rbuf(i), rec + (int64_t)i * REC, REC, j, LG); };
+  auto issue_rec = [&](int i) {
+    copy_async(reinterpret_cast<double*>(rbuf(i)), reinterpret_cast<const double*>(rec + (int64_t)i * REC),
+               REC * (int)sizeof(RT) / 8, j, LG);
+  };
 
   // ---------------- backward vector sweep ----------------
   if (xl) vs[j] = a.p.qN[inst * n + j];
@@ -357,8 +364,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
     cp_async_wait<1>();
     __syncwarp();
     const double* S = sbuf(i);
-    const double* R1 = rbuf(i + 1);  // V_{i+1}, S_{i+1}⁻¹
-    const double* R0 = rbuf(i);        // K_i, G_i⁻¹
+    const RT* R1 = rbuf(i + 1);  // V_{i+1}, S_{i+1}⁻¹
+    const RT* R0 = rbuf(i);        // K_i, G_i⁻¹
     // w = v_{i+1} + V_{i+1} c_{i+1}
     if (xl) {
       double w0 = vs[j], w1 = 0.0;
@@ -458,8 +465,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
     cp_async_wait<1>();
     __syncwarp();
     const double* S = sbuf(i);
-    const double* R0 = rbuf(i);        // V_i, K_i
-    const double* R1 = rbuf(i + 1);  // S_{i+1}⁻¹
+    const RT* R0 = rbuf(i);        // V_i, K_i
+    const RT* R1 = rbuf(i + 1);  // S_{i+1}⁻¹
     const double* xc = xb(i);
     double* xn = xb(i + 1);
     // y_i = V_i x_i + v_i ;  u_i = K_i x_i + k_i
@@ -518,7 +525,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
   }
   // y_N = V_N x_N + v_N (record N holds V_N = Q_N)
   if (xl) {
-    const double* RN = rbuf(N);
+    const RT* RN = rbuf(N);
     const double* xc = xb(N);
     double y0 = a.p.qN[inst * n + j], y1 = 0.0;
 #pragma unroll
@@ -716,7 +723,7 @@ struct SplitCfg {
     return cudaGetLastError();
   }
   static cudaError_t solve(const SplitArgs& a, cudaStream_t s) {
-    auto k = rr_solve_kernel<NX, NU, LG, WARPS, MINB, EXACT>;
+    auto k = a.f32 ? rr_solve_kernel<NX, NU, LG, WARPS, MINB, EXACT, true> : rr_solve_kernel<NX, NU, LG, WARPS, MINB, EXACT>;
     const size_t sm = sol_smem();
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
@@ -755,10 +762,15 @@ cudaError_t factor_launch(const SplitArgs& a, cudaStream_t s, bool* supported) {
     f.f = a.f;
     f.ws = nullptr;
     f.status = a.status;
-    f.frec = a.fr;
+    if (a.f32) f.frec32 = reinterpret_cast<float*>(a.fr);  // FP32 records (RR_FLAG_FACTOR_FP32)
+    else f.frec = a.fr;
     f.shared = a.shared;
     err = factor_mma_launch(f, s, supported);
     if (*supported) return err;
+  }
+  if (a.f32) {  // FP32 records are written by the 12x4 DMMA factor kernel only
+    *supported = false;
+    return cudaSuccess;
   }
   *supported = dispatch_split(a.nx, a.nu, [&](auto cfg) {
     err = decltype(cfg)::factor(a, s);

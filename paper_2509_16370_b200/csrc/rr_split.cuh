@@ -20,6 +20,7 @@ struct SplitArgs {
   int accumulate;    // rr_solve: RR_FLAG_ACCUMULATE (sol += solution)
   int shared;        // RR_FLAG_SHARED_DYN | RR_FLAG_SHARED_COST
   bool tma16;        // rr_factor: A, B, Q, M, R 16-byte aligned (the 12x4 DMMA/TMA factor kernel may run)
+  bool f32;          // RR_FLAG_FACTOR_FP32: FP32 factor records (12x4 only)
 };
 
 struct ResArgs {
@@ -36,6 +37,9 @@ struct ResArgs {
 __host__ __device__ inline int frec_doubles(int n, int m) {
   return (n * (n + 1) + n * m + m * (m + 1) / 2 + 1) & ~1;
 }
+
+// floats per FP32 factor record (RR_FLAG_FACTOR_FP32): the same layout, rounded to a 16-byte multiple
+__host__ __device__ inline int frec_floats(int n, int m) { return (frec_doubles(n, m) + 3) & ~3; }
 
 bool split_supported(int nx, int nu);
 cudaError_t factor_launch(const SplitArgs& a, cudaStream_t s, bool* supported);

@@ -173,12 +173,14 @@ struct StageMMA {
   // FAC = true: the factorization only (rr_factor): no Φ / φ, the u-block is eliminated with the
   // symmetric sweep operator (−G⁻¹ lands in the u-columns) and recq[q] points at factor record i
   // [V_i | S_i⁻¹ | K_i | G_i⁻¹] (record i+1 receives S_{i+1}⁻¹).
-  template <bool FAC = false, typename PFun, typename QFun, typename WaitFn, typename PrefFn>
+  // RT: element type of the records (double; float for the FP32 factor record of rr_factor,
+  // RR_FLAG_FACTOR_FP32 -- FAC only)
+  template <bool FAC = false, typename RT = double, typename PFun, typename QFun, typename WaitFn, typename PrefFn>
   __device__ static __forceinline__ void backward(double* const (&wkq)[2], const double* const (&Fq)[2],
                                                   const double* const (&cvq)[2], PFun&& Pat, QFun&& qjf,
                                                   WaitFn&& wait_inputs, PrefFn&& prefetch, double delta, int grp,
                                                   int j, int lane, double (&Vc)[NX], double (&U)[NZ],
-                                                  double& bj, double* const (&recq)[2], int stage,
+                                                  double& bj, RT* const (&recq)[2], int stage,
                                                   int32_t& st) {
     double* wk = grp ? wkq[1] : wkq[0];
     const double* F = grp ? Fq[1] : Fq[0];
@@ -559,13 +561,14 @@ struct StageMMA {
     if constexpr (FAC) {  // factor record i (and S_{i+1}⁻¹ into record i+1); no closed loop
       __syncwarp();
       prefetch();
-      double* rec = grp ? recq[1] : recq[0];
+      RT* rec = grp ? recq[1] : recq[0];
       constexpr int SN = NX * (NX + 1) / 2;
-      constexpr int REC = (NX * (NX + 1) + NX * NU + NU * (NU + 1) / 2 + 1) & ~1;
+      constexpr int RECD = (NX * (NX + 1) + NX * NU + NU * (NU + 1) / 2 + 1) & ~1;
+      constexpr int REC = sizeof(RT) == 4 ? ((RECD + 3) & ~3) : RECD;  // FP32 records: 16-byte multiple
       if (rec != nullptr) {
         if (j < NX) {
-          double* Vp = rec + j * (2 * NX - j - 1) / 2;
-          double* Sp = rec + REC + SN + j * (2 * NX - j - 1) / 2;  // record i+1: S_{i+1}⁻¹
+          RT* Vp = rec + j * (2 * NX - j - 1) / 2;
+          RT* Sp = rec + REC + SN + j * (2 * NX - j - 1) / 2;  // record i+1: S_{i+1}⁻¹
 #pragma unroll
           for (int r = 0; r < NX; ++r)
             if (r >= j) {
@@ -576,7 +579,7 @@ struct StageMMA {
           for (int u = 0; u < NU; ++u) rec[2 * SN + j * NU + u] = -U[NX + u];
         } else if (j < NZ) {
           const int w = j - NX;
-          double* Gp = rec + 2 * SN + NX * NU + w * (2 * NU - w - 1) / 2;
+          RT* Gp = rec + 2 * SN + NX * NU + w * (2 * NU - w - 1) / 2;
 #pragma unroll
           for (int u = 0; u < NU; ++u)
             if (u >= w) Gp[u] = -U[NX + u];
@@ -591,11 +594,11 @@ struct StageMMA {
     {  // record: S_{i+1}⁻¹, e, K, k, V, v (no closed-loop products)
       __syncwarp();
       prefetch();
-      double* rec = grp ? recq[1] : recq[0];
+      auto* rec = grp ? recq[1] : recq[0];
       if (rec != nullptr) {
         if (j < NX) {
-          double* Sp = rec + RC::S + j * (2 * NX - j - 1) / 2;
-          double* Vp = rec + RC::V + j * (2 * NX - j - 1) / 2;
+          auto* Sp = rec + RC::S + j * (2 * NX - j - 1) / 2;
+          auto* Vp = rec + RC::V + j * (2 * NX - j - 1) / 2;
 #pragma unroll
           for (int r = 0; r < NX; ++r)
             if (r >= j) {
@@ -664,7 +667,7 @@ struct StageMMA {
           for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aS[mt], bM);
         }
       }
-      double* rec = recq[q];
+      auto* rec = recq[q];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -676,11 +679,11 @@ struct StageMMA {
     }
     // (9) record K, k, V (packed), v; carry V_i, v_i
     if ((grp ? recq[1] : recq[0]) != nullptr) {
-      double* rec = grp ? recq[1] : recq[0];
+      auto* rec = grp ? recq[1] : recq[0];
       if (j < NX) {
 #pragma unroll
         for (int u = 0; u < NU; ++u) rec[RC::K + j * NU + u] = -U[NX + u];
-        double* Vp = rec + RC::V + j * (2 * NX - j - 1) / 2;
+        auto* Vp = rec + RC::V + j * (2 * NX - j - 1) / 2;
 #pragma unroll
         for (int r = 0; r < NX; ++r)
           if (r >= j) Vp[r] = U[r];

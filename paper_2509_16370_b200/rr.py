@@ -9,7 +9,7 @@ from typing import Optional
 
 import torch
 
-from ._lib import (RR_FLAG_ACCUMULATE, RRError, check, lib, rr_dims, rr_factor_buf, rr_problem, rr_residual_buf,
+from ._lib import (RR_FLAG_ACCUMULATE, RR_FLAG_FACTOR_FP32, RRError, check, lib, rr_dims, rr_factor_buf, rr_problem, rr_residual_buf,
                    rr_solution)
 
 PROBLEM_FIELDS = ("A", "B", "Q", "M", "R", "q", "r", "c", "QN", "qN", "c0", "delta")
@@ -154,10 +154,10 @@ def factor_record_doubles(nx: int, nu: int) -> int:
     return (nx * (nx + 1) + nx * nu + nu * (nu + 1) // 2 + 1) & ~1
 
 
-def factor_bytes(nx: int, nu: int, N: int, batch: int) -> int:
-    nb = lib().rr_factor_bytes(ctypes.byref(rr_dims(nx, nu, N, 0, batch)))
+def factor_bytes(nx: int, nu: int, N: int, batch: int, fp32: bool = False) -> int:
+    nb = lib().rr_factor_bytes(ctypes.byref(rr_dims(nx, nu, N, RR_FLAG_FACTOR_FP32 if fp32 else 0, batch)))
     if nb < 0:
-        raise RRError("rr_factor: no kernel compiled for nx=%d nu=%d" % (nx, nu))
+        raise RRError("rr_factor: no kernel compiled for nx=%d nu=%d%s" % (nx, nu, " (FP32 records)" if fp32 else ""))
     return int(nb)
 
 
@@ -173,23 +173,33 @@ def _stream(stream, device):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def rr_factor(prob, factor=None, fac=None, status=None, stream=None):
+def rr_factor(prob, factor=None, fac=None, status=None, stream=None, fp32=False):
     """Row a2 (matrix half of Eq.(RR)): returns (factor, status), factor a CUDA float64 tensor
     [batch, N+1, rr_factor_record_doubles] in the include/rr.h record layout
-    (V_i | S_i^-1 | K_i | G_i^-1).  fac: optional dict with V / K tensors to receive copies."""
+    (V_i | S_i^-1 | K_i | G_i^-1).  fac: optional dict with V / K tensors to receive copies.
+    fp32: FP32 records (RR_FLAG_FACTOR_FP32, 12 x 4): a float32 tensor [batch, N+1, R32]."""
     if not prob.delta.is_cuda:
         raise RRError("rr_factor needs CUDA tensors (no CPU fallback)")
     dev = prob.delta.device
-    factor_bytes(prob.nx, prob.nu, prob.N, prob.batch)  # raises if no kernel covers the shape
+    nb = factor_bytes(prob.nx, prob.nu, prob.N, prob.batch, fp32)  # raises if no kernel covers the shape
     if factor is None:
-        factor = torch.empty(prob.batch, prob.N + 1, factor_record_doubles(prob.nx, prob.nu),
-                             dtype=torch.float64, device=dev)
+        if fp32:
+            factor = torch.empty(prob.batch, prob.N + 1, (factor_record_doubles(prob.nx, prob.nu) + 3) & ~3,
+                                 dtype=torch.float32, device=dev)
+        else:
+            factor = torch.empty(prob.batch, prob.N + 1, factor_record_doubles(prob.nx, prob.nu),
+                                 dtype=torch.float64, device=dev)
+    if (factor.dtype == torch.float32) != bool(fp32) or factor.numel() * factor.element_size() < nb:
+        raise RRError("rr_factor: factor tensor dtype / size does not match fp32=%s" % fp32)
     if status is None:
         status = torch.empty(prob.batch, dtype=torch.int32, device=dev)
     check_problem(prob, dict(status=status))
     p = rr_problem(*[_p(getattr(prob, f)) for f in PROBLEM_FIELDS])
     f = rr_factor_buf(*[_p(fac.get(k)) if fac is not None else None for k in ("V", "v", "K", "k")])
-    rc = lib().rr_factor(ctypes.byref(dims_of(prob)), ctypes.byref(p), _p(factor), factor.numel() * 8,
+    d = dims_of(prob)
+    if fp32:
+        d.flags |= RR_FLAG_FACTOR_FP32
+    rc = lib().rr_factor(ctypes.byref(d), ctypes.byref(p), _p(factor, factor.dtype), factor.numel() * factor.element_size(),
                          ctypes.byref(f), _p(status, torch.int32), _stream(stream, dev))
     check(rc, "rr_factor")
     return factor, status
@@ -215,7 +225,11 @@ def rr_solve(prob, factor, out=None, fac=None, workspace=None, stream=None, accu
         if out is None:
             raise RRError("rr_solve(accumulate=True) needs `out` (the solution to update)")
         d.flags |= RR_FLAG_ACCUMULATE
-    rc = lib().rr_solve(ctypes.byref(d), ctypes.byref(p), _p(factor), factor.numel() * 8,
+    if factor.dtype == torch.float32:  # FP32 records of rr_factor(fp32=True)
+        d.flags |= RR_FLAG_FACTOR_FP32
+    elif factor.dtype != torch.float64:
+        raise RRError("rr_solve: factor must be float64 (or float32 records of rr_factor(fp32=True))")
+    rc = lib().rr_solve(ctypes.byref(d), ctypes.byref(p), _p(factor, factor.dtype), factor.numel() * factor.element_size(),
                         ctypes.byref(f), ctypes.byref(s), _p(workspace), workspace.numel() * 8,
                         _p(sol["status"], torch.int32), _stream(stream, dev))
     check(rc, "rr_solve")

@@ -45,3 +45,14 @@ def test_binding_rejects_cpu_tensors():
     p = synth.random_stable_lqr(4, 1, 3, 2, seed=0)
     with pytest.raises(m.RRError):
         m.rr_factor_solve(p)
+
+
+def test_fp32_factor_record_size_query():
+    """RR_FLAG_FACTOR_FP32 (include/rr.h): FP32 records for 12 x 4 only, R rounded up to 4 floats."""
+    import paper_2509_16370_b200 as m
+    R = m.factor_record_doubles(12, 4)
+    assert R == 214
+    assert m.factor_bytes(12, 4, 100, 8, fp32=True) == 8 * 101 * 216 * 4
+    assert m.factor_bytes(12, 4, 100, 8) == 8 * 101 * R * 8
+    with pytest.raises(m.RRError):
+        m.factor_bytes(4, 1, 10, 8, fp32=True)   # no FP32 kernel for this shape

@@ -186,3 +186,39 @@ def test_split_c2_full_size_sampled_parity():
     o = oracle.rr_solve_t2(sub.to("cpu"), nthreads=8)
     for k in ("x", "u", "y"):
         assert blockwise_rel(sol[k][idx].cpu().numpy(), o[k]) <= TOL, k
+
+
+@pytest.mark.parametrize("delta", [0.0, 1e-4, 1.0])
+def test_fp32_factor_record_and_refinement(delta):
+    """rr_factor with FP32 records (RR_FLAG_FACTOR_FP32) + rr_solve carries the FP32
+    rounding of the factor (error well above the FP64 path, far below 1); rr_residual +
+    rr_solve(ACCUMULATE) refinement contracts it by ~1e-6 per step: within the 1e-9 bar of
+    the oracle after two steps, and the records equal the FP64 records rounded to float."""
+    m = rr()
+    p = synth.random_stable_lqr(12, 4, 30, 64, seed=77, delta=delta)
+    o = oracle.rr_solve_t2(p)
+    dev = p.to("cuda")
+    F32, st = m.rr_factor(dev, fp32=True)
+    F64, st64 = m.rr_factor(dev)
+    sol = m.rr_solve(dev, F32)
+    torch.cuda.synchronize()
+    assert int(st.abs().sum()) == 0 and int(sol["status"].abs().sum()) == 0
+    assert F32.dtype == torch.float32 and F32.shape[-1] == 216
+    f32, f64 = F32.cpu().numpy(), F64.cpu().numpy().astype(np.float32)
+    np.testing.assert_array_equal(f32[:, :-1, :214], f64[:, :-1])      # records 0..N-1
+    np.testing.assert_array_equal(f32[:, -1, :156], f64[:, -1, :156])  # record N: V_N, S_N⁻¹ (K, G⁻¹ unused)
+    e0 = max(blockwise_rel(sol[k].cpu().numpy(), o[k]) for k in ("x", "u", "y"))
+    assert 1e-12 < e0 < 1e-3, e0
+    errs = [e0]
+    for _ in range(2):
+        m.rr_refine(dev, F32, sol, iters=1)
+        torch.cuda.synchronize()
+        errs.append(max(blockwise_rel(sol[k].cpu().numpy(), o[k]) for k in ("x", "u", "y")))
+    assert errs[1] < errs[0] * 1e-3 and errs[2] <= TOL, errs
+
+
+def test_fp32_factor_record_unsupported_shape():
+    m = rr()
+    p = synth.random_stable_lqr(4, 1, 5, 4, seed=1).to("cuda")
+    with pytest.raises(m.RRError):
+        m.rr_factor(p, fp32=True)
