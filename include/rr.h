@@ -149,7 +149,24 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* prob_host, co
                             int32_t* status_host, const rr_problem* prob_dev, const rr_solution* sol_dev,
                             int32_t* status_dev, void* workspace, int64_t workspace_bytes, void* stream);
 
-/* ============================ factorization / solve split (rows a2 | a3-a5) ============================
+/*
+ * rr_factor_solve_host_pipelined: rr_factor_solve_host with the copies overlapped with the solve.
+ * The batch is cut into `nchunks` contiguous instance ranges; chunk c runs on streams[c % nstreams]:
+ * H2D of its slices of every per-instance operand, rr_factor_solve on them, D2H of its x, u, y and
+ * status -- so the H2D of one chunk, the solve of another and the D2H of a third proceed together on
+ * the two copy engines and the SMs (the whole-batch version serialises them on one stream).
+ * Batch-shared operands (RR_FLAG_SHARED_*) are copied once on streams[0] first.  streams[0] is the
+ * completion stream: the other streams wait for it on entry and it waits for them on exit, so
+ * synchronising streams[0] completes the call.  workspace: >= sum over the chunks of
+ * rr_workspace_bytes(chunk dims) rounded up to 256 B each, 256-byte aligned (per-chunk slices: chunks
+ * on different streams run concurrently).  Results are bitwise those of rr_factor_solve_host.
+ */
+rr_err rr_factor_solve_host_pipelined(const rr_dims* dims, const rr_problem* prob_host, const rr_solution* sol_host,
+                                      int32_t* status_host, const rr_problem* prob_dev, const rr_solution* sol_dev,
+                                      int32_t* status_dev, void* workspace, int64_t workspace_bytes, int32_t nchunks,
+                                      void* const* streams, int32_t nstreams);
+
+/* ============================ factorization / solve split (rows a2 | a3-a5) ============================/* ============================ factorization / solve split (rows a2 | a3-a5) ============================
  * The paper's solver plugs problem-specific "KKT system factorization" and "KKT system solve"
  * callbacks into a shared backend.  rr_factor is the matrix half of Eq.(RR),
  * which depends only on (A, B, Q, M, R, Q_N, δ); rr_solve is the vector half plus the forward sweep

@@ -107,6 +107,12 @@ def lib():
                                                ctypes.POINTER(rr_solution), ctypes.c_void_p,
                                                ctypes.POINTER(rr_problem), ctypes.POINTER(rr_solution),
                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+            L.rr_factor_solve_host_pipelined.restype = ctypes.c_int32
+            L.rr_factor_solve_host_pipelined.argtypes = [ctypes.POINTER(rr_dims), ctypes.POINTER(rr_problem),
+                                                         ctypes.POINTER(rr_solution), ctypes.c_void_p,
+                                                         ctypes.POINTER(rr_problem), ctypes.POINTER(rr_solution),
+                                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                                         ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32]
             L.rr_factor_bytes.restype = ctypes.c_int64
             L.rr_factor_bytes.argtypes = [ctypes.POINTER(rr_dims)]
             L.rr_solve_workspace_bytes.restype = ctypes.c_int64

@@ -136,6 +136,121 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* ph, const rr_
 }
 
 
+rr_err rr_factor_solve_host_pipelined(const rr_dims* dims, const rr_problem* ph, const rr_solution* sh,
+                                      int32_t* status_host, const rr_problem* pd, const rr_solution* sd,
+                                      int32_t* status_dev, void* workspace, int64_t workspace_bytes, int32_t nchunks,
+                                      void* const* streams, int32_t nstreams) {
+  if (!dims_ok(dims)) return set_err(RR_E_INVALID, "rr_factor_solve_host_pipelined: invalid dims%s");
+  if (!ph || !sh || !pd || !sd || !status_host || !status_dev || !streams || nstreams < 1 || nchunks < 1)
+    return set_err(RR_E_INVALID, "rr_factor_solve_host_pipelined: null or invalid %s", "argument");
+  if (dims->batch == 0) return RR_OK;
+  const int64_t b = dims->batch, N = dims->N, n = dims->nx, m = dims->nu;
+  const int64_t sn = n * (n + 1) / 2, sm = m * (m + 1) / 2;
+  const bool shD = (dims->flags & RR_FLAG_SHARED_DYN) != 0, shP = (dims->flags & RR_FLAG_SHARED_COST) != 0;
+  const int64_t nc = nchunks > b ? b : nchunks;
+  // per-chunk workspace slices, each 256-byte aligned, carved from the caller's buffer
+  int64_t need = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    rr_dims dc = *dims;
+    dc.batch = b * (c + 1) / nc - b * c / nc;
+    const int64_t w = rr_workspace_bytes(&dc);
+    if (w < 0) return set_err(RR_E_UNSUPPORTED, "rr_factor_solve_host_pipelined: no kernel for this shape%s");
+    need += (w + 255) & ~(int64_t)255;
+  }
+  if (workspace == nullptr || workspace_bytes < need)
+    return set_err(RR_E_INVALID, "rr_factor_solve_host_pipelined: workspace smaller than %s",
+                   "the sum of rr_workspace_bytes over the chunks (+256 B alignment each)");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0)
+    return set_err(RR_E_INVALID, "rr_factor_solve_host_pipelined: workspace not %s", "256-byte aligned");
+  cudaStream_t s0 = static_cast<cudaStream_t>(streams[0]);
+  auto h2d = [&](const double* h, const double* d, int64_t off, int64_t cnt, cudaStream_t s) -> cudaError_t {
+    if (cnt == 0) return cudaSuccess;
+    if (!h || !d) return cudaErrorInvalidValue;
+    return cudaMemcpyAsync(const_cast<double*>(d) + off, h + off, sizeof(double) * cnt, cudaMemcpyHostToDevice, s);
+  };
+  cudaError_t e = cudaSuccess;
+  // batch-shared operands once, on streams[0], before the fork
+  if (shD) {
+    if ((e = h2d(ph->A, pd->A, 0, N * n * n, s0)) != cudaSuccess || (e = h2d(ph->B, pd->B, 0, N * n * m, s0)) != cudaSuccess)
+      return set_err(RR_E_CUDA, "rr_factor_solve_host_pipelined: H2D %s", cudaGetErrorString(e));
+  }
+  if (shP) {
+    if ((e = h2d(ph->Q, pd->Q, 0, N * sn, s0)) != cudaSuccess || (e = h2d(ph->M, pd->M, 0, N * n * m, s0)) != cudaSuccess ||
+        (e = h2d(ph->R, pd->R, 0, N * sm, s0)) != cudaSuccess || (e = h2d(ph->QN, pd->QN, 0, sn, s0)) != cudaSuccess)
+      return set_err(RR_E_CUDA, "rr_factor_solve_host_pipelined: H2D %s", cudaGetErrorString(e));
+  }
+  // fork: streams[1..] wait for everything enqueued on streams[0] so far
+  cudaEvent_t fork = nullptr;
+  if (nstreams > 1) {
+    if ((e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventRecord(fork, s0)) != cudaSuccess)
+      return set_err(RR_E_CUDA, "rr_factor_solve_host_pipelined: event %s", cudaGetErrorString(e));
+    for (int k = 1; k < nstreams; ++k)
+      if ((e = cudaStreamWaitEvent(static_cast<cudaStream_t>(streams[k]), fork, 0)) != cudaSuccess) break;
+    cudaEventDestroy(fork);  // released once the recorded work completes
+    if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_factor_solve_host_pipelined: event %s", cudaGetErrorString(e));
+  }
+  char* wsp = static_cast<char*>(workspace);
+  for (int64_t c = 0; c < nc && e == cudaSuccess; ++c) {
+    cudaStream_t s = static_cast<cudaStream_t>(streams[c % nstreams]);
+    const int64_t i0 = b * c / nc, cb = b * (c + 1) / nc - i0;
+    rr_dims dc = *dims;
+    dc.batch = cb;
+    // H2D of the chunk's slices (every per-instance operand is [batch][...] contiguous)
+    struct Op { const double* h; const double* d; int64_t per; bool inst; } ops[] = {
+        {ph->A, pd->A, N * n * n, !shD}, {ph->B, pd->B, N * n * m, !shD}, {ph->Q, pd->Q, N * sn, !shP},
+        {ph->M, pd->M, N * n * m, !shP}, {ph->R, pd->R, N * sm, !shP},    {ph->q, pd->q, N * n, true},
+        {ph->r, pd->r, N * m, true},     {ph->c, pd->c, N * n, true},     {ph->QN, pd->QN, sn, !shP},
+        {ph->qN, pd->qN, n, true},       {ph->c0, pd->c0, n, true},       {ph->delta, pd->delta, 1, true}};
+    for (const Op& o : ops)
+      if (o.inst && (e = h2d(o.h, o.d, i0 * o.per, cb * o.per, s)) != cudaSuccess) break;
+    if (e != cudaSuccess) break;
+    // the chunk's problem / solution views (batch-shared operands keep their base pointers)
+    rr_problem pc = *pd;
+    auto off = [&](const double* p, int64_t per, bool inst) { return (inst && p) ? p + i0 * per : p; };
+    pc.A = off(pd->A, N * n * n, !shD);
+    pc.B = off(pd->B, N * n * m, !shD);
+    pc.Q = off(pd->Q, N * sn, !shP);
+    pc.M = off(pd->M, N * n * m, !shP);
+    pc.R = off(pd->R, N * sm, !shP);
+    pc.q = off(pd->q, N * n, true);
+    pc.r = off(pd->r, N * m, true);
+    pc.c = off(pd->c, N * n, true);
+    pc.QN = off(pd->QN, sn, !shP);
+    pc.qN = off(pd->qN, n, true);
+    pc.c0 = off(pd->c0, n, true);
+    pc.delta = off(pd->delta, 1, true);
+    rr_solution sc = {sd->x + i0 * (N + 1) * n, sd->u ? sd->u + i0 * N * m : nullptr, sd->y + i0 * (N + 1) * n};
+    const int64_t wb = rr_workspace_bytes(&dc);
+    rr_err rc = rr_factor_solve(&dc, &pc, nullptr, &sc, wsp, wb, status_dev + i0, s);
+    if (rc != RR_OK) return rc;
+    wsp += (wb + 255) & ~(int64_t)255;
+    struct Out { double* h; const double* d; int64_t per; } outs[] = {
+        {sh->x, sd->x, (N + 1) * n}, {sh->u, sd->u, N * m}, {sh->y, sd->y, (N + 1) * n}};
+    for (const Out& o : outs) {
+      if (o.per == 0 || o.h == nullptr) continue;
+      if ((e = cudaMemcpyAsync(o.h + i0 * o.per, o.d + i0 * o.per, sizeof(double) * cb * o.per, cudaMemcpyDeviceToHost,
+                               s)) != cudaSuccess)
+        break;
+    }
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(status_host + i0, status_dev + i0, sizeof(int32_t) * cb, cudaMemcpyDeviceToHost, s);
+  }
+  if (e != cudaSuccess) return set_err(RR_E_CUDA, "rr_factor_solve_host_pipelined: copy %s", cudaGetErrorString(e));
+  // join: streams[0] waits for the others, so its completion is the call's completion
+  for (int k = 1; k < nstreams; ++k) {
+    cudaEvent_t join = nullptr;
+    if ((e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventRecord(join, static_cast<cudaStream_t>(streams[k]))) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s0, join, 0)) != cudaSuccess) {
+      if (join) cudaEventDestroy(join);
+      return set_err(RR_E_CUDA, "rr_factor_solve_host_pipelined: event %s", cudaGetErrorString(e));
+    }
+    cudaEventDestroy(join);
+  }
+  return RR_OK;
+}
+
 int32_t rr_factor_record_doubles(int32_t n, int32_t m) { return rrk::frec_doubles(n, m); }
 
 int64_t rr_factor_bytes(const rr_dims* dims) {

@@ -329,3 +329,24 @@ class HostMarshalled:
                                         self.sth, ctypes.byref(self.pd), ctypes.byref(self.sd), self.std,
                                         self.wsp, self.wsb, ctypes.c_void_p(s.cuda_stream))
         check(rc, "rr_factor_solve_host")
+
+    def pipelined_workspace_bytes(self, nchunks: int) -> int:
+        """Workspace rr_factor_solve_host_pipelined needs for `nchunks` chunks."""
+        b, tot = self.d.batch, 0
+        nc = min(nchunks, b)
+        for c in range(nc):
+            cb = b * (c + 1) // nc - b * c // nc
+            w = lib().rr_workspace_bytes(ctypes.byref(rr_dims(self.d.nx, self.d.nu, self.d.N, self.d.flags, cb)))
+            tot += (w + 255) & ~255
+        return tot
+
+    def launch_pipelined(self, streams, nchunks: int = 8, ws=None):
+        """rr_factor_solve_host_pipelined: chunks round-robin over `streams` (torch.cuda.Stream list;
+        streams[0] is the completion stream).  ws: a workspace of pipelined_workspace_bytes(nchunks)."""
+        if ws is None:
+            ws = self.ws
+        arr = (ctypes.c_void_p * len(streams))(*[s_.cuda_stream for s_ in streams])
+        rc = lib().rr_factor_solve_host_pipelined(ctypes.byref(self.d), ctypes.byref(self.ph), ctypes.byref(self.sh),
+                                                  self.sth, ctypes.byref(self.pd), ctypes.byref(self.sd), self.std,
+                                                  _p(ws), ws.numel() * 8, int(nchunks), arr, len(streams))
+        check(rc, "rr_factor_solve_host_pipelined")

@@ -72,3 +72,37 @@ def test_shared_large_shape_unsupported():
     p = synth.lti_problem(40, 20, 3, 2, seed=1).to("cuda")
     with pytest.raises(m.RRError):
         m.rr_factor_solve(p)
+
+
+@pytest.mark.parametrize("shared,nchunks,nstreams", [(False, 7, 3), (False, 1, 1), (True, 5, 2), (False, 50, 3)])
+def test_host_pipelined_equals_serial(shared, nchunks, nstreams):
+    """rr_factor_solve_host_pipelined (chunks round-robin over streams, copies overlapped with the
+    solve) gives bitwise the results of rr_factor_solve_host, per-instance and batch-shared operands,
+    more chunks than instances included."""
+    m = rr()
+    if shared:
+        p = synth.lti_problem(12, 4, 10, 23, seed=5)
+    else:
+        p = synth.random_stable_lqr(12, 4, 10, 23 if nchunks < 50 else 13, seed=5, delta=1e-4)
+    hp = synth.RRProblem(p.nx, p.nu, p.N, **{f: getattr(p, f).pin_memory() for f in p.FIELDS})
+    dp = p.to("cuda")
+    out = []
+    for pipelined in (False, True):
+        hs = {k: torch.full(v.shape, float("nan"), dtype=v.dtype).pin_memory() if v.is_floating_point()
+              else torch.zeros(v.shape, dtype=v.dtype).pin_memory() for k, v in m.alloc_solution(dp).items()}
+        ds = m.alloc_solution(dp)
+        call = m.HostMarshalled(hp, hs, dp, ds)
+        if pipelined:
+            streams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(nstreams - 1)]
+            ws = torch.empty((call.pipelined_workspace_bytes(nchunks) + 7) // 8, dtype=torch.float64, device="cuda")
+            call.launch_pipelined(streams, nchunks, ws)
+            streams[0].synchronize()
+        else:
+            call.launch()
+        torch.cuda.synchronize()
+        out.append(hs)
+    for k in ("x", "u", "y", "status"):
+        assert torch.equal(out[0][k], out[1][k]), k
+    o = oracle.rr_solve_t2(p.expanded() if shared else p)
+    for k in ("x", "u", "y"):
+        assert rel(out[1][k].numpy(), o[k]) <= 1e-9
