@@ -73,6 +73,9 @@ def parse():
                          "pit = single-instance latency, parallel-in-time vs sequential, long horizons")
     ap.add_argument("--c5-total", type=int, default=1048576, help=argparse.SUPPRESS)
     ap.add_argument("--ref-seconds", type=float, default=150.0, help=argparse.SUPPRESS)  # reference-arm budget
+    ap.add_argument("--no-others", action="store_true",
+                    help="default C2 run at N=1: skip the short runs of the other BASELINE configs attached "
+                         "to the line (other_workloads)")
     return ap.parse_args()
 
 
@@ -430,8 +433,38 @@ def main():
                 "C3 instances, T2 plain-C oracle", calib=2, cap=512)
         else:
             line["cpu_baseline"] = cpu_baseline(a.cpu_seconds)
+    if ws == 1 and a.workload == "c2" and not a.no_others:
+        # the other BASELINE configs (C3, C4, C5) and the split / IPM-solve paths, each a short run of
+        # this script in its own process (own timing, own roofline), summarised on this line so that
+        # every config has a number in the driver's bench record
+        del prob, sol, call
+        torch.cuda.empty_cache()
+        line["other_workloads"] = other_workloads(a)
     print(json.dumps(line), flush=True)
     barrier(ws)
+
+
+def other_workloads(a):
+    out = {}
+    steps = str(max(3, min(a.steps, 5)))
+    for w in ("c3", "c4", "c5", "split", "c4swing"):
+        cmd = [sys.executable, os.path.abspath(__file__), "--workload", w, "--steps", steps, "--warmup", "3",
+               "--no-cpu-baseline", "--no-e2e"]
+        t0 = time.perf_counter()
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+            d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+            keep = {k: d.get(k) for k in ("metric", "value", "unit", "ms_per_step", "config", "clocks", "status_nonzero",
+                                          "status_counts", "iterations", "gpu_launches")
+                    if d.get(k) is not None}
+            rf = d.get("roofline") or {}
+            keep["roofline"] = {k: rf.get(k) for k in ("bound", "achieved", "peak", "unit", "frac", "kernel", "kernels")
+                                if rf.get(k) is not None}
+            keep["wall_s"] = round(time.perf_counter() - t0, 1)
+            out[w] = keep
+        except Exception as e:  # noqa: BLE001 -- recorded, never fatal for the headline line
+            out[w] = {"error": "%s: %s" % (type(e).__name__, str(e)[:200])}
+    return out
 
 
 def run_c4(a, ws, rank, local):
