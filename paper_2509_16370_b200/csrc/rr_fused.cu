@@ -655,6 +655,20 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
       bool bad = (j < n) && !isfinite(xj);
       const int ui = j - NX;
       constexpr int ABP = ((n * n + n * m) + 1) & ~1;
+      // record offsets of row j of V_i (packed symmetric) or of K_i (lanes NX..), two per register
+      uint32_t yofs[NX / 2];
+#pragma unroll
+      for (int k = 0; k < NX; k += 2) {
+        uint32_t o[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kk = k + h;
+          o[h] = (j < NX) ? (uint32_t)(RC::V + (kk >= j ? pidx(NX, kk, j) : pidx(NX, j, kk)))
+                          : (uint32_t)(RC::K + kk * NU + (ui < NU ? ui : 0));
+        }
+        yofs[k >> 1] = o[0] | (o[1] << 16);
+      }
+      const int ybase = (j < NX) ? RC::v + j : RC::k + (ui < NU ? ui : 0);
       auto rbuf = [&](double* sl, int b) { return sl + b * RC::PAD; };
       auto abuf = [&](double* sl, int b) { return sl + 2 * RC::PAD + b * ABP; };
       double* xch = slot + 2 * RC::PAD + 2 * ABP;  // exchange: u (NU, padded to even) | z (NX) | x (NX)
@@ -699,24 +713,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
         const double* ab = abuf(slot, b);
         if (i + 1 < N) issue_fwd(i + 1, b ^ 1);
         wait_fwd(b);
-        // y_i = V_i x_i + v_i (lanes < NX);  u_i = K_i x_i + k_i (lanes NX..)
-        double a0 = 0.0, a1 = 0.0;
-        if (j < NX) {
-          a0 = rc[RC::v + j];
+        // y_i = V_i x_i + v_i (lanes < NX);  u_i = K_i x_i + k_i (lanes NX..): one code path for
+        // all lanes through the per-lane record offsets yofs (no divergent V / K branches)
+        double a0 = (j < NZ) ? rc[ybase] : 0.0, a1 = 0.0;
 #pragma unroll
-          for (int k = 0; k < NX; k += 2) {
-            const int i0 = k >= j ? pidx(NX, k, j) : pidx(NX, j, k);
-            const int i1 = k + 1 >= j ? pidx(NX, k + 1, j) : pidx(NX, j, k + 1);
-            a0 = fma(rc[RC::V + i0], xr[k], a0);
-            a1 = fma(rc[RC::V + i1], xr[k + 1], a1);
-          }
-        } else if (ui < NU) {
-          a0 = rc[RC::k + ui];
-#pragma unroll
-          for (int k = 0; k < NX; k += 2) {
-            a0 = fma(rc[RC::K + k * NU + ui], xr[k], a0);
-            a1 = fma(rc[RC::K + (k + 1) * NU + ui], xr[k + 1], a1);
-          }
+        for (int k = 0; k < NX; k += 2) {
+          const uint32_t o2 = yofs[k >> 1];
+          a0 = fma(rc[o2 & 0xffffu], xr[k], a0);
+          a1 = fma(rc[o2 >> 16], xr[k + 1], a1);
         }
         const double yu = a0 + a1;
         if (valid) {

@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 for k in 1 2; do
   for v in "$@"; do
     if [ "$v" = cur ]; then L=paper_2509_16370_b200/librr_b200.so; else L=paper_2509_16370_b200/librr_b200_$v.so; fi
-    RR_B200_LIB=$PWD/$L timeout 300 python bench.py --steps ${STEPS:-10} --no-cpu-baseline --no-e2e ${BENCH_ARGS:-} \
+    RR_B200_LIB=$PWD/$L timeout 300 python bench.py --steps ${STEPS:-10} --no-cpu-baseline --no-e2e --no-others ${BENCH_ARGS:-} \
       > gpurun_out/ab_${v}_$k.json 2> gpurun_out/ab_${v}_$k.err
     python - "$v" "$k" <<'PY'
 import json, sys

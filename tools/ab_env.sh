@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 for k in 1 2; do
   for spec in "$@"; do
     name=${spec%%:*}; envs=${spec#*:}
-    env $(echo "$envs" | tr ',' ' ') timeout 300 python bench.py --steps ${STEPS:-10} --no-cpu-baseline --no-e2e ${BENCH_ARGS:-} \
+    env $(echo "$envs" | tr ',' ' ') timeout 300 python bench.py --steps ${STEPS:-10} --no-cpu-baseline --no-e2e --no-others ${BENCH_ARGS:-} \
       > gpurun_out/abe_${name}_$k.json 2> gpurun_out/abe_${name}_$k.err
     python - "$name" "$k" <<'PY'
 import json, sys
