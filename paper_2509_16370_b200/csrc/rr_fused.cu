@@ -675,8 +675,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
       double* uch = xch;
       double* zch = xch + ((NU + 1) & ~1);
       double* xsh = zch + NX;
-      // records were written through the generic proxy; order them (and this slot's generic
-      // shared-memory writes) before the TMA (async-proxy) reads / refills
+      // records: the backward's TMA bulk stores must be complete before the TMA loads read them (lane 0
+      // issued both); generic shared-memory writes of this slot ordered before the TMA refills
+      if (lane == 0) bulk_wait0();
       asm volatile("fence.proxy.async;\n" ::: "memory");
       __syncwarp();
       auto issue_fwd = [&](int i, int b) {

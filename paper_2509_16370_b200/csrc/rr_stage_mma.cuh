@@ -224,6 +224,10 @@ struct StageMMA {
       wk[WM::X1 + NX * NX + j] = ve0 + ve1;  // column NX of Vs
     }
     __syncwarp();
+#ifndef RR_REC_STG
+    if (lane == 0) bulk_wait_read0();  // the previous stage's record bulk stores have read X2
+    __syncwarp();
+#endif
 #ifndef RR_SMEM_CHAIN
     // (2)-(5) per instance q, in DMMA registers: [W | We] = S⁻¹ Vs, X = Fᵀ W, U = Fᵀ Xᵀ + P.
     // A C fragment holds C[g][2t], C[g][2t+1]; used with the contraction index permuted to
@@ -594,7 +598,14 @@ struct StageMMA {
     {  // record: S_{i+1}⁻¹, e, K, k, V, v (no closed-loop products)
       __syncwarp();
       prefetch();
+#ifndef RR_REC_STG
+      // staged in this instance's X2 (U is in registers since the elimination) and written to HBM
+      // by one TMA bulk store per instance: the scattered 8-byte global stores of the packed columns
+      // cost L1 wavefronts on the LSU pipe the kernel is bound by
+      double* rec = (grp ? recq[1] : recq[0]) != nullptr ? wk + WM::X2 : nullptr;
+#else
       auto* rec = grp ? recq[1] : recq[0];
+#endif
       if (rec != nullptr) {
         if (j < NX) {
           auto* Sp = rec + RC::S + j * (2 * NX - j - 1) / 2;
@@ -613,6 +624,17 @@ struct StageMMA {
           rec[RC::k + (j - NX)] = -bj;
         }
       }
+#ifndef RR_REC_STG
+      static_assert(RC::SIZE <= 16 * WM::ULD && (RC::SIZE % 2) == 0, "record staging needs X2 and 16-byte size");
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          if (recq[q] != nullptr) bulk_s2g(recq[q], wkq[q] + WM::X2, 8u * RC::SIZE);
+        bulk_commit();
+      }
+#endif
 #pragma unroll
       for (int r = 0; r < NX; ++r) Vc[r] = (j < NX) ? U[r] : 0.0;
       __syncwarp();
