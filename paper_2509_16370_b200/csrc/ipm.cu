@@ -196,26 +196,12 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
   double* sbuf0 = slot;
   double* sbuf1 = slot + IB::PAD;
   double* sb = sbuf0;
+  bool pk = false;  // sb holds a stage loaded by the exact path: P packed (Q | M | R) in the P slot
   // ---- issue the loads of stage i (i == N: terminal) into the padded shared layout `dst` ----
   // Real elements travel by cp.async (8-byte LDGSTS, asynchronous); padding is stored directly.
   // finish_stage() completes Σ, r_z and the positivity check once the copies have landed.
   // the padded layout equals the global one when the dims are the template dims: contiguous copies
   const bool exact = (n == NX && m == NU && ngd == NG && ncd == NC);
-  // per-lane gather table of the unpacked P (exact path): entry e = j + t·LG of the NZ × NZ
-  // col-major P comes from Q (sel 0, packed 'L'), M (sel 1) or R (sel 2, packed); code = off·4 + sel
-  constexpr int PT = (NZ * NZ + LG - 1) / LG;
-  int pg[PT];
-#pragma unroll
-  for (int t = 0; t < PT; ++t) {
-    const int e = j + t * LG, r = e % NZ, c = e / NZ;
-    int code;
-    if (e >= NZ * NZ) code = 3;
-    else if (r < NX && c < NX) code = (r >= c ? pidx(NX, r, c) : pidx(NX, c, r)) * 4;
-    else if (r < NX) code = (r + (c - NX) * NX) * 4 + 1;
-    else if (c < NX) code = (c + (r - NX) * NX) * 4 + 1;
-    else code = (r >= c ? pidx(NU, r - NX, c - NX) : pidx(NU, c - NX, r - NX)) * 4 + 2;
-    pg[t] = code;
-  }
   auto issue_stage_data = [&](int i, double* dst) {
     const bool term = (i == N);
     const int ww = term ? n : w;
@@ -229,15 +215,12 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
     if (exact && !term) {
       copy_async(dst + IB::F, a.d_.A + si * NX * NX, NX * NX, j, LG);       // F = [A | B], ld NX
       copy_async(dst + IB::F + NX * NX, a.d_.B + si * NX * NU, NX * NU, j, LG);
-      {  // P = [[Q M]; [Mᵀ R]] unpacked through the per-lane gather table
-        const double* bq = a.d_.Q + si * (NX * (NX + 1) / 2);
-        const double* bm = a.d_.M + si * (NX * NU);
-        const double* br = a.d_.R + si * (NU * (NU + 1) / 2);
-#pragma unroll
-        for (int t = 0; t < PT; ++t) {
-          const int code = pg[t], sel = code & 3;
-          if (sel != 3) cp_async8(dst + IB::P + j + t * LG, (sel == 0 ? bq : (sel == 1 ? bm : br)) + (code >> 2));
-        }
+      {  // P packed as Q | M | R in the P slot (read through Pjs): contiguous copies instead of a
+         // per-element gather into the unpacked layout (fewer LDGSTS, fewer bank conflicts)
+        constexpr int SQ = NX * (NX + 1) / 2, SR = NU * (NU + 1) / 2;
+        copy_async(dst + IB::P, a.d_.Q + si * SQ, SQ, j, LG);
+        copy_async(dst + IB::P + SQ, a.d_.M + si * (NX * NU), NX * NU, j, LG);
+        copy_async(dst + IB::P + SQ + NX * NU, a.d_.R + si * SR, SR, j, LG);
       }
       copy_async(dst + IB::gf, a.d_.gradf + si * NZ, NZ, j, LG);
       copy_async(dst + IB::cv, a.d_.dres + si * NX, NX, j, LG);
@@ -364,10 +347,23 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
 #pragma unroll
     for (int e = 0; e < NC; ++e) cej[e] = eta * sb[IB::Ce + e + jc * NC];
   };
+  // P[s][j] of the current stage: packed Q | M | R (exact path, stages < N) or unpacked NZ × NZ
+  auto Pjs = [&](int s_) -> double {
+    if (pk) {
+      constexpr int MO = NX * (NX + 1) / 2, RO = MO + NX * NU;
+      const int jj = j < NZ ? j : 0;
+      int off;
+      if (s_ < NX) off = (jj < NX) ? ((s_ >= jj) ? pidx(NX, s_, jj) : pidx(NX, jj, s_)) : MO + s_ + (jj - NX) * NX;
+      else if (jj < NX) off = MO + jj + (s_ - NX) * NX;
+      else off = RO + ((s_ >= jj) ? pidx(NU, s_ - NX, jj - NX) : pidx(NU, jj - NX, s_ - NX));
+      return sb[IB::P + off];
+    }
+    return sb[IB::P + j * NZ + s_];
+  };
   // condensed P̃ column j: P + GᵀΣG + η C_eᵀC_e
   auto Pt = [&](int s) -> double {
     if (j >= NZ) return 0.0;
-    double v = sb[IB::P + j * NZ + s];
+    double v = Pjs(s);
 #pragma unroll
     for (int e = 0; e < NG; ++e) v = fma(sb[IB::G + e + s * NG], gsj[e], v);
 #pragma unroll
@@ -407,6 +403,7 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
   cp_async_commit();
   for (int i = N - 1; i >= 0; --i) {
     sb = ((N - 1 - i) & 1) ? sbuf0 : sbuf1;
+    pk = exact;
     if (i > 0) issue_stage_data(i - 1, ((N - 1 - i) & 1) ? sbuf1 : sbuf0);
     cp_async_commit();
     cp_async_wait<1>();
@@ -509,7 +506,7 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
     if (j < NZ) {
       double pd = 0.0;
 #pragma unroll
-      for (int c = 0; c < NZ; ++c) pd = fma(sb[IB::P + j * NZ + c], dz_full[c], pd);
+      for (int c = 0; c < NZ; ++c) pd = fma(Pjs(c), dz_full[c], pd);
       double dj = 0.0;
 #pragma unroll
       for (int c = 0; c < NZ; ++c) dj = (c == j) ? dz_full[c] : dj;
@@ -524,17 +521,18 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
   __syncwarp();
   if (N > 0) {
     issue_stage_data(0, sbuf0);
-    copy_async(rbuf, rec0, RC::SIZE, j, LG);
+    copy_async(rbuf, rec0, RC::PAD, j, LG);  // PAD (even): 16-byte copies
   } else {
     issue_stage_data(N, sbuf0);
   }
   cp_async_commit();
   for (int i = 0; i < N; ++i) {
     sb = (i & 1) ? sbuf1 : sbuf0;
+    pk = exact;
     const double* rc = (i & 1) ? rbuf + RC::PAD : rbuf;
     if (i + 1 < N) {
       issue_stage_data(i + 1, (i & 1) ? sbuf0 : sbuf1);
-      copy_async((i & 1) ? rbuf : rbuf + RC::PAD, rec0 + (int64_t)(i + 1) * RC::PAD, RC::SIZE, j, LG);
+      copy_async((i & 1) ? rbuf : rbuf + RC::PAD, rec0 + (int64_t)(i + 1) * RC::PAD, RC::PAD, j, LG);
     } else {
       issue_stage_data(N, (i & 1) ? sbuf0 : sbuf1);  // terminal data for after the loop
     }
@@ -603,6 +601,7 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
   cp_async_wait<0>();
   __syncwarp();
   sb = (N & 1) ? sbuf1 : sbuf0;
+  pk = false;
   finish_stage(N);
   cache_cols();
   {
