@@ -631,9 +631,27 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
     for (int off = LG / 2; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(gmask, v, off));
     return v;
   };
+  const double D = gsum(sD);
+  const double K0 = gsum(sK0) + a.d_.fval[inst];
+  const double K1 = gsum(sK1), K2 = gsum(sK2);
+  const double Abase = K0 - mu * gsum(sLog.value());
+  amax = gmin(amax);
+  admax = gmin(admax);
+  int32_t status = st;
+  int np = nonpos_stage;
+#pragma unroll
+  for (int off = LG / 2; off > 0; off >>= 1) {
+    status = max(status, __shfl_xor_sync(gmask, status, off));
+    np = min(np, __shfl_xor_sync(gmask, np, off));
+  }
+  if (status == 0 && (__ballot_sync(gmask, bad) & gmask)) status = RR_ST_NONFINITE;
+  if (np != 0x7fffffff) status = mk_status(RR_ST_NONPOS_SLACK, np);
   // dynamics terms of 𝒜 at α = 0 through the built-in model (as the oracle's merit evaluates them),
-  // stages distributed over the lanes of the group (one model evaluation per lane per LG stages)
-  if (model != IPM_MODEL_LQ) {
+  // stages distributed over the lanes: inside the first trial of the line search (sharing its loads
+  // of x̄, ū, y) when there is one, else in a pass of their own
+  const bool fuse0 = model != IPM_MODEL_LQ && status == 0 && !a.direction_only;
+  double A0 = Abase;
+  if (model != IPM_MODEL_LQ && !fuse0) {
     for (int i = j; i < N; i += LG) {
       const double* xb = a.it.x + (inst * (sN + 1) + i) * n;
       const double* ub = a.it.u + (inst * sN + i) * m;
@@ -652,22 +670,8 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
         }
       }
     }
+    A0 = Abase + gsum(sDyn0);
   }
-  const double D = gsum(sD);
-  const double K0 = gsum(sK0) + a.d_.fval[inst];
-  const double K1 = gsum(sK1), K2 = gsum(sK2);
-  const double A0 = K0 + gsum(sDyn0) - mu * gsum(sLog.value());
-  amax = gmin(amax);
-  admax = gmin(admax);
-  int32_t status = st;
-  int np = nonpos_stage;
-#pragma unroll
-  for (int off = LG / 2; off > 0; off >>= 1) {
-    status = max(status, __shfl_xor_sync(gmask, status, off));
-    np = min(np, __shfl_xor_sync(gmask, np, off));
-  }
-  if (status == 0 && (__ballot_sync(gmask, bad) & gmask)) status = RR_ST_NONFINITE;
-  if (np != 0x7fffffff) status = mk_status(RR_ST_NONPOS_SLACK, np);
 
   // ================= pass 3: Armijo backtracking over (x, s) with 𝒜 =================
   double alpha = amax, Aacc = __longlong_as_double(0x7ff8000000000000LL);
@@ -722,8 +726,23 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
               sdyn += yb[r] * cr + 0.5 * eta * cr * cr;
             }
           }
+          if (fuse0 && nb == 0) {  // the α = 0 terms on the same loads
+#pragma unroll
+            for (int r = 0; r < NX; ++r) xa[r] = (r < n) ? xb[r] : 0.0;
+#pragma unroll
+            for (int r = 0; r < NU; ++r) ua[r] = (r < m) ? ub[r] : 0.0;
+            model_step<NX, NU>(model, a.d_.model_params, xa, ua, xnm);
+#pragma unroll
+            for (int r = 0; r < NX; ++r) {
+              if (r < n) {
+                const double cr = xnm[r] - xb[n + r];
+                sDyn0 += yb[r] * cr + 0.5 * eta * cr * cr;
+              }
+            }
+          }
         }
       }
+      if (fuse0 && nb == 0) A0 = Abase + gsum(sDyn0);
       const double slog = gsum(sl.value());
       sdyn = gsum(sdyn);
       const bool allpos = __ballot_sync(gmask, !pos) == 0;
