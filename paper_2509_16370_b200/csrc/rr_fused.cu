@@ -323,11 +323,7 @@ struct MmaLayout {
   static constexpr int STG = NX * NX + 2 * NX * NU + NX * (NX + 1) / 2 + NU * (NU + 1) / 2 + 2 * NX + NU;
   static constexpr int STG_PAD = (STG + 1) & ~1;
   static constexpr int SLOT_B = STG_PAD + WorkM<NX, NU>::PAD;  // single stage buffer (prefetched mid-stage)
-#ifndef RR_FWD_PHI
   static constexpr int SLOT_F = 2 * RecM<NX, NU>::PAD + 2 * (((NX * NX + NX * NU) + 1) & ~1) + ((NU + 1) & ~1) + 2 * NX;
-#else
-  static constexpr int SLOT_F = 2 * RecM<NX, NU>::PAD + NX;
-#endif
   static constexpr int BAR = ((SLOT_B > SLOT_F ? SLOT_B : SLOT_F) + 1) & ~1;  // 2 mbarriers (TMA completion)
   static constexpr int SLOT = BAR + 2;
   // slot stride ≡ 8 (mod 16) doubles: the two instances of a warp (half-warps) reading the same
@@ -369,38 +365,30 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
   double* slot = grp ? slotq[1] : slotq[0];
   double* wkq[2] = {slotq[0] + LY::STG_PAD, slotq[1] + LY::STG_PAD};
 #ifndef RR_NO_PTAB
-  int* ptab = reinterpret_cast<int*>(smem + WARPS * 2 * LY::SLOT_PAD);
-  if (warp == 0) {
+  // P-gather offsets of this lane's U C-fragment positions (k = (mt·ZT + nt)·2 + e: row 8mt + g,
+  // column 8nt + 2t + e of P = [[Q M]; [Mᵀ R]] in the stage buffer), two 16-bit offsets per register
+  static_assert((NX + NU) % 8 == 0 && LY::STG < 65536, "register P-gather offsets need full 8-wide tiles");
+  uint32_t ptw[LY::PTAB / 2];
+  {
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int k = 0; k < LY::PTAB; ++k) {
-      const int e = k & 1, nt = (k >> 1) % LY::ZT, mt = (k >> 1) / LY::ZT;
-      const int s = 8 * mt + g, c = 8 * nt + 2 * t + e;
-      int off = -1;
-      if (s < NZ && c < NZ) {
-        if (s < NX && c < NX) off = oQ + (s >= c ? pidx(n, s, c) : pidx(n, c, s));
-        else if (s < NX) off = oM + s + (c - NX) * n;
-        else if (c < NX) off = oM + c + (s - NX) * n;
-        else off = oR + (s >= c ? pidx(m, s - NX, c - NX) : pidx(m, c - NX, s - NX));
+    for (int k2 = 0; k2 < LY::PTAB / 2; ++k2) {
+      uint32_t o2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = 2 * k2 + h;
+        const int e = k & 1, nt = (k >> 1) % LY::ZT, mt = (k >> 1) / LY::ZT;
+        const int s_ = 8 * mt + g, c = 8 * nt + 2 * t + e;
+        int off;
+        if (s_ < NX && c < NX) off = oQ + (s_ >= c ? pidx(n, s_, c) : pidx(n, c, s_));
+        else if (s_ < NX) off = oM + s_ + (c - NX) * n;
+        else if (c < NX) off = oM + c + (s_ - NX) * n;
+        else off = oR + (s_ >= c ? pidx(m, s_ - NX, c - NX) : pidx(m, c - NX, s_ - NX));
+        o2[h] = (uint32_t)off;
       }
-      ptab[k * 32 + lane] = off;  // [position][lane]: consecutive lanes, conflict-free
+      ptw[k2] = o2[0] | (o2[1] << 16);
     }
   }
-  __syncthreads();
-#endif
-#ifndef RR_NO_PTAB
-  // the table read once into registers (two 16-bit offsets per register) when every fragment
-  // position lies inside P: the per-stage gather then issues no table loads (−1.4% on C2);
-  // RR_PTAB_SMEM keeps the per-stage table reads
-#ifdef RR_PTAB_SMEM
-  constexpr bool PREG = false;
-#else
-  constexpr bool PREG = (NX + NU) % 8 == 0 && LY::STG < 65536;
-#endif
-  uint32_t ptw[LY::PTAB / 2];
-#pragma unroll
-  for (int k2 = 0; k2 < LY::PTAB / 2; ++k2)
-    ptw[k2] = PREG ? ((uint32_t)ptab[(2 * k2) * 32 + lane] | ((uint32_t)ptab[(2 * k2 + 1) * 32 + lane] << 16)) : 0u;
 #endif
   double* wk = grp ? wkq[1] : wkq[0];
   const int64_t sN = (int64_t)N;
@@ -550,15 +538,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
       auto P2 = [&](int q, int s, int t) -> double { return Pat(sbq[q], s, t); };
 #elif defined(RR_P_SIMT)
       auto P2 = [&](int s) -> double { return Pat(sb, s, j); };  // column j of this lane's P
-      (void)ptab;
 #else
       auto P2 = [&](int q, int k) -> double {
-        if constexpr (PREG) {  // offsets packed as 16-bit halves of per-lane registers (no table loads)
-          return sbq[q][(int)((ptw[k >> 1] >> (16 * (k & 1))) & 0xffffu)];
-        } else {
-          const int off = ptab[k * 32 + lane];
-          return off >= 0 ? sbq[q][off] : 0.0;
-        }
+        return sbq[q][(int)((ptw[k >> 1] >> (16 * (k & 1))) & 0xffffu)];  // offsets in registers
       };
       (void)Pat;
 #endif
@@ -801,7 +783,7 @@ template <int NX, int NU, int WARPS, int MINB, bool FAC = false, bool F32 = fals
 struct MmaCfg {
   static constexpr int IPB = WARPS * 2;
   static size_t smem_bytes() {
-    return sizeof(double) * (size_t)IPB * MmaLayout<NX, NU>::SLOT_PAD + sizeof(int) * 32 * MmaLayout<NX, NU>::PTAB;
+    return sizeof(double) * (size_t)IPB * MmaLayout<NX, NU>::SLOT_PAD;
   }
   static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * RecM<NX, NU>::PAD; }
   static cudaError_t launch(const FusedArgs& a0, cudaStream_t s) {
@@ -847,7 +829,8 @@ static bool dispatch_fused(int nx, int nu, F&& f) {
     if (v == 2) return f(FusedCfg<12, 4, 16, 4, 2, true>{});
     if (v == 3) return f(MmaCfg<12, 4, 2, 6>{});
     if (v == 4) return f(MmaCfg<12, 4, 4, 2>{});
-    return f(MmaCfg<12, 4, 4, 3>{});
+    if (v == 5) return f(MmaCfg<12, 4, 4, 3>{});  // A/B: 3 CTAs per SM (168 registers)
+    return f(MmaCfg<12, 4, 4, 4>{});              // 4 CTAs (16 warps) per SM: 128 registers, 55.5 KB
   }
   if (nx == 4 && nu == 1) return f(FusedCfg<4, 1, 8, 4, 4, true>{});
   if (nx == 2 && nu == 1) return f(FusedCfg<2, 1, 4, 4, 4, true>{});

@@ -40,14 +40,12 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 #endif
 }
 
-// Workspace record of the MMA kernel.
-//   default:     S_{i+1}⁻¹ packed | K | k | V packed | v | e = c_{i+1} − δv_{i+1}
-//                (forward: x⁺ = S⁻¹(A x + B u + e) with A, B re-read by TMA; the backward needs no
-//                closed-loop products; measured 15.4 -> 14.6 ms on C2 against the Φ record)
-//   RR_FWD_PHI:  [Φ | φ] row-major NX × (NX+2) | K | k | V packed | v      (forward: x⁺ = Φx + φ)
+// Workspace record of the MMA kernel (per instance and stage):
+//   S_{i+1}⁻¹ packed | K_i | k_i | V_i packed | v_i | e_i = c_{i+1} − δv_{i+1}
+// forward: x⁺ = S⁻¹(A x + B u + e) with A, B re-read by TMA, so the backward needs no closed-loop
+// products (measured 15.4 -> 14.6 ms on C2 against a [Φ | φ] record, round 1).
 template <int NX, int NU>
 struct RecM {
-#ifndef RR_FWD_PHI
   static constexpr int S = 0;
   static constexpr int K = NX * (NX + 1) / 2;
   static constexpr int k = K + NU * NX;
@@ -55,17 +53,6 @@ struct RecM {
   static constexpr int v = V + NX * (NX + 1) / 2;
   static constexpr int e = v + NX;
   static constexpr int SIZE = e + NX;
-  static constexpr int LD = NX + 2;  // (unused)
-  static constexpr int PHI = 0;      // (unused)
-#else
-  static constexpr int LD = NX + 2;
-  static constexpr int PHI = 0;
-  static constexpr int K = NX * LD;
-  static constexpr int k = K + NU * NX;
-  static constexpr int V = k + NU;
-  static constexpr int v = V + NX * (NX + 1) / 2;
-  static constexpr int SIZE = v + NX;
-#endif
   static constexpr int PAD = (SIZE + 1) & ~1;
 };
 
@@ -77,14 +64,15 @@ struct WorkM {
   static constexpr int NZ = NX + NU;
   using W = Work<NX, NU>;
   static_assert(W::Wb + NX * NX == W::SIZE, "Work<> must end with Wb");
-  static constexpr int MLD = ((NX + 1 + 15) / 16) * 16 + 4;  // row-major ld of M (≡ 4 mod 16: B fragments)
-  static constexpr int X1SZ = (NX * MLD > NX * 16 ? NX * MLD : NX * 16);
-
-  static constexpr int X1 = W::Wb;              // [V | Ve] (ld NX), then T (ld NX), then M (row-major, ld MLD)
-  static constexpr int X2 = X1 + X1SZ;          // W (ld NX, NX+1 cols), then U (ld ULD)
   static constexpr int ULD = 18;                // U leading dimension: conflict-free C-fragment stores
-  static_assert(16 * ULD >= NX * 16 && X2 - X1 >= NX * 16, "X1 / X2 must hold the swizzled T / W (NX rows x 16)");
-  static constexpr int E = X2 + 16 * ULD;       // e = c_{i+1} − δ v_{i+1} (NX, even)
+  // one region per instance, reused within a stage: [V | Ve] rows (ld NX; the B operand of W = S⁻¹Vs),
+  // then U (col-major, ld ULD; written once W is formed, read by the u-block elimination), then the
+  // forward record staged for its TMA bulk store (after the elimination holds U in registers)
+  static constexpr int X = W::Wb;
+  static constexpr int X1 = X, X2 = X;
+  static constexpr int XSZ = 16 * ULD;
+  static_assert(XSZ >= NX * NX + NX && XSZ >= NZ * ULD - (ULD - NZ), "X must hold Vs and U");
+  static constexpr int E = X + XSZ;             // e = c_{i+1} − δ v_{i+1} (NX, even)
   static constexpr int BP = E + ((NX + 1) & ~1);  // 2 publish slots for b_p in the u-block elimination
   static constexpr int SIZE = BP + 2;
   static constexpr int PAD = (SIZE + 1) & ~1;
@@ -187,6 +175,10 @@ struct StageMMA {
     const double* cv = grp ? cvq[1] : cvq[0];
     const int g = lane >> 2, t = lane & 3;
     // (1) S⁻¹ (no stage input needed), then Vs = [V | V e] (V symmetric: (V e)_j = column j · e)
+#ifndef RR_REC_STG
+    if (lane == 0) bulk_wait_read0();  // the previous stage's record bulk stores have read X (Vs goes there)
+    __syncwarp();
+#endif
 #ifndef RR_INVS_GRID
 #ifdef RR_AB_SKIP_INVS  // A/B probe only: cost of the SIMT S⁻¹ sweep (wrong results)
     if (j < NX) {
@@ -224,11 +216,6 @@ struct StageMMA {
       wk[WM::X1 + NX * NX + j] = ve0 + ve1;  // column NX of Vs
     }
     __syncwarp();
-#ifndef RR_REC_STG
-    if (lane == 0) bulk_wait_read0();  // the previous stage's record bulk stores have read X2
-    __syncwarp();
-#endif
-#ifndef RR_SMEM_CHAIN
     // (2)-(5) per instance q, in DMMA registers: [W | We] = S⁻¹ Vs, X = Fᵀ W, U = Fᵀ Xᵀ + P.
     // A C fragment holds C[g][2t], C[g][2t+1]; used with the contraction index permuted to
     // k-blocks {2t + 8kt} and {2t + 1 + 8kt} it IS the A fragment of C (row g, "column" t) and, for
@@ -356,149 +343,6 @@ struct StageMMA {
       }
       bj = b0 + b1;
     }
-#else
-    // (2) [W | W e] = S⁻¹ Vs -> X2 (ld NX)
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const double* Si = wkq[q] + WK::Si;
-      const double* Vs = wkq[q] + WM::X1;
-      double c[MT][CT][2];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < CT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
-#pragma unroll
-      for (int kt = 0; kt < KT; ++kt) {
-        double aS[MT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const int r = 8 * mt + g;
-          aS[mt] = (r < NX) ? Si[(4 * kt + t) * NX + r] : 0.0;
-        }
-#pragma unroll
-        for (int nt = 0; nt < CT; ++nt) {
-          const int col = 8 * nt + g;
-          const double bv = (col <= NX) ? Vs[col * NX + 4 * kt + t] : 0.0;
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aS[mt], bv);
-        }
-      }
-      double* Wb = wkq[q] + WM::X2;  // [W | We | 0 pad] row-major, swizzled (swz16)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < CT; ++nt) {
-          const int r = 8 * mt + g, col = 8 * nt + 2 * t;
-          if (r < NX) *reinterpret_cast<double2*>(Wb + swz16(r, col)) = make_double2(c[mt][nt][0], c[mt][nt][1]);
-        }
-    }
-    __syncwarp();
-    // (3) g = v + W e;  b_j = [q + Aᵀg; r + Bᵀg]_j
-    if (j < NX) wk[WK::gb + j] = wk[WK::vs + j] + wk[WM::X2 + swz16(j, NX)];
-    __syncwarp();
-    const int jc = (j < NZ) ? j : 0;
-    {
-      double gk[NX];
-      ST::bcast(wk + WK::gb, gk);
-      double b0 = qjf(), b1 = 0.0;
-      // column j of F read as 128-bit pairs; lanes with j & 4 walk the pairs rotated by one, so the
-      // 8 lanes of a quarter-warp (column stride NX = 12 doubles) hit 8 different 16-byte bank groups
-      // (unrotated: lanes j and j + 4 collide, 2 wavefronts per quarter)
-      const bool rot = (j & 4) != 0;
-#pragma unroll
-      for (int k = 0; k < NX; k += 2) {
-        const int kr = (k + 2) % NX;
-        const double2 f2 = *reinterpret_cast<const double2*>(F + jc * NX + (rot ? kr : k));
-        b0 = fma(f2.x, rot ? gk[kr] : gk[k], b0);
-        b1 = fma(f2.y, rot ? gk[kr + 1] : gk[k + 1], b1);
-      }
-      bj = b0 + b1;  // lane j owns entry j of b (distributed, not replicated)
-    }
-    // (4) T = W F (NX × NZ) -> X1 (ld NX)
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const double* Wb = wkq[q] + WM::X2;
-      const double* Fx = Fq[q];
-      double c[MT][ZT][2];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < ZT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
-#pragma unroll
-      for (int kt = 0; kt < KT; ++kt) {
-        double aW[MT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const int r = 8 * mt + g;
-          aW[mt] = (r < NX) ? Wb[swz16(r, 4 * kt + t)] : 0.0;
-        }
-#pragma unroll
-        for (int nt = 0; nt < ZT; ++nt) {
-          const int col = 8 * nt + g;
-          const double bF = (col < NZ) ? Fx[col * NX + 4 * kt + t] : 0.0;
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aW[mt], bF);
-        }
-      }
-      double* Tb = wkq[q] + WM::X1;  // T row-major, swizzled (swz16)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < ZT; ++nt) {
-          const int r = 8 * mt + g, col = 8 * nt + 2 * t;
-          if (r < NX) *reinterpret_cast<double2*>(Tb + swz16(r, col)) = make_double2(c[mt][nt][0], c[mt][nt][1]);
-        }
-    }
-    __syncwarp();
-    // (5) U = Fᵀ T + P (NZ × NZ) -> X2 (ld 16); A-fragment of Fᵀ = B-fragment layout of F
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const double* Tb = wkq[q] + WM::X1;
-      const double* Fx = Fq[q];
-      double c[ZT][ZT][2];
-#pragma unroll
-      for (int mt = 0; mt < ZT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < ZT; ++nt)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-#if defined(RR_NO_PTAB)
-            const int r = 8 * mt + g, col = 8 * nt + 2 * t + e;
-            c[mt][nt][e] = (r < NZ && col < NZ) ? Pat(q, r, col) : 0.0;
-#elif !defined(RR_P_SIMT)
-            c[mt][nt][e] = Pat(q, (mt * ZT + nt) * 2 + e);  // P-gather table (kernel)
-#else
-            c[mt][nt][e] = 0.0;  // RR_P_SIMT: P added in (6) column by column (measured 3% slower)
-#endif
-          }
-#pragma unroll
-      for (int kt = 0; kt < KT; ++kt) {
-        double aF[ZT];
-#pragma unroll
-        for (int mt = 0; mt < ZT; ++mt) {
-          const int col = 8 * mt + g;
-          aF[mt] = (col < NZ) ? Fx[col * NX + 4 * kt + t] : 0.0;
-        }
-#pragma unroll
-        for (int nt = 0; nt < ZT; ++nt) {
-          const int col = 8 * nt + g;
-          const double bT = (col < NZ) ? Tb[swz16(4 * kt + t, col)] : 0.0;
-#pragma unroll
-          for (int mt = 0; mt < ZT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aF[mt], bT);
-        }
-      }
-      double* Ub = wkq[q] + WM::X2;
-#pragma unroll
-      for (int mt = 0; mt < ZT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < ZT; ++nt) {
-          const int r = 8 * mt + g, col = 8 * nt + 2 * t;
-          Ub[col * WM::ULD + r] = c[mt][nt][0];
-          Ub[(col + 1) * WM::ULD + r] = c[mt][nt][1];
-        }
-    }
-    __syncwarp();
-#endif
     // (6) Gauss-Jordan on the u-block (SIMT, lane j owns column j)
 #pragma unroll
     for (int s = 0; s < NZ; s += 2) {
@@ -594,7 +438,6 @@ struct StageMMA {
       __syncwarp();
       return;
     }
-#ifndef RR_FWD_PHI
     {  // record: S_{i+1}⁻¹, e, K, k, V, v (no closed-loop products)
       __syncwarp();
       prefetch();
@@ -642,83 +485,6 @@ struct StageMMA {
       __syncwarp();
       return;
     }
-#endif
-    // (7) M = [A + B K | B k + c − δ v] -> X1 (ld NX, NX+1 columns)
-    if (j <= NX) {
-      double tcol[NX];
-      ST::bcast((j < NX) ? F + jc * NX : wk + WM::E, tcol);  // column j of A, or e for the φ column
-#pragma unroll
-      for (int u = 0; u < NU; ++u) {
-        const double coef = (j < NX) ? -U[NX + u] : -wk[WK::vb + NX + u];
-        const double* Fu = F + (NX + u) * NX;
-#pragma unroll
-        for (int r = 0; r < NX; r += 2) {
-          const double2 f2 = *reinterpret_cast<const double2*>(Fu + r);
-          tcol[r] = fma(f2.x, coef, tcol[r]);
-          tcol[r + 1] = fma(f2.y, coef, tcol[r + 1]);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < NX; ++r) wk[WM::X1 + r * WM::MLD + j] = tcol[r];  // M row-major (ld MLD)
-    }
-    __syncwarp();
-    prefetch();  // the stage inputs (F, P, q, r, c) are dead from here on
-    // (8) [Φ | φ] = S⁻¹ M -> record (row-major, ld NX+2), straight from the C fragments
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const double* Si = wkq[q] + WK::Si;
-      const double* Mb = wkq[q] + WM::X1;
-      double c[MT][CT][2];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < CT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
-#pragma unroll
-      for (int kt = 0; kt < KT; ++kt) {
-        double aS[MT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const int r = 8 * mt + g;
-          aS[mt] = (r < NX) ? Si[(4 * kt + t) * NX + r] : 0.0;
-        }
-#pragma unroll
-        for (int nt = 0; nt < CT; ++nt) {
-          const int col = 8 * nt + g;
-          const double bM = (col <= NX) ? Mb[(4 * kt + t) * WM::MLD + col] : 0.0;
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) dmma884(c[mt][nt][0], c[mt][nt][1], aS[mt], bM);
-        }
-      }
-      auto* rec = recq[q];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < CT; ++nt) {
-          const int r = 8 * mt + g, col = 8 * nt + 2 * t;
-          if (rec != nullptr && r < NX && col <= NX)
-            *reinterpret_cast<double2*>(rec + RC::PHI + r * RC::LD + col) = make_double2(c[mt][nt][0], c[mt][nt][1]);
-        }
-    }
-    // (9) record K, k, V (packed), v; carry V_i, v_i
-    if ((grp ? recq[1] : recq[0]) != nullptr) {
-      auto* rec = grp ? recq[1] : recq[0];
-      if (j < NX) {
-#pragma unroll
-        for (int u = 0; u < NU; ++u) rec[RC::K + j * NU + u] = -U[NX + u];
-        auto* Vp = rec + RC::V + j * (2 * NX - j - 1) / 2;
-#pragma unroll
-        for (int r = 0; r < NX; ++r)
-          if (r >= j) Vp[r] = U[r];
-        rec[RC::v + j] = bj;
-      } else if (j < NZ) {
-        rec[RC::k + (j - NX)] = -bj;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < NX; ++r) Vc[r] = (j < NX) ? U[r] : 0.0;
-    __syncwarp();
-    if (j < NX) wk[WK::vs + j] = bj;
-    __syncwarp();
   }
 };
 
