@@ -876,6 +876,12 @@ namespace rrk {
 cudaError_t factor_mma_launch(const FusedArgs& a, cudaStream_t s, bool* supported) {
   *supported = (a.nx == 12 && a.nu == 4);
   if (!*supported) return cudaSuccess;
+  // 3 CTAs per SM: at 4 (128 registers) the factor-only kernel spills, 11.40 vs 10.99 ms on C2
+  const char* v = getenv("RR_B200_FAC_CTAS");  // A/B knob: 4 = 4 CTAs per SM
+  if (v && atoi(v) == 4) {
+    if (a.frec32 != nullptr) return MmaCfg<12, 4, 4, 4, true, true>::launch(a, s);
+    return MmaCfg<12, 4, 4, 4, true>::launch(a, s);
+  }
   if (a.frec32 != nullptr) return MmaCfg<12, 4, 4, 3, true, true>::launch(a, s);  // FP32 records
   return MmaCfg<12, 4, 4, 3, true>::launch(a, s);
 }
