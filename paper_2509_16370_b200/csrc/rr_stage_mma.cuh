@@ -451,6 +451,25 @@ struct StageMMA {
 #endif
       if (rec != nullptr) {
         if (j < NX) {
+#ifndef RR_REC_STG
+          // row j of the (symmetric) S⁻¹ and V_i: entries (j, c), c <= j, at packed index pidx(j, c) =
+          // c(2n − c − 1)/2 + j -- for each c consecutive lanes write consecutive doubles (conflict-free)
+#pragma unroll
+          for (int c = 0; c < NX; ++c)
+            if (c <= j) {
+              const int pc = c * (2 * NX - c - 1) / 2 + j;
+              rec[RC::S + pc] = wk[WK::Si + c * NX + j];
+              rec[RC::V + pc] = U[c];
+            }
+          if constexpr (NU % 2 == 0 && (RC::K % 2) == 0) {  // column j of K (m × n col-major) as 16-byte pairs
+#pragma unroll
+            for (int u = 0; u < NU; u += 2)
+              *reinterpret_cast<double2*>(rec + RC::K + j * NU + u) = make_double2(-U[NX + u], -U[NX + u + 1]);
+          } else {
+#pragma unroll
+            for (int u = 0; u < NU; ++u) rec[RC::K + j * NU + u] = -U[NX + u];
+          }
+#else
           auto* Sp = rec + RC::S + j * (2 * NX - j - 1) / 2;
           auto* Vp = rec + RC::V + j * (2 * NX - j - 1) / 2;
 #pragma unroll
@@ -461,6 +480,7 @@ struct StageMMA {
             }
 #pragma unroll
           for (int u = 0; u < NU; ++u) rec[RC::K + j * NU + u] = -U[NX + u];
+#endif
           rec[RC::v + j] = bj;
           rec[RC::e + j] = wk[WM::E + j];
         } else if (j < NZ) {
