@@ -212,6 +212,47 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
       if (ok) cp_async8(dst + off, src);
       else dst[off] = pad;
     };
+    if constexpr (EXACT && NX == 4 && NU == 1 && NG == 4 && NC == 0 && LG == 8) {
+      if (!term && a.aligned16) {
+        // C4 copy plan: the stage's 41 16-byte chunks in 6 LDGSTS.128 rounds over the 8 lanes (lanes of
+        // one round serve different arrays) + one LDGSTS.64 round for the odd-sized ∇f, ū, R -- instead
+        // of 14 runtime-checked copy loops (their branches and address arithmetic were ~1/3 of the
+        // kernel's instructions).  Destinations: the IpmBuf offsets (P slot packed Q | M | R).
+        static_assert(IB::F == 0 && IB::P == 20 && IB::gf == 46 && IB::cv == 52 && IB::G == 56 && IB::gv == 76 &&
+                          IB::s == 80 && IB::z == 84 && IB::yi == 96 && IB::xb == 104 && IB::ub == 108,
+                      "C4 copy plan assumes the 4x1 (n_g 4) IpmBuf layout");
+        const int64_t sy = inst * (sN + 1) + i;
+        cp_async16(dst + IB::F + 2 * j, a.d_.A + si * 16 + 2 * j);    // A: 8 chunks
+        cp_async16(dst + IB::G + 2 * j, a.d_.Gj + si * 20 + 2 * j);   // G: chunks 0..7
+        {
+          const double* src;
+          int d;
+          if (j < 2) { src = a.d_.Gj + si * 20 + 16 + 2 * j; d = IB::G + 16 + 2 * j; }         // G 8..9
+          else if (j < 4) { src = a.d_.B + si * 4 + 2 * (j - 2); d = IB::F + 16 + 2 * (j - 2); }  // B
+          else if (j < 6) { src = a.d_.M + si * 4 + 2 * (j - 4); d = IB::P + 10 + 2 * (j - 4); }  // M
+          else { src = a.d_.dres + si * 4 + 2 * (j - 6); d = IB::cv + 2 * (j - 6); }            // dres
+          cp_async16(dst + d, src);
+        }
+        if (j < 7) {
+          const double* src = (j < 5) ? a.d_.Q + si * 10 + 2 * j : a.d_.gv + si * 4 + 2 * (j - 5);  // Q | g
+          cp_async16(dst + ((j < 5) ? IB::P + 2 * j : IB::gv + 2 * (j - 5)), src);
+        }
+        {
+          const double* src;
+          int d;
+          if (j < 4) { src = a.it.y + sy * 4 + 2 * j; d = IB::yi + 2 * j; }            // y_i | y_{i+1}
+          else if (j < 6) { src = a.it.x + sy * 4 + 2 * (j - 4); d = IB::xb + 2 * (j - 4); }  // x̄_i
+          else { src = a.it.s + si * 4 + 2 * (j - 6); d = IB::s + 2 * (j - 6); }        // s
+          cp_async16(dst + d, src);
+        }
+        if (j < 2) cp_async16(dst + IB::z + 2 * j, a.it.z + si * 4 + 2 * j);            // z
+        if (j < 7) {
+          const double* src = (j < 5) ? a.d_.gradf + si * 5 + j : ((j == 5) ? a.it.u + si : a.d_.R + si);
+          cp_async8(dst + ((j < 5) ? IB::gf + j : ((j == 5) ? IB::ub : IB::P + 14)), src);
+        }
+        return;
+      }
+    }
     if (exact && !term) {
       copy_async(dst + IB::F, a.d_.A + si * NX * NX, NX * NX, j, LG);       // F = [A | B], ld NX
       copy_async(dst + IB::F + NX * NX, a.d_.B + si * NX * NU, NX * NU, j, LG);
@@ -858,8 +899,13 @@ bool ipm_supported(const ipm_dims& d) {
   return dispatch_ipm(d, [](auto) { return true; });
 }
 
-cudaError_t ipm_launch(const IpmArgs& a, cudaStream_t s, bool* supported) {
+cudaError_t ipm_launch(const IpmArgs& a0, cudaStream_t s, bool* supported) {
   cudaError_t err = cudaSuccess;
+  IpmArgs a = a0;  // the C4 copy plan needs 16-byte aligned bases of the 16-byte-copied arrays
+  const void* ops[] = {a.d_.A, a.d_.B, a.d_.Q, a.d_.M, a.d_.dres, a.it.y, a.it.x, a.d_.Gj, a.d_.gv, a.it.s, a.it.z};
+  a.aligned16 = 1;
+  for (const void* p : ops)
+    if (p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) != 0) a.aligned16 = 0;
   *supported = dispatch_ipm(a.d, [&](auto cfg) {
     err = decltype(cfg)::launch(a, s);
     return true;

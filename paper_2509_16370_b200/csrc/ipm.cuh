@@ -18,6 +18,7 @@ struct IpmArgs {
   const int32_t* list = nullptr;   // ipm_solve: active instance ids (nullptr: all instances)
   const int32_t* count = nullptr;  // device count of `list`
   int direction_only = 0;          // ipm_direction: rows a1-a7 only (no line search, no update)
+  int aligned16 = 0;               // set by ipm_launch: 16-byte aligned operand bases (C4 copy plan)
 };
 
 int64_t ipm_ws_bytes(const ipm_dims& d);
