@@ -317,6 +317,7 @@ struct StageMMA {
           }
         }
       double* Ub = wkq[q] + WM::X2;
+      __syncwarp();  // U overwrites Vs (same region X): every lane's Vs fragment loads are done
 #pragma unroll
       for (int mt = 0; mt < ZT; ++mt)
 #pragma unroll

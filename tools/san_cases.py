@@ -60,3 +60,31 @@ b = random_lq_ocp(3, 2, 4, 5, seed=8, ng=2, ngN=1, nc=1, ncN=1, device="cuda")
 d = rr.ipm_direction(b)
 torch.cuda.synchronize()
 print("pit / quadrotor / direction", resq["status"].tolist(), repq["status"].tolist(), d["status"].tolist())
+# round 2: persistent K1-MMA warps with several pairs each (batch > resident slots), the staggered
+# (deferred forward) variant, FP32 factor records, the pipelined host path, linear_merit
+p = synth.random_stable_lqr(12, 4, 3, 4800, seed=7).to("cuda")
+out = rr.rr_factor_solve(p)
+os.environ["RR_DEFER_MOD"] = "3"
+out2 = rr.rr_factor_solve(p)
+os.environ.pop("RR_DEFER_MOD")
+torch.cuda.synchronize()
+print("persistent", int(out["status"].abs().sum()), bool(torch.equal(out["x"], out2["x"])))
+p = synth.random_stable_lqr(12, 4, 4, 6, seed=8).to("cuda")
+F32, st = rr.rr_factor(p, fp32=True)
+sol = rr.rr_solve(p, F32)
+rr.rr_refine(p, F32, sol, iters=1)
+torch.cuda.synchronize()
+print("fp32", int(st.abs().sum()), int(sol["status"].abs().sum()))
+pc = synth.random_stable_lqr(12, 4, 4, 11, seed=9)
+hp = synth.RRProblem(pc.nx, pc.nu, pc.N, **{f: getattr(pc, f).pin_memory() for f in pc.FIELDS})
+dp = pc.to("cuda")
+hs = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in rr.alloc_solution(dp).items()}
+call = rr.HostMarshalled(hp, hs, dp, rr.alloc_solution(dp))
+ws = torch.empty((call.pipelined_workspace_bytes(4) + 7) // 8, dtype=torch.float64, device="cuda")
+call.launch_pipelined([torch.cuda.current_stream(), torch.cuda.Stream()], 4, ws)
+torch.cuda.synchronize()
+print("pipelined", int(hs["status"].abs().sum()))
+b = cartpole_c4(3, seed=3, N=8, device="cuda")
+rep3 = rr.ipm_solve(b, max_iters=4, linear_merit=True)
+torch.cuda.synchronize()
+print("linear_merit", rep3["status"].tolist())
