@@ -124,6 +124,11 @@ __device__ void store_tile(double* g, const double* T, int rows, int cols, int l
   __syncwarp();
 }
 
+// δ of the reduction solve: max(δ, delta_floor) (PitArgs); the residual kernel keeps the caller's δ
+__device__ __forceinline__ double pit_delta(const PitArgs& a, int64_t inst) {
+  return fmax(a.p.delta[inst], a.delta_floor);
+}
+
 // ---- 1. stage assembly: warp per (instance, stage) ----
 __device__ void pit_assemble_item(const PitArgs& a, int64_t item, double* T, int lane) {  // T: 8 tiles
   const int n = a.nx, m = a.nu, N = a.N;
@@ -131,7 +136,7 @@ __device__ void pit_assemble_item(const PitArgs& a, int64_t item, double* T, int
   const int i = (int)(item % N);
   double *tA = T, *tB = T + TILE, *tG = T + 2 * TILE, *tHxu = T + 3 * TILE, *tW1 = T + 4 * TILE, *tW2 = T + 5 * TILE,
          *tE = T + 6 * TILE, *tv = T + 7 * TILE;
-  const double d = a.p.delta[inst];
+  const double d = pit_delta(a, inst);
   const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst) * N + i;
   const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : inst) * N + i;
   const int64_t s = inst * N + i;
@@ -255,7 +260,7 @@ __device__ void pit_diag_item(const PitArgs& a, int64_t item, int lane) {
   const int64_t inst = item / (N + 1);
   const int k = (int)(item % (N + 1));
   PitWs v = views(a.ws, inst, N, n, m);
-  const double d = a.p.delta[inst];
+  const double d = pit_delta(a, inst);
   const int sn = n * (n + 1) / 2;
   const int64_t iP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;
   // D_k = [k < N] E_xx,k + [k > 0] E_x'x',k−1 + [k == 0] I + [k == N] δQ_N ; the linear term g_k likewise
@@ -427,7 +432,7 @@ __device__ void pit_recover_item(const PitArgs& a, int64_t item, int lane) {
   const int n = a.nx, m = a.nu, N = a.N;
   const int64_t inst = item / (N + 1);
   const int i = (int)(item % (N + 1));
-  const double d = a.p.delta[inst];
+  const double d = pit_delta(a, inst);
   const double* x = a.s.x + inst * (int64_t)(N + 1) * n;
   double* y = a.s.y + inst * (int64_t)(N + 1) * n;
   if (i == 0) {  // y_0 = (c_0 − x_0)/δ
@@ -483,7 +488,7 @@ __device__ void pit_rhs_assemble_item(const PitArgs& a, int64_t item, int lane) 
   const int64_t inst = item / N;
   const int i = (int)(item % N);
   PitWs v = views(a.ws, inst, N, n, m);
-  const double d = a.p.delta[inst];
+  const double d = pit_delta(a, inst);
   const int64_t s = inst * N + i;
   const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst) * N + i;
   const double* A = a.p.A + sD * n * n;
@@ -531,7 +536,7 @@ __device__ void pit_rhs_diag_item(const PitArgs& a, int64_t item, int lane) {
     if (k < N) g += v.yb[(int64_t)k * n + lane];
     if (k > 0) g += v.b[(int64_t)k * n + lane];
     if (k == 0) g -= a.p.c0[inst * n + lane];
-    if (k == N) g += a.p.delta[inst] * a.p.qN[inst * n + lane];
+    if (k == N) g += pit_delta(a, inst) * a.p.qN[inst * n + lane];
     v.b[(int64_t)k * n + lane] = -g;
   }
 }
@@ -775,8 +780,9 @@ cudaError_t pit_launch(const PitArgs& a, cudaStream_t s) {
     pit_backsub_kernel<<<blocks_for(b * ((N - st) / (2 * st) + 1)), WPB * 32, 0, s>>>(a, st);
   }
   pit_recover_kernel<<<blocks_for(b * (N + 1)), WPB * 32, 0, s>>>(a);
-  // one step of iterative refinement in FP64 (residual kernel of rr_split.cu, re-solve with the
-  // stored reduction): the δ-scaled state system is conditioned like 1/δ, the recursion is not
+  // iterative refinement in FP64: residual of the caller's system (true δ), re-solve with the stored
+  // reduction (δ_s = max(δ, delta_floor)): corrects the 1/δ_s conditioning of the δ-scaled state
+  // system and, where the floor binds, the difference between the δ_s and the δ solutions
   const int n = a.nx, m = a.nu;
   rr_residual_buf rb;
   PitArgs c;

@@ -1,7 +1,7 @@
 """GPU parity of the parallel-in-time solve (rr_factor_solve_pit, the paper's future
 work P:688-691) against the oracle T2: the same unique solution of the regularized system, computed
-by block cyclic reduction on the δ-reduced state system.  FP64 bar 1e-9 (y is recovered through
-y = (Cz + c)/δ, so δ >= 1e-6 is required for that bar)."""
+by block cyclic reduction on the δ_s-reduced state system, δ_s = max(δ, 1e-4), followed by iterated
+refinement on the caller's δ (δ = 0, classic LQR, included).  FP64 bar 1e-9."""
 import numpy as np
 import pytest
 import torch
@@ -28,7 +28,7 @@ def rel(g, o):
 @pytest.mark.parametrize("nx,nu,N,batch", [(12, 4, 100, 3), (12, 4, 1, 4), (12, 4, 2, 2), (4, 1, 37, 5),
                                            (2, 1, 10, 1), (3, 2, 64, 2), (16, 16, 9, 2), (5, 3, 0, 2),
                                            (7, 6, 129, 2)])
-@pytest.mark.parametrize("delta", [1e-4, 1e-2, 1.0])
+@pytest.mark.parametrize("delta", [0.0, 1e-8, 1e-6, 1e-4, 1e-2, 1.0])
 def test_pit_parity(nx, nu, N, batch, delta):
     p = synth.random_stable_lqr(nx, nu, N, batch, seed=nx * 13 + N, delta=delta)
     out = rr().rr_factor_solve_pit(p.to("cuda"))
@@ -61,9 +61,17 @@ def test_pit_shared_and_failure():
     o = oracle.rr_solve_t2(p.expanded())
     for k in ("x", "u", "y"):
         assert rel(out[k].cpu().numpy(), o[k]) <= 1e-9
-    z = synth.random_stable_lqr(4, 1, 6, 3, seed=4).with_delta(0.0)   # δ = 0: outside the method
-    bad = m.rr_factor_solve_pit(z.to("cuda"))
-    assert np.all(bad["status"].cpu().numpy() != 0)
+    z = synth.random_stable_lqr(4, 1, 6, 3, seed=4).with_delta(0.0)   # δ = 0: classic LQR, by refinement
+    zo = m.rr_factor_solve_pit(z.to("cuda"))
+    oz = oracle.rr_solve_t2(z)
+    assert np.all(zo["status"].cpu().numpy() == 0)
+    for k in ("x", "u", "y"):
+        assert rel(zo[k].cpu().numpy(), oz[k]) <= 1e-9
+    bad_p = synth.random_stable_lqr(4, 1, 6, 3, seed=4)
+    bad_p.R[1, 2] = -1e6                                                  # R_i not PD in instance 1: no solution
+    bad = m.rr_factor_solve_pit(bad_p.to("cuda"))
+    st = bad["status"].cpu().numpy()
+    assert st[1] != 0 and st[0] == 0 and st[2] == 0
 
 
 def test_cuda_graph_capture_replay():
