@@ -21,6 +21,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <atomic>
 #include <type_traits>
 
 #include "rr_common.cuh"
@@ -576,6 +577,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
       }
     }
     if constexpr (FAC) {  // S_0⁻¹ -> record 0; status; NaN-fill a failed instance's records
+      if (lane == 0) bulk_wait0();  // the staged record bulk stores are complete (NaN-fill may overwrite them)
+      __syncwarp();
       ST::invS(Vc, delta, j, wk, 0, st);
       RT* rec = frecb + inst * (sN + 1) * FREC;
       if (valid && j < n)
@@ -792,10 +795,22 @@ struct MmaCfg {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     // persistent grid: every resident CTA slot once (the warps loop over instance pairs)
-    int dev = 0, nsm = 0, occ = 0;
+    // (SM count and occupancy are per device and kernel: queried once per device and cached -- the
+    // values are immutable, so a racing first call at worst queries twice)
+    int dev = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-    if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, WARPS * 32, sm)) != cudaSuccess) return e;
+    constexpr int MAXDEV = 64;
+    static std::atomic<int> cache[MAXDEV];  // (nsm << 8) | occ, 0 = not yet queried
+    int nsm = 0, occ = 0;
+    const int cv = (dev >= 0 && dev < MAXDEV) ? cache[dev].load(std::memory_order_relaxed) : 0;
+    if (cv != 0) {
+      nsm = cv >> 8;
+      occ = cv & 0xff;
+    } else {
+      if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, WARPS * 32, sm)) != cudaSuccess) return e;
+      if (dev >= 0 && dev < MAXDEV && occ > 0 && occ < 256) cache[dev].store((nsm << 8) | occ, std::memory_order_relaxed);
+    }
     FusedArgs a = a0;
     a.nsm = nsm;
     a.defer_mod = 1;  // measured: staggering by occ (3) is 1-2% slower on C2 (profiles/r02_stagger_ab.txt)

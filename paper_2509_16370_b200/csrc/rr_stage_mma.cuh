@@ -410,28 +410,55 @@ struct StageMMA {
     if constexpr (FAC) {  // factor record i (and S_{i+1}⁻¹ into record i+1); no closed loop
       __syncwarp();
       prefetch();
-      RT* rec = grp ? recq[1] : recq[0];
       constexpr int SN = NX * (NX + 1) / 2;
       constexpr int RECD = (NX * (NX + 1) + NX * NU + NU * (NU + 1) / 2 + 1) & ~1;
       constexpr int REC = sizeof(RT) == 4 ? ((RECD + 3) & ~3) : RECD;  // FP32 records: 16-byte multiple
+      // FP64 records: staged in X in the record layout [V_i | S_{i+1}⁻¹ | K_i | G_i⁻¹] and written by three
+      // TMA bulk stores (V, K, G⁻¹ -> record i; S_{i+1}⁻¹ -> record i+1's S slot); FP32: direct stores
+      constexpr bool STAGE = sizeof(RT) == 8 && (SN % 2) == 0 && ((RECD - 2 * SN) % 2) == 0;
+      RT* const grec = grp ? recq[1] : recq[0];
+      RT* rec = grec;
+      RT* recS = grec != nullptr ? grec + REC : nullptr;  // record i+1 (its S slot at + SN)
+      if constexpr (STAGE) {
+        rec = grec != nullptr ? reinterpret_cast<RT*>(wk + WM::X) : nullptr;
+        recS = rec;
+      }
       if (rec != nullptr) {
         if (j < NX) {
-          RT* Vp = rec + j * (2 * NX - j - 1) / 2;
-          RT* Sp = rec + REC + SN + j * (2 * NX - j - 1) / 2;  // record i+1: S_{i+1}⁻¹
+          // row j (= column j) of the symmetric V_i and S_{i+1}⁻¹ along packed columns: entries (j, c),
+          // c <= j, at c(2n − c − 1)/2 + j (consecutive lanes, consecutive addresses)
 #pragma unroll
-          for (int r = 0; r < NX; ++r)
-            if (r >= j) {
-              Vp[r] = U[r];
-              Sp[r] = wk[WK::Si + r * NX + j];
+          for (int c = 0; c < NX; ++c)
+            if (c <= j) {
+              const int pc = c * (2 * NX - c - 1) / 2 + j;
+              rec[pc] = (RT)U[c];
+              recS[SN + pc] = (RT)wk[WK::Si + c * NX + j];
             }
 #pragma unroll
-          for (int u = 0; u < NU; ++u) rec[2 * SN + j * NU + u] = -U[NX + u];
+          for (int u = 0; u < NU; ++u) rec[2 * SN + j * NU + u] = (RT)(-U[NX + u]);
         } else if (j < NZ) {
           const int w = j - NX;
           RT* Gp = rec + 2 * SN + NX * NU + w * (2 * NU - w - 1) / 2;
 #pragma unroll
           for (int u = 0; u < NU; ++u)
-            if (u >= w) Gp[u] = -U[NX + u];
+            if (u >= w) Gp[u] = (RT)(-U[NX + u]);
+        }
+      }
+      if constexpr (STAGE) {
+        static_assert(RECD <= WM::XSZ, "factor record staging needs X");
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (recq[q] == nullptr) continue;
+            const double* xs = wkq[q] + WM::X;
+            double* gr = reinterpret_cast<double*>(recq[q]);
+            bulk_s2g(gr, xs, 8u * SN);                                     // V_i
+            bulk_s2g(gr + 2 * SN, xs + 2 * SN, 8u * (RECD - 2 * SN));       // K_i | G_i⁻¹ (| pad)
+            bulk_s2g(gr + REC + SN, xs + SN, 8u * SN);                       // S_{i+1}⁻¹ -> record i+1
+          }
+          bulk_commit();
         }
       }
 #pragma unroll
