@@ -62,6 +62,14 @@ typedef int32_t rr_err;
  * queries; rr_factor_solve on the CTA kernels (n or m > 16) returns RR_E_UNSUPPORTED. */
 #define RR_FLAG_SHARED_DYN 2
 #define RR_FLAG_SHARED_COST 4
+/* Stage-invariant operands (LTI MPC, A_i = A for every stage): with
+ * RR_FLAG_STAGE_INVARIANT_DYN, A and B hold ONE stage block per instance ([batch][elems]; with
+ * RR_FLAG_SHARED_DYN too, one block for everything: [elems]); RR_FLAG_STAGE_INVARIANT_COST does the
+ * same for Q, M, R (Q_N is per instance or shared as before).  q, r, c stay per stage.  Accepted
+ * wherever RR_FLAG_SHARED_* is (rr_factor_solve for n, m <= 16, rr_factor, rr_solve, rr_residual,
+ * rr_factor_solve_pit, the host paths and the size queries). */
+#define RR_FLAG_STAGE_INVARIANT_DYN 16
+#define RR_FLAG_STAGE_INVARIANT_COST 32
 /* FP32 factor record (the paper's low-precision factorization + residual callback,
  * P:664-666): rr_factor stores its records in FP32 (same layout and element offsets, record stride
  * rr_factor_bytes()/(batch*(N+1)*4) = the double count rounded up to a multiple of 4 floats) and

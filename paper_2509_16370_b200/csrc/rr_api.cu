@@ -19,7 +19,9 @@ rr_err set_err(rr_err code, const char* fmt, const char* what = "") {
   return code;
 }
 
-constexpr int SHARED_FLAGS = RR_FLAG_SHARED_DYN | RR_FLAG_SHARED_COST;
+// operand-layout flags (batch-shared and stage-invariant A, B / Q, M, R; include/rr.h)
+constexpr int SHARED_FLAGS =
+    RR_FLAG_SHARED_DYN | RR_FLAG_SHARED_COST | RR_FLAG_STAGE_INVARIANT_DYN | RR_FLAG_STAGE_INVARIANT_COST;
 
 // TMA bulk copies (cp.async.bulk) need 16-byte-aligned global addresses; the per-stage block
 // offsets of every compiled TMA shape are multiples of 16 bytes, so the base pointers decide.
@@ -110,9 +112,11 @@ rr_err rr_factor_solve_host(const rr_dims* dims, const rr_problem* ph, const rr_
   const int64_t b = dims->batch, N = dims->N, n = dims->nx, m = dims->nu;
   const int64_t sn = n * (n + 1) / 2, sm = m * (m + 1) / 2;
   const int64_t bD = (dims->flags & RR_FLAG_SHARED_DYN) ? 1 : b, bP = (dims->flags & RR_FLAG_SHARED_COST) ? 1 : b;
+  const int64_t nD = (dims->flags & RR_FLAG_STAGE_INVARIANT_DYN) ? 1 : N;   // stage blocks of A, B
+  const int64_t nP = (dims->flags & RR_FLAG_STAGE_INVARIANT_COST) ? 1 : N;  // stage blocks of Q, M, R
   struct Op { const double* h; const double* d; int64_t cnt; } ops[] = {
-      {ph->A, pd->A, bD * N * n * n}, {ph->B, pd->B, bD * N * n * m}, {ph->Q, pd->Q, bP * N * sn},
-      {ph->M, pd->M, bP * N * n * m}, {ph->R, pd->R, bP * N * sm},    {ph->q, pd->q, b * N * n},
+      {ph->A, pd->A, bD * nD * n * n}, {ph->B, pd->B, bD * nD * n * m}, {ph->Q, pd->Q, bP * nP * sn},
+      {ph->M, pd->M, bP * nP * n * m}, {ph->R, pd->R, bP * nP * sm},    {ph->q, pd->q, b * N * n},
       {ph->r, pd->r, b * N * m},      {ph->c, pd->c, b * N * n},      {ph->QN, pd->QN, bP * sn},
       {ph->qN, pd->qN, b * n},       {ph->c0, pd->c0, b * n},       {ph->delta, pd->delta, b}};
   for (const Op& o : ops) {
@@ -148,6 +152,8 @@ rr_err rr_factor_solve_host_pipelined(const rr_dims* dims, const rr_problem* ph,
   const int64_t b = dims->batch, N = dims->N, n = dims->nx, m = dims->nu;
   const int64_t sn = n * (n + 1) / 2, sm = m * (m + 1) / 2;
   const bool shD = (dims->flags & RR_FLAG_SHARED_DYN) != 0, shP = (dims->flags & RR_FLAG_SHARED_COST) != 0;
+  const int64_t nD = (dims->flags & RR_FLAG_STAGE_INVARIANT_DYN) ? 1 : N;   // stage blocks of A, B
+  const int64_t nP = (dims->flags & RR_FLAG_STAGE_INVARIANT_COST) ? 1 : N;  // stage blocks of Q, M, R
   const int64_t nc = nchunks > b ? b : nchunks;
   // per-chunk workspace slices, each 256-byte aligned, carved from the caller's buffer
   int64_t need = 0;
@@ -172,12 +178,12 @@ rr_err rr_factor_solve_host_pipelined(const rr_dims* dims, const rr_problem* ph,
   cudaError_t e = cudaSuccess;
   // batch-shared operands once, on streams[0], before the fork
   if (shD) {
-    if ((e = h2d(ph->A, pd->A, 0, N * n * n, s0)) != cudaSuccess || (e = h2d(ph->B, pd->B, 0, N * n * m, s0)) != cudaSuccess)
+    if ((e = h2d(ph->A, pd->A, 0, nD * n * n, s0)) != cudaSuccess || (e = h2d(ph->B, pd->B, 0, nD * n * m, s0)) != cudaSuccess)
       return set_err(RR_E_CUDA, "rr_factor_solve_host_pipelined: H2D %s", cudaGetErrorString(e));
   }
   if (shP) {
-    if ((e = h2d(ph->Q, pd->Q, 0, N * sn, s0)) != cudaSuccess || (e = h2d(ph->M, pd->M, 0, N * n * m, s0)) != cudaSuccess ||
-        (e = h2d(ph->R, pd->R, 0, N * sm, s0)) != cudaSuccess || (e = h2d(ph->QN, pd->QN, 0, sn, s0)) != cudaSuccess)
+    if ((e = h2d(ph->Q, pd->Q, 0, nP * sn, s0)) != cudaSuccess || (e = h2d(ph->M, pd->M, 0, nP * n * m, s0)) != cudaSuccess ||
+        (e = h2d(ph->R, pd->R, 0, nP * sm, s0)) != cudaSuccess || (e = h2d(ph->QN, pd->QN, 0, sn, s0)) != cudaSuccess)
       return set_err(RR_E_CUDA, "rr_factor_solve_host_pipelined: H2D %s", cudaGetErrorString(e));
   }
   // fork: streams[1..] wait for everything enqueued on streams[0] so far
@@ -199,8 +205,8 @@ rr_err rr_factor_solve_host_pipelined(const rr_dims* dims, const rr_problem* ph,
     dc.batch = cb;
     // H2D of the chunk's slices (every per-instance operand is [batch][...] contiguous)
     struct Op { const double* h; const double* d; int64_t per; bool inst; } ops[] = {
-        {ph->A, pd->A, N * n * n, !shD}, {ph->B, pd->B, N * n * m, !shD}, {ph->Q, pd->Q, N * sn, !shP},
-        {ph->M, pd->M, N * n * m, !shP}, {ph->R, pd->R, N * sm, !shP},    {ph->q, pd->q, N * n, true},
+        {ph->A, pd->A, nD * n * n, !shD}, {ph->B, pd->B, nD * n * m, !shD}, {ph->Q, pd->Q, nP * sn, !shP},
+        {ph->M, pd->M, nP * n * m, !shP}, {ph->R, pd->R, nP * sm, !shP},    {ph->q, pd->q, N * n, true},
         {ph->r, pd->r, N * m, true},     {ph->c, pd->c, N * n, true},     {ph->QN, pd->QN, sn, !shP},
         {ph->qN, pd->qN, n, true},       {ph->c0, pd->c0, n, true},       {ph->delta, pd->delta, 1, true}};
     for (const Op& o : ops)
@@ -209,11 +215,11 @@ rr_err rr_factor_solve_host_pipelined(const rr_dims* dims, const rr_problem* ph,
     // the chunk's problem / solution views (batch-shared operands keep their base pointers)
     rr_problem pc = *pd;
     auto off = [&](const double* p, int64_t per, bool inst) { return (inst && p) ? p + i0 * per : p; };
-    pc.A = off(pd->A, N * n * n, !shD);
-    pc.B = off(pd->B, N * n * m, !shD);
-    pc.Q = off(pd->Q, N * sn, !shP);
-    pc.M = off(pd->M, N * n * m, !shP);
-    pc.R = off(pd->R, N * sm, !shP);
+    pc.A = off(pd->A, nD * n * n, !shD);
+    pc.B = off(pd->B, nD * n * m, !shD);
+    pc.Q = off(pd->Q, nP * sn, !shP);
+    pc.M = off(pd->M, nP * n * m, !shP);
+    pc.R = off(pd->R, nP * sm, !shP);
     pc.q = off(pd->q, N * n, true);
     pc.r = off(pd->r, N * m, true);
     pc.c = off(pd->c, N * n, true);

@@ -18,6 +18,17 @@ __host__ __device__ constexpr int group_stride(int slot, int lg) {
   return lg >= 16 ? ((slot + 1) & ~1) : ((slot + 1) & ~1) + ((lg - (((slot + 1) & ~1) % 16) + 16) % 16);
 }
 
+// Block index of stage i of a dynamics (A, B) or cost (Q, M, R) operand of instance `inst`
+// (include/rr.h RR_FLAG_SHARED_* / RR_FLAG_STAGE_INVARIANT_*): [batch][N] | [N] | [batch] | [1].
+__host__ __device__ __forceinline__ int64_t dyn_blk(int fl, int64_t inst, int64_t N, int64_t i) {
+  const int64_t b = (fl & RR_FLAG_SHARED_DYN) ? 0 : inst;
+  return (fl & RR_FLAG_STAGE_INVARIANT_DYN) ? b : b * N + i;
+}
+__host__ __device__ __forceinline__ int64_t cost_blk(int fl, int64_t inst, int64_t N, int64_t i) {
+  const int64_t b = (fl & RR_FLAG_SHARED_COST) ? 0 : inst;
+  return (fl & RR_FLAG_STAGE_INVARIANT_COST) ? b : b * N + i;
+}
+
 // LAPACK 'L' packed index of (r, c) with r >= c in an n×n symmetric matrix.
 __host__ __device__ __forceinline__ int pidx(int n, int r, int c) { return c * (2 * n - c - 1) / 2 + r; }
 

@@ -82,10 +82,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_kernel(const FusedA
   int32_t st = 0;
 
   // batch-shared operands (include/rr.h RR_FLAG_SHARED_*): instance index 0 for them
-  const int64_t instD = (a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst;
   const int64_t instP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;
   auto issue_stage = [&](int i, double* dst) {
-    const int64_t s = inst * sN + i, sD = instD * sN + i, sP = instP * sN + i;
+    const int64_t s = inst * sN + i, sD = dyn_blk(a.shared, inst, sN, i), sP = cost_blk(a.shared, inst, sN, i);
     copy_async(dst + oA, a.p.A + sD * n * n, n * n, j, LG);
     copy_async(dst + oB, a.p.B + sD * n * m, n * m, j, LG);
     copy_async(dst + oQ, a.p.Q + sP * sn, sn, j, LG);
@@ -460,8 +459,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const int64_t sq = instq[q] * sN + i;
-            const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : instq[q]) * sN + i;
-            const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : instq[q]) * sN + i;
+            const int64_t sD = dyn_blk(a.shared, instq[q], sN, i);
+            const int64_t sP = cost_blk(a.shared, instq[q], sN, i);
             double* d = slotq[q];
             uint64_t* bq = barq[q];
             mbar_arrive_expect_tx(bq, STG_BYTES);
@@ -480,8 +479,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
         (void)s;
         (void)dst;
       } else {
-        const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst) * sN + i;
-        const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : inst) * sN + i;
+        const int64_t sD = dyn_blk(a.shared, inst, sN, i);
+        const int64_t sP = cost_blk(a.shared, inst, sN, i);
         copy_async(dst + oA, a.p.A + sD * n * n, n * n, j, 16);
         copy_async(dst + oB, a.p.B + sD * n * m, n * m, j, 16);
         copy_async(dst + oQ, a.p.Q + sP * sn, sn, j, 16);
@@ -670,7 +669,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_fused_mma_kernel(const Fu
           fence_proxy_async();
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : instq[q]) * sN + i;
+            const int64_t sD = dyn_blk(a.shared, instq[q], sN, i);
             mbar_arrive_expect_tx(&barq[q][b], 8u * (RC::SIZE + n * n + n * m));
             bulk_g2s(rbuf(slotq[q], b), a.ws + (instq[q] * sN + i) * RC::PAD, 8u * RC::SIZE, &barq[q][b]);
             bulk_g2s(abuf(slotq[q], b), a.p.A + sD * n * n, 8u * n * n, &barq[q][b]);

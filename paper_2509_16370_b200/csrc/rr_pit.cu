@@ -137,8 +137,8 @@ __device__ void pit_assemble_item(const PitArgs& a, int64_t item, double* T, int
   double *tA = T, *tB = T + TILE, *tG = T + 2 * TILE, *tHxu = T + 3 * TILE, *tW1 = T + 4 * TILE, *tW2 = T + 5 * TILE,
          *tE = T + 6 * TILE, *tv = T + 7 * TILE;
   const double d = pit_delta(a, inst);
-  const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst) * N + i;
-  const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : inst) * N + i;
+  const int64_t sD = dyn_blk(a.shared, inst, N, i);
+  const int64_t sP = cost_blk(a.shared, inst, N, i);
   const int64_t s = inst * N + i;
   const int sn = n * (n + 1) / 2, smm = m * (m + 1) / 2;
   load_tile(tA, a.p.A + sD * n * n, n, n, lane);
@@ -444,7 +444,7 @@ __device__ void pit_recover_item(const PitArgs& a, int64_t item, int lane) {
   const int st = i - 1;  // stage producing x_i: u_{st}, y_i
   PitWs v = views(a.ws, inst, N, n, m);
   const int64_t s = inst * N + st;
-  const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst) * N + st;
+  const int64_t sD = dyn_blk(a.shared, inst, N, st);
   const double* B = a.p.B + sD * n * m;
   const double* A = a.p.A + sD * n * n;
   const double* xi = x + (int64_t)st * n;
@@ -490,7 +490,7 @@ __device__ void pit_rhs_assemble_item(const PitArgs& a, int64_t item, int lane) 
   PitWs v = views(a.ws, inst, N, n, m);
   const double d = pit_delta(a, inst);
   const int64_t s = inst * N + i;
-  const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst) * N + i;
+  const int64_t sD = dyn_blk(a.shared, inst, N, i);
   const double* A = a.p.A + sD * n * n;
   const double* B = a.p.B + sD * n * m;
   const double* c = a.p.c + s * n;
@@ -608,8 +608,8 @@ __device__ void pit_residual_item(const PitArgs& a, const rr_residual_buf& rb, i
     return;
   }
   const int64_t s = inst * N + i;
-  const int64_t sD = ((a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst) * N + i;
-  const int64_t sP = ((a.shared & RR_FLAG_SHARED_COST) ? 0 : inst) * N + i;
+  const int64_t sD = dyn_blk(a.shared, inst, N, i);
+  const int64_t sP = cost_blk(a.shared, inst, N, i);
   const double *A = a.p.A + sD * n * n, *B = a.p.B + sD * n * m;
   const double *Q = a.p.Q + sP * sn, *M = a.p.M + sP * n * m, *R = a.p.R + sP * smm;
   const double* xi = x + (int64_t)i * n;

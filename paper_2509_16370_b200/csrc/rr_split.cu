@@ -86,10 +86,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_factor_kernel(const Split
   double* rec = a.fr + inst * (sN + 1) * REC;
   int32_t st = 0;
 
-  const int64_t instD = (a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst;  // batch-shared operands
   const int64_t instP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;
   auto issue_stage = [&](int i, double* dst) {
-    const int64_t sD = instD * sN + i, sP = instP * sN + i;
+    const int64_t sD = dyn_blk(a.shared, inst, sN, i), sP = cost_blk(a.shared, inst, sN, i);
     copy_async(dst + oA, a.p.A + sD * n * n, n * n, j, LG);
     copy_async(dst + oB, a.p.B + sD * n * m, n * m, j, LG);
     copy_async(dst + oQ, a.p.Q + sP * sn, sn, j, LG);
@@ -332,9 +331,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_solve_kernel(const SplitA
   const bool xl = j < n, ul = ui >= 0 && ui < m;
   const bool acc = a.accumulate;             // RR_FLAG_ACCUMULATE: sol += solution (refinement)
 
-  const int64_t instD = (a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst;  // batch-shared A, B
   auto issue_stage = [&](int i) {
-    const int64_t s = inst * sN + i, sD = instD * sN + i;
+    const int64_t s = inst * sN + i, sD = dyn_blk(a.shared, inst, sN, i);
     double* dst = sbuf(i);
     copy_async(dst + oA, a.p.A + sD * n * n, n * n, j, LG);
     copy_async(dst + oB, a.p.B + sD * n * m, n * m, j, LG);
@@ -597,10 +595,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) rr_residual_kernel(const Res
   const int ui = j - NX;
   const bool xl = j < n, ul = ui >= 0 && ui < m;
 
-  const int64_t instD = (a.shared & RR_FLAG_SHARED_DYN) ? 0 : inst;  // batch-shared operands
   const int64_t instP = (a.shared & RR_FLAG_SHARED_COST) ? 0 : inst;
   auto issue = [&](int i) {
-    const int64_t s = inst * sN + i, sD = instD * sN + i, sP = instP * sN + i;
+    const int64_t s = inst * sN + i, sD = dyn_blk(a.shared, inst, sN, i), sP = cost_blk(a.shared, inst, sN, i);
     double* d = buf(i);
     copy_async(d + oA, a.p.A + sD * n * n, n * n, j, LG);
     copy_async(d + oB, a.p.B + sD * n * m, n * m, j, LG);

@@ -37,7 +37,9 @@ def check_problem(prob, sol=None):
     fl = shared_flags(prob)
     bD = 1 if fl & RR_FLAG_SHARED_DYN else b
     bP = 1 if fl & RR_FLAG_SHARED_COST else b
-    want = dict(A=bD * N * n * n, B=bD * N * n * m, Q=bP * N * _sym(n), M=bP * N * n * m, R=bP * N * _sym(m),
+    nD = 1 if fl & RR_FLAG_STAGE_INVARIANT_DYN else N
+    nP = 1 if fl & RR_FLAG_STAGE_INVARIANT_COST else N
+    want = dict(A=bD * nD * n * n, B=bD * nD * n * m, Q=bP * nP * _sym(n), M=bP * nP * n * m, R=bP * nP * _sym(m),
                 q=b * N * n, r=b * N * m, c=b * N * n, QN=bP * _sym(n), qN=b * n, c0=b * n, delta=b)
     dev = prob.delta.device
     for f in PROBLEM_FIELDS:
@@ -60,20 +62,34 @@ def check_problem(prob, sol=None):
 
 
 RR_FLAG_SHARED_DYN, RR_FLAG_SHARED_COST = 2, 4
+RR_FLAG_STAGE_INVARIANT_DYN, RR_FLAG_STAGE_INVARIANT_COST = 16, 32
+
+
+def _layout(t, N: int, name: str):
+    """(batch_shared, stage_invariant) of a stage operand from its shape: [b, N, e] per instance and
+    stage; [N, e] batch-shared; [b, 1, e] stage-invariant (N > 1); [1, e] both (N > 1)."""
+    if t.dim() == 3:
+        return False, (t.shape[1] == 1 and N > 1)
+    if t.dim() == 2:
+        return True, (t.shape[0] == 1 and N > 1)
+    raise RRError("problem.%s: expected [batch, N, elems], [N, elems], [batch, 1, elems] or [1, elems]" % name)
 
 
 def shared_flags(prob) -> int:
-    """Batch-shared operands (include/rr.h RR_FLAG_SHARED_*) from the tensor ranks: A, B of shape
-    [N, elems] (no batch dimension) are shared dynamics; Q, M, R [N, elems] and Q_N [elems] shared costs."""
+    """Operand-layout flags (include/rr.h RR_FLAG_SHARED_* / RR_FLAG_STAGE_INVARIANT_*) from the tensor
+    shapes: A, B (and Q, M, R with Q_N) without a batch dimension are batch-shared; with a stage
+    dimension of 1 (N > 1) they are stage-invariant (LTI)."""
     f = 0
-    if prob.A.dim() == 2:
-        if prob.B.dim() != 2:
-            raise RRError("A and B must both be shared ([N, elems]) or both per instance")
-        f |= RR_FLAG_SHARED_DYN
-    if prob.Q.dim() == 2:
-        if prob.M.dim() != 2 or prob.R.dim() != 2 or prob.QN.dim() != 1:
-            raise RRError("Q, M, R ([N, elems]) and QN ([elems]) must be shared together")
-        f |= RR_FLAG_SHARED_COST
+    dA, dB = _layout(prob.A, prob.N, "A"), _layout(prob.B, prob.N, "B")
+    if dA != dB:
+        raise RRError("A and B must have the same layout (batch-shared / stage-invariant)")
+    f |= (RR_FLAG_SHARED_DYN if dA[0] else 0) | (RR_FLAG_STAGE_INVARIANT_DYN if dA[1] else 0)
+    cQ, cM, cR = (_layout(getattr(prob, k), prob.N, k) for k in ("Q", "M", "R"))
+    if not (cQ == cM == cR):
+        raise RRError("Q, M and R must have the same layout (batch-shared / stage-invariant)")
+    if cQ[0] != (prob.QN.dim() == 1):
+        raise RRError("Q_N must be batch-shared ([elems]) exactly when Q, M, R are")
+    f |= (RR_FLAG_SHARED_COST if cQ[0] else 0) | (RR_FLAG_STAGE_INVARIANT_COST if cQ[1] else 0)
     return f
 
 

@@ -144,14 +144,17 @@ class RRProblem:
         return sum(getattr(self, f).numel() * 8 for f in self.FIELDS)
 
     def expanded(self) -> "RRProblem":
-        """Per-instance copy of a problem with batch-shared operands (RR_FLAG_SHARED_*): A, B, Q, M, R
-        of shape [N, elems] and Q_N [elems] are broadcast to the batch."""
+        """Per-instance, per-stage copy of a problem with batch-shared (RR_FLAG_SHARED_*: A, B, Q, M, R
+        of shape [N, elems], Q_N [elems]) and / or stage-invariant (RR_FLAG_STAGE_INVARIANT_*: stage
+        dimension 1, i.e. [b, 1, elems] or [1, elems]) operands: broadcast to [b, N, elems]."""
         b = self.batch
         kw = {}
         for f in self.FIELDS:
             t = getattr(self, f)
-            if f in ("A", "B", "Q", "M", "R") and t.dim() == 2:
-                t = t.unsqueeze(0).expand(b, *t.shape)
+            if f in ("A", "B", "Q", "M", "R"):
+                if t.dim() == 2:
+                    t = t.unsqueeze(0)
+                t = t.expand(b, self.N, t.shape[-1])
             elif f == "QN" and t.dim() == 1:
                 t = t.unsqueeze(0).expand(b, t.shape[0])
             kw[f] = t.contiguous()
@@ -211,6 +214,22 @@ def lti_problem(nx: int, nu: int, N: int, batch: int, seed: int, delta: float = 
     if shared_cost:
         kw["Q"], kw["M"], kw["R"], kw["QN"] = (base.Q[0].contiguous(), base.M[0].contiguous(),
                                                base.R[0].contiguous(), base.QN[0].contiguous())
+    return RRProblem(nx, nu, N, **kw)
+
+
+def lti_invariant_problem(nx: int, nu: int, N: int, batch: int, seed: int, delta: float = 1e-4,
+                          shared: bool = False, device="cpu") -> RRProblem:
+    """Time-invariant (LTI-MPC) batch (RR_FLAG_STAGE_INVARIANT_*): per instance ONE stage
+    block of A, B, Q, M, R (the stage-0 blocks of the C2 recipe) used at every stage, stored with a
+    stage dimension of 1 ([b, 1, elems]); shared=True: also batch-shared (one block for all, [1, elems];
+    Q_N [elems]).  Right-hand sides q, r, c, q_N, c_0 and δ per instance and stage as in the C2 recipe."""
+    base = random_stable_lqr(nx, nu, N, 1 if shared else batch, seed, delta, first=0, device=device)
+    rhs = random_stable_lqr(nx, nu, N, batch, seed, delta, first=1, device=device)
+    kw = {f: getattr(rhs, f) for f in RRProblem.FIELDS}
+    for f in ("A", "B", "Q", "M", "R"):
+        blk = getattr(base, f)[:, :1].contiguous()          # [b or 1, 1, elems]
+        kw[f] = blk[0].contiguous() if shared else blk
+    kw["QN"] = base.QN[0].contiguous() if shared else base.QN
     return RRProblem(nx, nu, N, **kw)
 
 

@@ -56,3 +56,23 @@ def test_fp32_factor_record_size_query():
     assert m.factor_bytes(12, 4, 100, 8) == 8 * 101 * R * 8
     with pytest.raises(m.RRError):
         m.factor_bytes(4, 1, 10, 8, fp32=True)   # no FP32 kernel for this shape
+
+
+def test_operand_layout_flags_from_shapes():
+    """include/rr.h RR_FLAG_SHARED_* / RR_FLAG_STAGE_INVARIANT_*: the binding infers them from the
+    operand shapes ([b, N, e] | [N, e] batch-shared | [b, 1, e] stage-invariant | [1, e] both)."""
+    import paper_2509_16370_b200 as m
+    import synth
+    R = m.rr
+    assert m.shared_flags(synth.random_stable_lqr(4, 1, 5, 3, seed=0)) == 0
+    assert m.shared_flags(synth.lti_problem(4, 1, 5, 3, seed=0)) == R.RR_FLAG_SHARED_DYN | R.RR_FLAG_SHARED_COST
+    assert m.shared_flags(synth.lti_invariant_problem(4, 1, 5, 3, seed=0)) == \
+        R.RR_FLAG_STAGE_INVARIANT_DYN | R.RR_FLAG_STAGE_INVARIANT_COST
+    assert m.shared_flags(synth.lti_invariant_problem(4, 1, 5, 3, seed=0, shared=True)) == \
+        R.RR_FLAG_SHARED_DYN | R.RR_FLAG_SHARED_COST | R.RR_FLAG_STAGE_INVARIANT_DYN | R.RR_FLAG_STAGE_INVARIANT_COST
+    p = synth.lti_invariant_problem(4, 1, 5, 3, seed=0)
+    p.B = p.B.expand(3, 5, 4).contiguous()                 # A stage-invariant, B not: refused
+    with pytest.raises(m.RRError):
+        m.shared_flags(p)
+    e = synth.lti_invariant_problem(4, 1, 5, 3, seed=0, shared=True).expanded()
+    assert e.A.shape == (3, 5, 16) and e.QN.shape == (3, 10) and m.shared_flags(e) == 0

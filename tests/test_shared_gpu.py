@@ -106,3 +106,56 @@ def test_host_pipelined_equals_serial(shared, nchunks, nstreams):
     o = oracle.rr_solve_t2(p.expanded() if shared else p)
     for k in ("x", "u", "y"):
         assert rel(out[1][k].numpy(), o[k]) <= 1e-9
+
+
+@pytest.mark.parametrize("nx,nu,N,batch", [(12, 4, 20, 37), (4, 1, 15, 33), (3, 2, 7, 9), (16, 16, 4, 5)])
+@pytest.mark.parametrize("shared", [False, True])
+def test_stage_invariant_equals_expanded(nx, nu, N, batch, shared):
+    """RR_FLAG_STAGE_INVARIANT_DYN | _COST (LTI MPC): one stage block of A, B, Q, M, R per
+    instance (or, with shared, for the whole batch) serves every stage.  rr_factor_solve, the split
+    API, rr_residual and the parallel-in-time solve give bitwise the results of the expanded problem,
+    and the oracle's within 1e-9."""
+    m = rr()
+    p = synth.lti_invariant_problem(nx, nu, N, batch, seed=nx + N, delta=1e-3, shared=shared)
+    e = p.expanded()
+    assert m.shared_flags(p) & (m.rr.RR_FLAG_STAGE_INVARIANT_DYN | m.rr.RR_FLAG_STAGE_INVARIANT_COST)
+    ps, pe = p.to("cuda"), e.to("cuda")
+    a, b = m.rr_factor_solve(ps), m.rr_factor_solve(pe)
+    Fs, _ = m.rr_factor(ps)
+    Fe, _ = m.rr_factor(pe)
+    ss, se = m.rr_solve(ps, Fs), m.rr_solve(pe, Fe)
+    rs, ns = m.rr_residual(ps, ss)
+    re_, ne = m.rr_residual(pe, se)
+    pa, pb = m.rr_factor_solve_pit(ps), m.rr_factor_solve_pit(pe)
+    torch.cuda.synchronize()
+    for k in ("x", "u", "y", "status"):
+        assert torch.equal(a[k], b[k]), k
+        assert torch.equal(ss[k], se[k]), k
+        assert torch.equal(pa[k], pb[k]), k
+    sn = nx * (nx + 1) // 2
+    used = 2 * sn + nx * nu + nu * (nu + 1) // 2
+    assert torch.equal(Fs[:, :N, :used], Fe[:, :N, :used]) and torch.equal(Fs[:, N, :2 * sn], Fe[:, N, :2 * sn])
+    assert torch.equal(ns, ne)
+    o = oracle.rr_solve_t2(e)
+    for k in ("x", "u", "y"):
+        assert rel(a[k].cpu().numpy(), o[k]) <= 1e-9
+
+
+def test_stage_invariant_host_paths():
+    m = rr()
+    p = synth.lti_invariant_problem(12, 4, 10, 16, seed=3)
+    hp = synth.RRProblem(p.nx, p.nu, p.N, **{f: getattr(p, f).pin_memory() for f in p.FIELDS})
+    dp = p.to("cuda")
+    o = oracle.rr_solve_t2(p.expanded())
+    for pipelined in (False, True):
+        hs = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in m.alloc_solution(dp).items()}
+        call = m.HostMarshalled(hp, hs, dp, m.alloc_solution(dp))
+        if pipelined:
+            ws = torch.empty((call.pipelined_workspace_bytes(3) + 7) // 8, dtype=torch.float64, device="cuda")
+            call.launch_pipelined([torch.cuda.current_stream(), torch.cuda.Stream()], 3, ws)
+        else:
+            call.launch()
+        torch.cuda.synchronize()
+        for k in ("x", "u", "y"):
+            assert rel(hs[k].numpy(), o[k]) <= 1e-9, (pipelined, k)
+    assert call.h2d_bytes < p.expanded().nbytes() / 4
