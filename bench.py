@@ -64,13 +64,14 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample wall time")
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "split", "f32", "c4solve", "c4swing", "pit"],
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "split", "f32", "c4solve", "c4swing", "pit", "lti"],
                     help="c2 (default, BASELINE configs[1]); c3 = 4,096 dense n64 m32 N50 (configs[2]); "
                          "c4 = ipm_step on 16,384 cart-pole instances (configs[3]); c5 = 1,048,576 "
                          "quadrotor n12 m4 N200 sharded over the ranks, chunks of 65,536 (configs[4]); split = "
                          "rr_factor + rr_solve + rr_residual on the C2 workload, each kernel timed; c4solve = ipm_solve "
                          "(20 IPM iterations) on the C4 cart-pole batch; c1 = single double-integrator instance latency; "
-                         "pit = single-instance latency, parallel-in-time vs sequential, long horizons")
+                         "pit = single-instance latency, parallel-in-time vs sequential, long horizons; lti = the C2 shape "
+                         "as an LTI fleet (one A, B, Q, M, R for all instances and stages)")
     ap.add_argument("--c5-total", type=int, default=1048576, help=argparse.SUPPRESS)
     ap.add_argument("--ref-seconds", type=float, default=150.0, help=argparse.SUPPRESS)  # reference-arm budget
     ap.add_argument("--no-others", action="store_true",
@@ -302,17 +303,28 @@ def main():
         ALG_BYTES_PER_STAGE, ALG_FLOPS_PER_STAGE = 206208, 2420000
         if a.batch == 65536:
             a.batch = BATCH
+    lti = a.workload == "lti"
+    if lti:
+        # LTI fleet MPC on the C2 shape: ONE stage block of A, B, Q, M, R (and Q_N) for
+        # the whole batch and every stage (RR_FLAG_SHARED_* | RR_FLAG_STAGE_INVARIANT_*), per-instance
+        # q, r, c per stage, q_N, c_0, δ.  Per (instance, stage) the fused sweep then reads 20 input
+        # doubles; model: q, r, c once 160 + policy written and read 2 x 1,136 + c re-read 96 +
+        # x, u, y 224 = 2,752 B (the stage is compute / shared-memory bound at this intensity)
+        ALG_BYTES_PER_STAGE = 2752
     B = a.batch
     first = rank * B  # weak scaling: every rank owns B instances (global ids [rB, (r+1)B))
     # ---- inputs resident in HBM (generation excluded from timing) ----
-    prob = synth.empty_problem(NX, NU, HORIZON, B, device=dev)
-    gchunk = 4096 if NX <= 16 else 256
-    for s in range(0, B, gchunk):
-        e = min(B, s + gchunk)
-        p = synth.random_stable_lqr(NX, NU, HORIZON, e - s, SEED, DELTA, first=first + s, device=dev)
-        for f in synth.RRProblem.FIELDS:
-            getattr(prob, f)[s:e].copy_(getattr(p, f))
-        del p
+    if lti:
+        prob = synth.lti_invariant_problem(NX, NU, HORIZON, B, SEED, DELTA, shared=True, device=dev)
+    else:
+        prob = synth.empty_problem(NX, NU, HORIZON, B, device=dev)
+        gchunk = 4096 if NX <= 16 else 256
+        for s in range(0, B, gchunk):
+            e = min(B, s + gchunk)
+            p = synth.random_stable_lqr(NX, NU, HORIZON, e - s, SEED, DELTA, first=first + s, device=dev)
+            for f in synth.RRProblem.FIELDS:
+                getattr(prob, f)[s:e].copy_(getattr(p, f))
+            del p
     sol = rr.alloc_solution(prob)
     call = rr.Marshalled(prob, sol)   # fac = NULL: outputs x, u, y (policy stays in the workspace)
     stream = torch.cuda.current_stream(dev)
@@ -351,11 +363,16 @@ def main():
         # N = 1: the whole batch; N > 1: 16,384 instances per rank (the pinned host copies of the full
         # batch would be ~20 GB per rank; end-to-end throughput is PCIe-bound and per-instance constant)
         EB = B if ws == 1 else min(B, 16384)
-        hp = synth.empty_problem(NX, NU, HORIZON, EB, device="cpu", pin_memory=True)
-        for f in synth.RRProblem.FIELDS:
-            getattr(hp, f).copy_(getattr(prob, f)[:EB])
+        if lti:  # same (shared / stage-invariant) layouts on the host and in the staging buffers
+            EB = B
+            hp = synth.RRProblem(NX, NU, HORIZON, **{f: getattr(prob, f).cpu().pin_memory() for f in synth.RRProblem.FIELDS})
+        else:
+            hp = synth.empty_problem(NX, NU, HORIZON, EB, device="cpu", pin_memory=True)
+            for f in synth.RRProblem.FIELDS:
+                getattr(hp, f).copy_(getattr(prob, f)[:EB])
         hs = {k: torch.empty((EB,) + tuple(v.shape[1:]), dtype=v.dtype, pin_memory=True) for k, v in sol.items()}
-        stage_p = synth.empty_problem(NX, NU, HORIZON, EB, device=dev)
+        stage_p = (synth.RRProblem(NX, NU, HORIZON, **{f: torch.empty_like(getattr(prob, f)) for f in synth.RRProblem.FIELDS})
+                   if lti else synth.empty_problem(NX, NU, HORIZON, EB, device=dev))
         stage_s = rr.alloc_solution(stage_p)
         hcall = rr.HostMarshalled(hp, hs, stage_p, stage_s, ws=call.ws)
         # pipelined: 16 chunks round-robin over 3 streams (H2D of one chunk, the solve of another and
@@ -406,7 +423,7 @@ def main():
                 "hbm_gbs_alg": achieved}
     else:
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic("rr_fused_c2"),
+                "frac": achieved / peak, "traffic": None if lti else ncu_traffic("rr_fused_c2"),
                 "kernel": "rr_fused_mma_kernel<12,4> (DMMA stage, TMA loads)", "kernel_ms": kern_ms,
                 "alg_bytes_per_stage": ALG_BYTES_PER_STAGE, "peak_source": peak_src,
                 "fp64_alg_tflops": fp64_tflops}
@@ -414,8 +431,11 @@ def main():
         "metric": METRIC, "value": solves, "unit": "solves/s", "n_gpus": ws, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "%s: %d random stable regularized LQR per GPU, n_x=%d n_u=%d N=%d delta=%g, FP64"
-                               % ("C3" if c3 else "C2", B, NX, NU, HORIZON, DELTA),
+        "config": {"workload": ("LTI fleet (C2 shape, one A, B, Q, M, R for all instances and stages; per-instance "
+                                 "q, r, c, q_N, c_0): %d regularized LQR per GPU, n_x=%d n_u=%d N=%d delta=%g, FP64"
+                                 % (B, NX, NU, HORIZON, DELTA)) if lti else
+                               ("%s: %d random stable regularized LQR per GPU, n_x=%d n_u=%d N=%d delta=%g, FP64"
+                                % ("C3" if c3 else "C2", B, NX, NU, HORIZON, DELTA)),
                    "global_batch": B * ws, "seq_len": HORIZON, "parallelism": "batch-shard x%d" % ws,
                    "l2": "inputs %.1f GB/GPU > 126 MB L2 (no flush needed)" % (prob.nbytes() / 1e9)},
         "stage_updates_per_s": solves * HORIZON,
@@ -433,6 +453,9 @@ def main():
                 "C3 instances, T2 plain-C oracle", calib=2, cap=512)
         else:
             line["cpu_baseline"] = cpu_baseline(a.cpu_seconds)
+            if lti:
+                line["cpu_baseline"]["note"] = ("sampled on C2 instances: the plain-C oracle does the same "
+                                                "work per instance whatever the operand layout")
     if ws == 1 and a.workload == "c2" and not a.no_others:
         # the other BASELINE configs (C3, C4, C5) and the split / IPM-solve paths, each a short run of
         # this script in its own process (own timing, own roofline), summarised on this line so that
