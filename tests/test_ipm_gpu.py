@@ -164,3 +164,27 @@ def test_spec_scalar_step_exact_on_gpu():
     assert np.all(np.abs(g["D"] + 99 / 32) <= 1e-15) and np.all(g["alpha_p"] == 1.0)
     assert np.all(np.abs(g["merit0"] - 4.0) <= 1e-15)
     assert np.all(np.abs(g["merit_acc"] - 3.848760597239781) <= 2e-15)
+
+
+def test_ipm_c4_unaligned_operands_equal_aligned():
+    """The exact C4 kernel copies the stage data with a static plan of 16-byte LDGSTS when every
+    copied operand base is 16-byte aligned, else with the generic 8-byte copies (ipm_launch decides):
+    an 8-byte-offset view of A and of the iterate x gives bitwise the aligned results."""
+    import paper_2509_16370_b200 as rr
+    b = cartpole_c4(24, N=30).to("cuda")
+    c = b.clone()
+
+    def offset_view(t):  # same values, base address shifted by 8 bytes
+        buf = torch.empty(t.numel() + 1, dtype=t.dtype, device=t.device)
+        v = buf[1:].view(t.shape)
+        v.copy_(t)
+        assert v.data_ptr() % 16 == 8
+        return v
+    c.data["A"] = offset_view(c.data["A"])
+    c.it["x"] = offset_view(c.it["x"])
+    ra, rc = rr.ipm_step(b), rr.ipm_step(c)
+    torch.cuda.synchronize()
+    for k in ("status", "dx", "du", "ds", "dz", "dy", "alpha_p", "D", "merit0", "merit_acc"):
+        assert torch.equal(ra[k], rc[k]), k
+    for k in ("x", "u", "s", "z", "y"):
+        assert torch.equal(b.it[k], c.it[k]), k
