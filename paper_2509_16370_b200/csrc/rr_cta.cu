@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "rr_common.cuh"
 #include "rr_cta.cuh"
@@ -993,6 +994,410 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
   if (tid == 0) a.status[inst] = status;
 }
 
+// ==========================================================================================
+// K4b -- the C3 shape at TWO instances per SM (two CTAs of 8 warps, ~105 KB of shared memory each).
+// K4 above keeps one instance per SM (all stage matrices resident, ~224 KB), so its serial pivot
+// chains (the S⁻¹ diagonal-block sweeps on one warp, the G⁻¹ sweep on four) leave the tensor pipe
+// idle for about half of every stage (tools/cta_phase_probe).  K4b halves the footprint so that a
+// second instance's contractions run on the SM while the first one sweeps:
+//   * only B_i is staged in shared memory (cp.async, one stage ahead); A_i, Q_i, M_i, R_i, q, r, c
+//     are read from L2, pulled there one stage ahead by bulk L2 prefetches (cp.async.bulk.prefetch);
+//   * W = S⁻¹V is formed explicitly and in place over V (symmetric; W = V(I + δV)⁻¹), so that
+//     T = W F is split into T_B = W B (kept in shared memory) and T_A = W A (formed beside the G⁻¹
+//     sweep), H = Uux = T_Bᵀ A + Mᵀ (= Bᵀ W A), G = Bᵀ T_B + R, Uxx = Aᵀ T_A + Q;
+//   * the forward sweep reads its record and A_i, B_i straight from L2 (prefetched two stages ahead).
+// Same record layout, status semantics and outputs as K4 (Eq.(RR); forward P:496-509,
+// P:640-644; duals P:627-650).
+template <int NX, int NU>
+struct Cta2Layout {
+  using K4 = CtaLayout<NX, NU>;
+  static constexpr int NZ = NX + NU;
+  static constexpr int SN = K4::SN, SMU = K4::SMU;
+  static constexpr int RV = 0;              // V_{i+1} -> W (in place) -> Uxx -> V_i   (ld NX)
+  static constexpr int RS = RV + NX * NX;   // S -> −S⁻¹ | then G = Uuu (ld NU) and H = Uux (ld NU, NX cols)
+  static constexpr int Gs = RS, Hs = RS + NU * NU;
+  static constexpr int RB_SZ0 = (NX * NX > 2 * NX * NU) ? NX * NX : 2 * NX * NU;
+  static constexpr int RB = RS + NX * NX;   // B (ld NX) | T_B (ld NX) = S-sweep scratch = K̃ (ld NU); T_A over all
+  static constexpr int Bs = RB, TB = RB + NX * NU, YS = TB, Kt = TB, TA = RB;
+  static_assert(NU * NU + NU * NX <= NX * NX, "G and H must fit the S region");
+  static_assert(NX * 16 <= NX * NU && NU * NX <= NX * NU, "scratch / K̃ must fit the T_B slot");
+  static constexpr int VEC = RB + RB_SZ0;
+  static constexpr int vs = VEC, ve = vs + NX, ee = ve + NX, gg = ee + NX, bb = gg + NX, kt = bb + NZ,
+                       gpb = kt + NU, xs = gpb + 2 * NU, us = xs + NX, zs = us + NU, pr2 = zs + NX;
+  static constexpr int TOTAL = pr2 + NX;
+  static constexpr int REC = K4::REC;
+};
+
+// 16×16 tile accumulation c += op_A · B over K on one warp (no init / store: the caller owns c).
+template <int K, typename LoadA, typename LoadB>
+__device__ __forceinline__ void tile_acc16(int r0, int c0, LoadA&& la, LoadB&& lb, double (&c)[2][2][2], int lane) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll 8
+  for (int kt = 0; kt < K / 4; ++kt) {
+    double av[2], bv[2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) av[a] = la(r0 + 8 * a + g, 4 * kt + t);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) bv[b] = lb(4 * kt + t, c0 + 8 * b + g);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) dmma884(c[a][b][0], c[a][b][1], av[a], bv[b]);
+  }
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int NX, int NU, int NTHREADS>
+__global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a) {
+  using L = Cta2Layout<NX, NU>;
+  using RL = CtaLayout<NX, NU>;  // record layout
+  constexpr int NZ = NX + NU;
+  constexpr int n = NX, m = NU;
+  constexpr int NW = NTHREADS / 32;
+  static_assert(NW == 8, "K4b is written for 8 warps (4 sweep + 4 side warps in the G⁻¹ phase)");
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t inst = blockIdx.x;
+  const int N = a.N;
+  const int64_t sN = N;
+  const double delta = a.p.delta[inst];
+  double* rec0 = a.ws + inst * sN * L::REC;
+  int32_t st = 0;
+
+  auto X = [](int r, int c) { return swz<NX>(r, c); };
+  auto Y = [](int r, int c) { return swz<NU>(r, c); };
+  // B_i -> Bs (16-byte chunks, rows r, r+1, to their swizzled positions)
+  auto issue_B = [&](int i) {
+    const double* gB = a.p.B + (inst * sN + i) * n * m;
+    for (int e = 2 * tid; e < n * m; e += 2 * NTHREADS) {
+      const int r = e % n, c = e / n;
+      cp_async16(sm + L::Bs + X(r, c), gB + r + c * n);
+    }
+    cp_async_commit();
+  };
+  auto prefetch_stage = [&](int i) {  // the L2-read operands of backward stage i (one thread per array)
+    const int64_t s = inst * sN + i;
+    if (tid == 0) bulk_prefetch_l2(a.p.A + s * n * n, 8u * n * n);
+    else if (tid == 32) bulk_prefetch_l2(a.p.Q + s * L::SN, 8u * L::SN);
+    else if (tid == 64) bulk_prefetch_l2(a.p.M + s * n * m, 8u * n * m);
+    else if (tid == 96) bulk_prefetch_l2(a.p.R + s * L::SMU, 8u * L::SMU);
+    else if (tid == 128) bulk_prefetch_l2(a.p.q + s * n, 8u * n);
+    else if (tid == 160) bulk_prefetch_l2(a.p.r + s * m, 8u * m);
+    else if (tid == 192) bulk_prefetch_l2(a.p.c + s * n, 8u * n);
+  };
+  auto prefetch_fwd = [&](int i) {  // record i, A_i, B_i for the forward sweep
+    const int64_t s = inst * sN + i;
+    if (tid == 0) bulk_prefetch_l2(rec0 + (int64_t)i * L::REC, 8u * L::REC);
+    else if (tid == 32) bulk_prefetch_l2(a.p.A + s * n * n, 8u * n * n);
+    else if (tid == 64) bulk_prefetch_l2(a.p.B + s * n * m, 8u * n * m);
+  };
+
+  // V_N = Q_N -> RV (ld NX), v_N = q_N
+  {
+    const double* QN = a.p.QN + inst * L::SN;
+    for (int e = tid; e < n * n; e += NTHREADS) {
+      const int r = e % n, c = e / n;
+      sm[L::RV + X(r, c)] = r >= c ? QN[pidx(n, r, c)] : QN[pidx(n, c, r)];
+    }
+    for (int r = tid; r < n; r += NTHREADS) sm[L::vs + r] = a.p.qN[inst * n + r];
+    if (a.f.V != nullptr)
+      for (int e = tid; e < L::SN; e += NTHREADS) a.f.V[(inst * (sN + 1) + N) * L::SN + e] = QN[e];
+    if (a.f.v != nullptr)
+      for (int r = tid; r < n; r += NTHREADS) a.f.v[(inst * (sN + 1) + N) * n + r] = a.p.qN[inst * n + r];
+  }
+  if (N > 0) {
+    issue_B(N - 1);
+    prefetch_stage(N - 1);
+  }
+  __syncthreads();
+  auto no_side = [](int, int, int, int) {};
+
+  for (int i = N - 1; i >= 0; --i) {
+    const int64_t s = inst * sN + i;
+    const double* gA = a.p.A + s * n * n;
+    const double* gQ = a.p.Q + s * L::SN;
+    const double* gM = a.p.M + s * n * m;
+    const double* gR = a.p.R + s * L::SMU;
+    if (i > 0) prefetch_stage(i - 1);
+    double* rec = rec0 + (int64_t)i * L::REC;
+    // (1) S = I + δV_{i+1} -> RS;  e = c_{i+1} − δ v_{i+1};  V e
+    for (int e = tid; e < n * n; e += NTHREADS) {
+      const int r = e % n, c = e / n;
+      sm[L::RS + X(r, c)] = delta * sm[L::RV + X(r, c)] + (r == c ? 1.0 : 0.0);
+    }
+    for (int r = tid; r < n; r += NTHREADS) {
+      const double ev = a.p.c[s * n + r] - delta * sm[L::vs + r];
+      sm[L::ee + r] = ev;
+      rec[RL::re + r] = ev;
+    }
+    __syncthreads();
+    cta_matvec<NX, NX, NTHREADS>(
+        [&](int r, int k) { return sm[L::RV + X(r, k)]; }, [&](int k) { return sm[L::ee + k]; },
+        [&](int) { return 0.0; }, [&](int r, double v) { sm[L::ve + r] = v; }, tid);
+    // (2) RS <- −S⁻¹ (block sweep; scratch in the T_B slot)
+    bool fail = false;
+    cta_sweep_blk<NX, NTHREADS>(sm + L::RS, sm + L::YS, tid, &fail, no_side);
+    if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, i);
+    // (3) W = S⁻¹ V in place over V (tiles in registers, one barrier between the reads and the
+    //     writes);  g = v_{i+1} + S⁻¹ V e;  record S⁻¹
+    cp_async_wait<0>();  // B_i (landed long ago; made visible by the barrier below)
+    {
+      constexpr int MT = NX / 16, NTW = MT * MT, TPW = (NTW + NW - 1) / NW;
+      double c[TPW][2][2][2];
+#pragma unroll
+      for (int q = 0; q < TPW; ++q) {
+#pragma unroll
+        for (int x = 0; x < 8; ++x) (&c[q][0][0][0])[x] = 0.0;
+        const int tile = warp + q * NW;
+        if (tile < NTW)
+          tile_acc16<NX>(
+              (tile % MT) * 16, (tile / MT) * 16, [&](int r, int k) { return -sm[L::RS + X(r, k)]; },
+              [&](int k, int cc) { return sm[L::RV + X(k, cc)]; }, c[q], lane);
+      }
+      cta_matvec<NX, NX, NTHREADS>(
+          [&](int r, int k) { return -sm[L::RS + X(r, k)]; }, [&](int k) { return sm[L::ve + k]; },
+          [&](int r) { return sm[L::vs + r]; }, [&](int r, double v) { sm[L::gg + r] = v; }, tid);
+      for (int e = tid; e < n * n; e += NTHREADS) {
+        const int r = e % n, cc = e / n;
+        if (r >= cc) rec[RL::rS + pidx(n, r, cc)] = -sm[L::RS + X(r, cc)];
+      }
+      __syncthreads();
+      const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+      for (int q = 0; q < TPW; ++q) {
+        const int tile = warp + q * NW;
+        if (tile < NTW) {
+          const int r0 = (tile % MT) * 16, c0 = (tile / MT) * 16;
+#pragma unroll
+          for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int y = 0; y < 2; ++y)
+#pragma unroll
+              for (int z = 0; z < 2; ++z) sm[L::RV + X(r0 + 8 * x + g, c0 + 8 * y + 2 * t + z)] = c[q][x][y][z];
+        }
+      }
+    }
+    __syncthreads();
+    // (4) T_B = W B -> TB
+    {
+      constexpr int NTB = (NX / 16) * ((NU + 15) / 16);
+      for (int tt = warp; tt < NTB; tt += NW)
+        warp_tile_mn<NX, NU, NX>(
+            tt, [&](int r, int k) { return sm[L::RV + X(r, k)]; }, [&](int k, int cc) { return sm[L::Bs + X(k, cc)]; },
+            [&](int, int) { return 0.0; }, [&](int r, int cc, double v) { sm[L::TB + X(r, cc)] = v; }, lane);
+    }
+    __syncthreads();
+    // (5) G = Bᵀ T_B + R (lower tiles, mirrored) -> Gs;  H = T_Bᵀ A + Mᵀ -> Hs;  b = (q; r) + Fᵀ g
+    {
+      constexpr int MTU = (NU + 15) / 16, NGT = MTU * (MTU + 1) / 2, NH = MTU * (NX / 16);
+      for (int task = warp; task < NGT + NH; task += NW) {
+        if (task < NGT) {
+          int R, C;
+          lower_tile(task, R, C);
+          const bool mir = R != C;
+          warp_tile_at<NU, NU, NX>(
+              16 * R, 16 * C, [&](int r, int k) { return sm[L::Bs + X(k, r)]; },
+              [&](int k, int cc) { return sm[L::TB + X(k, cc)]; },
+              [&](int r, int cc) { return r >= cc ? gR[pidx(m, r, cc)] : gR[pidx(m, cc, r)]; },
+              [&](int r, int cc, double v) {
+                sm[L::Gs + Y(r, cc)] = v;
+                if (mir) sm[L::Gs + Y(cc, r)] = v;
+              },
+              lane);
+        } else {
+          warp_tile_mn<NU, NX, NX>(
+              task - NGT, [&](int r, int k) { return sm[L::TB + X(k, r)]; }, [&](int k, int cc) { return gA[k + cc * n]; },
+              [&](int r, int cc) { return gM[cc + r * n]; }, [&](int r, int cc, double v) { sm[L::Hs + Y(r, cc)] = v; },
+              lane);
+        }
+      }
+      cta_matvec<NZ, NX, NTHREADS>(
+          [&](int r, int k) { return r < NX ? gA[k + r * n] : sm[L::Bs + X(k, r - NX)]; },
+          [&](int k) { return sm[L::gg + k]; },
+          [&](int r) { return r < NX ? a.p.q[s * n + r] : a.p.r[s * m + r - NX]; },
+          [&](int r, double v) { sm[L::bb + r] = v; }, tid);
+    }
+    __syncthreads();
+    // (6) G⁻¹ (coop sweep on warps 0-3, Gs <- −G⁻¹)  ‖  warps 4-7: T_A = W A -> TA, then Uxx = Aᵀ T_A + Q
+    //     (lower tiles) -> RV over W
+    cta_sweep_any<NU, NTHREADS>(sm + L::Gs, m, sm + L::gpb, tid, &fail, [&](int, int, int slot, int nslots) {
+      constexpr int MTX = NX / 16, NTA = MTX * MTX, NXX = MTX * (MTX + 1) / 2;
+      for (int tt = slot; tt < NTA; tt += nslots)
+        warp_tile_mn<NX, NX, NX>(
+            tt, [&](int r, int k) { return sm[L::RV + X(r, k)]; }, [&](int k, int cc) { return gA[k + cc * n]; },
+            [&](int, int) { return 0.0; }, [&](int r, int cc, double v) { sm[L::TA + X(r, cc)] = v; }, lane);
+      asm volatile("bar.sync 2, %0;\n" ::"n"(NTHREADS / 2) : "memory");
+      for (int tt = slot; tt < NXX; tt += nslots) {
+        int R, C;
+        lower_tile(tt, R, C);
+        warp_tile_at<NX, NX, NX>(
+            16 * R, 16 * C, [&](int r, int k) { return gA[k + r * n]; }, [&](int k, int cc) { return sm[L::TA + X(k, cc)]; },
+            [&](int r, int cc) { return r >= cc ? gQ[pidx(n, r, cc)] : gQ[pidx(n, cc, r)]; },
+            [&](int r, int cc, double v) { sm[L::RV + X(r, cc)] = v; }, lane);
+      }
+    });
+    if (fail && st == 0) st = mk_status(RR_ST_G_NOT_PD, i);
+    // (7) K̃ = G⁻¹ H -> Kt (T_A is dead), k̃ = G⁻¹ b_u;  B_{i−1} streams into Bs behind it
+    if (i > 0) issue_B(i - 1);
+    cta_gemm<NU, NX, NU, false>(
+        [&](int r, int k) { return -sm[L::Gs + Y(r, k)]; }, [&](int k, int cc) { return sm[L::Hs + Y(k, cc)]; },
+        [&](int, int) { return 0.0; }, [&](int r, int cc, double v) { sm[L::Kt + Y(r, cc)] = v; }, warp, NW, lane);
+    cta_matvec<NU, NU, NTHREADS>(
+        [&](int r, int k) { return -sm[L::Gs + Y(r, k)]; }, [&](int k) { return sm[L::bb + NX + k]; },
+        [&](int) { return 0.0; }, [&](int r, double v) { sm[L::kt + r] = v; }, tid);
+    __syncthreads();
+    // (8) V_i = Uxx − Hᵀ K̃ (lower tiles, mirrored) in place;  v_i = b_x − Hᵀ k̃
+    cta_gemm_lower<NX, NU>(
+        [&](int r, int k) { return -sm[L::Hs + Y(k, r)]; }, [&](int k, int cc) { return sm[L::Kt + Y(k, cc)]; },
+        [&](int r, int cc) { return sm[L::RV + X(r, cc)]; },
+        [&](int r, int cc, double v, bool mir) {
+          sm[L::RV + X(r, cc)] = v;
+          if (mir) sm[L::RV + X(cc, r)] = v;
+        },
+        warp, NW, lane);
+    cta_matvec<NX, NU, NTHREADS>(
+        [&](int r, int k) { return -sm[L::Hs + Y(k, r)]; }, [&](int k) { return sm[L::kt + k]; },
+        [&](int r) { return sm[L::bb + r]; }, [&](int r, double v) { sm[L::vs + r] = v; }, tid);
+    __syncthreads();
+    // (9) record K = −K̃ (ld NU), k = −k̃, V_i, v_i; optional factor outputs
+    for (int e = tid; e < m * n; e += NTHREADS) rec[RL::rK + e] = -sm[L::Kt + Y(e % m, e / m)];
+    for (int u = tid; u < m; u += NTHREADS) rec[RL::rk + u] = -sm[L::kt + u];
+    {
+      double* fV = a.f.V != nullptr ? a.f.V + (inst * (sN + 1) + i) * L::SN : nullptr;
+      for (int e = tid; e < n * n; e += NTHREADS) {
+        const int r = e % n, c = e / n;
+        if (r >= c) {
+          const double v = sm[L::RV + X(r, c)];
+          rec[RL::rV + pidx(n, r, c)] = v;
+          if (fV != nullptr) fV[pidx(n, r, c)] = v;
+        }
+      }
+    }
+    for (int r = tid; r < n; r += NTHREADS) rec[RL::rv + r] = sm[L::vs + r];
+    if (a.f.K != nullptr)
+      for (int e = tid; e < m * n; e += NTHREADS) a.f.K[(inst * sN + i) * m * n + e] = -sm[L::Kt + Y(e % m, e / m)];
+    if (a.f.k != nullptr)
+      for (int u = tid; u < m; u += NTHREADS) a.f.k[(inst * sN + i) * m + u] = -sm[L::kt + u];
+    if (a.f.v != nullptr)
+      for (int r = tid; r < n; r += NTHREADS) a.f.v[(inst * (sN + 1) + i) * n + r] = sm[L::vs + r];
+    // (the next stage's barrier after (1) orders these reads before RV / vs / Kt are rewritten)
+  }
+  cp_async_wait<0>();
+  if (N > 0) prefetch_fwd(0);
+  if (N > 1) prefetch_fwd(1);
+  __syncthreads();
+
+  // x_0 = (I + δV_0)⁻¹ (c_0 − δ v_0)
+  for (int e = tid; e < n * n; e += NTHREADS) {
+    const int r = e % n, c = e / n;
+    sm[L::RS + X(r, c)] = delta * sm[L::RV + X(r, c)] + (r == c ? 1.0 : 0.0);
+  }
+  for (int r = tid; r < n; r += NTHREADS) sm[L::ee + r] = a.p.c0[inst * n + r] - delta * sm[L::vs + r];
+  __syncthreads();
+  {
+    bool fail = false;
+    cta_sweep_blk<NX, NTHREADS>(sm + L::RS, sm + L::YS, tid, &fail, no_side);
+    if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, 0);
+  }
+  cta_matvec<NX, NX, NTHREADS>(
+      [&](int r, int k) { return -sm[L::RS + X(r, k)]; }, [&](int k) { return sm[L::ee + k]; }, [&](int) { return 0.0; },
+      [&](int r, double v) { sm[L::xs + r] = v; }, tid);
+  __shared__ int sst;
+  if (tid == 0) sst = 0;
+  __syncthreads();
+  if (st != 0) atomicMax(&sst, st);
+  __syncthreads();
+  int32_t status = sst;
+
+  double* xo = a.s.x + inst * (sN + 1) * n;
+  double* uo = a.s.u + inst * sN * m;
+  double* yo = a.s.y + inst * (sN + 1) * n;
+  for (int r = tid; r < n; r += NTHREADS) xo[r] = sm[L::xs + r];
+  bool bad = false;
+  // forward, operands from L2 (record i, A_i, B_i prefetched two stages ahead):
+  //   u_i = K_i x_i + k_i,  y_i = V_i x_i + v_i,  z = A_i x_i + e_i,  x_{i+1} = S⁻¹_{i+1} (z + B_i u_i)
+  for (int i = 0; i < N; ++i) {
+    const double* rc = rec0 + (int64_t)i * L::REC;
+    const double* gA = a.p.A + (inst * sN + i) * n * n;
+    const double* gB = a.p.B + (inst * sN + i) * n * m;
+    if (i + 2 < N) prefetch_fwd(i + 2);
+    cta_matvec<NU, NX, NTHREADS>(
+        [&](int r, int k) { return rc[RL::rK + r + k * m]; }, [&](int k) { return sm[L::xs + k]; },
+        [&](int r) { return rc[RL::rk + r]; },
+        [&](int r, double v) {
+          sm[L::us + r] = v;
+          uo[(int64_t)i * m + r] = v;
+          bad |= !isfinite(v);
+        },
+        tid);
+    cta_matvec<NX, NX, NTHREADS>(
+        [&](int r, int k) { return rc[RL::rV + (r >= k ? pidx(n, r, k) : pidx(n, k, r))]; },
+        [&](int k) { return sm[L::xs + k]; }, [&](int r) { return rc[RL::rv + r]; },
+        [&](int r, double v) {
+          yo[(int64_t)i * n + r] = v;
+          bad |= !isfinite(v);
+        },
+        tid);
+    cta_matvec<NX, NX, NTHREADS>(
+        [&](int r, int k) { return gA[r + k * n]; }, [&](int k) { return sm[L::xs + k]; },
+        [&](int r) { return rc[RL::re + r]; }, [&](int r, double v) { sm[L::zs + r] = v; }, tid);
+    __syncthreads();
+    cta_matvec<NX, NU, NTHREADS>(
+        [&](int r, int k) { return gB[r + k * n]; }, [&](int k) { return sm[L::us + k]; },
+        [&](int r) { return sm[L::zs + r]; }, [&](int r, double v) { sm[L::pr2 + r] = v; }, tid);
+    __syncthreads();
+    cta_matvec<NX, NX, NTHREADS>(
+        [&](int r, int k) { return rc[RL::rS + (r >= k ? pidx(n, r, k) : pidx(n, k, r))]; },
+        [&](int k) { return sm[L::pr2 + k]; }, [&](int) { return 0.0; },
+        [&](int r, double v) {
+          sm[L::xs + r] = v;
+          xo[(int64_t)(i + 1) * n + r] = v;
+          bad |= !isfinite(v);
+        },
+        tid);
+    __syncthreads();
+  }
+  {  // y_N = Q_N x_N + q_N
+    const double* QN = a.p.QN + inst * L::SN;
+    cta_matvec<NX, NX, NTHREADS>(
+        [&](int r, int k) { return k >= r ? QN[pidx(n, k, r)] : QN[pidx(n, r, k)]; }, [&](int k) { return sm[L::xs + k]; },
+        [&](int r) { return a.p.qN[inst * n + r]; },
+        [&](int r, double v) {
+          yo[sN * n + r] = v;
+          bad |= !isfinite(v);
+        },
+        tid);
+  }
+  if (__syncthreads_or(bad) && status == 0) status = RR_ST_NONFINITE;
+  if (status != 0) {
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    for (int64_t e = tid; e < (sN + 1) * n; e += NTHREADS) {
+      xo[e] = nan;
+      yo[e] = nan;
+    }
+    for (int64_t e = tid; e < sN * m; e += NTHREADS) uo[e] = nan;
+  }
+  if (tid == 0) a.status[inst] = status;
+}
+
+template <int NX, int NU>
+struct Cta2Cfg {
+  static constexpr int NTHREADS = 256;
+  static size_t smem_bytes() { return sizeof(double) * (size_t)Cta2Layout<NX, NU>::TOTAL; }
+  static int64_t ws_doubles(int64_t batch, int N) { return batch * (int64_t)N * CtaLayout<NX, NU>::REC; }
+  static cudaError_t launch(const FusedArgs& a, cudaStream_t s) {
+    auto k = rr_cta2_kernel<NX, NU, NTHREADS>;
+    const size_t smb = smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
+    if (e != cudaSuccess) return e;
+    k<<<(unsigned)a.batch, NTHREADS, smb, s>>>(a);
+    return cudaGetLastError();
+  }
+};
+
 template <int NX, int NU, int NT_ = 256>
 struct CtaCfg {
   static constexpr int NTHREADS = NT_;
@@ -1010,7 +1415,12 @@ struct CtaCfg {
 
 template <typename F>
 static bool dispatch_cta(int nx, int nu, F&& f) {
-  if (nx == 64 && nu == 32) return f(CtaCfg<64, 32, 512>{});
+  if (nx == 64 && nu == 32) {
+    // K4b (two instances per SM) by default; RR_B200_CTA=1 selects K4 (one instance per SM, 16 warps)
+    const char* v = getenv("RR_B200_CTA");
+    if (v == nullptr || v[0] != '1') return f(Cta2Cfg<64, 32>{});
+    return f(CtaCfg<64, 32, 512>{});
+  }
   if (nx == 32 && nu == 16) return f(CtaCfg<32, 16>{});
   if (nx == 24 && nu == 8) return f(CtaCfg<24, 8>{});
   return false;
