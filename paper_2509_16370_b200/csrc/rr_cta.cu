@@ -586,7 +586,7 @@ __device__ __forceinline__ void cta_sweep_any(double* A, int lda, double* scratc
 }
 
 // One 16×16 super-tile at (m0, n0) of C = op_A · B + init (K multiple of 4) on one warp, masked to M × N.
-template <int M, int N, int K, typename LoadA, typename LoadB, typename Init, typename Store>
+template <int M, int N, int K, int UNR = 4, typename LoadA, typename LoadB, typename Init, typename Store>
 __device__ __forceinline__ void warp_tile_at(int m0, int n0, LoadA&& la, LoadB&& lb, Init&& init, Store&& store,
                                              int lane) {
   const int g = lane >> 2, t = lane & 3;
@@ -600,7 +600,7 @@ __device__ __forceinline__ void warp_tile_at(int m0, int n0, LoadA&& la, LoadB&&
         const int r = m0 + 8 * a + g, col = n0 + 8 * b + 2 * t + e;
         c[a][b][e] = (r < M && col < N) ? init(r, col) : 0.0;
       }
-#pragma unroll 4
+#pragma unroll UNR
   for (int kt = 0; kt < K / 4; ++kt) {
     double av[2], bv[2];
 #pragma unroll
@@ -630,10 +630,10 @@ __device__ __forceinline__ void warp_tile_at(int m0, int n0, LoadA&& la, LoadB&&
 }
 
 // Tile index tt (column-major tile order) of an M×N result.
-template <int M, int N, int K, typename LoadA, typename LoadB, typename Init, typename Store>
+template <int M, int N, int K, int UNR = 4, typename LoadA, typename LoadB, typename Init, typename Store>
 __device__ __forceinline__ void warp_tile_mn(int tt, LoadA&& la, LoadB&& lb, Init&& init, Store&& store, int lane) {
   constexpr int MT = (M + 15) / 16;
-  warp_tile_at<M, N, K>((tt % MT) * 16, (tt / MT) * 16, la, lb, init, store, lane);
+  warp_tile_at<M, N, K, UNR>((tt % MT) * 16, (tt / MT) * 16, la, lb, init, store, lane);
 }
 
 // (R, C) of the t-th lower tile (R >= C) in row-major lower order.
@@ -995,59 +995,90 @@ __global__ void __launch_bounds__(NTHREADS, 1) rr_cta_kernel(const FusedArgs a) 
 }
 
 // ==========================================================================================
-// K4b -- the C3 shape at TWO instances per SM (two CTAs of 8 warps, ~105 KB of shared memory each).
+// K4b -- the C3 shape at TWO instances per SM (two CTAs of 8 warps, ~108 KB of shared memory each).
 // K4 above keeps one instance per SM (all stage matrices resident, ~224 KB), so its serial pivot
 // chains (the S⁻¹ diagonal-block sweeps on one warp, the G⁻¹ sweep on four) leave the tensor pipe
 // idle for about half of every stage (tools/cta_phase_probe).  K4b halves the footprint so that a
 // second instance's contractions run on the SM while the first one sweeps:
 //   * only B_i is staged in shared memory (cp.async, one stage ahead); A_i, Q_i, M_i, R_i, q, r, c
 //     are read from L2, pulled there one stage ahead by bulk L2 prefetches (cp.async.bulk.prefetch);
-//   * W = S⁻¹V is formed explicitly and in place over V (symmetric; W = V(I + δV)⁻¹), so that
-//     T = W F is split into T_B = W B (kept in shared memory) and T_A = W A (formed beside the G⁻¹
-//     sweep), H = Uux = T_Bᵀ A + Mᵀ (= Bᵀ W A), G = Bᵀ T_B + R, Uxx = Aᵀ T_A + Q;
-//   * the forward sweep reads its record and A_i, B_i straight from L2 (prefetched two stages ahead).
+//   * W = S⁻¹V (symmetric: W = V(I + δV)⁻¹) is formed explicitly, in place over V; T = W F is
+//     formed at once (T_A = W A over the dead S⁻¹, T_B = W B beside B), so that G = Bᵀ T_B + R and
+//     H = Uux = Bᵀ T_A + Mᵀ come from shared memory and only Uxx = Aᵀ T_A + Q runs beside the G⁻¹
+//     sweep (A from L2);
+//   * V_i = Uxx − Hᵀ K̃ is formed in registers and stored over the dead G, H (V's home region);
+//   * the forward sweep stages its per-stage record [K k V v e S⁻¹] by TMA bulk copies into two
+//     shared buffers (one stage ahead) and reads A_i, B_i from L2 (prefetched two stages ahead).
 // Same record layout, status semantics and outputs as K4 (Eq.(RR); forward P:496-509,
 // P:640-644; duals P:627-650).
 template <int NX, int NU>
 struct Cta2Layout {
   using K4 = CtaLayout<NX, NU>;
   static constexpr int NZ = NX + NU;
-  static constexpr int SN = K4::SN, SMU = K4::SMU;
-  static constexpr int RV = 0;              // V_{i+1} -> W (in place) -> Uxx -> V_i   (ld NX)
-  static constexpr int RS = RV + NX * NX;   // S -> −S⁻¹ | then G = Uuu (ld NU) and H = Uux (ld NU, NX cols)
-  static constexpr int Gs = RS, Hs = RS + NU * NU;
-  static constexpr int RB_SZ0 = (NX * NX > 2 * NX * NU) ? NX * NX : 2 * NX * NU;
-  static constexpr int RB = RS + NX * NX;   // B (ld NX) | T_B (ld NX) = S-sweep scratch = K̃ (ld NU); T_A over all
-  static constexpr int Bs = RB, TB = RB + NX * NU, YS = TB, Kt = TB, TA = RB;
-  static_assert(NU * NU + NU * NX <= NX * NX, "G and H must fit the S region");
-  static_assert(NX * 16 <= NX * NU && NU * NX <= NX * NU, "scratch / K̃ must fit the T_B slot");
-  static constexpr int VEC = RB + RB_SZ0;
+  static constexpr int SN = K4::SN, SMU = K4::SMU, REC = K4::REC;
+  // backward: three NX×NX regions
+  static constexpr int RV = 0;             // V_{i+1} -> W (in place) -> G (ld NU) | H (ld NU) -> V_i
+  static constexpr int RS = RV + NX * NX;  // S -> −S⁻¹ -> T_A (ld NX) -> K̃ (ld NU)
+  static constexpr int RB = RS + NX * NX;  // B (ld NX) | T_B (ld NX) = S-sweep scratch;  Uxx (ld NX) over both
+  static constexpr int Gs = RV, Hs = RV + NU * NU, TA = RS, Kt = RS, Bs = RB, TB = RB + NX * NU, YS = TB,
+                       Ux = RB;
+  static_assert(NU * NU + NU * NX <= NX * NX && 2 * NX * NU <= NX * NX && NX * 16 <= NX * NU,
+                "K4b layout assumes n_u = n_x / 2");
+  // forward: two record buffers over the dead backward regions
+  static constexpr int FR0 = 0, FR1 = REC;
+  static constexpr int VEC0 = RB + NX * NX > 2 * REC ? RB + NX * NX : 2 * REC;
+  static constexpr int VEC = (VEC0 + 1) & ~1;
   static constexpr int vs = VEC, ve = vs + NX, ee = ve + NX, gg = ee + NX, bb = gg + NX, kt = bb + NZ,
                        gpb = kt + NU, xs = gpb + 2 * NU, us = xs + NX, zs = us + NU, pr2 = zs + NX;
   static constexpr int TOTAL = pr2 + NX;
-  static constexpr int REC = K4::REC;
 };
-
-// 16×16 tile accumulation c += op_A · B over K on one warp (no init / store: the caller owns c).
-template <int K, typename LoadA, typename LoadB>
-__device__ __forceinline__ void tile_acc16(int r0, int c0, LoadA&& la, LoadB&& lb, double (&c)[2][2][2], int lane) {
-  const int g = lane >> 2, t = lane & 3;
-#pragma unroll 8
-  for (int kt = 0; kt < K / 4; ++kt) {
-    double av[2], bv[2];
-#pragma unroll
-    for (int a = 0; a < 2; ++a) av[a] = la(r0 + 8 * a + g, 4 * kt + t);
-#pragma unroll
-    for (int b = 0; b < 2; ++b) bv[b] = lb(4 * kt + t, c0 + 8 * b + g);
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) dmma884(c[a][b][0], c[a][b][1], av[a], bv[b]);
-  }
-}
 
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// One 16×16 tile of C = op_A · B + init on one warp (K multiple of 4) where one operand lives in L2
+// (GA: op_A, else B): all of that operand's fragments (2 per k-step) are loaded before the first DMMA,
+// so a tile waits for one L2 round trip instead of one per unrolled batch; the init values (global
+// too) are loaded up front and added after the contraction.  No masking (M, N multiples of 16).
+template <int K, bool GA, typename LoadA, typename LoadB, typename Init, typename Store>
+__device__ __forceinline__ void warp_tile_l2(int m0, int n0, LoadA&& la, LoadB&& lb, Init&& init, Store&& store,
+                                             int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  double pre[K / 4][2], ini[2][2][2], c[2][2][2];
+#pragma unroll
+  for (int kt = 0; kt < K / 4; ++kt)
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+      pre[kt][x] = GA ? la(m0 + 8 * x + g, 4 * kt + t) : lb(4 * kt + t, n0 + 8 * x + g);
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        ini[x][y][z] = init(m0 + 8 * x + g, n0 + 8 * y + 2 * t + z);
+        c[x][y][z] = 0.0;
+      }
+#pragma unroll
+  for (int kt = 0; kt < K / 4; ++kt) {
+    double o[2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) o[x] = GA ? lb(4 * kt + t, n0 + 8 * x + g) : la(m0 + 8 * x + g, 4 * kt + t);
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        if (GA) dmma884(c[x][y][0], c[x][y][1], pre[kt][x], o[y]);
+        else dmma884(c[x][y][0], c[x][y][1], o[x], pre[kt][y]);
+      }
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int z = 0; z < 2; ++z) store(m0 + 8 * x + g, n0 + 8 * y + 2 * t + z, c[x][y][z] + ini[x][y][z]);
 }
 
 template <int NX, int NU, int NTHREADS>
@@ -1078,7 +1109,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
     }
     cp_async_commit();
   };
-  auto prefetch_stage = [&](int i) {  // the L2-read operands of backward stage i (one thread per array)
+  auto prefetch_stage = [&](int i) {  // backward stage i's operands into L2 (one thread per array)
     const int64_t s = inst * sN + i;
     if (tid == 0) bulk_prefetch_l2(a.p.A + s * n * n, 8u * n * n);
     else if (tid == 32) bulk_prefetch_l2(a.p.Q + s * L::SN, 8u * L::SN);
@@ -1087,12 +1118,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
     else if (tid == 128) bulk_prefetch_l2(a.p.q + s * n, 8u * n);
     else if (tid == 160) bulk_prefetch_l2(a.p.r + s * m, 8u * m);
     else if (tid == 192) bulk_prefetch_l2(a.p.c + s * n, 8u * n);
-  };
-  auto prefetch_fwd = [&](int i) {  // record i, A_i, B_i for the forward sweep
-    const int64_t s = inst * sN + i;
-    if (tid == 0) bulk_prefetch_l2(rec0 + (int64_t)i * L::REC, 8u * L::REC);
-    else if (tid == 32) bulk_prefetch_l2(a.p.A + s * n * n, 8u * n * n);
-    else if (tid == 64) bulk_prefetch_l2(a.p.B + s * n * m, 8u * n * m);
+    else if (tid == 224) bulk_prefetch_l2(a.p.B + s * n * m, 8u * n * m);
   };
 
   // V_N = Q_N -> RV (ld NX), v_N = q_N
@@ -1112,8 +1138,9 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
     issue_B(N - 1);
     prefetch_stage(N - 1);
   }
-  __syncthreads();
   auto no_side = [](int, int, int, int) {};
+  static_assert(NX <= NTHREADS, "one thread per row of c");
+  double c_next = (tid < n && N > 0) ? a.p.c[(inst * sN + N - 1) * n + tid] : 0.0;  // c_{i+1}, a stage ahead
 
   for (int i = N - 1; i >= 0; --i) {
     const int64_t s = inst * sN + i;
@@ -1121,41 +1148,63 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
     const double* gQ = a.p.Q + s * L::SN;
     const double* gM = a.p.M + s * n * m;
     const double* gR = a.p.R + s * L::SMU;
-    if (i > 0) prefetch_stage(i - 1);
     double* rec = rec0 + (int64_t)i * L::REC;
+    __syncthreads();  // the previous stage's record reads (RS = K̃) before S is written
+    RR_PROF(i, 0);
+    if (i > 0) prefetch_stage(i - 1);
+    const double c_cur = c_next;
+    if (i > 0 && tid < n) c_next = a.p.c[(s - 1) * n + tid];
     // (1) S = I + δV_{i+1} -> RS;  e = c_{i+1} − δ v_{i+1};  V e
     for (int e = tid; e < n * n; e += NTHREADS) {
       const int r = e % n, c = e / n;
       sm[L::RS + X(r, c)] = delta * sm[L::RV + X(r, c)] + (r == c ? 1.0 : 0.0);
     }
-    for (int r = tid; r < n; r += NTHREADS) {
-      const double ev = a.p.c[s * n + r] - delta * sm[L::vs + r];
-      sm[L::ee + r] = ev;
-      rec[RL::re + r] = ev;
+    if (tid < n) {
+      const double ev = c_cur - delta * sm[L::vs + tid];
+      sm[L::ee + tid] = ev;
+      rec[RL::re + tid] = ev;
     }
     __syncthreads();
     cta_matvec<NX, NX, NTHREADS>(
         [&](int r, int k) { return sm[L::RV + X(r, k)]; }, [&](int k) { return sm[L::ee + k]; },
         [&](int) { return 0.0; }, [&](int r, double v) { sm[L::ve + r] = v; }, tid);
+    RR_PROF(i, 1);
     // (2) RS <- −S⁻¹ (block sweep; scratch in the T_B slot)
     bool fail = false;
-    cta_sweep_blk<NX, NTHREADS>(sm + L::RS, sm + L::YS, tid, &fail, no_side);
+    cta_sweep_blk<NX, NTHREADS>(sm + L::RS, sm + L::YS, tid, &fail, no_side
+#ifdef RR_CTA_PROFILE
+                                ,
+                                (blockIdx.x == 0 && i == RR_CTA_PROFILE) ? 12 : -1
+#endif
+    );
     if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, i);
+    RR_PROF(i, 2);
     // (3) W = S⁻¹ V in place over V (tiles in registers, one barrier between the reads and the
     //     writes);  g = v_{i+1} + S⁻¹ V e;  record S⁻¹
-    cp_async_wait<0>();  // B_i (landed long ago; made visible by the barrier below)
+    cp_async_wait<0>();  // B_i (made visible by the barriers below)
     {
       constexpr int MT = NX / 16, NTW = MT * MT, TPW = (NTW + NW - 1) / NW;
+      const int g = lane >> 2, t = lane & 3;
       double c[TPW][2][2][2];
 #pragma unroll
       for (int q = 0; q < TPW; ++q) {
+        const int tile = warp + q * NW, r0 = (tile % MT) * 16, c0 = (tile / MT) * 16;
 #pragma unroll
         for (int x = 0; x < 8; ++x) (&c[q][0][0][0])[x] = 0.0;
-        const int tile = warp + q * NW;
-        if (tile < NTW)
-          tile_acc16<NX>(
-              (tile % MT) * 16, (tile / MT) * 16, [&](int r, int k) { return -sm[L::RS + X(r, k)]; },
-              [&](int k, int cc) { return sm[L::RV + X(k, cc)]; }, c[q], lane);
+        if (tile < NTW) {
+#pragma unroll 8
+          for (int kk = 0; kk < NX / 4; ++kk) {
+            double av[2], bv[2];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) av[x] = -sm[L::RS + X(r0 + 8 * x + g, 4 * kk + t)];
+#pragma unroll
+            for (int y = 0; y < 2; ++y) bv[y] = sm[L::RV + X(4 * kk + t, c0 + 8 * y + g)];
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+              for (int y = 0; y < 2; ++y) dmma884(c[q][x][y][0], c[q][x][y][1], av[x], bv[y]);
+          }
+        }
       }
       cta_matvec<NX, NX, NTHREADS>(
           [&](int r, int k) { return -sm[L::RS + X(r, k)]; }, [&](int k) { return sm[L::ve + k]; },
@@ -1165,12 +1214,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
         if (r >= cc) rec[RL::rS + pidx(n, r, cc)] = -sm[L::RS + X(r, cc)];
       }
       __syncthreads();
-      const int g = lane >> 2, t = lane & 3;
 #pragma unroll
       for (int q = 0; q < TPW; ++q) {
-        const int tile = warp + q * NW;
+        const int tile = warp + q * NW, r0 = (tile % MT) * 16, c0 = (tile / MT) * 16;
         if (tile < NTW) {
-          const int r0 = (tile % MT) * 16, c0 = (tile / MT) * 16;
 #pragma unroll
           for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -1181,24 +1228,34 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
       }
     }
     __syncthreads();
-    // (4) T_B = W B -> TB
+    RR_PROF(i, 3);
+    // (4) T = W F:  T_B = W B -> TB (B in shared memory),  T_A = W A -> TA over the dead S⁻¹ (A in L2)
     {
-      constexpr int NTB = (NX / 16) * ((NU + 15) / 16);
-      for (int tt = warp; tt < NTB; tt += NW)
-        warp_tile_mn<NX, NU, NX>(
-            tt, [&](int r, int k) { return sm[L::RV + X(r, k)]; }, [&](int k, int cc) { return sm[L::Bs + X(k, cc)]; },
-            [&](int, int) { return 0.0; }, [&](int r, int cc, double v) { sm[L::TB + X(r, cc)] = v; }, lane);
+      constexpr int NTB = (NX / 16) * (NU / 16), NTA = (NX / 16) * (NX / 16);
+      for (int tt = warp; tt < NTB + NTA; tt += NW) {
+        if (tt < NTB)
+          warp_tile_mn<NX, NU, NX>(
+              tt, [&](int r, int k) { return sm[L::RV + X(r, k)]; }, [&](int k, int cc) { return sm[L::Bs + X(k, cc)]; },
+              [&](int, int) { return 0.0; }, [&](int r, int cc, double v) { sm[L::TB + X(r, cc)] = v; }, lane);
+        else
+          warp_tile_l2<NX, false>(
+              ((tt - NTB) % (NX / 16)) * 16, ((tt - NTB) / (NX / 16)) * 16, [&](int r, int k) { return sm[L::RV + X(r, k)]; },
+              [&](int k, int cc) { return gA[k + cc * n]; }, [&](int, int) { return 0.0; },
+              [&](int r, int cc, double v) { sm[L::TA + X(r, cc)] = v; }, lane);
+      }
     }
     __syncthreads();
-    // (5) G = Bᵀ T_B + R (lower tiles, mirrored) -> Gs;  H = T_Bᵀ A + Mᵀ -> Hs;  b = (q; r) + Fᵀ g
+    RR_PROF(i, 4);
+    // (5) G = Bᵀ T_B + R (lower tiles, mirrored) -> Gs;  H = Bᵀ T_A + Mᵀ -> Hs (both over the dead W);
+    //     b = (q; r) + Fᵀ g
     {
-      constexpr int MTU = (NU + 15) / 16, NGT = MTU * (MTU + 1) / 2, NH = MTU * (NX / 16);
+      constexpr int MTU = NU / 16, NGT = MTU * (MTU + 1) / 2, NH = MTU * (NX / 16);
       for (int task = warp; task < NGT + NH; task += NW) {
         if (task < NGT) {
           int R, C;
           lower_tile(task, R, C);
           const bool mir = R != C;
-          warp_tile_at<NU, NU, NX>(
+          warp_tile_l2<NX, true>(  // (both operands in shared memory; R, the init, from L2)
               16 * R, 16 * C, [&](int r, int k) { return sm[L::Bs + X(k, r)]; },
               [&](int k, int cc) { return sm[L::TB + X(k, cc)]; },
               [&](int r, int cc) { return r >= cc ? gR[pidx(m, r, cc)] : gR[pidx(m, cc, r)]; },
@@ -1208,10 +1265,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
               },
               lane);
         } else {
-          warp_tile_mn<NU, NX, NX>(
-              task - NGT, [&](int r, int k) { return sm[L::TB + X(k, r)]; }, [&](int k, int cc) { return gA[k + cc * n]; },
-              [&](int r, int cc) { return gM[cc + r * n]; }, [&](int r, int cc, double v) { sm[L::Hs + Y(r, cc)] = v; },
-              lane);
+          warp_tile_l2<NX, true>(
+              ((task - NGT) % MTU) * 16, ((task - NGT) / MTU) * 16, [&](int r, int k) { return sm[L::Bs + X(k, r)]; },
+              [&](int k, int cc) { return sm[L::TA + X(k, cc)]; }, [&](int r, int cc) { return gM[cc + r * n]; },
+              [&](int r, int cc, double v) { sm[L::Hs + Y(r, cc)] = v; }, lane);
         }
       }
       cta_matvec<NZ, NX, NTHREADS>(
@@ -1221,27 +1278,23 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
           [&](int r, double v) { sm[L::bb + r] = v; }, tid);
     }
     __syncthreads();
-    // (6) G⁻¹ (coop sweep on warps 0-3, Gs <- −G⁻¹)  ‖  warps 4-7: T_A = W A -> TA, then Uxx = Aᵀ T_A + Q
-    //     (lower tiles) -> RV over W
+    RR_PROF(i, 5);
+    // (6) G⁻¹ (coop sweep on warps 0-3, Gs <- −G⁻¹)  ‖  warps 4-7: Uxx = Aᵀ T_A + Q (lower tiles) -> Ux
+    //     over the dead B / T_B (A from L2)
     cta_sweep_any<NU, NTHREADS>(sm + L::Gs, m, sm + L::gpb, tid, &fail, [&](int, int, int slot, int nslots) {
-      constexpr int MTX = NX / 16, NTA = MTX * MTX, NXX = MTX * (MTX + 1) / 2;
-      for (int tt = slot; tt < NTA; tt += nslots)
-        warp_tile_mn<NX, NX, NX>(
-            tt, [&](int r, int k) { return sm[L::RV + X(r, k)]; }, [&](int k, int cc) { return gA[k + cc * n]; },
-            [&](int, int) { return 0.0; }, [&](int r, int cc, double v) { sm[L::TA + X(r, cc)] = v; }, lane);
-      asm volatile("bar.sync 2, %0;\n" ::"n"(NTHREADS / 2) : "memory");
+      constexpr int MTX = NX / 16, NXX = MTX * (MTX + 1) / 2;
       for (int tt = slot; tt < NXX; tt += nslots) {
         int R, C;
         lower_tile(tt, R, C);
-        warp_tile_at<NX, NX, NX>(
+        warp_tile_l2<NX, true>(
             16 * R, 16 * C, [&](int r, int k) { return gA[k + r * n]; }, [&](int k, int cc) { return sm[L::TA + X(k, cc)]; },
             [&](int r, int cc) { return r >= cc ? gQ[pidx(n, r, cc)] : gQ[pidx(n, cc, r)]; },
-            [&](int r, int cc, double v) { sm[L::RV + X(r, cc)] = v; }, lane);
+            [&](int r, int cc, double v) { sm[L::Ux + X(r, cc)] = v; }, lane);
       }
     });
     if (fail && st == 0) st = mk_status(RR_ST_G_NOT_PD, i);
-    // (7) K̃ = G⁻¹ H -> Kt (T_A is dead), k̃ = G⁻¹ b_u;  B_{i−1} streams into Bs behind it
-    if (i > 0) issue_B(i - 1);
+    RR_PROF(i, 6);
+    // (7) K̃ = G⁻¹ H -> Kt over the dead T_A;  k̃ = G⁻¹ b_u
     cta_gemm<NU, NX, NU, false>(
         [&](int r, int k) { return -sm[L::Gs + Y(r, k)]; }, [&](int k, int cc) { return sm[L::Hs + Y(k, cc)]; },
         [&](int, int) { return 0.0; }, [&](int r, int cc, double v) { sm[L::Kt + Y(r, cc)] = v; }, warp, NW, lane);
@@ -1249,20 +1302,68 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
         [&](int r, int k) { return -sm[L::Gs + Y(r, k)]; }, [&](int k) { return sm[L::bb + NX + k]; },
         [&](int) { return 0.0; }, [&](int r, double v) { sm[L::kt + r] = v; }, tid);
     __syncthreads();
-    // (8) V_i = Uxx − Hᵀ K̃ (lower tiles, mirrored) in place;  v_i = b_x − Hᵀ k̃
-    cta_gemm_lower<NX, NU>(
-        [&](int r, int k) { return -sm[L::Hs + Y(k, r)]; }, [&](int k, int cc) { return sm[L::Kt + Y(k, cc)]; },
-        [&](int r, int cc) { return sm[L::RV + X(r, cc)]; },
-        [&](int r, int cc, double v, bool mir) {
-          sm[L::RV + X(r, cc)] = v;
-          if (mir) sm[L::RV + X(cc, r)] = v;
-        },
-        warp, NW, lane);
-    cta_matvec<NX, NU, NTHREADS>(
-        [&](int r, int k) { return -sm[L::Hs + Y(k, r)]; }, [&](int k) { return sm[L::kt + k]; },
-        [&](int r) { return sm[L::bb + r]; }, [&](int r, double v) { sm[L::vs + r] = v; }, tid);
+    RR_PROF(i, 7);
+    // (8) V_i = Uxx − Hᵀ K̃ (lower tiles in registers), v_i = b_x − Hᵀ k̃;  then V_i (mirrored) -> RV
+    //     over the dead G, H
+    {
+      constexpr int MT = NX / 16, NTL = MT * (MT + 1) / 2, TPW = (NTL + NW - 1) / NW;
+      const int g = lane >> 2, t = lane & 3;
+      double c[TPW][2][2][2];
+#pragma unroll
+      for (int q = 0; q < TPW; ++q) {
+        const int tile = warp + q * NW;
+        if (tile < NTL) {
+          int R, C;
+          lower_tile(tile, R, C);
+          const int r0 = 16 * R, c0 = 16 * C;
+#pragma unroll
+          for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int y = 0; y < 2; ++y)
+#pragma unroll
+              for (int z = 0; z < 2; ++z) c[q][x][y][z] = sm[L::Ux + X(r0 + 8 * x + g, c0 + 8 * y + 2 * t + z)];
+#pragma unroll
+          for (int kk = 0; kk < NU / 4; ++kk) {
+            double av[2], bv[2];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) av[x] = -sm[L::Hs + Y(4 * kk + t, r0 + 8 * x + g)];
+#pragma unroll
+            for (int y = 0; y < 2; ++y) bv[y] = sm[L::Kt + Y(4 * kk + t, c0 + 8 * y + g)];
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+              for (int y = 0; y < 2; ++y) dmma884(c[q][x][y][0], c[q][x][y][1], av[x], bv[y]);
+          }
+        }
+      }
+      cta_matvec<NX, NU, NTHREADS>(
+          [&](int r, int k) { return -sm[L::Hs + Y(k, r)]; }, [&](int k) { return sm[L::kt + k]; },
+          [&](int r) { return sm[L::bb + r]; }, [&](int r, double v) { sm[L::vs + r] = v; }, tid);
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < TPW; ++q) {
+        const int tile = warp + q * NW;
+        if (tile < NTL) {
+          int R, C;
+          lower_tile(tile, R, C);
+          const int r0 = 16 * R, c0 = 16 * C;
+#pragma unroll
+          for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int y = 0; y < 2; ++y)
+#pragma unroll
+              for (int z = 0; z < 2; ++z) {
+                const int r = r0 + 8 * x + g, cc = c0 + 8 * y + 2 * t + z;
+                sm[L::RV + X(r, cc)] = c[q][x][y][z];
+                if (R != C) sm[L::RV + X(cc, r)] = c[q][x][y][z];
+              }
+        }
+      }
+    }
     __syncthreads();
-    // (9) record K = −K̃ (ld NU), k = −k̃, V_i, v_i; optional factor outputs
+    RR_PROF(i, 8);
+    // (9) B_{i−1} streams into Bs (Uxx is dead);  record K = −K̃ (ld NU), k = −k̃, V_i, v_i; factor outputs
+    if (i > 0) issue_B(i - 1);
     for (int e = tid; e < m * n; e += NTHREADS) rec[RL::rK + e] = -sm[L::Kt + Y(e % m, e / m)];
     for (int u = tid; u < m; u += NTHREADS) rec[RL::rk + u] = -sm[L::kt + u];
     {
@@ -1283,12 +1384,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
       for (int u = tid; u < m; u += NTHREADS) a.f.k[(inst * sN + i) * m + u] = -sm[L::kt + u];
     if (a.f.v != nullptr)
       for (int r = tid; r < n; r += NTHREADS) a.f.v[(inst * (sN + 1) + i) * n + r] = sm[L::vs + r];
-    // (the next stage's barrier after (1) orders these reads before RV / vs / Kt are rewritten)
   }
   cp_async_wait<0>();
-  if (N > 0) prefetch_fwd(0);
-  if (N > 1) prefetch_fwd(1);
   __syncthreads();
+  RR_PROF(RR_CTA_PROFILE_FWD, 9);
 
   // x_0 = (I + δV_0)⁻¹ (c_0 − δ v_0)
   for (int e = tid; e < n * n; e += NTHREADS) {
@@ -1296,6 +1395,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
     sm[L::RS + X(r, c)] = delta * sm[L::RV + X(r, c)] + (r == c ? 1.0 : 0.0);
   }
   for (int r = tid; r < n; r += NTHREADS) sm[L::ee + r] = a.p.c0[inst * n + r] - delta * sm[L::vs + r];
+  // records 0 and 1, A, B of the first forward stages into L2 while x_0 is solved
+  auto prefetch_fwd = [&](int i) {
+    const int64_t s = inst * sN + i;
+    if (tid == 0) bulk_prefetch_l2(rec0 + (int64_t)i * L::REC, 8u * L::REC);
+    else if (tid == 32) bulk_prefetch_l2(a.p.A + s * n * n, 8u * n * n);
+    else if (tid == 64) bulk_prefetch_l2(a.p.B + s * n * m, 8u * n * m);
+  };
+  for (int i = 0; i < N && i < 2; ++i) prefetch_fwd(i);
   __syncthreads();
   {
     bool fail = false;
@@ -1306,10 +1413,15 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
       [&](int r, int k) { return -sm[L::RS + X(r, k)]; }, [&](int k) { return sm[L::ee + k]; }, [&](int) { return 0.0; },
       [&](int r, double v) { sm[L::xs + r] = v; }, tid);
   __shared__ int sst;
-  if (tid == 0) sst = 0;
+  __shared__ __align__(8) uint64_t fbar[2];
+  if (tid == 0) {
+    sst = 0;
+    mbar_init(&fbar[0], 1);
+    mbar_init(&fbar[1], 1);
+  }
   __syncthreads();
   if (st != 0) atomicMax(&sst, st);
-  __syncthreads();
+  __syncthreads();  // also: RS / RV (the record buffers' area) no longer read
   int32_t status = sst;
 
   double* xo = a.s.x + inst * (sN + 1) * n;
@@ -1317,13 +1429,25 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
   double* yo = a.s.y + inst * (sN + 1) * n;
   for (int r = tid; r < n; r += NTHREADS) xo[r] = sm[L::xs + r];
   bool bad = false;
-  // forward, operands from L2 (record i, A_i, B_i prefetched two stages ahead):
+  // forward: record i by TMA into buffer i & 1 one stage ahead; A_i, B_i from L2
   //   u_i = K_i x_i + k_i,  y_i = V_i x_i + v_i,  z = A_i x_i + e_i,  x_{i+1} = S⁻¹_{i+1} (z + B_i u_i)
+  auto issue_fwd = [&](int i) {  // one thread
+    fence_proxy_async();  // the CTA's earlier generic accesses of the buffer (after a barrier) before the TMA write
+    mbar_arrive_expect_tx(&fbar[i & 1], 8u * L::REC);
+    bulk_g2s(sm + ((i & 1) ? L::FR1 : L::FR0), rec0 + (int64_t)i * L::REC, 8u * L::REC, &fbar[i & 1]);
+  };
+  if (tid == 0 && N > 0) issue_fwd(0);
+  RR_PROF(RR_CTA_PROFILE_FWD, 10);
   for (int i = 0; i < N; ++i) {
-    const double* rc = rec0 + (int64_t)i * L::REC;
+    const double* rc = sm + ((i & 1) ? L::FR1 : L::FR0);
     const double* gA = a.p.A + (inst * sN + i) * n * n;
     const double* gB = a.p.B + (inst * sN + i) * n * m;
     if (i + 2 < N) prefetch_fwd(i + 2);
+    mbar_wait_parity(&fbar[i & 1], (i >> 1) & 1);
+    if (tid == 0 && i + 1 < N) issue_fwd(i + 1);  // its buffer was last read by stage i−1 (barriers since)
+    cta_matvec<NX, NX, NTHREADS>(
+        [&](int r, int k) { return gA[r + k * n]; }, [&](int k) { return sm[L::xs + k]; },
+        [&](int r) { return rc[RL::re + r]; }, [&](int r, double v) { sm[L::zs + r] = v; }, tid);
     cta_matvec<NU, NX, NTHREADS>(
         [&](int r, int k) { return rc[RL::rK + r + k * m]; }, [&](int k) { return sm[L::xs + k]; },
         [&](int r) { return rc[RL::rk + r]; },
@@ -1341,9 +1465,6 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
           bad |= !isfinite(v);
         },
         tid);
-    cta_matvec<NX, NX, NTHREADS>(
-        [&](int r, int k) { return gA[r + k * n]; }, [&](int k) { return sm[L::xs + k]; },
-        [&](int r) { return rc[RL::re + r]; }, [&](int r, double v) { sm[L::zs + r] = v; }, tid);
     __syncthreads();
     cta_matvec<NX, NU, NTHREADS>(
         [&](int r, int k) { return gB[r + k * n]; }, [&](int k) { return sm[L::us + k]; },
@@ -1372,6 +1493,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
         tid);
   }
   if (__syncthreads_or(bad) && status == 0) status = RR_ST_NONFINITE;
+  RR_PROF(RR_CTA_PROFILE_FWD, 11);
   if (status != 0) {
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
     for (int64_t e = tid; e < (sN + 1) * n; e += NTHREADS) {

@@ -50,6 +50,8 @@ def main(rep, so, kname):
     iN, iE = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
     base = int(rows[0][iA], 16)
     bl, be = collections.Counter(), collections.Counter()
+    stall_cols = [(i, c[6:]) for i, c in enumerate(h) if c.startswith("stall_")]
+    bs = collections.defaultdict(collections.Counter)  # per line: samples per stall reason
     tot, mism = 0, 0
     for x in rows:
         try:
@@ -67,10 +69,19 @@ def main(rep, so, kname):
             mism += 1
         bl[ln] += n
         be[ln] += e
+        for i, c in stall_cols:
+            try:
+                bs[ln][c] += int(x[i])
+            except (ValueError, IndexError):
+                pass
         tot += n
     print("instructions %d, opcode mismatches %d (nonzero => binary differs from the profiled one)" % (len(insts), mism))
     for ln, n in bl.most_common(int(os.environ.get("TOP", "40"))):
-        print("%5.2f%%  %8.1fM inst  %s" % (100 * n / max(tot, 1), be[ln] / 1e6, ln))
+        why = ""
+        if os.environ.get("STALLS"):  # top stall reasons of the line
+            tl = max(sum(bs[ln].values()), 1)
+            why = "  " + " ".join("%s %.0f%%" % (c, 100 * v / tl) for c, v in bs[ln].most_common(3) if v)
+        print("%5.2f%%  %8.1fM inst  %s%s" % (100 * n / max(tot, 1), be[ln] / 1e6, ln, why))
 
 
 if __name__ == "__main__":
