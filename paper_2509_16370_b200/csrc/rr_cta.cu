@@ -1438,16 +1438,38 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
   };
   if (tid == 0 && N > 0) issue_fwd(0);
   RR_PROF(RR_CTA_PROFILE_FWD, 10);
+  // A_i x and B_i u on registers: thread (row = tid / 4, part = tid % 4) holds A_i[row][part + 4j] and
+  // B_i[row][part + 4j] (the cta_matvec mapping for 64 rows), loaded from L2 one stage ahead
+  static_assert(NTHREADS == 4 * NX && NX % 4 == 0 && NU % 4 == 0, "forward register mapping");
+  const int frow = tid >> 2, fpart = tid & 3;
+  double pa[NX / 4], pb[NU / 4];
+  auto load_AB = [&](int i, double (&qa)[NX / 4], double (&qb)[NU / 4]) {
+    const double* gA = a.p.A + (inst * sN + i) * n * n + frow;
+    const double* gB = a.p.B + (inst * sN + i) * n * m + frow;
+#pragma unroll
+    for (int jj = 0; jj < NX / 4; ++jj) qa[jj] = gA[(fpart + 4 * jj) * n];
+#pragma unroll
+    for (int jj = 0; jj < NU / 4; ++jj) qb[jj] = gB[(fpart + 4 * jj) * n];
+  };
+  auto reduce4 = [](double v) {
+    v += __shfl_xor_sync(RR_FULL_MASK, v, 2);
+    return v + __shfl_xor_sync(RR_FULL_MASK, v, 1);
+  };
+  if (N > 0) load_AB(0, pa, pb);
   for (int i = 0; i < N; ++i) {
     const double* rc = sm + ((i & 1) ? L::FR1 : L::FR0);
-    const double* gA = a.p.A + (inst * sN + i) * n * n;
-    const double* gB = a.p.B + (inst * sN + i) * n * m;
+    double na[NX / 4], nb[NU / 4];
+    if (i + 1 < N) load_AB(i + 1, na, nb);  // lands during this stage
     if (i + 2 < N) prefetch_fwd(i + 2);
     mbar_wait_parity(&fbar[i & 1], (i >> 1) & 1);
     if (tid == 0 && i + 1 < N) issue_fwd(i + 1);  // its buffer was last read by stage i−1 (barriers since)
-    cta_matvec<NX, NX, NTHREADS>(
-        [&](int r, int k) { return gA[r + k * n]; }, [&](int k) { return sm[L::xs + k]; },
-        [&](int r) { return rc[RL::re + r]; }, [&](int r, double v) { sm[L::zs + r] = v; }, tid);
+    {  // z = A_i x_i + e_i
+      double acc = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < NX / 4; ++jj) acc = fma(pa[jj], sm[L::xs + fpart + 4 * jj], acc);
+      acc = reduce4(acc);
+      if (fpart == 0) sm[L::zs + frow] = rc[RL::re + frow] + acc;
+    }
     cta_matvec<NU, NX, NTHREADS>(
         [&](int r, int k) { return rc[RL::rK + r + k * m]; }, [&](int k) { return sm[L::xs + k]; },
         [&](int r) { return rc[RL::rk + r]; },
@@ -1466,9 +1488,13 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
         },
         tid);
     __syncthreads();
-    cta_matvec<NX, NU, NTHREADS>(
-        [&](int r, int k) { return gB[r + k * n]; }, [&](int k) { return sm[L::us + k]; },
-        [&](int r) { return sm[L::zs + r]; }, [&](int r, double v) { sm[L::pr2 + r] = v; }, tid);
+    {  // w = z + B_i u_i
+      double acc = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < NU / 4; ++jj) acc = fma(pb[jj], sm[L::us + fpart + 4 * jj], acc);
+      acc = reduce4(acc);
+      if (fpart == 0) sm[L::pr2 + frow] = sm[L::zs + frow] + acc;
+    }
     __syncthreads();
     cta_matvec<NX, NX, NTHREADS>(
         [&](int r, int k) { return rc[RL::rS + (r >= k ? pidx(n, r, k) : pidx(n, k, r))]; },
@@ -1480,6 +1506,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
         },
         tid);
     __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < NX / 4; ++jj) pa[jj] = na[jj];
+#pragma unroll
+    for (int jj = 0; jj < NU / 4; ++jj) pb[jj] = nb[jj];
   }
   {  // y_N = Q_N x_N + q_N
     const double* QN = a.p.QN + inst * L::SN;
