@@ -1126,7 +1126,9 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
     const double* QN = a.p.QN + inst * L::SN;
     for (int e = tid; e < n * n; e += NTHREADS) {
       const int r = e % n, c = e / n;
-      sm[L::RV + X(r, c)] = r >= c ? QN[pidx(n, r, c)] : QN[pidx(n, c, r)];
+      const double v = r >= c ? QN[pidx(n, r, c)] : QN[pidx(n, c, r)];
+      sm[L::RV + X(r, c)] = v;
+      sm[L::RS + X(r, c)] = delta * v + (r == c ? 1.0 : 0.0);  // S = I + δV_N for the first stage
     }
     for (int r = tid; r < n; r += NTHREADS) sm[L::vs + r] = a.p.qN[inst * n + r];
     if (a.f.V != nullptr)
@@ -1149,16 +1151,11 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
     const double* gM = a.p.M + s * n * m;
     const double* gR = a.p.R + s * L::SMU;
     double* rec = rec0 + (int64_t)i * L::REC;
-    __syncthreads();  // the previous stage's record reads (RS = K̃) before S is written
     RR_PROF(i, 0);
     if (i > 0) prefetch_stage(i - 1);
     const double c_cur = c_next;
     if (i > 0 && tid < n) c_next = a.p.c[(s - 1) * n + tid];
-    // (1) S = I + δV_{i+1} -> RS;  e = c_{i+1} − δ v_{i+1};  V e
-    for (int e = tid; e < n * n; e += NTHREADS) {
-      const int r = e % n, c = e / n;
-      sm[L::RS + X(r, c)] = delta * sm[L::RV + X(r, c)] + (r == c ? 1.0 : 0.0);
-    }
+    // (1) e = c_{i+1} − δ v_{i+1};  V e  (S = I + δV_{i+1} is in RS: formed with V_{i+1} by stage i+1)
     if (tid < n) {
       const double ev = c_cur - delta * sm[L::vs + tid];
       sm[L::ee + tid] = ev;
@@ -1297,7 +1294,13 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
     // (7) K̃ = G⁻¹ H -> Kt over the dead T_A;  k̃ = G⁻¹ b_u
     cta_gemm<NU, NX, NU, false>(
         [&](int r, int k) { return -sm[L::Gs + Y(r, k)]; }, [&](int k, int cc) { return sm[L::Hs + Y(k, cc)]; },
-        [&](int, int) { return 0.0; }, [&](int r, int cc, double v) { sm[L::Kt + Y(r, cc)] = v; }, warp, NW, lane);
+        [&](int, int) { return 0.0; },
+        [&](int r, int cc, double v) {
+          sm[L::Kt + Y(r, cc)] = v;
+          rec[RL::rK + r + cc * m] = -v;  // K_i = −K̃ (ld NU)
+          if (a.f.K != nullptr) a.f.K[(inst * sN + i) * m * n + r + cc * m] = -v;
+        },
+        warp, NW, lane);
     cta_matvec<NU, NU, NTHREADS>(
         [&](int r, int k) { return -sm[L::Gs + Y(r, k)]; }, [&](int k) { return sm[L::bb + NX + k]; },
         [&](int) { return 0.0; }, [&](int r, double v) { sm[L::kt + r] = v; }, tid);
@@ -1347,6 +1350,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
           int R, C;
           lower_tile(tile, R, C);
           const int r0 = 16 * R, c0 = 16 * C;
+          double* fV = a.f.V != nullptr ? a.f.V + (inst * (sN + 1) + i) * L::SN : nullptr;
 #pragma unroll
           for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -1354,32 +1358,27 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
 #pragma unroll
               for (int z = 0; z < 2; ++z) {
                 const int r = r0 + 8 * x + g, cc = c0 + 8 * y + 2 * t + z;
-                sm[L::RV + X(r, cc)] = c[q][x][y][z];
-                if (R != C) sm[L::RV + X(cc, r)] = c[q][x][y][z];
+                const double v = c[q][x][y][z], sv = delta * v + (r == cc ? 1.0 : 0.0);
+                sm[L::RV + X(r, cc)] = v;  // V_i, and S = I + δV_i for stage i − 1 (RS: K̃ is dead)
+                sm[L::RS + X(r, cc)] = sv;
+                if (R != C) {
+                  sm[L::RV + X(cc, r)] = v;
+                  sm[L::RS + X(cc, r)] = sv;
+                }
+                if (r >= cc) {
+                  rec[RL::rV + pidx(n, r, cc)] = v;
+                  if (fV != nullptr) fV[pidx(n, r, cc)] = v;
+                }
               }
         }
       }
     }
     __syncthreads();
     RR_PROF(i, 8);
-    // (9) B_{i−1} streams into Bs (Uxx is dead);  record K = −K̃ (ld NU), k = −k̃, V_i, v_i; factor outputs
+    // (9) B_{i−1} streams into Bs (Uxx is dead);  record k = −k̃, v_i (K_i, V_i were written from registers)
     if (i > 0) issue_B(i - 1);
-    for (int e = tid; e < m * n; e += NTHREADS) rec[RL::rK + e] = -sm[L::Kt + Y(e % m, e / m)];
     for (int u = tid; u < m; u += NTHREADS) rec[RL::rk + u] = -sm[L::kt + u];
-    {
-      double* fV = a.f.V != nullptr ? a.f.V + (inst * (sN + 1) + i) * L::SN : nullptr;
-      for (int e = tid; e < n * n; e += NTHREADS) {
-        const int r = e % n, c = e / n;
-        if (r >= c) {
-          const double v = sm[L::RV + X(r, c)];
-          rec[RL::rV + pidx(n, r, c)] = v;
-          if (fV != nullptr) fV[pidx(n, r, c)] = v;
-        }
-      }
-    }
     for (int r = tid; r < n; r += NTHREADS) rec[RL::rv + r] = sm[L::vs + r];
-    if (a.f.K != nullptr)
-      for (int e = tid; e < m * n; e += NTHREADS) a.f.K[(inst * sN + i) * m * n + e] = -sm[L::Kt + Y(e % m, e / m)];
     if (a.f.k != nullptr)
       for (int u = tid; u < m; u += NTHREADS) a.f.k[(inst * sN + i) * m + u] = -sm[L::kt + u];
     if (a.f.v != nullptr)
@@ -1389,11 +1388,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
   __syncthreads();
   RR_PROF(RR_CTA_PROFILE_FWD, 9);
 
-  // x_0 = (I + δV_0)⁻¹ (c_0 − δ v_0)
-  for (int e = tid; e < n * n; e += NTHREADS) {
-    const int r = e % n, c = e / n;
-    sm[L::RS + X(r, c)] = delta * sm[L::RV + X(r, c)] + (r == c ? 1.0 : 0.0);
-  }
+  // x_0 = (I + δV_0)⁻¹ (c_0 − δ v_0)  (S = I + δV_0 was formed by stage 0)
   for (int r = tid; r < n; r += NTHREADS) sm[L::ee + r] = a.p.c0[inst * n + r] - delta * sm[L::vs + r];
   // records 0 and 1, A, B of the first forward stages into L2 while x_0 is solved
   auto prefetch_fwd = [&](int i) {
