@@ -19,10 +19,16 @@
 //
 // B200 organisation: every step is a map over (instance, index) with one warp per item (n, m <= 16:
 // lane j owns column j, n×n blocks staged in the warp's shared-memory tile), so a batch-1 problem
-// with N = 4096 exposes 2048-way parallelism at the first level.  3 launches per level.
+// with N = 4096 exposes 2048-way parallelism at the first level.  Up to 2,048 items per step, all steps
+// run in ONE cooperative launch (pit_fused_kernel: persistent warps, a grid-wide barrier between
+// steps) instead of ~3 launches per level and refinement pass; wider problems (and RR_PIT_STEPS=1,
+// for A/B) launch one kernel per step.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+
+#include <cooperative_groups.h>
+#include <stdlib.h>
 
 #include "rr_common.cuh"
 #include "rr_pit.cuh"
@@ -728,6 +734,68 @@ __global__ void __launch_bounds__(WPB * 32) pit_residual_kernel(PitArgs a, rr_re
 }
 #undef PIT_ITEM_PROLOGUE
 
+// ---- all steps in one cooperative launch: persistent warps, grid-wide barrier between steps ----
+__global__ void __launch_bounds__(WPB * 32) pit_fused_kernel(PitArgs a, PitArgs c, rr_residual_buf rb, int levels) {
+  extern __shared__ __align__(16) double sm[];
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * WPB + warp, nw = (int64_t)gridDim.x * WPB;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  double* T = sm + warp * 8 * TILE;
+  const int64_t b = a.batch;
+  const int N = a.N, n = a.nx, m = a.nu;
+  auto items = [&](int64_t count, auto&& f) {  // warp-per-item map, then the grid barrier
+    for (int64_t it = gw; it < count; it += nw) f(it);
+    grid.sync();
+  };
+  for (int64_t t = gt; t < b; t += nt) a.status[t] = 0;
+  grid.sync();
+  if (N > 0) items(b * N, [&](int64_t it) { pit_assemble_item(a, it, T, lane); });
+  items(b * (N + 1), [&](int64_t it) { pit_diag_item(a, it, lane); });
+  for (int st = 1; st <= N; st *= 2) {
+    items(b * ((N - st) / (2 * st) + 1), [&](int64_t it) { pit_elim_item(a, st, it, T, lane); });
+    items(b * (N / (2 * st) + 1), [&](int64_t it) { pit_update_item(a, st, it, T, lane); });
+  }
+  items(b, [&](int64_t it) { pit_root_item(a, it, T, lane); });
+  for (int l = levels - 1; l >= 0; --l) {
+    const int st = 1 << l;
+    items(b * ((N - st) / (2 * st) + 1), [&](int64_t it) { pit_backsub_item(a, st, it, lane); });
+  }
+  items(b * (N + 1), [&](int64_t it) { pit_recover_item(a, it, lane); });
+  for (int r = 0; r < a.refine; ++r) {
+    items(b * (N + 1), [&](int64_t it) { pit_residual_item(a, rb, it, lane); });
+    if (N > 0) items(b * N, [&](int64_t it) { pit_rhs_assemble_item(c, it, lane); });
+    items(b * (N + 1), [&](int64_t it) { pit_rhs_diag_item(c, it, lane); });
+    for (int st = 1; st <= N; st *= 2) {
+      items(b * ((N - st) / (2 * st) + 1), [&](int64_t it) { pit_rhs_elim_item(c, st, it, lane); });
+      items(b * (N / (2 * st) + 1), [&](int64_t it) { pit_rhs_update_item(c, st, it, lane); });
+    }
+    items(b, [&](int64_t it) { pit_rhs_root_item(c, it, lane); });
+    for (int l = levels - 1; l >= 0; --l) {
+      const int st = 1 << l;
+      items(b * ((N - st) / (2 * st) + 1), [&](int64_t it) { pit_backsub_item(c, st, it, lane); });
+    }
+    items(b * (N + 1), [&](int64_t it) { pit_recover_item(c, it, lane); });
+    const int64_t nx1 = b * (N + 1) * n, nu1 = b * (int64_t)N * m;
+    for (int64_t t = gt; t < nx1; t += nt) {
+      a.s.x[t] += c.s.x[t];
+      a.s.y[t] += c.s.y[t];
+    }
+    for (int64_t t = gt; t < nu1; t += nt) a.s.u[t] += c.s.u[t];
+    grid.sync();
+  }
+  const int64_t per = (int64_t)(N + 1) * n * 2 + (int64_t)N * m;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  for (int64_t t = gt; t < b * per; t += nt) {  // NaN-fill the outputs of failed instances
+    const int64_t bi = t / per, e = t % per;
+    if (a.status[bi] == 0) continue;
+    if (e < (N + 1) * n) a.s.x[bi * (N + 1) * n + e] = nan;
+    else if (e < 2 * (N + 1) * n) a.s.y[bi * (N + 1) * n + e - (N + 1) * n] = nan;
+    else a.s.u[bi * N * m + e - 2 * (N + 1) * n] = nan;
+  }
+}
+
 unsigned blocks_for(int64_t items) { return (unsigned)((items + WPB - 1) / WPB); }
 
 }  // namespace
@@ -758,9 +826,48 @@ static void pit_buffers(const PitArgs& a, rr_residual_buf& rb, PitArgs& c) {
   c.s = rr_solution{cx, cu, cy};
 }
 
+// One cooperative launch of every step (default); false if the device cannot run it co-resident.
+static bool pit_fused_launch(const PitArgs& a, cudaStream_t s, cudaError_t* err) {
+  const char* v = getenv("RR_PIT_STEPS");
+  if (v != nullptr && v[0] == '1') return false;
+  int dev = 0, coop = 0, nsm = 0, per_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (!coop || nsm <= 0) return false;
+  const size_t smb = sizeof(double) * WPB * 8 * TILE;
+  if (cudaFuncSetAttribute(pit_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb) != cudaSuccess)
+    return false;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pit_fused_kernel, WPB * 32, smb) != cudaSuccess ||
+      per_sm <= 0)
+    return false;
+  // as many CTAs as the widest step has warps' worth of items, capped by co-residency.  Wide problems
+  // keep the per-step launches: measured (bench --workload pit, batch 1) fused vs per-step launches
+  // 0.38 vs 0.52 ms at N = 64, 0.53 vs 0.74 ms at N = 512, 1.05 vs 1.07 ms at N = 4096 (0.81 ms when
+  // the per-step launches are replayed from a CUDA graph, where the fused kernel stays at 1.06 ms)
+  const int64_t widest = a.batch * (int64_t)(a.N + 1);
+  if (widest > 2048) return false;
+  const int64_t want = (widest + WPB - 1) / WPB;
+  const int64_t cap = (int64_t)per_sm * nsm;
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  int levels = 0;
+  for (int st = 1; st <= a.N; st *= 2) ++levels;
+  rr_residual_buf rb;
+  PitArgs c;
+  pit_buffers(a, rb, c);
+  PitArgs aa = a;
+  void* args[] = {&aa, &c, &rb, &levels};
+  *err = cudaLaunchCooperativeKernel((const void*)pit_fused_kernel, dim3(grid), dim3(WPB * 32), args, smb, s);
+  return true;
+}
+
 cudaError_t pit_launch(const PitArgs& a, cudaStream_t s) {
   const int64_t b = a.batch;
   const int N = a.N;
+  {
+    cudaError_t e = cudaSuccess;
+    if (b > 0 && pit_fused_launch(a, s, &e)) return e;
+  }
   pit_status_init<<<(unsigned)((b + 255) / 256), 256, 0, s>>>(a);
   const size_t sm8 = sizeof(double) * WPB * 8 * TILE, sm4 = sizeof(double) * WPB * 4 * TILE;
   // per call (the attribute is per device; no global state in the library)
