@@ -418,7 +418,9 @@ def main():
         dmma_peak, dmma_src = measure_dmma_peak()
         roof = {"bound": "tensor", "achieved": fp64_tflops, "peak": dmma_peak, "unit": "TFLOP/s",
                 "frac": fp64_tflops / dmma_peak, "traffic": ncu_traffic("rr_cta_c3"),
-                "kernel": "rr_cta_kernel<64,32>", "kernel_ms": kern_ms, "dtype_peak": "fp64 DMMA",
+                "kernel": ("rr_cta_kernel<64,32> (K4, one instance per SM)" if os.environ.get("RR_B200_CTA") == "1"
+                           else "rr_cta2_kernel<64,32> (K4b, two instances per SM)"),
+                "kernel_ms": kern_ms, "dtype_peak": "fp64 DMMA",
                 "alg_flops_per_stage": ALG_FLOPS_PER_STAGE, "peak_source": dmma_src,
                 "hbm_gbs_alg": achieved}
     else:
