@@ -24,6 +24,9 @@ struct IpmArgs {
 int64_t ipm_ws_bytes(const ipm_dims& d);
 cudaError_t ipm_launch(const IpmArgs& a, cudaStream_t s, bool* supported);
 bool ipm_supported(const ipm_dims& d);
+// the C4 shape on one thread per instance (ipm_c4t.cu)
+bool ipm_c4t_applies(const IpmArgs& a);
+cudaError_t ipm_c4t_launch(const IpmArgs& a, cudaStream_t s);
 // caller-evaluated line search (ipm_user.cu)
 cudaError_t ipm_merit_launch(const ipm_dims& d, const ipm_stage_data& data, const ipm_iterate& it, const ipm_result& r,
                              const double* alpha, const ipm_trial_values& tv, double* merit, cudaStream_t s);

@@ -166,11 +166,14 @@ def test_spec_scalar_step_exact_on_gpu():
     assert np.all(np.abs(g["merit_acc"] - 3.848760597239781) <= 2e-15)
 
 
-def test_ipm_c4_unaligned_operands_equal_aligned():
-    """The exact C4 kernel copies the stage data with a static plan of 16-byte LDGSTS when every
-    copied operand base is 16-byte aligned, else with the generic 8-byte copies (ipm_launch decides):
-    an 8-byte-offset view of A and of the iterate x gives bitwise the aligned results."""
+def test_ipm_c4_unaligned_operands_equal_aligned(monkeypatch):
+    """The exact C4 lane-group kernel copies the stage data with a static plan of 16-byte LDGSTS when
+    every copied operand base is 16-byte aligned, else with the generic 8-byte copies (ipm_launch
+    decides): an 8-byte-offset view of A and of the iterate x gives bitwise the aligned results.
+    (RR_IPM_C4T=0 pins the lane-group kernel: the thread-per-instance A/B variant, RR_IPM_C4T=1, only
+    takes aligned inputs.)"""
     import paper_2509_16370_b200 as rr
+    monkeypatch.setenv("RR_IPM_C4T", "0")
     b = cartpole_c4(24, N=30).to("cuda")
     c = b.clone()
 
