@@ -88,3 +88,19 @@ b = cartpole_c4(3, seed=3, N=8, device="cuda")
 rep3 = rr.ipm_solve(b, max_iters=4, linear_merit=True)
 torch.cuda.synchronize()
 print("linear_merit", rep3["status"].tolist())
+# round 2, session 3: K4b (C3 shape, two CTAs per SM) and K4, the fused cooperative parallel-in-time
+# launch (small problems), the thread-per-instance C4 ipm_step (A/B variant)
+p = synth.random_stable_lqr(64, 32, 3, 3, seed=10).to("cuda")
+o4b = rr.rr_factor_solve(p, want_factor=True)
+os.environ["RR_B200_CTA"] = "1"
+o4 = rr.rr_factor_solve(p)
+os.environ.pop("RR_B200_CTA")
+p = synth.random_stable_lqr(12, 4, 9, 3, seed=11, delta=1e-4).to("cuda")
+opit = rr.rr_factor_solve_pit(p)
+os.environ["RR_IPM_C4T"] = "1"
+b = cartpole_c4(37, seed=3, N=8, device="cuda")
+rc4t = rr.ipm_step(b)
+os.environ.pop("RR_IPM_C4T")
+torch.cuda.synchronize()
+print("session 3", int(o4b["status"].abs().sum()), int(o4["status"].abs().sum()), int(opit["status"].abs().sum()),
+      rc4t["status"].tolist()[:4])
