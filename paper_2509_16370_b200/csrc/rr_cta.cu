@@ -1176,19 +1176,22 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
     );
     if (fail && st == 0) st = mk_status(RR_ST_S_NOT_PD, i);
     RR_PROF(i, 2);
-    // (3) W = S⁻¹ V in place over V (tiles in registers, one barrier between the reads and the
-    //     writes);  g = v_{i+1} + S⁻¹ V e;  record S⁻¹
+    // (3) W = S⁻¹ V in place over V (symmetric: W = V(I + δV)⁻¹; the 10 lower 16×16 tiles in
+    //     registers, mirrored on the store after one barrier);  g = v_{i+1} + S⁻¹ V e;  record S⁻¹
     cp_async_wait<0>();  // B_i (made visible by the barriers below)
     {
-      constexpr int MT = NX / 16, NTW = MT * MT, TPW = (NTW + NW - 1) / NW;
+      constexpr int MT = NX / 16, NTL = MT * (MT + 1) / 2, TPW = (NTL + NW - 1) / NW;
       const int g = lane >> 2, t = lane & 3;
       double c[TPW][2][2][2];
 #pragma unroll
       for (int q = 0; q < TPW; ++q) {
-        const int tile = warp + q * NW, r0 = (tile % MT) * 16, c0 = (tile / MT) * 16;
+        const int tile = warp + q * NW;
 #pragma unroll
         for (int x = 0; x < 8; ++x) (&c[q][0][0][0])[x] = 0.0;
-        if (tile < NTW) {
+        if (tile < NTL) {
+          int R, C;
+          lower_tile(tile, R, C);
+          const int r0 = 16 * R, c0 = 16 * C;
 #pragma unroll 8
           for (int kk = 0; kk < NX / 4; ++kk) {
             double av[2], bv[2];
@@ -1213,14 +1216,21 @@ __global__ void __launch_bounds__(NTHREADS, 2) rr_cta2_kernel(const FusedArgs a)
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < TPW; ++q) {
-        const int tile = warp + q * NW, r0 = (tile % MT) * 16, c0 = (tile / MT) * 16;
-        if (tile < NTW) {
+        const int tile = warp + q * NW;
+        if (tile < NTL) {
+          int R, C;
+          lower_tile(tile, R, C);
+          const int r0 = 16 * R, c0 = 16 * C;
 #pragma unroll
           for (int x = 0; x < 2; ++x)
 #pragma unroll
             for (int y = 0; y < 2; ++y)
 #pragma unroll
-              for (int z = 0; z < 2; ++z) sm[L::RV + X(r0 + 8 * x + g, c0 + 8 * y + 2 * t + z)] = c[q][x][y][z];
+              for (int z = 0; z < 2; ++z) {
+                const int r = r0 + 8 * x + g, cc = c0 + 8 * y + 2 * t + z;
+                sm[L::RV + X(r, cc)] = c[q][x][y][z];
+                if (R != C) sm[L::RV + X(cc, r)] = c[q][x][y][z];
+              }
         }
       }
     }
