@@ -174,7 +174,7 @@ rr_err rr_factor_solve_host_pipelined(const rr_dims* dims, const rr_problem* pro
                                       int32_t* status_dev, void* workspace, int64_t workspace_bytes, int32_t nchunks,
                                       void* const* streams, int32_t nstreams);
 
-/* ============================ factorization / solve split (rows a2 | a3-a5) ============================/* ============================ factorization / solve split (rows a2 | a3-a5) ============================
+/* ============================ factorization / solve split (rows a2 | a3-a5) ============================
  * The paper's solver plugs problem-specific "KKT system factorization" and "KKT system solve"
  * callbacks into a shared backend.  rr_factor is the matrix half of Eq.(RR),
  * which depends only on (A, B, Q, M, R, Q_N, δ); rr_solve is the vector half plus the forward sweep

@@ -264,8 +264,9 @@ __global__ void __launch_bounds__(WARPS * 32, EXACT ? 4 : 1) ipm_step_kernel(con
       put(IB::z + e, term ? a.it.zN + inst * ng + e : a.it.z + si * ng + e, ok, 1.0);
     }
     const double* Csrc = term ? a.d_.CeN + inst * (int64_t)nc * n : a.d_.Ce + si * (int64_t)nc * ww;
+    constexpr int NCD = NC > 0 ? NC : 1;  // (no iterations when NC == 0)
     for (int e = j; e < NC * NZ; e += LG) {
-      const int q = e % NC, c = e / NC;
+      const int q = e % NCD, c = e / NCD;
       const double* src = nullptr;
       if (q < nc) {
         if (c < NX) { if (c < n) src = Csrc + q + (int64_t)c * nc; }

@@ -38,7 +38,7 @@ namespace rrk {
 
 namespace {
 
-constexpr int NX = 4, NU = 1, NZ = 5, NG = 4;
+constexpr int NX = 4, NZ = 5, NG = 4;  // n, n + m (m = 1), n_g
 // forward record per stage (doubles), stored [stage][entry][instance]
 constexpr int R_PHI = 0, R_phi = 16, R_K = 20, R_k = 24, R_V = 25, R_v = 35, RCP = 40;
 
