@@ -104,3 +104,26 @@ def test_cuda_graph_capture_replay():
     torch.cuda.synchronize()
     for k in ("x", "u", "y"):
         assert torch.equal(out_pit[k], ref_pit[k]) and torch.equal(call.sol[k], ref_seq[k]), k
+
+
+@pytest.mark.parametrize("nx,nu,N,batch,delta", [(12, 4, 64, 1, 1e-4), (4, 1, 30, 9, 0.0), (5, 3, 17, 6, 1e-2)])
+def test_pit_single_launch_equals_step_launches(nx, nu, N, batch, delta, monkeypatch):
+    """Up to 2,048 items per step the whole solve runs as one cooperative launch (grid barrier
+    between steps); RR_PIT_STEPS=1 forces one launch per step.  Each item does the same arithmetic in
+    both, so the results are bitwise equal (and at the parity bar against the oracle)."""
+    p = synth.random_stable_lqr(nx, nu, N, batch, seed=900 + N, delta=delta)
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("RR_PIT_STEPS", flag)
+        o = rr().rr_factor_solve_pit(p.to("cuda"))
+        torch.cuda.synchronize()
+        outs.append({k: v.cpu() for k, v in o.items()})
+    for k in ("x", "u", "y", "status"):
+        assert torch.equal(outs[0][k], outs[1][k]), k
+    ref = oracle.rr_solve_t2(p, nthreads=4)
+    g = {k: outs[0][k].numpy() for k in ("x", "u", "y", "status")}
+    assert np.array_equal(g["status"], ref["status"])
+    for k in ("x", "u", "y"):
+        num = np.abs(g[k] - ref[k]).reshape(batch, -1).max(1)
+        den = np.maximum(np.abs(ref[k]).reshape(batch, -1).max(1), 1e-300)
+        assert float((num / den).max()) <= 1e-9, k
